@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Benchmark: optimisation steps/s (bin + fwd + loss + bwd + Adam + psnr) of the
+B200 compositor on BASELINE.json's metric config (c3: 1024x809, 3000
+fingerprint + 2000 autograph primitives) with synthetic, seeded inputs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  --impl reference times the reference's CPU
+algorithm (the C/OpenMP oracle port, oracle/) on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))
+
+METRIC = "optimisation steps/sec (fwd+bwd+Adam) at 1024x809, 5000 prims; % HBM roofline"
+UNIT = "steps/s"
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def _peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "src": "fallback"}
+
+
+def algorithmic_bytes(P: int, K16: int, N: int, atlas_texels: int) -> dict:
+    """B_step = 68 P + 12 K16 + 288 N + 16 * texels (fp32 model)."""
+    A = 16 * atlas_texels
+    return {
+        "step": 68 * P + 12 * K16 + 288 * N + A,
+        # per-kernel split of the same model
+        "forward": 48 * P + 4 * K16 + A,
+        "backward": 20 * P + 4 * K16 + 32 * N,
+        "bin": 4 * K16 + 32 * N,
+        "adam": 224 * N,
+    }
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling via NVML during the timed region."""
+
+    def __init__(self, index: int = 0, period: float = 0.05):
+        self.samples: list[tuple[int, int]] = []
+        self.reasons_seen: set[str] = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        self.ok = False
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.period = period
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    _REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        "display_clock_setting": 0x100,
+    }
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, rs))
+                for name, bit in self._REASONS.items():
+                    if rs & bit and name != "gpu_idle":
+                        self.reasons_seen.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self) -> dict:
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml-unavailable"]}
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        sm = [s for s, _ in self.samples]
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons_seen), "samples": len(sm)}
+
+
+def cpu_baseline(config: str, max_seconds: float = 15.0, max_steps: int = 20) -> dict:
+    """The reference's CPU algorithm (C/OpenMP oracle port) on this host, bounded sample."""
+    import cpu_oracle as orc
+
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.fit import effective_padding
+
+    orc.build()
+    w = synth.make_workload(config)
+    loop = orc.Loop(w.scene, w.target, w.cfg, effective_padding(w.cfg), tile=32)
+    total = w.steps
+    loop.step(0, total)  # untimed warm-up step (reference protocol: warmup + untimed step)
+    times = []
+    t_all = time.perf_counter()
+    it = 1
+    while it < total and len(times) < max_steps and time.perf_counter() - t_all < max_seconds:
+        t0 = time.perf_counter()
+        loop.step(it, total)
+        times.append(time.perf_counter() - t0)
+        it += 1
+    med = float(np.median(times))
+    return {"value": 1.0 / med, "unit": UNIT, "cores": orc.threads(), "kind": "port",
+            "sample": f"{config}: {len(times)} timed run_loop-body steps (median; after 1 untimed)",
+            "ms_per_step": med * 1e3, "cpu_model": _cpu_model()}
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import cpu_oracle as orc
+
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.fit import effective_padding
+
+    orc.build()
+    w = synth.make_workload(args.config)
+    loop = orc.Loop(w.scene, w.target, w.cfg, effective_padding(w.cfg), tile=32)
+    total = max(w.steps, args.warmup + args.steps)
+    for it in range(args.warmup):
+        loop.step(it, total)
+    t0 = time.perf_counter()
+    for it in range(args.warmup, args.warmup + args.steps):
+        loop.step(it, total)
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": _config(args.config, w),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": orc.threads(), "kind": "port",
+                         "sample": f"{args.config}: {args.steps} run_loop-body steps after "
+                                   f"{args.warmup} warm-up (C/OpenMP port of the reference, "
+                                   f"float64, bit-identical to it on golden vectors)",
+                         "cpu_model": _cpu_model()},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config(name: str, w) -> dict:
+    sc = w.scene
+    return {"workload": f"{name}: {sc.canvas_w}x{sc.canvas_h}, {sc.n} prims, "
+                        f"{len(sc.templates)} templates, loss {w.loss.kind}",
+            "canvas": [sc.canvas_w, sc.canvas_h], "primitives": sc.n,
+            "templates": len(sc.templates), "render_tile": 16,
+            "l2": "flushed (256 MiB write) before every timed step"}
+
+
+def graph_kernel_count(graph) -> int | None:
+    try:
+        from cuda.bindings import runtime as rt
+
+        g = graph.raw_cuda_graph()
+        err, nodes, num = rt.cudaGraphGetNodes(g, 0)
+        err, nodes, num = rt.cudaGraphGetNodes(g, num)
+        kinds = 0
+        for nd in nodes:
+            e, t = rt.cudaGraphNodeGetType(nd)
+            if t == rt.cudaGraphNodeType.cudaGraphNodeTypeKernel:
+                kinds += 1
+        return kinds
+    except Exception:
+        return None
+
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.dist import make_allreduce, row_bands
+    from paper_2602_22625_b200.fit import StepEngine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = synth.make_workload(args.config)
+    sc = w.scene
+    H, W = sc.canvas_h, sc.canvas_w
+    nty = -(-H // 16)
+    band = row_bands(nty, world)[rank]
+    prof_steps = 20
+    e2e_steps = max(10, args.steps // 2)
+    total = max(w.steps, args.warmup + args.steps + prof_steps + e2e_steps + 2)
+    w.cfg.num_iterations = total
+    eng = StepEngine(sc, w.cfg, w.loss, total, band=band,
+                     allreduce=make_allreduce() if world > 1 else None, use_graph=True)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    # warm-up (step 0 eager + CUDA-graph capture, then replays)
+    eng.run(args.warmup)
+    torch.cuda.synchronize()
+    eng.check()
+    K16 = int(eng.comp.status[0].item())
+
+    # timed region: K graph replays, L2 flushed (untimed) before each
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for e0, e1 in evs:
+        flush.zero_()
+        e0.record()
+        eng.step()
+        e1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    ms_total = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = 1e3 / ms_step  # whole-job steps/s (every rank advances the same step)
+
+    # per-kernel timing (eager, events on the launching stream, L2 flushed)
+    comp = eng.comp
+    stage_ms = {"bin": 0.0, "forward": 0.0, "backward": 0.0, "adam": 0.0}
+    from paper_2602_22625_b200 import _native as nat
+    from paper_2602_22625_b200.compositor import adam_launch
+
+    for _ in range(prof_steps):
+        flush.zero_()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev[0].record()
+        comp.preprocess(eng.params)
+        comp.bin()
+        ev[1].record()
+        comp.forward(save=True, eps_skip=eng.eps_skip, bg_rgb=eng.bg_rgb, bg_img=eng.bg_img,
+                     loss_kind=eng.loss_kind, target=eng.target, target_alpha=eng.target_alpha,
+                     alpha_w=eng.alpha_w, sums=eng.sums, P_total=eng.P)
+        ev[2].record()
+        comp.backward(comp.dI, eng.gbuf,
+                      dA=comp.dA if eng.loss_kind == nat.PF_LOSS_SPATIAL else None,
+                      bg_rgb=eng.bg_rgb, bg_img=eng.bg_img)
+        ev[3].record()
+        if eng.allreduce is not None:
+            eng.allreduce(eng.gbuf)
+        adam_launch(eng.params, eng.grads, eng.m, eng.v, frozen=eng.frozen, gains=eng.gains,
+                    n=eng.n, lr_table=eng.lr_table, bc1_table=eng.bc1_table,
+                    bc2_table=eng.bc2_table, iter_counter=eng.iter, clamp=True,
+                    s_min=w.cfg.scale_min, s_max=w.cfg.scale_max, zero_grads=True, sums=eng.sums,
+                    loss_kind=eng.loss_kind, alpha_w=eng.alpha_w, P_total=eng.P,
+                    hist_loss=eng.hist_loss, hist_psnr=eng.hist_psnr, counter=eng.adam_counter)
+        ev[4].record()
+        torch.cuda.synchronize()
+        eng.done += 1
+        for k, name in enumerate(("bin", "forward", "backward", "adam")):
+            stage_ms[name] += ev[k].elapsed_time(ev[k + 1]) / prof_steps
+
+    # end-to-end through the public step API with HOST buffers each step:
+    # H2D of the packed parameter vector (pinned), graph replay, D2H of the
+    # updated vector + the step's loss.
+    n = eng.n
+    h_params = torch.empty(n * 8, dtype=torch.float64, pin_memory=True)
+    h_params.copy_(eng.params.view(-1).cpu())
+    h_loss = torch.empty(1, dtype=torch.float64, pin_memory=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_start.record()
+    for _ in range(e2e_steps):
+        it = eng.done
+        eng.params.view(-1).copy_(h_params, non_blocking=True)
+        eng.step()
+        h_params.copy_(eng.params.view(-1), non_blocking=True)
+        h_loss.copy_(eng.hist_loss[it : it + 1], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    e_end.record()
+    torch.cuda.synchronize()
+    e2e_ms = e_start.elapsed_time(e_end) / e2e_steps
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    eng.check()
+
+    nodes = graph_kernel_count(eng.graph) if eng.graph is not None else None
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peaks = _peaks()
+    ab = algorithmic_bytes(eng.P, K16, n, eng.atlas.texels)
+    dom = max(("forward", "backward"), key=lambda k: stage_ms[k])
+    achieved = ab[dom] / (stage_ms[dom] * 1e-3) / 1e9
+    cpu = cpu_baseline(args.config) if (world == 1 and not args.no_cpu) else None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded structure-aware init; procedural templates; smooth random target)",
+        "config": {**_config(args.config, w), "parallelism": f"rowband{world}",
+                   "K16": K16, "band": [band.ty_begin, band.ty_end]},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved,
+                     "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                     "peak_src": peaks["src"], "algorithmic_bytes": ab[dom],
+                     "kernel_ms": stage_ms[dom],
+                     "step_frac": ab["step"] * value / 1e9 / peaks["hbm_gbs"]},
+        "stage_ms": stage_ms,
+        "e2e": {"value": 1e3 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": n * 8 * 8,
+                "d2h_bytes_per_step": n * 8 * 8 + 8},
+        "gpu_launches": (nodes * args.steps) if nodes else None,
+        "kernels_per_step": nodes,
+        "clocks": clk,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,182 @@
+/*
+ * primfit_b200.h — C ABI of the B200 (sm_100a) differentiable bitmap compositor.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `primfit` (arxiv 2602.22625, DiffBMP): one optimisation step of
+ * fit.run_loop (pkg/src/primfit/fit.py:448-505) =
+ *     bin_tiles -> render_forward(save=True) -> loss_mse -> backward -> adam_step -> psnr
+ *
+ * The reference has no FFI; its native layer is four numba kernels with flat
+ * positional array arguments (pkg/src/primfit/_kernels.py:76-363) driven by the
+ * L2 Python API (raster.py, grad.py, fit.py).  Each entry point below names the
+ * reference unit it replaces.  Conventions, identical for every entry point:
+ *
+ *   - every pointer argument is a DEVICE pointer unless the comment says "host";
+ *   - every output buffer is caller-allocated (reference ownership model,
+ *     raster.py:327-342 allocates before calling the kernels);
+ *   - every call is stream-ordered on `stream` (a cudaStream_t, passed as void*
+ *     so the header has no CUDA dependency) and never synchronises;
+ *   - the return value is 0 (PF_OK) or a nonzero code: a cudaError_t value from
+ *     the launch, or one of the PF_ERR_* codes below.  No exceptions cross the ABI.
+ *
+ * Parameter layout (scene.py:36, PARAM_GROUPS): params is float64 [n][8] with
+ * columns x, y, scale, rotation, opacity_logit, c0, c1, c2 (primitive-major,
+ * exactly the reference's packed vector from pack_params, scene.py:183-191).
+ *
+ * Template atlas (raster.py:63-96, PackedScene.tex/toff/tw/th): float64,
+ * PLANAR [4][texels] (R plane, G plane, B plane, A plane); template t occupies
+ * texels [tpl_base[t], tpl_base[t] + tpl_w[t]*tpl_h[t]) of every plane,
+ * row-major (texel index base + v*w + u, _kernels.py:40).
+ *
+ * Canvas tiles are row-major (t = ty*ntx + tx, _kernels.py:88-89).  A "row band"
+ * [ty_begin, ty_end) restricts binning/rendering to those tile rows (multi-GPU
+ * row-band sharding); band-local tile index tb = (ty - ty_begin)*ntx + tx.
+ * The full canvas is ty_begin = 0, ty_end = ceil(H / tile).
+ */
+#ifndef PRIMFIT_B200_H
+#define PRIMFIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PF_OK 0
+#define PF_ERR_ARG 1001      /* bad argument (null pointer, negative size, ...) */
+#define PF_ERR_SCRATCH 1002  /* scratch buffer smaller than pf_bin_scratch_bytes */
+#define PF_ERR_TILE 1003     /* render kernels support tile == 16 only */
+
+/* Loss kinds fused into pf_forward (fit.py:112-171 evaluate_loss). */
+#define PF_LOSS_NONE 0
+#define PF_LOSS_MSE 1        /* loss_mse, fit.py:112-116 */
+#define PF_LOSS_SPATIAL 2    /* loss_spatial, fit.py:128-151 */
+
+/* ABI version; bumped on any signature change. */
+int pf_abi_version(void);
+
+/* Bytes of the per-primitive device record written by pf_preprocess
+ * (replaces PackedScene, raster.py:45-96, as the kernels' view of a scene). */
+size_t pf_record_bytes(void);
+
+/* Render tile edge the forward/backward kernels are built for (16). */
+int pf_render_tile(void);
+
+/* Scratch bytes pf_preprocess + pf_bin need for n primitives, n_tiles band
+ * tiles and `capacity` (tile, primitive) bin entries. Host-only query. */
+size_t pf_bin_scratch_bytes(int n, int n_tiles, int capacity);
+
+/* Saved-forward entry capacity for `capacity` bin entries (256 per entry). */
+long long pf_saved_capacity(int capacity);
+
+/*
+ * K1 — per-primitive preprocess + bin count.
+ * Replaces: the per-pair inline transform/sigmoid math of every numba kernel
+ * (_kernels.py:106-123), pack_scene (raster.py:63-96) and the bbox part of
+ * bin_tiles (raster.py:246-257, bbox_half_side raster.py:222-224).
+ *   zorder   [n]  primitive indices in ascending z (PackedScene.order, raster.py:92)
+ *   tpl_q    [n_tpl] aspect q used for primitives of that template (th/tw when
+ *                    preserve_aspect, else 1.0; raster.py:88-91)
+ *   tpl_hyp  [n_tpl] hypot(1, max(1, q)) (host-computed, bit-identical to
+ *                    math.hypot in bbox_half_side)
+ *   padding        bbox padding (fit.effective_padding, fit.py:338-341)
+ *   rec      out   n * pf_record_bytes() bytes
+ *   scratch        pf_bin_scratch_bytes(n, n_band_tiles, capacity) bytes
+ */
+int pf_preprocess(const double* params, const int32_t* template_id, const int32_t* zorder, int n,
+                  const int32_t* tpl_base, const int32_t* tpl_w, const int32_t* tpl_h,
+                  const double* tpl_q, const double* tpl_hyp, int n_tpl,
+                  double alpha_max, double mu_blend, double padding,
+                  int W, int H, int tile, int ty_begin, int ty_end, int capacity,
+                  void* rec, void* scratch, size_t scratch_bytes, void* stream);
+
+/*
+ * K2 — tile binning: exclusive scan of per-primitive counts (z order), fill of
+ * (tile, z-position) keys, stable radix sort on the tile key, exclusive scan of
+ * per-tile counts.  Output is bit-identical to bin_tiles (raster.py:227-265):
+ * CSR offsets/indices, primitive indices ascending in z inside each tile.
+ *   bin_off  out [n_band_tiles + 1]   (TileBins.offsets)
+ *   bin_idx  out [capacity]           (TileBins.indices; first K valid)
+ *   status   out int32[4]: [0] = K (total entries), [1] = overflow flag (K > capacity)
+ */
+int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity,
+           void* scratch, size_t scratch_bytes,
+           int32_t* bin_off, int32_t* bin_idx, int32_t* status, void* stream);
+
+/*
+ * K3 — tiled front-to-back forward (16x16 tiles), optionally saving the
+ * per-pixel contribution lists for the backward and optionally fusing the loss.
+ * Replaces: forward_nosave / count_entries + fill_entries (_kernels.py:76-255),
+ * render_forward (raster.py:290-363), and (when loss_kind != NONE) loss_mse /
+ * loss_spatial (fit.py:112-151).
+ *   tex        [4][texels] planar float64 atlas
+ *   bg_img     float32 [H][W][3] per-pixel background, or NULL for solid (bg_r,bg_g,bg_b)
+ *   ent_j/ent_T/ent_n  saved state (NULL = render only): ent_j uint16 and ent_T
+ *              float64 of pf_saved_capacity(capacity) entries, ent_n int32 [H*W]
+ *   img        out float32 [H][W][3]; alpha out float32 [H][W] (band rows written)
+ *   target     float32 [H][W][3]; target_alpha float32 [H][W] (SPATIAL only)
+ *   dI         out float32 [H][W][3] = dL/dI; dA out float32 [H][W] (SPATIAL)
+ *   part       scratch float64 [n_band_tiles * 4]; counter: uint32 zeroed once
+ *   sums       out float64[3]: sum (I-t)^2, sum ((I-t)*mask)^2, sum (I_a - t_a)^2
+ *   inv_3P, inv_P  1/(3*H*W), 1/(H*W) of the FULL canvas (band-independent)
+ */
+int pf_forward(const void* rec, int n, const double* tex, int texels,
+               const int32_t* bin_off, const int32_t* bin_idx, const int32_t* status,
+               int W, int H, int ty_begin, int ty_end,
+               double eps_skip, double mu_blend,
+               double bg_r, double bg_g, double bg_b, const float* bg_img,
+               uint16_t* ent_j, double* ent_T, int32_t* ent_n,
+               float* img, float* alpha,
+               int loss_kind, const float* target, const float* target_alpha, double alpha_w,
+               double inv_3P, double inv_P,
+               float* dI, float* dA, double* part, uint32_t* counter, double* sums,
+               void* stream);
+
+/*
+ * K4 — backward: back-to-front over each pixel's saved contributions,
+ * warp-level (shfl_xor butterfly) reduction of the 8 per-primitive gradients
+ * before float64 atomics into grads.
+ * Replaces: backward_tiles + reduce_partials (_kernels.py:258-363,
+ * grad.py:134-206).  grads is ACCUMULATED into (caller zeroes it).
+ *   dI float32 [H][W][3] (dL/dI), dA float32 [H][W] or NULL (dL/dA = 0)
+ *   grads  float64 [n][8], columns as params
+ */
+int pf_backward(const void* rec, int n, const double* tex, int texels,
+                const int32_t* bin_off, const int32_t* bin_idx, const int32_t* status,
+                const uint16_t* ent_j, const double* ent_T, const int32_t* ent_n,
+                const float* dI, const float* dA,
+                double bg_r, double bg_g, double bg_b, const float* bg_img,
+                double mu_blend, int W, int H, int ty_begin, int ty_end,
+                double* grads, void* stream);
+
+/*
+ * K5 — fused Adam step (+ loss/psnr history, + gradient zeroing for the next step).
+ * Replaces: adam_step (fit.py:195-238), lr_schedule lookup (fit.py:174-186),
+ * psnr (fit.py:241-247) and the HistoryEntry bookkeeping (fit.py:505).
+ * Two modes:
+ *   table mode (iter != NULL): it = *iter; lr = lr_table[it]; bias corrections
+ *     bc1_table[it] = 1 - 0.9^t, bc2_table[it] = 1 - 0.999^t (host-computed);
+ *     hist_loss[it], hist_psnr[it] written from sums; *iter incremented.
+ *   scalar mode (iter == NULL): lr, bc1, bc2 given as scalars; no history.
+ *   gains8   host pointer to 8 per-column gains (NULL = all 1)
+ *   frozen   uint8 [n] or NULL (OptimState.frozen)
+ *   clamp    nonzero: clip the scale column to [s_min, s_max] (all rows)
+ *   zero_grads nonzero: grads[0..8n) set to 0 after use
+ *   sums     float64[3] from pf_forward (after any allreduce); loss_kind/alpha_w
+ *            select mse or spatial for the history value
+ *   counter  uint32 zeroed once (last-block detection)
+ */
+int pf_adam(double* params, double* grads, double* m, double* v, const uint8_t* frozen,
+            const double* gains8, int n,
+            const double* lr_table, const double* bc1_table, const double* bc2_table, int32_t* iter,
+            double lr, double bc1, double bc2,
+            int clamp, double s_min, double s_max, int zero_grads,
+            const double* sums, int loss_kind, double alpha_w, double inv_3P, double inv_P,
+            double* hist_loss, double* hist_psnr, uint32_t* counter, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PRIMFIT_B200_H */

@@ -1,0 +1,243 @@
+"""Device-resident compositor: owns the HBM buffers and launches the C-ABI stages.
+
+One ``Compositor`` is bound to a scene *structure* (template ids, z order,
+template atlas, canvas, row band) and a bin capacity; parameters change every
+step and are passed as a float64 (N, 8) CUDA tensor.  The stages map to the
+reference's per-iteration calls in fit.run_loop (pkg/src/primfit/fit.py:486-501):
+
+    preprocess()+bin()  ->  bin_tiles        (raster.py:227-265)
+    forward()           ->  render_forward   (raster.py:290-363) [+ loss, fit.py:112-151]
+    backward()          ->  backward         (grad.py:134-206)
+    adam()              ->  adam_step        (fit.py:195-238)
+
+HBM layout: params/grads/moments float64 [N][8]; primitive
+records 192 B/prim; atlas float64 planar [4][texels]; bins int32 CSR; saved
+forward = uint16 list position + float64 transmittance per contributing
+(pixel, primitive) at slot 256*bin_off[t] + k*256 + pixel; pixel buffers float32.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .errors import BinOverflow
+
+RENDER_TILE = 16
+
+
+def _stream_handle(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class DeviceAtlas:
+    """Template atlas in HBM: planar float64 RGBA + per-template metadata.
+
+    Replaces PackedScene.tex/toff/tw/th (raster.py:79-87); ``q`` is the v-axis
+    aspect (th/tw when preserve_aspect, else 1, raster.py:88-91) and ``hyp`` the
+    bbox factor hypot(1, max(1, q)) computed with Python's math.hypot so the
+    binning bbox is bit-identical to bbox_half_side (raster.py:222-224).
+    """
+
+    def __init__(self, templates, preserve_aspect: bool, device="cuda"):
+        rgbas = [np.asarray(t.rgba, dtype=np.float64) for t in templates]
+        self.n_templates = len(rgbas)
+        self.tw = np.asarray([a.shape[1] for a in rgbas], dtype=np.int32)
+        self.th = np.asarray([a.shape[0] for a in rgbas], dtype=np.int32)
+        sizes = self.tw.astype(np.int64) * self.th.astype(np.int64)
+        self.base = np.concatenate(([0], np.cumsum(sizes)))[:-1].astype(np.int32)
+        self.texels = int(sizes.sum())
+        planar = np.zeros((4, max(self.texels, 1)), dtype=np.float64)
+        for a, b, sz in zip(rgbas, self.base, sizes):
+            planar[:, b : b + sz] = a.reshape(-1, 4).T
+        if preserve_aspect:
+            self.q = self.th.astype(np.float64) / self.tw.astype(np.float64)
+        else:
+            self.q = np.ones(self.n_templates, dtype=np.float64)
+        self.hyp = np.asarray([math.hypot(1.0, max(1.0, float(q))) for q in self.q])
+        dev = torch.device(device)
+        self.tex = torch.from_numpy(planar).to(dev)
+        self.d_base = torch.from_numpy(self.base).to(dev)
+        self.d_w = torch.from_numpy(self.tw).to(dev)
+        self.d_h = torch.from_numpy(self.th).to(dev)
+        self.d_q = torch.from_numpy(self.q).to(dev)
+        self.d_hyp = torch.from_numpy(self.hyp).to(dev)
+
+
+def bin_capacity(scales: np.ndarray, tids: np.ndarray, hyp: np.ndarray, padding: float,
+                 tile: int, ntx: int, nty_band: int) -> int:
+    """Upper bound on (tile, primitive) entries for the given per-primitive scales.
+
+    A bbox of half side r covers at most floor(2r/tile)+2 tiles per axis.  The
+    Adam step clamps scale to s_max, so bounding with s_max makes the bound
+    hold for the whole fit (no device->host sync, no overflow).
+    """
+    if len(scales) == 0:
+        return 0
+    r = np.asarray(scales, dtype=np.float64) * hyp[tids] + padding
+    span = np.floor(2.0 * r / tile) + 2.0
+    per = np.minimum(span, ntx) * np.minimum(span, max(nty_band, 1))
+    return int(min(per.sum(), float(2**31 - 1)))
+
+
+@dataclass
+class Band:
+    ty_begin: int
+    ty_end: int
+
+
+class Compositor:
+    """HBM buffers + stage launchers for one scene structure on one device."""
+
+    def __init__(self, template_id: np.ndarray, z: np.ndarray, atlas: DeviceAtlas, W: int,
+                 H: int, *, alpha_max: float, mu_blend: float, padding: float,
+                 capacity: int, band: Band | None = None, bin_tile: int = RENDER_TILE,
+                 device="cuda", d_tid: torch.Tensor | None = None,
+                 d_zorder: torch.Tensor | None = None):
+        self.lib = nat.load()
+        self.device = torch.device(device)
+        self.n = int(len(template_id))
+        self.atlas = atlas
+        self.W, self.H = int(W), int(H)
+        self.alpha_max, self.mu_blend, self.padding = float(alpha_max), float(mu_blend), float(padding)
+        self.tile = int(bin_tile)
+        self.ntx = -(-self.W // self.tile)
+        self.nty = -(-self.H // self.tile)
+        self.band = band or Band(0, self.nty)
+        self.n_tiles = (self.band.ty_end - self.band.ty_begin) * self.ntx
+        self.capacity = int(capacity)
+        dev = self.device
+        if d_tid is None:
+            d_tid = torch.from_numpy(np.ascontiguousarray(template_id, dtype=np.int32)).to(dev)
+        if d_zorder is None:
+            order = np.argsort(np.asarray(z, dtype=np.int64), kind="stable").astype(np.int32)
+            d_zorder = torch.from_numpy(order).to(dev)
+        self.d_tid, self.d_zorder = d_tid, d_zorder
+        rb = int(self.lib.pf_record_bytes())
+        self.rec = torch.empty(max(self.n, 1) * rb, dtype=torch.uint8, device=dev)
+        self.scratch_bytes = int(self.lib.pf_bin_scratch_bytes(self.n, self.n_tiles, self.capacity))
+        self.scratch = torch.empty(self.scratch_bytes, dtype=torch.uint8, device=dev)
+        self.bin_off = torch.zeros(self.n_tiles + 1, dtype=torch.int32, device=dev)
+        self.bin_idx = torch.zeros(max(self.capacity, 1), dtype=torch.int32, device=dev)
+        self.status = torch.zeros(4, dtype=torch.int32, device=dev)
+        self._saved_alloc = False
+
+    # -- buffers for rendering (allocated lazily; binning-only users skip them)
+    def alloc_render(self, save: bool, loss: bool = False, spatial: bool = False):
+        if self.tile != RENDER_TILE:
+            raise ValueError(f"render kernels need bin tile {RENDER_TILE}, got {self.tile}")
+        dev, P = self.device, self.W * self.H
+        if not hasattr(self, "img"):
+            self.img = torch.empty(P * 3, dtype=torch.float32, device=dev)
+            self.alpha = torch.empty(P, dtype=torch.float32, device=dev)
+        if save and not self._saved_alloc:
+            cap = int(self.lib.pf_saved_capacity(max(self.capacity, 1)))
+            self.ent_j = torch.empty(cap, dtype=torch.int16, device=dev)
+            self.ent_T = torch.empty(cap, dtype=torch.float64, device=dev)
+            self.ent_n = torch.zeros(P, dtype=torch.int32, device=dev)
+            self._saved_alloc = True
+        if loss and not hasattr(self, "dI"):
+            self.dI = torch.empty(P * 3, dtype=torch.float32, device=dev)
+            self.part = torch.zeros(max(self.n_tiles, 1) * 4, dtype=torch.float64, device=dev)
+            self.fwd_counter = torch.zeros(1, dtype=torch.int32, device=dev)
+        if spatial and not hasattr(self, "dA"):
+            self.dA = torch.empty(P, dtype=torch.float32, device=dev)
+
+    # -- K1 + K2
+    def preprocess(self, params: torch.Tensor, stream=None) -> None:
+        a = self.atlas
+        st = nat.check(
+            self.lib.pf_preprocess(
+                params.data_ptr(), self.d_tid.data_ptr(), self.d_zorder.data_ptr(), self.n,
+                a.d_base.data_ptr(), a.d_w.data_ptr(), a.d_h.data_ptr(), a.d_q.data_ptr(),
+                a.d_hyp.data_ptr(), a.n_templates, self.alpha_max, self.mu_blend, self.padding,
+                self.W, self.H, self.tile, self.band.ty_begin, self.band.ty_end, self.capacity,
+                self.rec.data_ptr(), self.scratch.data_ptr(), self.scratch_bytes,
+                _stream_handle(stream)),
+            "pf_preprocess")
+        return st
+
+    def bin(self, stream=None) -> None:
+        nat.check(
+            self.lib.pf_bin(self.n, self.W, self.H, self.tile, self.band.ty_begin,
+                            self.band.ty_end, self.capacity, self.scratch.data_ptr(),
+                            self.scratch_bytes, self.bin_off.data_ptr(),
+                            self.bin_idx.data_ptr(), self.status.data_ptr(),
+                            _stream_handle(stream)),
+            "pf_bin")
+
+    def check_overflow(self) -> int:
+        """Synchronising read of K; raises BinOverflow when capacity was exceeded."""
+        k, ovf = (int(v) for v in self.status[:2].cpu())
+        if ovf:
+            raise BinOverflow(f"{k} bin entries exceed capacity {self.capacity}")
+        return k
+
+    # -- K3
+    def forward(self, *, save: bool, eps_skip: float, bg_rgb=(1.0, 1.0, 1.0),
+                bg_img: torch.Tensor | None = None, loss_kind: int = nat.PF_LOSS_NONE,
+                target: torch.Tensor | None = None, target_alpha: torch.Tensor | None = None,
+                alpha_w: float = 0.0, sums: torch.Tensor | None = None, P_total: int | None = None,
+                stream=None) -> None:
+        spatial = loss_kind == nat.PF_LOSS_SPATIAL
+        self.alloc_render(save, loss_kind != nat.PF_LOSS_NONE, spatial)
+        P = float(P_total if P_total is not None else self.W * self.H)
+        p = nat.ptr
+        lossy = loss_kind != nat.PF_LOSS_NONE
+        nat.check(
+            self.lib.pf_forward(
+                self.rec.data_ptr(), self.n, self.atlas.tex.data_ptr(), self.atlas.texels,
+                self.bin_off.data_ptr(), self.bin_idx.data_ptr(), self.status.data_ptr(),
+                self.W, self.H, self.band.ty_begin, self.band.ty_end, float(eps_skip),
+                self.mu_blend, float(bg_rgb[0]), float(bg_rgb[1]), float(bg_rgb[2]), p(bg_img),
+                p(self.ent_j) if save else None, p(self.ent_T) if save else None,
+                p(self.ent_n) if save else None, self.img.data_ptr(), self.alpha.data_ptr(),
+                int(loss_kind), p(target), p(target_alpha), float(alpha_w), 1.0 / (3.0 * P),
+                1.0 / P, p(self.dI) if lossy else None, p(self.dA) if spatial else None,
+                p(self.part) if lossy else None, p(self.fwd_counter) if lossy else None,
+                p(sums), _stream_handle(stream)),
+            "pf_forward")
+
+    # -- K4
+    def backward(self, dI: torch.Tensor, grads: torch.Tensor, *, dA: torch.Tensor | None = None,
+                 bg_rgb=(1.0, 1.0, 1.0), bg_img: torch.Tensor | None = None,
+                 stream=None) -> None:
+        p = nat.ptr
+        nat.check(
+            self.lib.pf_backward(
+                self.rec.data_ptr(), self.n, self.atlas.tex.data_ptr(), self.atlas.texels,
+                self.bin_off.data_ptr(), self.bin_idx.data_ptr(), self.status.data_ptr(),
+                self.ent_j.data_ptr(), self.ent_T.data_ptr(), self.ent_n.data_ptr(),
+                dI.data_ptr(), p(dA), float(bg_rgb[0]), float(bg_rgb[1]), float(bg_rgb[2]),
+                p(bg_img), self.mu_blend, self.W, self.H, self.band.ty_begin,
+                self.band.ty_end, grads.data_ptr(), _stream_handle(stream)),
+            "pf_backward")
+
+
+def adam_launch(params, grads, m, v, *, frozen=None, gains=None, n: int,
+                lr_table=None, bc1_table=None, bc2_table=None, iter_counter=None,
+                lr=0.0, bc1=1.0, bc2=1.0, clamp=False, s_min=0.0, s_max=0.0,
+                zero_grads=True, sums=None, loss_kind=nat.PF_LOSS_MSE, alpha_w=0.0,
+                P_total=1, hist_loss=None, hist_psnr=None, counter=None, stream=None):
+    """K5 launcher (both modes of pf_adam)."""
+    lib = nat.load()
+    p = nat.ptr
+    g8 = None
+    if gains is not None:
+        g8 = (C.c_double * 8)(*[float(g) for g in gains])
+    P = float(P_total)
+    nat.check(
+        lib.pf_adam(
+            params.data_ptr(), grads.data_ptr(), m.data_ptr(), v.data_ptr(), p(frozen),
+            C.addressof(g8) if g8 is not None else None, int(n), p(lr_table), p(bc1_table),
+            p(bc2_table), p(iter_counter), float(lr), float(bc1), float(bc2), int(bool(clamp)),
+            float(s_min), float(s_max), int(bool(zero_grads)), p(sums), int(loss_kind),
+            float(alpha_w), 1.0 / (3.0 * P), 1.0 / P, p(hist_loss), p(hist_psnr), p(counter),
+            _stream_handle(stream)),
+        "pf_adam")

@@ -1,0 +1,439 @@
+"""Losses, Adam and the fit loop (drop-in for pkg/src/primfit/fit.py) on the CUDA path.
+
+The hot path is ``run_loop`` (reference fit.py:403-521): every iteration is
+bin -> forward(save) -> loss -> backward -> Adam -> psnr.  Here one iteration
+is five stream-ordered native stages (K1..K5, include/primfit_b200.h) with no
+host synchronisation: the lr schedule and Adam bias corrections are device
+tables, the iteration counter and the loss/psnr history live in HBM, and the
+whole step is captured once into a CUDA graph and replayed.
+
+The small host helpers (``loss_mse``, ``psnr``, ``lr_schedule``,
+``gains_vector``) keep the reference's numpy signatures for API users; inside
+``run_loop`` their work is fused into the kernels (loss in K3, psnr and the
+schedule lookup in K5).
+"""
+
+from __future__ import annotations
+
+import csv
+import math
+from collections.abc import Callable
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .compositor import Band, Compositor, DeviceAtlas, adam_launch, bin_capacity
+from .errors import LayoutMismatch, MissingAlphaTarget, ShapeMismatch
+from .raster import DEFAULT_EPS_SKIP, _device, noisy_background
+from .scene import NOISE_BACKGROUND, FloatArray, ParamLayout, pack_params, param_matrix, structure_arrays, unpack_params, validate_scene
+
+ADAM_BETA1 = 0.9
+ADAM_BETA2 = 0.999
+ADAM_EPS = 1e-8
+GRAY_WEIGHTS = np.asarray([0.299, 0.587, 0.114])
+_GAIN_GROUPS = ("x", "y", "scale", "rotation", "opacity", "color", "color", "color")
+
+
+@dataclass
+class FitConfig:
+    """Hot-path subset of the reference FitConfig (config.py:20-99), same defaults.
+
+    run_loop accepts any object with these attributes, including the
+    reference's own FitConfig.
+    """
+
+    num_iterations: int = 100
+    num_primitives: int = 500
+    learning_rate: float = 0.1
+    lr_gain_x: float = 10.0
+    lr_gain_y: float = 10.0
+    lr_gain_scale: float = 10.0
+    lr_gain_rotation: float = 1.0
+    lr_gain_opacity: float = 1.5
+    lr_gain_color: float = 1.0
+    do_decay: bool = True
+    decay_final_fraction: float = 0.1
+    loss: str = "mse"
+    mse_weight: float = 1.0
+    gray_l1_weight: float = 0.0
+    alpha_loss_weight: float = 0.3
+    do_gaussian_blur: bool = True
+    blur_sigma: float = 1.0
+    scale_min: float = 2.0
+    scale_max: float = 16.0
+    alpha_max: float = 1.0
+    mu_blend: float = 0.0
+    preserve_aspect: bool = False
+    do_reinit: bool = False
+    tile_size: int = 32
+    tile_padding: float = 2.0
+    eps_skip: float = DEFAULT_EPS_SKIP
+    seed: int = 0
+    compute_psnr: bool = True
+    dump_every: int = 0
+
+
+@dataclass
+class LossSpec:
+    """Which loss to evaluate and against what (reference fit.py:61-76)."""
+
+    kind: str = "mse"  # mse | spatial_constrained | combined
+    target: FloatArray | None = None
+    target_alpha: FloatArray | None = None
+    mse_w: float = 1.0
+    gray_l1_w: float = 0.0
+    alpha_w: float = 0.3
+
+    def __post_init__(self) -> None:
+        if min(self.mse_w, self.gray_l1_w, self.alpha_w) < 0:
+            raise ValueError("loss weights must be nonnegative")
+        if self.kind == "spatial_constrained" and self.target_alpha is None:
+            raise MissingAlphaTarget("spatial_constrained needs target_alpha")
+
+
+@dataclass(eq=False)
+class OptimState:
+    """Adam moments + freeze flags (reference fit.py:79-95)."""
+
+    m: FloatArray
+    v: FloatArray
+    step: int
+    frozen: np.ndarray
+
+    @classmethod
+    def fresh(cls, layout: ParamLayout) -> "OptimState":
+        return cls(np.zeros(layout.size), np.zeros(layout.size), 0,
+                   np.zeros(layout.n_primitives, dtype=bool))
+
+
+@dataclass
+class HistoryEntry:
+    iteration: int
+    loss: float
+    psnr: float
+    lr: float
+    reinit_count: int
+
+
+def _check_image_pair(a, b) -> None:
+    if a.shape != b.shape:
+        raise ShapeMismatch(f"shape {a.shape} vs {b.shape}")
+
+
+def loss_mse(I: FloatArray, target: FloatArray):
+    """mean((I-t)^2) and its gradient 2(I-t)/size (reference fit.py:112-116)."""
+    _check_image_pair(I, target)
+    diff = I - target
+    return float(np.mean(diff**2)), 2.0 * diff / diff.size
+
+
+def loss_spatial(I: FloatArray, I_alpha: FloatArray, spec: LossSpec):
+    """Masked colour MSE + alpha_w * coverage MSE (reference fit.py:128-151)."""
+    if spec.target_alpha is None:
+        raise MissingAlphaTarget("spatial loss needs target_alpha")
+    _check_image_pair(I, spec.target)
+    ta = spec.target_alpha
+    if ta.shape != I_alpha.shape:
+        raise ShapeMismatch(f"alpha shape {ta.shape} vs {I_alpha.shape}")
+    mask = (ta > 0).astype(np.float64)
+    diff = (I - spec.target) * mask[:, :, None]
+    color = float(np.sum(diff**2) / diff.size)
+    adiff = I_alpha - ta
+    alpha = float(np.mean(adiff**2))
+    return color + spec.alpha_w * alpha, 2.0 * diff / diff.size, spec.alpha_w * 2.0 * adiff / adiff.size
+
+
+def evaluate_loss(spec: LossSpec, I: FloatArray, I_alpha: FloatArray):
+    """Dispatch on spec.kind -> (value, dL/dI, dL/dA or None) (reference fit.py:154-171)."""
+    if spec.kind == "mse":
+        value, dI = loss_mse(I, spec.target)
+        return value, dI, None
+    if spec.kind == "spatial_constrained":
+        return loss_spatial(I, I_alpha, spec)
+    if spec.kind == "combined":
+        raise NotImplementedError("combined (gray-L1) loss is outside the ported hot path")
+    raise ValueError(f"unknown loss kind {spec.kind!r}")
+
+
+def lr_schedule(iteration: int, total: int, base_lr: float, decay_enabled: bool = True,
+                final_fraction: float = 0.1) -> float:
+    """base * final^(it/(total-1)) (reference fit.py:174-186)."""
+    if not 0 <= iteration < total:
+        raise ValueError(f"iteration {iteration} outside [0, {total})")
+    if not decay_enabled or total <= 1:
+        return base_lr
+    return base_lr * final_fraction ** (iteration / (total - 1))
+
+
+def gains_vector(layout: ParamLayout, gains: dict[str, float]) -> FloatArray:
+    """Per-group gains expanded to one multiplier per packed scalar (fit.py:189-192)."""
+    per_col = np.asarray([gains.get(g, 1.0) for g in _GAIN_GROUPS])
+    return np.tile(per_col, layout.n_primitives)
+
+
+def psnr(I: FloatArray, target: FloatArray) -> float:
+    """10 log10(1/mse), inf when identical (reference fit.py:241-247)."""
+    _check_image_pair(I, target)
+    mse = float(np.mean((I - target) ** 2))
+    if mse == 0.0:
+        return math.inf
+    return 10.0 * math.log10(1.0 / mse)
+
+
+def effective_padding(cfg) -> float:
+    """tile_padding + 3*blur_sigma (reference fit.py:338-341)."""
+    blur = cfg.blur_sigma if cfg.do_gaussian_blur else 0.0
+    return cfg.tile_padding + 3.0 * blur
+
+
+def _gains8(gains) -> list[float] | None:
+    if gains is None:
+        return None
+    g = np.asarray(gains, dtype=np.float64)
+    if g.size % 8 or g.size == 0:
+        raise LayoutMismatch(f"gains of size {g.size} are not 8 per primitive")
+    rows = g.reshape(-1, 8)
+    if not np.all(rows == rows[0]):
+        raise ValueError("the fused Adam kernel takes per-column gains (as gains_vector builds)")
+    return rows[0].tolist()
+
+
+def adam_step(params: FloatArray, grads: FloatArray, state: OptimState, lr: float,
+              gains: FloatArray | None = None, frozen: np.ndarray | None = None,
+              s_min: float | None = None, s_max: float | None = None,
+              layout: ParamLayout | None = None) -> FloatArray:
+    """One Adam update on the GPU (K5, scalar mode); mutates state like fit.py:195-238."""
+    params = np.asarray(params, dtype=np.float64)
+    grads = np.asarray(grads, dtype=np.float64)
+    if params.shape != grads.shape or params.shape != state.m.shape:
+        raise LayoutMismatch(
+            f"params {params.shape}, grads {grads.shape}, moments {state.m.shape} must agree")
+    if layout is None:
+        layout = ParamLayout(params.size // 8)
+    if frozen is None:
+        frozen = state.frozen
+    dev = _device()
+    n = layout.n_primitives
+    state.step += 1
+    t = state.step
+    d_p = torch.from_numpy(params.copy()).to(dev)
+    d_g = torch.from_numpy(grads.copy()).to(dev)
+    d_m = torch.from_numpy(np.ascontiguousarray(state.m, dtype=np.float64)).to(dev)
+    d_v = torch.from_numpy(np.ascontiguousarray(state.v, dtype=np.float64)).to(dev)
+    d_f = torch.from_numpy(np.asarray(frozen, dtype=bool).astype(np.uint8)).to(dev)
+    clamp = s_min is not None and s_max is not None
+    adam_launch(d_p, d_g, d_m, d_v, frozen=d_f, gains=_gains8(gains), n=n, lr=lr,
+                bc1=1 - ADAM_BETA1**t, bc2=1 - ADAM_BETA2**t, clamp=clamp,
+                s_min=s_min if clamp else 0.0, s_max=s_max if clamp else 0.0, zero_grads=False)
+    state.m[:] = d_m.cpu().numpy()
+    state.v[:] = d_v.cpu().numpy()
+    return d_p.cpu().numpy()
+
+
+def _cfg_gains(cfg) -> list[float]:
+    g = {"x": cfg.lr_gain_x, "y": cfg.lr_gain_y, "scale": cfg.lr_gain_scale,
+         "rotation": cfg.lr_gain_rotation, "opacity": cfg.lr_gain_opacity,
+         "color": cfg.lr_gain_color}
+    return [float(g[k]) for k in _GAIN_GROUPS]
+
+
+class StepEngine:
+    """Device-resident optimisation loop: K1..K5 per step, CUDA-graph replayed.
+
+    ``band`` restricts the render to a row band of tiles (multi-GPU); then
+    ``allreduce`` (a callable on the float64 gradient+loss buffer) runs between
+    the backward and the Adam step.
+    """
+
+    def __init__(self, scene, cfg, loss_spec: LossSpec, total: int, state: OptimState | None = None,
+                 *, band: Band | None = None, allreduce: Callable | None = None,
+                 use_graph: bool = True, device=None):
+        if getattr(cfg, "do_reinit", False):
+            raise NotImplementedError("low-opacity reinit is outside the ported hot path")
+        if loss_spec.kind not in ("mse", "spatial_constrained"):
+            raise NotImplementedError(f"loss {loss_spec.kind!r} is outside the ported hot path")
+        validate_scene(scene)
+        self.dev = device or _device()
+        self.scene = scene
+        self.cfg = cfg
+        self.total = int(total)
+        H, W = scene.canvas_h, scene.canvas_w
+        self.H, self.W, self.P = H, W, H * W
+        target = np.asarray(loss_spec.target, dtype=np.float64)
+        if target.shape != (H, W, 3):
+            raise ShapeMismatch(f"target shape {target.shape} != {(H, W, 3)}")
+        self.loss_kind = nat.PF_LOSS_MSE if loss_spec.kind == "mse" else nat.PF_LOSS_SPATIAL
+        self.alpha_w = float(loss_spec.alpha_w)
+        vec, layout = pack_params(scene)
+        self.layout = layout
+        self.n = n = layout.n_primitives
+        self.state = state if state is not None else OptimState.fresh(layout)
+        self.step0 = int(self.state.step)
+        dev = self.dev
+        self.params = torch.from_numpy(vec.reshape(n, 8).copy()).to(dev)
+        self.m = torch.from_numpy(np.asarray(self.state.m, dtype=np.float64).copy()).to(dev)
+        self.v = torch.from_numpy(np.asarray(self.state.v, dtype=np.float64).copy()).to(dev)
+        self.frozen = torch.from_numpy(np.asarray(self.state.frozen, dtype=bool).astype(np.uint8)).to(dev)
+        self.gains = _cfg_gains(cfg)
+        its = range(self.total)
+        self.lr_host = [lr_schedule(i, self.total, cfg.learning_rate, cfg.do_decay,
+                                    cfg.decay_final_fraction) for i in its]
+        bc1 = [1 - ADAM_BETA1 ** (self.step0 + i + 1) for i in its]
+        bc2 = [1 - ADAM_BETA2 ** (self.step0 + i + 1) for i in its]
+        self.lr_table = torch.tensor(self.lr_host, dtype=torch.float64, device=dev)
+        self.bc1_table = torch.tensor(bc1, dtype=torch.float64, device=dev)
+        self.bc2_table = torch.tensor(bc2, dtype=torch.float64, device=dev)
+        self.iter = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.adam_counter = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.hist_loss = torch.zeros(max(self.total, 1), dtype=torch.float64, device=dev)
+        self.hist_psnr = torch.zeros(max(self.total, 1), dtype=torch.float64, device=dev)
+        self.gbuf = torch.zeros(n * 8 + 4, dtype=torch.float64, device=dev)
+        self.grads = self.gbuf[: n * 8]
+        self.sums = self.gbuf[n * 8 :]
+        self.target = torch.from_numpy(target.astype(np.float32).reshape(-1)).to(dev)
+        self.target_alpha = None
+        if self.loss_kind == nat.PF_LOSS_SPATIAL:
+            self.target_alpha = torch.from_numpy(
+                np.asarray(loss_spec.target_alpha, dtype=np.float32).reshape(-1)).to(dev)
+        self.noise_bg = isinstance(scene.background, str) and scene.background == NOISE_BACKGROUND
+        self.bg_rgb = (0.0, 0.0, 0.0) if self.noise_bg else tuple(
+            float(c) for c in np.asarray(scene.background, dtype=np.float64))
+        self.bg_img = torch.zeros(self.P * 3, dtype=torch.float32, device=dev) if self.noise_bg else None
+        tid, z = structure_arrays(scene)
+        self.padding = effective_padding(cfg)
+        self.atlas = DeviceAtlas(scene.templates, bool(scene.preserve_aspect), dev)
+        band = band or Band(0, -(-H // 16))
+        scales = np.maximum(vec.reshape(n, 8)[:, 2], float(cfg.scale_max)) if n else np.zeros(0)
+        cap = bin_capacity(scales, tid, self.atlas.hyp, self.padding, 16, -(-W // 16),
+                           band.ty_end - band.ty_begin)
+        self.comp = Compositor(tid, z, self.atlas, W, H, alpha_max=scene.alpha_max,
+                               mu_blend=scene.mu_blend, padding=self.padding, capacity=cap,
+                               band=band, device=dev)
+        self.comp.alloc_render(save=True, loss=True, spatial=self.loss_kind == nat.PF_LOSS_SPATIAL)
+        self.allreduce = allreduce
+        self.use_graph = use_graph
+        self.graph: torch.cuda.CUDAGraph | None = None
+        self.eps_skip = float(cfg.eps_skip)
+        self.done = 0
+
+    # one full optimisation step, stream-ordered, no host sync
+    def launch_step(self) -> None:
+        c = self.comp
+        c.preprocess(self.params)
+        c.bin()
+        c.forward(save=True, eps_skip=self.eps_skip, bg_rgb=self.bg_rgb, bg_img=self.bg_img,
+                  loss_kind=self.loss_kind, target=self.target, target_alpha=self.target_alpha,
+                  alpha_w=self.alpha_w, sums=self.sums, P_total=self.P)
+        c.backward(c.dI, self.gbuf, dA=c.dA if self.loss_kind == nat.PF_LOSS_SPATIAL else None,
+                   bg_rgb=self.bg_rgb, bg_img=self.bg_img)
+        if self.allreduce is not None:
+            self.allreduce(self.gbuf)
+        adam_launch(self.params, self.grads, self.m, self.v, frozen=self.frozen, gains=self.gains,
+                    n=self.n, lr_table=self.lr_table, bc1_table=self.bc1_table,
+                    bc2_table=self.bc2_table, iter_counter=self.iter, clamp=True,
+                    s_min=self.cfg.scale_min, s_max=self.cfg.scale_max, zero_grads=True,
+                    sums=self.sums, loss_kind=self.loss_kind, alpha_w=self.alpha_w,
+                    P_total=self.P, hist_loss=self.hist_loss, hist_psnr=self.hist_psnr,
+                    counter=self.adam_counter)
+
+    def capture(self) -> None:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.launch_step()
+        self.graph = g
+
+    def step(self, rng: np.random.Generator | None = None) -> None:
+        if self.done >= self.total:
+            raise ValueError(f"iteration {self.done} outside [0, {self.total})")
+        if self.noise_bg:
+            if rng is None:
+                raise ValueError("noise background needs the caller's rng")
+            bg = noisy_background(self.W, self.H, rng).astype(np.float32).reshape(-1)
+            self.bg_img.copy_(torch.from_numpy(bg), non_blocking=False)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.launch_step()
+            if self.use_graph:
+                self.capture()  # step 0 ran eagerly (warm-up); later steps replay
+        self.done += 1
+
+    def run(self, k: int, rng=None) -> None:
+        for _ in range(k):
+            self.step(rng)
+
+    # host views (synchronising)
+    def check(self) -> None:
+        self.comp.check_overflow()
+
+    def params_host(self) -> np.ndarray:
+        return self.params.cpu().numpy().reshape(-1)
+
+    def sync_state(self) -> OptimState:
+        self.state.m[:] = self.m.cpu().numpy()
+        self.state.v[:] = self.v.cpu().numpy()
+        self.state.step = self.step0 + self.done
+        return self.state
+
+    def push_host(self, vec: np.ndarray, state: OptimState) -> None:
+        """Re-upload params/moments/frozen in place (graph pointers stay valid)."""
+        self.params.copy_(torch.from_numpy(np.asarray(vec, dtype=np.float64).reshape(self.n, 8)))
+        self.m.copy_(torch.from_numpy(np.asarray(state.m, dtype=np.float64)))
+        self.v.copy_(torch.from_numpy(np.asarray(state.v, dtype=np.float64)))
+        self.frozen.copy_(torch.from_numpy(np.asarray(state.frozen, dtype=bool).astype(np.uint8)))
+
+    def history(self, compute_psnr: bool = True) -> list[HistoryEntry]:
+        k = self.done
+        loss = self.hist_loss[:k].cpu().numpy()
+        ps = self.hist_psnr[:k].cpu().numpy()
+        return [HistoryEntry(i, float(loss[i]), float(ps[i]) if compute_psnr else math.nan,
+                             self.lr_host[i], 0) for i in range(k)]
+
+
+def run_loop(scene, cfg, loss_spec: LossSpec, rng: np.random.Generator,
+             iterations: int | None = None, state: OptimState | None = None, nlv=None,
+             log_path: str | Path | None = None, dump_dir: str | Path | None = None,
+             hooks: dict[int, Callable] | None = None):
+    """GPU fit loop with the reference's contract (fit.py:403-521).
+
+    Returns (scene after the last update, history, state).  History entries
+    describe the render before each update, as in the reference.
+    """
+    if dump_dir is not None and getattr(cfg, "dump_every", 0) > 0:
+        raise NotImplementedError("per-iteration image dumps are outside the ported hot path")
+    total = cfg.num_iterations if iterations is None else iterations
+    vec, layout = pack_params(scene)
+    if state is None:
+        state = OptimState.fresh(layout)
+    eng = StepEngine(scene, cfg, loss_spec, total, state)
+    it = 0
+    while it < total:
+        if hooks and it in hooks:
+            cur = unpack_params(eng.params_host(), layout, scene)
+            st = eng.sync_state()
+            cur = hooks[it](cur, st)
+            vec2, layout2 = pack_params(cur)
+            if layout2 != layout:
+                raise LayoutMismatch("hooks must keep the primitive count")
+            scene = cur
+            eng.push_host(vec2, st)
+        nxt = total
+        if hooks:
+            later = [k for k in hooks if k > it]
+            if later:
+                nxt = min(nxt, min(later))
+        eng.run(nxt - it, rng)
+        it = nxt
+    eng.check()
+    state = eng.sync_state()
+    history = eng.history(getattr(cfg, "compute_psnr", True))
+    if log_path is not None:
+        with open(log_path, "w", newline="") as fh:
+            w = csv.writer(fh)
+            w.writerow(["iter", "loss", "psnr", "lr", "reinit_count"])
+            for h in history:
+                w.writerow([h.iteration, repr(h.loss), str(h.psnr), repr(h.lr), h.reinit_count])
+    return unpack_params(eng.params_host(), layout, scene), history, state

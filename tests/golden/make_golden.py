@@ -1,0 +1,232 @@
+"""Generate golden vectors by running the REFERENCE package (primfit) itself.
+
+Run in the build container (where /root/reference exists):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+
+Writes tests/golden/*.npz.  Each case stores the inputs (packed params,
+template ids, z, templates, canvas, background, flags) and the reference's
+outputs: bin_tiles at tile 16 and 32 (padding 2 and 5), render_forward
+image/alpha at eps 0 and default eps, the saved-entry count, backward
+gradients for an MSE pull-back (and an alpha objective where noted), and
+Adam / run_loop rollouts.  Scenes come from the reference's own test
+fixtures (conftest.random_scene, small_scene, grad.gradcheck_scene,
+test_grad's saturated-alpha scene) plus aspect / mu_blend / noise-background
+/ spatial-loss variants and a structure-aware init check for the synthetic
+workload generator.  These files are committed; the GPU box never reads
+/root/reference.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+from pathlib import Path
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+os.environ.setdefault("NUMBA_NUM_THREADS", "4")
+REF = Path("/root/reference/pkg")
+sys.path.insert(0, str(REF / "src"))
+sys.path.insert(0, str(REF / "tests"))
+OUT = Path(__file__).resolve().parent
+sys.path.insert(0, str(OUT.parent.parent))
+
+import numpy as np  # noqa: E402
+from conftest import random_scene, soft_disk  # noqa: E402  (reference test fixtures)
+from primfit import config as rconfig  # noqa: E402
+from primfit import fit as rfit  # noqa: E402
+from primfit import grad as rgrad  # noqa: E402
+from primfit import prep as rprep  # noqa: E402
+from primfit import raster as rr  # noqa: E402
+from primfit.scene import PrimitiveParams, PrimitiveTemplate, Scene, pack_params  # noqa: E402
+
+
+def scene_arrays(scene) -> dict:
+    vec, _ = pack_params(scene)
+    d = {
+        "params": vec.reshape(-1, 8),
+        "tid": np.asarray([p.template_id for p in scene.primitives], dtype=np.int32),
+        "z": np.asarray([p.z for p in scene.primitives], dtype=np.int64),
+        "canvas": np.asarray([scene.canvas_w, scene.canvas_h]),
+        "alpha_max": np.float64(scene.alpha_max),
+        "mu_blend": np.float64(scene.mu_blend),
+        "preserve_aspect": np.bool_(scene.preserve_aspect),
+        "n_templates": np.int64(len(scene.templates)),
+    }
+    if isinstance(scene.background, str):
+        d["background_noise"] = np.bool_(True)
+    else:
+        d["background"] = np.asarray(scene.background, dtype=np.float64)
+    for k, t in enumerate(scene.templates):
+        d[f"tpl{k}"] = t.rgba
+    return d
+
+
+def render_case(name: str, scene, target=None, *, bg=None, dA_target=None, extra=None):
+    d = scene_arrays(scene)
+    for tile, pad in ((16, 2.0), (32, 2.0), (16, 5.0)):
+        b = rr.bin_tiles(scene, tile, pad)
+        d[f"bin{tile}_p{int(pad)}_off"] = b.offsets
+        d[f"bin{tile}_p{int(pad)}_idx"] = b.indices
+    if bg is not None:
+        d["bg_image"] = bg
+    bins = rr.bin_tiles(scene)
+    out0, _ = rr.render_forward(scene, bins, background=bg, eps_skip=0.0)
+    d["img_eps0"], d["alpha_eps0"] = out0.color, out0.alpha
+    out, saved = rr.render_forward(scene, bins, background=bg, save=True)
+    d["img"], d["alpha"] = out.color, out.alpha
+    d["n_entries"] = np.int64(saved.n_entries)
+    if target is None:
+        target = np.random.default_rng(1234).random((scene.canvas_h, scene.canvas_w, 3))
+    d["target"] = target
+    value, dI = rfit.loss_mse(out.color, target)
+    d["loss"] = np.float64(value)
+    d["dI"] = dI
+    d["grads"] = rgrad.backward(scene, saved, dI).data
+    # eps 0 saved pass + grads, for the tight fast-vs-dense style checks
+    out0s, saved0 = rr.render_forward(scene, bins, background=bg, save=True, eps_skip=0.0)
+    _, dI0 = rfit.loss_mse(out0s.color, target)
+    d["dI_eps0"] = dI0
+    d["grads_eps0"] = rgrad.backward(scene, saved0, dI0).data
+    if dA_target is not None:
+        dA = 2.0 * (out.alpha - dA_target) / dA_target.size
+        dIz = np.zeros_like(out.color)
+        d["dA"] = dA
+        d["grads_alpha_obj"] = rgrad.backward(scene, saved, dIz, dL_dA=dA).data
+    if extra:
+        d.update(extra)
+    np.savez_compressed(OUT / f"{name}.npz", **d)
+    print(name, "n", scene.n, "K16", len(d["bin16_p2_idx"]), "E", saved.n_entries)
+
+
+def small_scene():
+    prims = [
+        PrimitiveParams(x=10.0, y=12.0, scale=5.0, rotation=0.3, opacity_logit=1.0,
+                        color_logits=(0.2, -0.4, 0.8), z=0),
+        PrimitiveParams(x=20.0, y=18.0, scale=7.0, rotation=-1.1, opacity_logit=0.0,
+                        color_logits=(-0.5, 0.5, 0.0), z=1),
+        PrimitiveParams(x=16.0, y=8.0, scale=4.0, rotation=2.0, opacity_logit=-1.0,
+                        color_logits=(1.0, 0.0, -1.0), z=2),
+    ]
+    return Scene(primitives=prims, templates=[PrimitiveTemplate(soft_disk())], canvas_w=32,
+                 canvas_h=28, background=(0.1, 0.2, 0.3))
+
+
+def saturated_scene():
+    t = np.zeros((35, 35, 4))
+    t[9:-9, 9:-9, 3] = 1.0
+    t[:, :, :3] = 0.3
+    tpl = rprep.gaussian_blur_template(
+        rprep.gaussian_blur_template(PrimitiveTemplate(t), 1.2), 1.0)
+    prims = [
+        PrimitiveParams(x=12.0, y=12.0, scale=8.0, opacity_logit=40.0,
+                        color_logits=(1.0, 0.0, -1.0), z=0),
+        PrimitiveParams(x=13.0, y=12.0, scale=8.0, opacity_logit=0.5,
+                        color_logits=(-1.0, 0.5, 0.2), z=1),
+    ]
+    return Scene(primitives=prims, templates=[tpl], canvas_w=24, canvas_h=24,
+                 background=(0.2, 0.2, 0.2))
+
+
+def aspect_scene(seed: int):
+    rng = np.random.default_rng(seed)
+    tpls = []
+    for (h, w) in ((12, 30), (26, 10)):
+        raw = np.zeros((h, w, 4))
+        raw[2:-2, 2:-2, 3] = 0.3 + 0.7 * rng.random((h - 4, w - 4))
+        raw[:, :, :3] = rng.random((h, w, 3))
+        tpls.append(rprep.gaussian_blur_template(PrimitiveTemplate(raw), 1.0))
+    n = 14
+    zp = rng.permutation(n)
+    prims = [PrimitiveParams(x=float(rng.uniform(-5, 60)), y=float(rng.uniform(-5, 50)),
+                             scale=float(rng.uniform(2.0, 12.0)),
+                             rotation=float(rng.uniform(-7, 7)),
+                             opacity_logit=float(rng.uniform(-2, 3)),
+                             color_logits=tuple(float(v) for v in rng.uniform(-2, 2, 3)),
+                             template_id=int(rng.integers(0, 2)), z=int(zp[i])) for i in range(n)]
+    return Scene(prims, tpls, 56, 44, background=(0.9, 0.5, 0.1), alpha_max=0.8, mu_blend=0.35,
+                 preserve_aspect=True)
+
+
+def main():
+    OUT.mkdir(parents=True, exist_ok=True)
+    render_case("small_scene", small_scene())
+    for seed in range(6):
+        sc = random_scene(seed, n=12, w=40, h=36)
+        render_case(f"random_s{seed}", sc,
+                    np.random.default_rng(seed + 100).random((36, 40, 3)))
+    # alpha objective (test_grad.py:59-70)
+    sc = random_scene(5, n=6)
+    ta = np.zeros((sc.canvas_h, sc.canvas_w))
+    ta[8:30, 8:30] = 1.0
+    render_case("alpha_obj_s5", sc, dA_target=ta)
+    for seed in (1, 7):
+        sc, tgt = rgrad.gradcheck_scene(seed)
+        render_case(f"gradcheck_s{seed}", sc, tgt)
+    render_case("saturated", saturated_scene(), np.full((24, 24, 3), 0.6))
+    for seed in (0, 1):
+        render_case(f"aspect_mu_s{seed}", aspect_scene(seed))
+    # per-pixel (noise) background
+    sc = random_scene(9, n=15, w=48, h=40)
+    sc.background = "noise"
+    bg = rr.noisy_background(48, 40, np.random.default_rng(77))
+    render_case("noise_bg", sc, bg=bg)
+    # medium scene: many prims, several tiles, long lists
+    sc = random_scene(21, n=300, w=160, h=120, n_templates=3)
+    render_case("medium_n300", sc, np.random.default_rng(5).random((120, 160, 3)))
+
+    # Adam rollout with frozen rows, gains and clamp (fit.py:195-238)
+    rng = np.random.default_rng(4)
+    from primfit.scene import ParamLayout
+    n = 5
+    layout = ParamLayout(n)
+    p0 = rng.normal(size=layout.size) + 5.0
+    state = rfit.OptimState.fresh(layout)
+    state.frozen[2] = True
+    gains = rfit.gains_vector(layout, {"x": 10.0, "y": 10.0, "scale": 10.0, "opacity": 1.5})
+    cur = p0.copy()
+    gs, outs = [], []
+    for t in range(1, 5):
+        g = rng.normal(size=layout.size)
+        cur = rfit.adam_step(cur, g, state, 0.05 * t, gains, s_min=4.0, s_max=6.0, layout=layout)
+        gs.append(g)
+        outs.append(cur.copy())
+    np.savez_compressed(OUT / "adam_rollout.npz", p0=p0, grads=np.stack(gs), outs=np.stack(outs),
+                        m=state.m, v=state.v, frozen=state.frozen, gains=gains,
+                        lrs=np.asarray([0.05 * t for t in range(1, 5)]))
+
+    # run_loop rollout (the hot path's caller, fit.py:403-521)
+    from paper_2602_22625_b200 import synth
+    tpls = [PrimitiveTemplate(t.rgba) for t in synth.prepare([synth.disc(32)])]
+    target = synth.smooth_target(64, 48, seed=3)
+    cfg = rconfig.FitConfig(num_iterations=6, num_primitives=40, seed=3, scale_min=2.0,
+                            scale_max=9.0)
+    scene = rfit.init_scene(target, tpls, cfg, np.random.default_rng(3))
+    spec = rfit.LossSpec(kind="mse", target=target)
+    scene_end, hist, st = rfit.run_loop(scene, cfg, spec, np.random.default_rng(3))
+    d = scene_arrays(scene)
+    d.update(target=target, final_params=pack_params(scene_end)[0].reshape(-1, 8),
+             hist_loss=np.asarray([h.loss for h in hist]),
+             hist_psnr=np.asarray([h.psnr for h in hist]),
+             hist_lr=np.asarray([h.lr for h in hist]), m=st.m, v=st.v,
+             iters=np.int64(6), scale_min=2.0, scale_max=9.0,
+             padding=np.float64(rfit.effective_padding(cfg)))
+    np.savez_compressed(OUT / "run_loop_small.npz", **d)
+    print("run_loop", hist[0].loss, hist[-1].loss)
+
+    # structure-aware init of the synthetic workloads (c1, and a c3 crop count)
+    w1 = synth.make_workload("c1")
+    cfg1 = rconfig.FitConfig(num_primitives=200, seed=0, scale_min=2.0, scale_max=16.0)
+    ref1 = rfit.init_scene(w1.target, [PrimitiveTemplate(t.rgba) for t in w1.scene.templates],
+                           cfg1, np.random.default_rng(0))
+    np.savez_compressed(OUT / "synth_c1_init.npz", params=pack_params(ref1)[0].reshape(-1, 8),
+                        tid=np.asarray([p.template_id for p in ref1.primitives]),
+                        z=np.asarray([p.z for p in ref1.primitives]),
+                        tpl0=ref1.templates[0].rgba,
+                        target_sha=hashlib.sha256(w1.target.tobytes()).hexdigest())
+    print("synth c1 ok")
+
+
+if __name__ == "__main__":
+    main()
