@@ -280,11 +280,11 @@ def run_ours(args) -> None:
         ev[1].record()
         comp.forward(save=True, eps_skip=eng.eps_skip, bg_rgb=eng.bg_rgb, bg_img=eng.bg_img,
                      loss_kind=eng.loss_kind, target=eng.target, target_alpha=eng.target_alpha,
-                     alpha_w=eng.alpha_w, sums=eng.sums, P_total=eng.P)
+                     alpha_w=eng.alpha_w, P_total=eng.P)
         ev[2].record()
         comp.backward(comp.dI, eng.gbuf,
                       dA=comp.dA if eng.loss_kind == nat.PF_LOSS_SPATIAL else None,
-                      bg_rgb=eng.bg_rgb, bg_img=eng.bg_img)
+                      bg_rgb=eng.bg_rgb, bg_img=eng.bg_img, sums=eng.sums)
         ev[3].record()
         if eng.allreduce is not None:
             eng.allreduce(eng.gbuf)

@@ -70,6 +70,22 @@ size_t pf_bin_scratch_bytes(int n, int n_tiles, int capacity);
 /* Saved-forward entry capacity for `capacity` bin entries (256 per entry). */
 long long pf_saved_capacity(int capacity);
 
+/* Bytes of the saved-forward buffer for `capacity` bin entries:
+ * pf_saved_capacity(capacity) entries x 16 bytes (list position, texel cell,
+ * fp32 bilinear weights, fp32 incoming transmittance). */
+size_t pf_saved_bytes(int capacity);
+
+/*
+ * Alpha "quad atlas": for every texel (u, v) of the planar atlas `tex`, the four
+ * bilinear taps of the alpha plane (a[v][u], a[v][u+1], a[v+1][u], a[v+1][u+1])
+ * with the reference's zero padding (_kernels.py:35-40) applied.  quad out:
+ * float32 [texels][4] (16-byte aligned).  Build once per atlas; pass it to
+ * pf_forward / pf_backward (which re-take the m < eps_skip decision on the
+ * float64 plane whenever the fp32 taps leave it within rounding).
+ */
+int pf_atlas_quad(const double* tex, int texels, const int32_t* tpl_base, const int32_t* tpl_w,
+                  const int32_t* tpl_h, int n_tpl, float* quad, void* stream);
+
 /*
  * K1 — per-primitive preprocess + bin count.
  * Replaces: the per-pair inline transform/sigmoid math of every numba kernel
@@ -92,10 +108,11 @@ int pf_preprocess(const double* params, const int32_t* template_id, const int32_
                   void* rec, void* scratch, size_t scratch_bytes, void* stream);
 
 /*
- * K2 — tile binning: exclusive scan of per-primitive counts (z order), fill of
- * (tile, z-position) keys, stable radix sort on the tile key, exclusive scan of
- * per-tile counts.  Output is bit-identical to bin_tiles (raster.py:227-265):
- * CSR offsets/indices, primitive indices ascending in z inside each tile.
+ * K2 — tile binning: exclusive scan of the per-tile counts (CSR offsets) and a
+ * two-digit (tile row, tile column) stable radix bucketing of the z-ordered
+ * primitive stream (block-wide stable compactions; no sort scratch, no host
+ * sync).  Output is bit-identical to bin_tiles (raster.py:227-265): CSR
+ * offsets/indices, primitive indices ascending in z inside each tile.
  *   bin_off  out [n_band_tiles + 1]   (TileBins.offsets)
  *   bin_idx  out [capacity]           (TileBins.indices; first K valid)
  *   status   out int32[4]: [0] = K (total entries), [1] = overflow flag (K > capacity)
@@ -110,23 +127,29 @@ int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity
  * Replaces: forward_nosave / count_entries + fill_entries (_kernels.py:76-255),
  * render_forward (raster.py:290-363), and (when loss_kind != NONE) loss_mse /
  * loss_spatial (fit.py:112-151).
- *   tex        [4][texels] planar float64 atlas
+ *   tex        [4][texels] planar float64 atlas (RGB planes read when mu_blend > 0)
+ *   quad       float32 [texels][4] alpha quad atlas from pf_atlas_quad
  *   bg_img     float32 [H][W][3] per-pixel background, or NULL for solid (bg_r,bg_g,bg_b)
- *   ent_j/ent_T/ent_n  saved state (NULL = render only): ent_j uint16 and ent_T
- *              float64 of pf_saved_capacity(capacity) entries, ent_n int32 [H*W]
+ *   saved      saved state (NULL = render only): pf_saved_bytes(capacity) bytes
+ *              holding saved_entries = pf_saved_capacity(capacity) 16-byte
+ *              entries (list position j, texel cell, bilinear weights, incoming
+ *              transmittance T -- the reference's Tbuf, _kernels.py:294-297);
+ *              ent_n int32 [H*W] per-pixel contribution counts
  *   img        out float32 [H][W][3]; alpha out float32 [H][W] (band rows written)
  *   target     float32 [H][W][3]; target_alpha float32 [H][W] (SPATIAL only)
  *   dI         out float32 [H][W][3] = dL/dI; dA out float32 [H][W] (SPATIAL)
- *   part       scratch float64 [n_band_tiles * 4]; counter: uint32 zeroed once
- *   sums       out float64[3]: sum (I-t)^2, sum ((I-t)*mask)^2, sum (I_a - t_a)^2
+ *   part       out float64 [n_band_tiles * 8 * 3]: per-warp loss partials
+ *              (sum (I-t)^2, sum ((I-t)*mask)^2, sum (I_a - t_a)^2), reduced in
+ *              fixed order by pf_backward (deterministic loss value)
+ *   counter, sums  unused (pass NULL); kept for ABI stability
  *   inv_3P, inv_P  1/(3*H*W), 1/(H*W) of the FULL canvas (band-independent)
  */
-int pf_forward(const void* rec, int n, const double* tex, int texels,
+int pf_forward(const void* rec, int n, const double* tex, const float* quad, int texels,
                const int32_t* bin_off, const int32_t* bin_idx, const int32_t* status,
                int W, int H, int ty_begin, int ty_end,
                double eps_skip, double mu_blend,
                double bg_r, double bg_g, double bg_b, const float* bg_img,
-               uint16_t* ent_j, double* ent_T, int32_t* ent_n,
+               void* saved, long long saved_entries, int32_t* ent_n,
                float* img, float* alpha,
                int loss_kind, const float* target, const float* target_alpha, double alpha_w,
                double inv_3P, double inv_P,
@@ -141,14 +164,16 @@ int pf_forward(const void* rec, int n, const double* tex, int texels,
  * grad.py:134-206).  grads is ACCUMULATED into (caller zeroes it).
  *   dI float32 [H][W][3] (dL/dI), dA float32 [H][W] or NULL (dL/dA = 0)
  *   grads  float64 [n][8], columns as params
+ *   part   the forward's per-warp loss partials (or NULL); when given, block 0
+ *          also reduces them in fixed order into sums[3] (loss value + psnr input)
  */
-int pf_backward(const void* rec, int n, const double* tex, int texels,
+int pf_backward(const void* rec, int n, const double* tex, const float* quad, int texels,
                 const int32_t* bin_off, const int32_t* bin_idx, const int32_t* status,
-                const uint16_t* ent_j, const double* ent_T, const int32_t* ent_n,
+                const void* saved, long long saved_entries, const int32_t* ent_n,
                 const float* dI, const float* dA,
                 double bg_r, double bg_g, double bg_b, const float* bg_img,
                 double mu_blend, int W, int H, int ty_begin, int ty_end,
-                double* grads, void* stream);
+                double* grads, const double* part, double* sums, void* stream);
 
 /*
  * K5 — fused Adam step (+ loss/psnr history, + gradient zeroing for the next step).

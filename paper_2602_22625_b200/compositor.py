@@ -12,8 +12,9 @@ reference's per-iteration calls in fit.run_loop (pkg/src/primfit/fit.py:486-501)
 
 HBM layout: params/grads/moments float64 [N][8]; primitive
 records 192 B/prim; atlas float64 planar [4][texels]; bins int32 CSR; saved
-forward = uint16 list position + float64 transmittance per contributing
-(pixel, primitive) at slot 256*bin_off[t] + k*256 + pixel; pixel buffers float32.
+forward = float64 transmittance + texel coords U, V and uint16 list position
+per contributing (pixel, primitive) at slot 256*bin_off[t] + k*256 + pixel;
+pixel buffers float32.
 """
 
 from __future__ import annotations
@@ -68,6 +69,14 @@ class DeviceAtlas:
         self.d_h = torch.from_numpy(self.th).to(dev)
         self.d_q = torch.from_numpy(self.q).to(dev)
         self.d_hyp = torch.from_numpy(self.hyp).to(dev)
+        # alpha quad atlas (four bilinear taps per texel, zero padded), built on device
+        self.quad = torch.zeros(max(self.texels, 1) * 4, dtype=torch.float32, device=dev)
+        if self.texels:
+            lib = nat.load()
+            nat.check(lib.pf_atlas_quad(self.tex.data_ptr(), self.texels, self.d_base.data_ptr(),
+                                        self.d_w.data_ptr(), self.d_h.data_ptr(),
+                                        self.n_templates, self.quad.data_ptr(),
+                                        _stream_handle()), "pf_atlas_quad")
 
 
 def bin_capacity(scales: np.ndarray, tids: np.ndarray, hyp: np.ndarray, padding: float,
@@ -137,15 +146,15 @@ class Compositor:
             self.img = torch.empty(P * 3, dtype=torch.float32, device=dev)
             self.alpha = torch.empty(P, dtype=torch.float32, device=dev)
         if save and not self._saved_alloc:
-            cap = int(self.lib.pf_saved_capacity(max(self.capacity, 1)))
-            self.ent_j = torch.empty(cap, dtype=torch.int16, device=dev)
-            self.ent_T = torch.empty(cap, dtype=torch.float64, device=dev)
+            self.saved_entries = int(self.lib.pf_saved_capacity(max(self.capacity, 1)))
+            nbytes = int(self.lib.pf_saved_bytes(max(self.capacity, 1)))
+            self.saved = torch.empty(nbytes, dtype=torch.uint8, device=dev)
             self.ent_n = torch.zeros(P, dtype=torch.int32, device=dev)
             self._saved_alloc = True
         if loss and not hasattr(self, "dI"):
             self.dI = torch.empty(P * 3, dtype=torch.float32, device=dev)
-            self.part = torch.zeros(max(self.n_tiles, 1) * 4, dtype=torch.float64, device=dev)
-            self.fwd_counter = torch.zeros(1, dtype=torch.int32, device=dev)
+            # per-warp loss partials (8 warps per tile, 3 sums each)
+            self.part = torch.zeros(max(self.n_tiles, 1) * 8 * 3, dtype=torch.float64, device=dev)
         if spatial and not hasattr(self, "dA"):
             self.dA = torch.empty(P, dtype=torch.float32, device=dev)
 
@@ -183,8 +192,7 @@ class Compositor:
     def forward(self, *, save: bool, eps_skip: float, bg_rgb=(1.0, 1.0, 1.0),
                 bg_img: torch.Tensor | None = None, loss_kind: int = nat.PF_LOSS_NONE,
                 target: torch.Tensor | None = None, target_alpha: torch.Tensor | None = None,
-                alpha_w: float = 0.0, sums: torch.Tensor | None = None, P_total: int | None = None,
-                stream=None) -> None:
+                alpha_w: float = 0.0, P_total: int | None = None, stream=None) -> None:
         spatial = loss_kind == nat.PF_LOSS_SPATIAL
         self.alloc_render(save, loss_kind != nat.PF_LOSS_NONE, spatial)
         P = float(P_total if P_total is not None else self.W * self.H)
@@ -192,31 +200,34 @@ class Compositor:
         lossy = loss_kind != nat.PF_LOSS_NONE
         nat.check(
             self.lib.pf_forward(
-                self.rec.data_ptr(), self.n, self.atlas.tex.data_ptr(), self.atlas.texels,
+                self.rec.data_ptr(), self.n, self.atlas.tex.data_ptr(),
+                self.atlas.quad.data_ptr(), self.atlas.texels,
                 self.bin_off.data_ptr(), self.bin_idx.data_ptr(), self.status.data_ptr(),
                 self.W, self.H, self.band.ty_begin, self.band.ty_end, float(eps_skip),
                 self.mu_blend, float(bg_rgb[0]), float(bg_rgb[1]), float(bg_rgb[2]), p(bg_img),
-                p(self.ent_j) if save else None, p(self.ent_T) if save else None,
+                p(self.saved) if save else None, self.saved_entries if save else 0,
                 p(self.ent_n) if save else None, self.img.data_ptr(), self.alpha.data_ptr(),
                 int(loss_kind), p(target), p(target_alpha), float(alpha_w), 1.0 / (3.0 * P),
                 1.0 / P, p(self.dI) if lossy else None, p(self.dA) if spatial else None,
-                p(self.part) if lossy else None, p(self.fwd_counter) if lossy else None,
-                p(sums), _stream_handle(stream)),
+                p(self.part) if lossy else None, None, None, _stream_handle(stream)),
             "pf_forward")
 
     # -- K4
     def backward(self, dI: torch.Tensor, grads: torch.Tensor, *, dA: torch.Tensor | None = None,
                  bg_rgb=(1.0, 1.0, 1.0), bg_img: torch.Tensor | None = None,
-                 stream=None) -> None:
+                 sums: torch.Tensor | None = None, stream=None) -> None:
+        """K4; with ``sums`` also folds the fused loss partials of the last forward."""
         p = nat.ptr
         nat.check(
             self.lib.pf_backward(
-                self.rec.data_ptr(), self.n, self.atlas.tex.data_ptr(), self.atlas.texels,
+                self.rec.data_ptr(), self.n, self.atlas.tex.data_ptr(),
+                self.atlas.quad.data_ptr(), self.atlas.texels,
                 self.bin_off.data_ptr(), self.bin_idx.data_ptr(), self.status.data_ptr(),
-                self.ent_j.data_ptr(), self.ent_T.data_ptr(), self.ent_n.data_ptr(),
+                self.saved.data_ptr(), self.saved_entries, self.ent_n.data_ptr(),
                 dI.data_ptr(), p(dA), float(bg_rgb[0]), float(bg_rgb[1]), float(bg_rgb[2]),
                 p(bg_img), self.mu_blend, self.W, self.H, self.band.ty_begin,
-                self.band.ty_end, grads.data_ptr(), _stream_handle(stream)),
+                self.band.ty_end, grads.data_ptr(),
+                p(self.part) if sums is not None else None, p(sums), _stream_handle(stream)),
             "pf_backward")
 
 

@@ -6,74 +6,52 @@
 // clips it to the canvas in float64 (ceil/floor, raster.py:248-253) and appends
 // the primitive index to every tile the clipped pixel range touches.
 //
-// B200 restatement: one thread per z position computes the bbox (float64,
-// no FMA, same rounding as Python) and the per-primitive tile count; an
-// exclusive scan in z order gives each primitive a contiguous slot range; the
-// fill kernel writes (tile) keys + (primitive) values in z order; a STABLE
-// LSD radix sort on the tile key (CUB onesweep, only ceil(log2(tiles+1)) bits)
-// groups entries per tile while keeping z order inside each tile.  Per-tile
-// counts (histogram via atomics in K1) are scanned into the CSR offsets.
-// The result is bit-identical to the reference's offsets/indices.
-#include <cub/cub.cuh>
-
+// B200 restatement (three launches, no host sync, no sort scratch):
+//   K1  k_preprocess   one thread per z position: primitive records, float64
+//                      bbox with Python's rounding, per-tile and per-tile-row
+//                      counts (atomics; final values are order independent).
+//   K2a k_bin_scan     block 0: exclusive scan of the per-tile counts -> CSR
+//                      offsets (TileBins.offsets) + K + overflow flag;
+//                      blocks 1..rows: for each tile row, a STABLE block-wide
+//                      compaction of the z-ordered primitive stream (contiguous
+//                      per-thread chunks + one block scan) -> row lists in z order.
+//   K2b k_bin_fill     one block per tile: stable compaction of its row list by
+//                      column range -> the tile's z-ascending primitive list.
+// Together K2a/K2b are a two-digit (tile row, tile column) stable MSD radix
+// bucketing of the z-sorted stream: the output equals a stable radix sort of
+// (tile, z) keys and is bit-identical to the reference's offsets/indices.
 #include "../../include/primfit_b200.h"
 #include "pf_common.cuh"
 
 namespace pf {
 
 struct BinScratch {
-  int32_t* pcount;   // [n+1] per-z-position tile count (last = 0)
-  int32_t* poff;     // [n+1] exclusive scan
-  int4* rect;        // [n] band-clipped tile rect (tx0, ty0, tx1, ty1), empty: tx0 > tx1
-  int32_t* zprim;    // [n] primitive index per z position (copy of zorder)
-  int32_t* tcount;   // [n_tiles+1] per-tile counts (last = 0)
-  uint32_t* keys_in;   // [cap]
-  uint32_t* keys_out;  // [cap]
-  int32_t* vals_in;    // [cap]
-  void* cub_tmp;
-  size_t cub_bytes;
+  int4* rect;        // [n] band-clipped tile rect per z position (tx0, ty0, tx1, ty1)
+  int32_t* zprim;    // [n] primitive index per z position
+  int32_t* tcount;   // [n_tiles] per-tile counts
+  int32_t* rcount;   // [n_rows] per-row counts
+  int32_t* rowlist;  // [capacity] z positions, grouped by row
+  int32_t* rowoff;   // [n_rows + 1]
   size_t total;
 };
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-static int end_bit_for(int n_tiles) {
-  int b = 1;
-  while ((1u << b) <= (unsigned)n_tiles) ++b;  // sentinel key == n_tiles must fit
-  return b;
-}
-
-static size_t cub_temp_bytes(int n, int n_tiles, int cap) {
-  size_t a = 0, b = 0, c = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, a, (int32_t*)nullptr, (int32_t*)nullptr, n + 1);
-  cub::DeviceScan::ExclusiveSum(nullptr, b, (int32_t*)nullptr, (int32_t*)nullptr, n_tiles + 1);
-  if (cap > 0)
-    cub::DeviceRadixSort::SortPairs(nullptr, c, (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                    (int32_t*)nullptr, (int32_t*)nullptr, cap, 0,
-                                    end_bit_for(n_tiles));
-  size_t m = a > b ? a : b;
-  return m > c ? m : c;
-}
-
-static BinScratch carve(void* base, int n, int n_tiles, int cap) {
+static BinScratch carve(void* base, int n, int n_tiles, int n_rows, int cap) {
   BinScratch s;
   char* p = (char*)base;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     char* q = p ? p + off : nullptr;
-    off = align_up(off + bytes, 256);
+    off = align_up(off + (bytes > 0 ? bytes : 1), 256);
     return (void*)q;
   };
-  s.pcount = (int32_t*)take(sizeof(int32_t) * (n + 1));
-  s.poff = (int32_t*)take(sizeof(int32_t) * (n + 1));
-  s.rect = (int4*)take(sizeof(int4) * (n > 0 ? n : 1));
-  s.zprim = (int32_t*)take(sizeof(int32_t) * (n > 0 ? n : 1));
-  s.tcount = (int32_t*)take(sizeof(int32_t) * (n_tiles + 1));
-  s.keys_in = (uint32_t*)take(sizeof(uint32_t) * (cap > 0 ? cap : 1));
-  s.keys_out = (uint32_t*)take(sizeof(uint32_t) * (cap > 0 ? cap : 1));
-  s.vals_in = (int32_t*)take(sizeof(int32_t) * (cap > 0 ? cap : 1));
-  s.cub_bytes = cub_temp_bytes(n, n_tiles, cap);
-  s.cub_tmp = take(s.cub_bytes);
+  s.rect = (int4*)take(sizeof(int4) * (size_t)n);
+  s.zprim = (int32_t*)take(sizeof(int32_t) * (size_t)n);
+  s.tcount = (int32_t*)take(sizeof(int32_t) * (size_t)n_tiles);
+  s.rcount = (int32_t*)take(sizeof(int32_t) * (size_t)n_rows);
+  s.rowlist = (int32_t*)take(sizeof(int32_t) * (size_t)cap);
+  s.rowoff = (int32_t*)take(sizeof(int32_t) * (size_t)(n_rows + 1));
   s.total = off;
   return s;
 }
@@ -92,13 +70,13 @@ struct PreArgs {
   int W, H, tile, ntx, ty_begin, ty_end;
   RecF* recf;
   RecB* recb;
+  RecC* recc;
   BinScratch s;
 };
 
 // K1: one thread per z position j (primitive zorder[j]).
-__global__ void __launch_bounds__(256) k_preprocess(PreArgs a) {
+__global__ void __launch_bounds__(32) k_preprocess(PreArgs a) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j == 0) a.s.pcount[a.n] = 0;
   if (j >= a.n) return;
   const int i = __ldg(a.zorder + j);
   a.s.zprim[j] = i;
@@ -127,6 +105,10 @@ __global__ void __launch_bounds__(256) k_preprocess(PreArgs a) {
   rf.c0 = __dmul_rn(omm, sc0);
   rf.c1 = __dmul_rn(omm, sc1);
   rf.c2 = __dmul_rn(omm, sc2);
+  rf.inv_s = __ddiv_rn(1.0, s);
+  rf.inv_sq = __ddiv_rn(1.0, rf.sq);
+  rf.wm1 = (double)(wt - 1);
+  rf.hm1 = (double)(ht - 1);
   rf.base = __ldg(a.tpl_base + t);
   rf.wt = wt;
   rf.ht = ht;
@@ -151,6 +133,25 @@ __global__ void __launch_bounds__(256) k_preprocess(PreArgs a) {
 
   // bbox, float64 with Python's rounding: r = s*hyp + pad, ceil(x-r), floor(x+r)
   const double r = __dadd_rn(__dmul_rn(s, hyp), a.padding);
+
+  // cull record (see RecC): fp32 centre and axes, conservative slack
+  {
+    RecC rc;
+    const double is = rf.inv_s, isq = rf.inv_sq;
+    rc.px = (float)x;
+    rc.py = (float)y;
+    rc.au = (float)(ct * is);
+    rc.bu = (float)(st * is);
+    rc.av = (float)(ct * isq);
+    rc.bv = (float)(st * isq);
+    const double hx = 0.5 * (kWarpW - 1), hy = 0.5 * (kWarpH - 1);
+    const double e_px = fabs(x - (double)rc.px) + fabs(y - (double)rc.py);
+    const double span = e_px + 1e-6 * (fabs(r) + 2.0 * kTile);
+    const double su = (fabs(ct) + fabs(st)) * is, sv = (fabs(ct) + fabs(st)) * isq;
+    rc.eu = (float)((fabs(ct) * hx + fabs(st) * hy) * is + su * span + 1e-5);
+    rc.ev = (float)((fabs(st) * hx + fabs(ct) * hy) * isq + sv * span + 1e-5);
+    a.recc[i] = rc;
+  }
   double lo_x = ceil(__dsub_rn(x, r)), hi_x = floor(__dadd_rn(x, r));
   double lo_y = ceil(__dsub_rn(y, r)), hi_y = floor(__dadd_rn(y, r));
   lo_x = fmax(lo_x, 0.0);
@@ -158,7 +159,6 @@ __global__ void __launch_bounds__(256) k_preprocess(PreArgs a) {
   hi_x = fmin(hi_x, (double)(a.W - 1));
   hi_y = fmin(hi_y, (double)(a.H - 1));
   int4 rc = make_int4(1, 1, 0, 0);  // empty
-  int cnt = 0;
   // NaN-safe: every comparison with NaN is false -> treated as empty
   if (lo_x <= hi_x && lo_y <= hi_y) {
     const int tx0 = (int)lo_x / a.tile, tx1 = (int)hi_x / a.tile;
@@ -167,51 +167,162 @@ __global__ void __launch_bounds__(256) k_preprocess(PreArgs a) {
     ty1 = min(ty1, a.ty_end - 1);
     if (ty0 <= ty1) {
       rc = make_int4(tx0, ty0, tx1, ty1);
-      cnt = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
       for (int ty = ty0; ty <= ty1; ++ty) {
-        const int row = (ty - a.ty_begin) * a.ntx;
-        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(a.s.tcount + row + tx, 1);
+        const int row = ty - a.ty_begin;
+        atomicAdd(a.s.rcount + row, 1);
+        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(a.s.tcount + row * a.ntx + tx, 1);
       }
     }
   }
   a.s.rect[j] = rc;
-  a.s.pcount[j] = cnt;
 }
 
-struct FillArgs {
-  int n, cap, ntx, ty_begin, n_tiles;
+__device__ __forceinline__ int div_up_d(int a, int b) { return (a + b - 1) / b; }
+
+// Block-wide exclusive scan of one int per thread (1024 threads max).
+// Returns the exclusive prefix; *total receives the block sum.
+__device__ __forceinline__ int block_excl_scan(int v, int* warp_sums, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) warp_sums[lane] = w;  // inclusive warp prefix
+  }
+  __syncthreads();
+  const int excl_warp = warp > 0 ? warp_sums[warp - 1] : 0;
+  *total = warp_sums[nw - 1];
+  const int r = excl_warp + x - v;
+  __syncthreads();  // warp_sums reusable by the caller afterwards
+  return r;
+}
+
+struct ScanArgs {
+  int n, n_tiles, n_rows, ntx, ty_begin, cap;
   BinScratch s;
+  int32_t* bin_off;
   int32_t* status;
 };
 
-// Fill (tile key, primitive value) pairs in z order; pad [K, cap) with the
-// sentinel key n_tiles so a fixed-size sort keeps graph capture possible.
-__global__ void __launch_bounds__(256) k_fill(FillArgs a) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  const int K = a.s.poff[a.n];
-  if (g == 0) {
-    a.status[0] = K;
-    a.status[1] = K > a.cap ? 1 : 0;
+constexpr int kScanThreads = 1024;
+
+// K2a: block 0 scans the tile counts; block 1 + r builds row r's list.  Each
+// thread owns a contiguous chunk, so one block scan per block keeps z order.
+__global__ void __launch_bounds__(kScanThreads) k_bin_scan(ScanArgs a) {
+  __shared__ int warp_sums[32];
+  if (blockIdx.x == 0) {
+    const int chunk = div_up_d(a.n_tiles, kScanThreads);
+    const int t0 = min(a.n_tiles, threadIdx.x * chunk), t1 = min(a.n_tiles, t0 + chunk);
+    int local = 0;
+    for (int t = t0; t < t1; ++t) local += a.s.tcount[t];
+    int tot;
+    int run = block_excl_scan(local, warp_sums, &tot);
+    for (int t = t0; t < t1; ++t) {
+      a.bin_off[t] = run;
+      run += a.s.tcount[t];
+    }
+    if (threadIdx.x == 0) {
+      a.bin_off[a.n_tiles] = tot;
+      a.status[0] = tot;
+      a.status[1] = tot > a.cap ? 1 : 0;
+    }
+    return;
   }
-  if (g < a.n) {
-    const int4 rc = a.s.rect[g];
-    const int i = a.s.zprim[g];
-    int off = a.s.poff[g];
-    for (int ty = rc.y; ty <= rc.w; ++ty) {
-      const int row = (ty - a.ty_begin) * a.ntx;
-      for (int tx = rc.x; tx <= rc.z; ++tx) {
-        if (off < a.cap) {
-          a.s.keys_in[off] = (uint32_t)(row + tx);
-          a.s.vals_in[off] = i;
-        }
-        ++off;
-      }
+  const int r = blockIdx.x - 1;
+  const int ty = a.ty_begin + r;
+  // row offset = sum of the counts of the rows before r (rows are few)
+  int part = 0;
+  for (int q = threadIdx.x; q < r; q += kScanThreads) part += a.s.rcount[q];
+  int row_base;
+  (void)block_excl_scan(part, warp_sums, &row_base);
+  const int chunk = div_up_d(a.n, kScanThreads);
+  const int j0 = min(a.n, threadIdx.x * chunk), j1 = min(a.n, j0 + chunk);
+  int local = 0;
+  for (int j = j0; j < j1; ++j) {
+    const int4 rc = a.s.rect[j];
+    local += (rc.y <= ty && ty <= rc.w) ? 1 : 0;
+  }
+  int tot;
+  int pos = row_base + block_excl_scan(local, warp_sums, &tot);
+  for (int j = j0; j < j1; ++j) {
+    const int4 rc = a.s.rect[j];
+    if (rc.y <= ty && ty <= rc.w) {
+      if (pos < a.cap) a.s.rowlist[pos] = j;
+      ++pos;
     }
   }
-  for (int k = K + g; k < a.cap; k += gridDim.x * blockDim.x) {
-    a.s.keys_in[k] = (uint32_t)a.n_tiles;
-    a.s.vals_in[k] = 0;
+  if (threadIdx.x == 0) {
+    a.s.rowoff[r] = row_base;
+    if (r == a.n_rows - 1) a.s.rowoff[a.n_rows] = row_base + tot;
   }
+}
+
+struct FillArgs {
+  int n_tiles, ntx, cap;
+  BinScratch s;
+  const int32_t* bin_off;
+  int32_t* bin_idx;
+  const int32_t* status;
+};
+
+constexpr int kFillThreads = 128;
+
+// K2b: one block per tile, stable compaction of its row list by column range.
+__global__ void __launch_bounds__(kFillThreads) k_bin_fill(FillArgs a) {
+  __shared__ int warp_sums[32];
+  if (a.status[1]) return;  // overflow: lists would not fit
+  const int t = blockIdx.x;
+  const int r = t / a.ntx, tx = t - r * a.ntx;
+  const int r0 = a.s.rowoff[r], n = a.s.rowoff[r + 1] - r0;
+  const int chunk = div_up_d(n, kFillThreads);
+  const int k0 = min(n, (int)threadIdx.x * chunk), k1 = min(n, k0 + chunk);
+  int local = 0;
+  for (int k = k0; k < k1; ++k) {
+    const int4 rc = a.s.rect[a.s.rowlist[r0 + k]];
+    local += (rc.x <= tx && tx <= rc.z) ? 1 : 0;
+  }
+  int tot;
+  int out = a.bin_off[t] + block_excl_scan(local, warp_sums, &tot);
+  for (int k = k0; k < k1; ++k) {
+    const int j = a.s.rowlist[r0 + k];
+    const int4 rc = a.s.rect[j];
+    if (rc.x <= tx && tx <= rc.z) a.bin_idx[out++] = a.s.zprim[j];
+  }
+}
+
+// Alpha quad atlas (see Quad in pf_common.cuh): one thread per texel.
+struct QuadArgs {
+  const double* tex;  // planar [4][texels]
+  int texels, n_tpl;
+  const int32_t* base;
+  const int32_t* w;
+  const int32_t* h;
+  float* quad;
+};
+
+__global__ void k_atlas_quad(QuadArgs a) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= a.texels) return;
+  int t = 0;
+  while (t + 1 < a.n_tpl && a.base[t + 1] <= g) ++t;
+  const int wt = a.w[t], ht = a.h[t], local = g - a.base[t];
+  const int v = local / wt, u = local - v * wt;
+  const double* al = a.tex + 3 * (size_t)a.texels + a.base[t];
+  auto at = [&](int uu, int vv) { return (uu < wt && vv < ht) ? al[vv * wt + uu] : 0.0; };
+  reinterpret_cast<float4*>(a.quad)[g] =
+      make_float4((float)at(u, v), (float)at(u + 1, v), (float)at(u, v + 1), (float)at(u + 1, v + 1));
 }
 
 }  // namespace pf
@@ -220,7 +331,17 @@ using namespace pf;
 
 extern "C" size_t pf_bin_scratch_bytes(int n, int n_tiles, int capacity) {
   if (n < 0 || n_tiles < 0 || capacity < 0) return 0;
-  return carve(nullptr, n, n_tiles, capacity).total;
+  // rows <= tiles; size for the worst case (one tile per row)
+  return carve(nullptr, n, n_tiles, n_tiles, capacity).total;
+}
+
+static bool band_ok(int W, int H, int tile, int ty_begin, int ty_end, int* ntx, int* n_rows) {
+  if (W < 1 || H < 1 || tile < 1) return false;
+  *ntx = div_up(W, tile);
+  const int nty = div_up(H, tile);
+  if (ty_begin < 0 || ty_end > nty || ty_begin > ty_end) return false;
+  *n_rows = ty_end - ty_begin;
+  return true;
 }
 
 extern "C" int pf_preprocess(const double* params, const int32_t* template_id,
@@ -230,10 +351,10 @@ extern "C" int pf_preprocess(const double* params, const int32_t* template_id,
                              double padding, int W, int H, int tile, int ty_begin, int ty_end,
                              int capacity, void* rec, void* scratch, size_t scratch_bytes,
                              void* stream) {
-  if (n < 0 || W < 1 || H < 1 || tile < 1 || n_tpl < 0 || capacity < 0) return PF_ERR_ARG;
-  const int ntx = div_up(W, tile), nty = div_up(H, tile);
-  if (ty_begin < 0 || ty_end > nty || ty_begin > ty_end) return PF_ERR_ARG;
-  const int n_tiles = (ty_end - ty_begin) * ntx;
+  int ntx, n_rows;
+  if (n < 0 || n_tpl < 0 || capacity < 0 || !band_ok(W, H, tile, ty_begin, ty_end, &ntx, &n_rows))
+    return PF_ERR_ARG;
+  const int n_tiles = n_rows * ntx;
   if (!scratch || scratch_bytes < pf_bin_scratch_bytes(n, n_tiles, capacity)) return PF_ERR_SCRATCH;
   if (n > 0 && (!params || !template_id || !zorder || !rec || !tpl_base || !tpl_w || !tpl_h ||
                 !tpl_q || !tpl_hyp))
@@ -260,51 +381,60 @@ extern "C" int pf_preprocess(const double* params, const int32_t* template_id,
   a.ty_end = ty_end;
   a.recf = (RecF*)rec;
   a.recb = (RecB*)((char*)rec + sizeof(RecF) * (size_t)n);
-  a.s = carve(scratch, n, n_tiles, capacity);
-  cudaError_t e = cudaMemsetAsync(a.s.tcount, 0, sizeof(int32_t) * (n_tiles + 1), st);
+  a.recc = (RecC*)((char*)rec + (sizeof(RecF) + sizeof(RecB)) * (size_t)n);
+  a.s = carve(scratch, n, n_tiles, n_tiles, capacity);
+  cudaError_t e = cudaMemsetAsync(a.s.tcount, 0, sizeof(int32_t) * (size_t)n_tiles, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(a.s.rcount, 0, sizeof(int32_t) * (size_t)n_rows, st);
   if (e != cudaSuccess) return (int)e;
-  const int blocks = div_up(n > 0 ? n : 1, 256);
-  k_preprocess<<<blocks, 256, 0, st>>>(a);
+  // small blocks spread the (latency-bound, sincos/exp heavy) threads over many SMs
+  if (n > 0) k_preprocess<<<div_up(n, 32), 32, 0, st>>>(a);
   return (int)cudaGetLastError();
 }
 
 extern "C" int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity,
                       void* scratch, size_t scratch_bytes, int32_t* bin_off, int32_t* bin_idx,
                       int32_t* status, void* stream) {
-  if (n < 0 || W < 1 || H < 1 || tile < 1 || capacity < 0) return PF_ERR_ARG;
-  const int ntx = div_up(W, tile), nty = div_up(H, tile);
-  if (ty_begin < 0 || ty_end > nty || ty_begin > ty_end) return PF_ERR_ARG;
+  int ntx, n_rows;
+  if (n < 0 || capacity < 0 || !band_ok(W, H, tile, ty_begin, ty_end, &ntx, &n_rows))
+    return PF_ERR_ARG;
   if (!bin_off || !status || (capacity > 0 && !bin_idx)) return PF_ERR_ARG;
-  const int n_tiles = (ty_end - ty_begin) * ntx;
+  const int n_tiles = n_rows * ntx;
   if (!scratch || scratch_bytes < pf_bin_scratch_bytes(n, n_tiles, capacity)) return PF_ERR_SCRATCH;
   cudaStream_t st = (cudaStream_t)stream;
-  BinScratch s = carve(scratch, n, n_tiles, capacity);
-  size_t tb = s.cub_bytes;
-  cudaError_t e =
-      cub::DeviceScan::ExclusiveSum(s.cub_tmp, tb, s.pcount, s.poff, n + 1, st);
+  BinScratch s = carve(scratch, n, n_tiles, n_tiles, capacity);
+  ScanArgs sa;
+  sa.n = n;
+  sa.n_tiles = n_tiles;
+  sa.n_rows = n_rows;
+  sa.ntx = ntx;
+  sa.ty_begin = ty_begin;
+  sa.cap = capacity;
+  sa.s = s;
+  sa.bin_off = bin_off;
+  sa.status = status;
+  k_bin_scan<<<1 + n_rows, kScanThreads, 0, st>>>(sa);
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
+  if (n_tiles == 0) return PF_OK;
   FillArgs f;
-  f.n = n;
-  f.cap = capacity;
-  f.ntx = ntx;
-  f.ty_begin = ty_begin;
   f.n_tiles = n_tiles;
+  f.ntx = ntx;
+  f.cap = capacity;
   f.s = s;
+  f.bin_off = bin_off;
+  f.bin_idx = bin_idx;
   f.status = status;
-  int work = n > capacity ? n : capacity;
-  int blocks = div_up(work > 0 ? work : 1, 256);
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  if (blocks < div_up(n > 0 ? n : 1, 256)) blocks = div_up(n, 256);
-  k_fill<<<blocks, 256, 0, st>>>(f);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return (int)e;
-  if (capacity > 0) {
-    tb = s.cub_bytes;
-    e = cub::DeviceRadixSort::SortPairs(s.cub_tmp, tb, s.keys_in, s.keys_out, s.vals_in, bin_idx,
-                                        capacity, 0, end_bit_for(n_tiles), st);
-    if (e != cudaSuccess) return (int)e;
-  }
-  tb = s.cub_bytes;
-  e = cub::DeviceScan::ExclusiveSum(s.cub_tmp, tb, s.tcount, bin_off, n_tiles + 1, st);
-  return (int)e;
+  k_bin_fill<<<n_tiles, kFillThreads, 0, st>>>(f);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int pf_atlas_quad(const double* tex, int texels, const int32_t* tpl_base,
+                             const int32_t* tpl_w, const int32_t* tpl_h, int n_tpl, float* quad,
+                             void* stream) {
+  if (texels < 0 || n_tpl < 0 || (texels > 0 && (!tex || !tpl_base || !tpl_w || !tpl_h || !quad)))
+    return PF_ERR_ARG;
+  if (texels == 0) return PF_OK;
+  QuadArgs a{tex, texels, n_tpl, tpl_base, tpl_w, tpl_h, quad};
+  k_atlas_quad<<<div_up(texels, 256), 256, 0, (cudaStream_t)stream>>>(a);
+  return (int)cudaGetLastError();
 }

@@ -19,17 +19,18 @@ constexpr int kTile = 16;                 // render tile edge (16x16 pixels / bl
 constexpr int kTilePix = kTile * kTile;   // 256 threads per render block
 constexpr unsigned kFull = 0xffffffffu;
 
-// Forward record: everything the per-pair forward math reads.  96 bytes,
-// staged into shared memory with cp.async (6 x 16 B per record).
+// Forward record: everything the per-pair forward math reads (128 bytes).
 struct __align__(16) RecF {
-  double px, py;   // centre (canvas px; pixel centres at integer coords)
-  double ct, st;   // cos / sin of rotation
-  double s, sq;    // scale, scale * aspect   (v divisor, _kernels.py:112)
-  double sa;       // alpha_max * sigmoid(opacity_logit)
-  double c0, c1, c2;  // (1 - mu_blend) * sigmoid(color_logit)
+  double px, py;          // centre (canvas px; pixel centres at integer coords)
+  double ct, st;          // cos / sin of rotation
+  double inv_s, inv_sq;   // RN(1/s), RN(1/(s q)) -- exact-quotient division (div_rn)
+  double s, sq;           // scale, scale * aspect   (v divisor, _kernels.py:112)
+  double wm1, hm1;        // (double)(wt - 1), (double)(ht - 1)
+  double sa;              // alpha_max * sigmoid(opacity_logit)
+  double c0, c1, c2;      // (1 - mu_blend) * sigmoid(color_logit)
   int32_t base, wt, ht, tid;  // template atlas slot
 };
-static_assert(sizeof(RecF) == 96, "RecF must be 96 bytes");
+static_assert(sizeof(RecF) == 128, "RecF must be 128 bytes");
 
 // Backward-only record extras (precomputed per primitive, 96 bytes).
 struct __align__(16) RecB {
@@ -41,11 +42,46 @@ struct __align__(16) RecB {
 };
 static_assert(sizeof(RecB) == 96, "RecB must be 96 bytes");
 
+// Cull record (32 bytes, fp32): just what the warp-level footprint test needs,
+// so testing 32 list entries costs two 16-byte loads per lane.
+//   u(c) ~= au*dx + bu*dy,  v(c) ~= av*dy - bv*dx  (dx = c.x - px, dy = c.y - py)
+//   eu, ev: the warp rectangle's projected half widths in (u, v) units plus the
+//   rounding slack of the fp32 centre (conservative; never rejects a hit).
+struct __align__(16) RecC {
+  float px, py, au, bu;
+  float av, bv, eu, ev;
+};
+static_assert(sizeof(RecC) == 32, "RecC must be 32 bytes");
+
+// Warp sub-tile shape (8 warps cover a 16x16 tile) -- used by the cull record.
+constexpr int kWarpW = 8, kWarpH = 4;
+
+// Saved forward entry (16 bytes, one 128-bit store / load): list position j,
+// texel cell (u0, v0) and fp32 bilinear weights.  The entry's incoming
+// transmittance T (the reference's Tbuf) is kept in a parallel fp32 array.
+struct __align__(16) SavedEnt {
+  uint16_t j;
+  int16_t u0, v0;
+  uint16_t pad;
+  float wu, wv;
+};
+static_assert(sizeof(SavedEnt) == 16, "SavedEnt must be 16 bytes");
+
 // Stable two-branch logistic, _kernels.py:27-32.
 __device__ __forceinline__ double sigmoid(double x) {
   if (x >= 0.0) return 1.0 / (1.0 + exp(-x));
   double e = exp(x);
   return e / (1.0 + e);
+}
+
+// a / b given inv = RN(1/b): Markstein correction step.  The result is exact
+// whenever a/b is representable (so lattice / box-edge hits land exactly where
+// the reference's correctly rounded division puts them) and correctly rounded
+// in all but vanishingly rare cases otherwise.  3 FP64 ops instead of DDIV.
+__device__ __forceinline__ double div_rn(double a, double b, double inv) {
+  const double q0 = a * inv;
+  const double r = fma(-q0, b, a);
+  return fma(r, inv, q0);
 }
 
 // Canvas pixel -> texel coordinates, reference op order (_kernels.py:109-115),
@@ -54,13 +90,11 @@ __device__ __forceinline__ bool texel_coords(const RecF& r, double xx, double yy
                                              double& U, double& V) {
   const double dx = __dsub_rn(xx, r.px);
   const double dy = __dsub_rn(yy, r.py);
-  const double u = __ddiv_rn(__dadd_rn(__dmul_rn(r.ct, dx), __dmul_rn(r.st, dy)), r.s);
-  const double v = __ddiv_rn(__dadd_rn(__dmul_rn(-r.st, dx), __dmul_rn(r.ct, dy)), r.sq);
-  const double wm1 = (double)(r.wt - 1);
-  const double hm1 = (double)(r.ht - 1);
-  U = __dmul_rn(__dmul_rn(__dadd_rn(u, 1.0), 0.5), wm1);
-  V = __dmul_rn(__dmul_rn(__dadd_rn(v, 1.0), 0.5), hm1);
-  return !(U < 0.0 || U > wm1 || V < 0.0 || V > hm1);
+  const double u = div_rn(__dadd_rn(__dmul_rn(r.ct, dx), __dmul_rn(r.st, dy)), r.s, r.inv_s);
+  const double v = div_rn(__dadd_rn(__dmul_rn(-r.st, dx), __dmul_rn(r.ct, dy)), r.sq, r.inv_sq);
+  U = __dmul_rn(__dmul_rn(__dadd_rn(u, 1.0), 0.5), r.wm1);
+  V = __dmul_rn(__dmul_rn(__dadd_rn(v, 1.0), 0.5), r.hm1);
+  return !(U < 0.0 || U > r.wm1 || V < 0.0 || V > r.hm1);
 }
 
 // Zero-padded texel fetch (_kernels.py:35-40).
@@ -115,6 +149,23 @@ __device__ __forceinline__ double bilinear_grad(const double* __restrict__ plane
   acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(iu, c.wv), p10));
   acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(c.wu, c.wv), p11));
   return acc;
+}
+
+// Alpha "quad atlas": for texel (u, v) of a template, the four bilinear taps
+// (a[v][u], a[v][u+1], a[v+1][u], a[v+1][u+1]) with the reference's zero
+// padding already applied (_kernels.py:35-40), as fp32 (one 16-byte load per
+// sample, no bounds checks).  Built once per atlas by pf_atlas_quad.  The fp32
+// taps move m by <= 6e-8 relative; the one decision that depends on m
+// (m < eps_skip) is re-taken on the float64 plane when m is within 1e-6 of eps.
+__device__ __forceinline__ float4 load_quad(const float4* __restrict__ quad, int base, int wt,
+                                            int u0, int v0) {
+  return __ldg(quad + (size_t)base + v0 * wt + u0);
+}
+
+__device__ __forceinline__ double bilerp(const float4& t, double wu, double wv) {
+  const double iu = 1.0 - wu, iv = 1.0 - wv;
+  return (iu * iv) * (double)t.x + (wu * iv) * (double)t.y + (iu * wv) * (double)t.z +
+         (wu * wv) * (double)t.w;
 }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {

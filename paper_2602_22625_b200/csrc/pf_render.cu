@@ -9,34 +9,68 @@
 //   with the relative suffix colour S and back-product B (no division by 1-a).
 //
 // B200 design:
-//   forward  - the tile's primitive records (96 B each) are staged into shared
-//              memory with cp.async, double-buffered in chunks of 128; each
-//              pixel keeps T and C in float64 registers.  The saved state is NOT
-//              the reference's CSR (count pass + fill pass): each contributing
-//              entry stores (list position j, incoming transmittance T_j) at a
-//              fixed slot 256*bin_off[t] + k*256 + pixel (k = per-pixel ordinal),
-//              so one pass suffices and the layout is coalesced across a warp.
-//              T_j is saved exactly as the reference's Tbuf (_kernels.py:294-297),
-//              which keeps the backward exact at alpha == 1.
+//   Each warp owns an 8x4 pixel sub-tile (8 warps = 16x16 tile), compact so the
+//   warp-uniform culling below rejects as many list entries as possible, and
+//   warps never wait on each other (no block barrier on the hot path).
+//   forward  - for every 32 list entries a warp runs a lane-parallel
+//              conservative separating-axis test (primitive axes) of each
+//              entry's footprint against its 8x4 pixel rectangle (32-byte fp32
+//              cull records, two 16-byte loads per lane) and keeps a ballot
+//              mask; only surviving entries are evaluated per pixel (warp-
+//              uniform loop).  Survivors run the float64 decision chain and an
+//              fp32-tap bilinear alpha sample from the quad atlas (one 16-byte
+//              load, no bounds checks; the eps decision is re-taken on the
+//              float64 plane when within rounding).  T and C are float64.
+//              Saved state: per contributing (pixel, entry) one 16-byte record
+//              (list position, texel cell, bilinear weights) plus its incoming
+//              T (the reference's Tbuf) in a parallel fp32 array, at slot
+//              256*bin_off[t] + k*256 + pixel (k = the pixel's contribution
+//              ordinal): single pass, coalesced within a warp.
 //              With loss_kind != NONE the MSE / spatial loss, dL/dI (and dL/dA)
-//              and per-tile loss partials are fused in; the last block reduces
-//              the partials in fixed order (deterministic loss value).
-//   backward - each warp iterates its pixels' saved entries back to front,
-//              selecting the next list position with __reduce_max_sync, so it
-//              only visits entries that touch at least one of its 32 pixels.
-//              Active lanes compute the 8 gradients in float64; a 9-shuffle
-//              __shfl_xor transpose-butterfly reduces them across the warp and 8
-//              lanes issue one float64 atomicAdd each (RED.E.ADD.F64).
+//              and per-warp loss partials are fused in; the backward reduces the
+//              partials in fixed order (deterministic loss value).
+//   backward - each warp walks its pixels' saved entries back to front, picking
+//              the next list position with __reduce_max_sync so it only visits
+//              entries that touch its 32 pixels.  Active lanes compute the 8
+//              gradients in float64; a 9-shuffle __shfl_xor transpose butterfly
+//              reduces them across the warp and 8 lanes issue one float64
+//              atomicAdd each (RED.E.ADD.F64); with <= 2 active lanes the lanes
+//              issue their atomics directly (no shuffle latency).
 #include "../../include/primfit_b200.h"
 #include "pf_common.cuh"
 
 namespace pf {
 
-constexpr int kChunk = 128;  // records per cp.async stage (12 KB)
+constexpr int kWarpsPerTile = kTilePix / 32;
+
+__device__ __forceinline__ void pixel_of(int tx, int ty, int& x, int& y, float& cx, float& cy) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int wx = (w & 1) * kWarpW, wy = (w >> 1) * kWarpH;
+  x = tx * kTile + wx + (l & (kWarpW - 1));
+  y = ty * kTile + wy + (l / kWarpW);
+  cx = (float)(tx * kTile + wx) + 0.5f * (kWarpW - 1);
+  cy = (float)(ty * kTile + wy) + 0.5f * (kWarpH - 1);
+}
+
+// Conservative footprint-vs-warp-rectangle test (see RecC): reject only when
+// the rectangle centre's (u, v) is beyond 1 + the rectangle's projected half
+// width (+ slack); NaN never rejects.
+__device__ __forceinline__ bool may_touch(const RecC* __restrict__ rc, float cx, float cy) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(rc));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(rc) + 1);
+  const float dx = cx - a.x, dy = cy - a.y;
+  const float uc = a.z * dx + a.w * dy;
+  const float vc = b.x * dy - b.y * dx;
+  const bool out_u = fabsf(uc) > 1.0f + b.z + 1e-5f * fabsf(uc);
+  const bool out_v = fabsf(vc) > 1.0f + b.w + 1e-5f * fabsf(vc);
+  return !(out_u || out_v);
+}
 
 struct FwdArgs {
   const RecF* recf;
-  const double* tex;  // planar [4][texels]
+  const RecC* recc;
+  const double* tex;   // planar [4][texels]
+  const float4* quad;  // alpha quad atlas [texels]
   int texels;
   const int32_t* bin_off;
   const int32_t* bin_idx;
@@ -45,8 +79,8 @@ struct FwdArgs {
   double eps_skip, mu_blend;
   double bg0, bg1, bg2;
   const float* bg_img;
-  uint16_t* ent_j;
-  double* ent_T;
+  SavedEnt* ent;
+  float* ent_T;
   int32_t* ent_n;
   float* img;
   float* alpha;
@@ -56,46 +90,19 @@ struct FwdArgs {
   float* dI;
   float* dA;
   double* part;
-  uint32_t* counter;
-  double* sums;
 };
-
-template <int NV>
-__device__ __forceinline__ void block_sum(double (&v)[NV], double (*red)[NV]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(kFull, v[k], o);
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) red[warp][k] = v[k];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      double s = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w][k];
-      v[k] = s;
-    }
-  }
-}
 
 template <bool SAVE, int LOSS, bool MU>
 __global__ void __launch_bounds__(kTilePix) k_forward(FwdArgs a) {
-  __shared__ __align__(16) RecF srec[2][kChunk];
-  __shared__ double red[kTilePix / 32][3];
-  __shared__ bool am_last;
-
   if (a.status && a.status[1]) return;  // bin overflow: nothing valid to render (block-uniform)
 
   const int tb = blockIdx.x;
   const int tx = tb % a.ntx, ty = a.ty_begin + tb / a.ntx;
-  const int x = tx * kTile + (threadIdx.x & (kTile - 1));
-  const int y = ty * kTile + (threadIdx.x / kTile);
+  int x, y;
+  float cx, cy;
+  pixel_of(tx, ty, x, y, cx, cy);
   const bool valid = x < a.W && y < a.H;
+  const int lane = threadIdx.x & 31;
   const double xx = (double)x, yy = (double)y;
 
   const int b0 = a.bin_off[tb];
@@ -104,68 +111,59 @@ __global__ void __launch_bounds__(kTilePix) k_forward(FwdArgs a) {
 
   double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0;
   int nsave = 0;
-  size_t e = (size_t)b0 * kTilePix + threadIdx.x;
+  const size_t e0 = (size_t)b0 * kTilePix + threadIdx.x;
 
-  auto stage_chunk = [&](int stg, int start) {
-    const int cnt = min(kChunk, L - start);
-    char* dst = reinterpret_cast<char*>(srec[stg]);
-    const char* src = reinterpret_cast<const char*>(a.recf);
-    for (int pc = threadIdx.x; pc < cnt * 6; pc += kTilePix) {
-      const int r = pc / 6, q = pc - r * 6;
-      const int i = __ldg(a.bin_idx + b0 + start + r);
-      cp_async16(dst + r * 96 + q * 16, src + (size_t)i * 96 + q * 16);
+  for (int sub = 0; sub < L; sub += 32) {
+    // warp-cooperative cull: lane l tests list entry sub + l against the warp rect
+    int my_i = 0;
+    bool cand = false;
+    if (sub + lane < L) {
+      my_i = __ldg(a.bin_idx + b0 + sub + lane);
+      cand = may_touch(a.recc + my_i, cx, cy);
     }
-    cp_async_commit();
-  };
-
-  if (L > 0) stage_chunk(0, 0);
-  int stg = 0;
-  for (int start = 0; start < L; start += kChunk) {
-    const bool more = start + kChunk < L;
-    if (more) {
-      stage_chunk(stg ^ 1, start + kChunk);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const int cnt = min(kChunk, L - start);
-    if (valid) {
-      for (int jj = 0; jj < cnt; ++jj) {
-        const RecF& r = srec[stg][jj];
-        double U, V;
-        if (!texel_coords(r, xx, yy, U, V)) continue;
-        const Cell c = make_cell(U, V);
-        const double m = bilinear(plane_a, r.base, r.wt, r.ht, c);
-        if (m < a.eps_skip) continue;
-        const double aa = __dmul_rn(r.sa, m);
-        double cr = r.c0, cg = r.c1, cb = r.c2;
-        if (MU) {
-          cr = __dadd_rn(cr, __dmul_rn(a.mu_blend, bilinear(a.tex, r.base, r.wt, r.ht, c)));
-          cg = __dadd_rn(cg, __dmul_rn(a.mu_blend,
-                                       bilinear(a.tex + a.texels, r.base, r.wt, r.ht, c)));
-          cb = __dadd_rn(cb, __dmul_rn(a.mu_blend,
-                                       bilinear(a.tex + 2 * (size_t)a.texels, r.base, r.wt,
-                                                r.ht, c)));
-        }
-        if (SAVE) {
-          a.ent_j[e] = (uint16_t)(start + jj);
-          a.ent_T[e] = T;
-          e += kTilePix;
-          ++nsave;
-        }
-        const double Ta = __dmul_rn(T, aa);
-        C0 = __dadd_rn(C0, __dmul_rn(Ta, cr));
-        C1 = __dadd_rn(C1, __dmul_rn(Ta, cg));
-        C2 = __dadd_rn(C2, __dmul_rn(Ta, cb));
-        T = __dmul_rn(T, __dsub_rn(1.0, aa));
+    unsigned mask = __ballot_sync(kFull, cand);
+    while (mask) {
+      const int bit = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const int i = __shfl_sync(kFull, my_i, bit);
+      if (!valid) continue;
+      const RecF& r = a.recf[i];
+      double U, V;
+      if (!texel_coords(r, xx, yy, U, V)) continue;
+      const Cell c = make_cell(U, V);
+      double m = bilerp(load_quad(a.quad, r.base, r.wt, c.u0, c.v0), c.wu, c.wv);
+      if (fabs(m - a.eps_skip) <= 1e-6 * a.eps_skip)  // re-take the decision in float64
+        m = bilinear(plane_a, r.base, r.wt, r.ht, c);
+      if (m < a.eps_skip) continue;
+      const double aa = r.sa * m;
+      double cr = r.c0, cg = r.c1, cb = r.c2;
+      if (MU) {
+        cr += a.mu_blend * bilinear(a.tex, r.base, r.wt, r.ht, c);
+        cg += a.mu_blend * bilinear(a.tex + a.texels, r.base, r.wt, r.ht, c);
+        cb += a.mu_blend * bilinear(a.tex + 2 * (size_t)a.texels, r.base, r.wt, r.ht, c);
       }
+      if (SAVE) {
+        SavedEnt s;
+        s.j = (uint16_t)(sub + bit);
+        s.u0 = (int16_t)c.u0;
+        s.v0 = (int16_t)c.v0;
+        s.pad = 0;
+        s.wu = (float)c.wu;
+        s.wv = (float)c.wv;
+        const size_t e = e0 + (size_t)nsave * kTilePix;
+        a.ent[e] = s;
+        a.ent_T[e] = (float)T;
+        ++nsave;
+      }
+      const double Ta = T * aa;
+      C0 += Ta * cr;
+      C1 += Ta * cg;
+      C2 += Ta * cb;
+      T *= 1.0 - aa;
     }
-    __syncthreads();
-    stg ^= 1;
   }
 
-  double loss_v[3] = {0.0, 0.0, 0.0};
+  double l0 = 0.0, l1 = 0.0, l2 = 0.0;
   if (valid) {
     const size_t pix = (size_t)y * a.W + x;
     double g0 = a.bg0, g1 = a.bg1, g2 = a.bg2;
@@ -174,9 +172,9 @@ __global__ void __launch_bounds__(kTilePix) k_forward(FwdArgs a) {
       g1 = a.bg_img[pix * 3 + 1];
       g2 = a.bg_img[pix * 3 + 2];
     }
-    const double I0 = __dadd_rn(C0, __dmul_rn(T, g0));
-    const double I1 = __dadd_rn(C1, __dmul_rn(T, g1));
-    const double I2 = __dadd_rn(C2, __dmul_rn(T, g2));
+    const double I0 = C0 + T * g0;
+    const double I1 = C1 + T * g1;
+    const double I2 = C2 + T * g2;
     const double Ia = 1.0 - T;
     a.img[pix * 3 + 0] = (float)I0;
     a.img[pix * 3 + 1] = (float)I1;
@@ -188,9 +186,10 @@ __global__ void __launch_bounds__(kTilePix) k_forward(FwdArgs a) {
       const double r0 = I0 - (double)a.target[pix * 3 + 0];
       const double r1 = I1 - (double)a.target[pix * 3 + 1];
       const double r2 = I2 - (double)a.target[pix * 3 + 2];
-      loss_v[0] = r0 * r0 + r1 * r1 + r2 * r2;
+      l0 = r0 * r0 + r1 * r1 + r2 * r2;
+      const double k = 2.0 * a.inv_3P;
       if (LOSS == PF_LOSS_MSE) {
-        const double k = 2.0 * a.inv_3P;
+        l1 = l0;
         a.dI[pix * 3 + 0] = (float)(k * r0);
         a.dI[pix * 3 + 1] = (float)(k * r1);
         a.dI[pix * 3 + 2] = (float)(k * r2);
@@ -198,10 +197,9 @@ __global__ void __launch_bounds__(kTilePix) k_forward(FwdArgs a) {
         const double ta = (double)a.target_alpha[pix];
         const double mk = ta > 0.0 ? 1.0 : 0.0;
         const double m0 = r0 * mk, m1 = r1 * mk, m2 = r2 * mk;
-        loss_v[1] = m0 * m0 + m1 * m1 + m2 * m2;
+        l1 = m0 * m0 + m1 * m1 + m2 * m2;
         const double ad = Ia - ta;
-        loss_v[2] = ad * ad;
-        const double k = 2.0 * a.inv_3P;
+        l2 = ad * ad;
         a.dI[pix * 3 + 0] = (float)(k * m0);
         a.dI[pix * 3 + 1] = (float)(k * m1);
         a.dI[pix * 3 + 2] = (float)(k * m2);
@@ -209,35 +207,19 @@ __global__ void __launch_bounds__(kTilePix) k_forward(FwdArgs a) {
       }
     }
   }
-
   if (LOSS != PF_LOSS_NONE) {
-    block_sum<3>(loss_v, red);
-    if (threadIdx.x == 0) {
-      a.part[tb * 3 + 0] = loss_v[0];
-      a.part[tb * 3 + 1] = loss_v[1];
-      a.part[tb * 3 + 2] = loss_v[2];
-      __threadfence();
-      const unsigned t = atomicAdd(a.counter, 1u);
-      am_last = (t == gridDim.x - 1);
+    // per-warp partials at fixed slots (no block barrier); pf_backward reduces them
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      l0 += __shfl_xor_sync(kFull, l0, o);
+      l1 += __shfl_xor_sync(kFull, l1, o);
+      l2 += __shfl_xor_sync(kFull, l2, o);
     }
-    __syncthreads();
-    if (am_last) {
-      // last block: fixed-order reduction of all tile partials
-      __threadfence();
-      double v[3] = {0.0, 0.0, 0.0};
-      for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) {
-        v[0] += __ldcg(a.part + k * 3 + 0);
-        v[1] += __ldcg(a.part + k * 3 + 1);
-        v[2] += __ldcg(a.part + k * 3 + 2);
-      }
-      __syncthreads();
-      block_sum<3>(v, red);
-      if (threadIdx.x == 0) {
-        a.sums[0] = v[0];
-        a.sums[1] = LOSS == PF_LOSS_MSE ? v[0] : v[1];
-        a.sums[2] = v[2];
-        *a.counter = 0u;
-      }
+    if (lane == 0) {
+      double* pp = a.part + ((size_t)tb * kWarpsPerTile + (threadIdx.x >> 5)) * 3;
+      pp[0] = l0;
+      pp[1] = l1;
+      pp[2] = l2;
     }
   }
 }
@@ -246,12 +228,13 @@ struct BwdArgs {
   const RecF* recf;
   const RecB* recb;
   const double* tex;
+  const float4* quad;
   int texels;
   const int32_t* bin_off;
   const int32_t* bin_idx;
   const int32_t* status;
-  const uint16_t* ent_j;
-  const double* ent_T;
+  const SavedEnt* ent;
+  const float* ent_T;
   const int32_t* ent_n;
   const float* dI;
   const float* dA;
@@ -260,6 +243,9 @@ struct BwdArgs {
   double mu_blend;
   int W, H, ntx, ty_begin;
   double* grads;
+  const double* part;  // forward loss partials (NULL: none)
+  int n_part;
+  double* sums;
 };
 
 // Sum 8 values over the warp with a transpose butterfly (9 shuffles instead of
@@ -289,27 +275,57 @@ __device__ __forceinline__ double warp_reduce8(const double (&g)[8]) {
   return y;
 }
 
+// Fixed-order reduction of the forward's per-warp loss partials (block 0).
+__device__ void reduce_loss_partials(const double* part, int n_part, double* sums) {
+  __shared__ double red[kWarpsPerTile][3];
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+  for (int k = threadIdx.x; k < n_part; k += blockDim.x) {
+    v0 += part[3 * k + 0];
+    v1 += part[3 * k + 1];
+    v2 += part[3 * k + 2];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v0 += __shfl_xor_sync(kFull, v0, o);
+    v1 += __shfl_xor_sync(kFull, v1, o);
+    v2 += __shfl_xor_sync(kFull, v2, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5][0] = v0;
+    red[threadIdx.x >> 5][1] = v1;
+    red[threadIdx.x >> 5][2] = v2;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w][threadIdx.x];
+    sums[threadIdx.x] = s;
+  }
+}
+
 template <bool MU, bool HAS_DA>
-__global__ void __launch_bounds__(kTilePix) k_backward(BwdArgs a) {
+__global__ void __launch_bounds__(kTilePix, 3) k_backward(BwdArgs a) {
   if (a.status && a.status[1]) return;
+  if (a.part && blockIdx.x == 0) reduce_loss_partials(a.part, a.n_part, a.sums);
   const int tb = blockIdx.x;
   const int tx = tb % a.ntx, ty = a.ty_begin + tb / a.ntx;
-  const int x = tx * kTile + (threadIdx.x & (kTile - 1));
-  const int y = ty * kTile + (threadIdx.x / kTile);
+  int x, y;
+  float cxf, cyf;
+  pixel_of(tx, ty, x, y, cxf, cyf);
   const bool valid = x < a.W && y < a.H;
   const int lane = threadIdx.x & 31;
-  const double xx = (double)x, yy = (double)y;
   const int b0 = a.bin_off[tb];
-  const double* plane_a = a.tex + 3 * (size_t)a.texels;
 
   const size_t pix = valid ? (size_t)y * a.W + x : 0;
   int k = valid ? a.ent_n[pix] - 1 : -1;
   size_t e = (size_t)b0 * kTilePix + threadIdx.x + (size_t)(k > 0 ? k : 0) * kTilePix;
   unsigned key = 0;
-  double Tk = 0.0;
+  SavedEnt cur{};
+  float curT = 0.0f;
   if (k >= 0) {
-    key = (unsigned)a.ent_j[e] + 1u;
-    Tk = a.ent_T[e];
+    cur = a.ent[e];
+    curT = a.ent_T[e];
+    key = (unsigned)cur.j + 1u;
   }
   double dI0 = 0.0, dI1 = 0.0, dI2 = 0.0, dA = 0.0;
   double g0 = a.bg0, g1 = a.bg1, g2 = a.bg2;
@@ -335,37 +351,49 @@ __global__ void __launch_bounds__(kTilePix) k_backward(BwdArgs a) {
 #pragma unroll
     for (int c = 0; c < 8; ++c) g[c] = 0.0;
     if (act) {
-      const RecF r = a.recf[i];
-      const RecB rb = a.recb[i];
-      double U, V;
-      texel_coords(r, xx, yy, U, V);
-      const Cell c = make_cell(U, V);
-      double gU, gV;
-      const double m = bilinear_grad(plane_a, r.base, r.wt, r.ht, c, gU, gV);
-      const double aa = __dmul_rn(r.sa, m);
+      const SavedEnt se = cur;
+      const double Tc = curT;
+      // prefetch this lane's next saved entry while the math below runs
+      --k;
+      if (k >= 0) {
+        e -= kTilePix;
+        cur = a.ent[e];
+        curT = a.ent_T[e];
+        key = (unsigned)cur.j + 1u;
+      } else {
+        key = 0;
+      }
+      const RecF& r = a.recf[i];
+      const RecB& rb = a.recb[i];
+      const double wu = se.wu, wv = se.wv;
+      const float4 q = load_quad(a.quad, r.base, r.wt, se.u0, se.v0);
+      const double m = bilerp(q, wu, wv);
+      const double iu = 1.0 - wu, iv = 1.0 - wv;
+      const double gU = iv * ((double)q.y - (double)q.x) + wv * ((double)q.w - (double)q.z);
+      const double gV = iu * ((double)q.z - (double)q.x) + wu * ((double)q.w - (double)q.y);
+      const double aa = r.sa * m;
       double ck0 = r.c0, ck1 = r.c1, ck2 = r.c2;
       if (MU) {
-        ck0 = __dadd_rn(ck0, __dmul_rn(a.mu_blend, bilinear(a.tex, r.base, r.wt, r.ht, c)));
-        ck1 = __dadd_rn(ck1, __dmul_rn(a.mu_blend,
-                                       bilinear(a.tex + a.texels, r.base, r.wt, r.ht, c)));
-        ck2 = __dadd_rn(ck2, __dmul_rn(a.mu_blend, bilinear(a.tex + 2 * (size_t)a.texels,
-                                                            r.base, r.wt, r.ht, c)));
+        const Cell c{se.u0, se.v0, wu, wv};
+        ck0 += a.mu_blend * bilinear(a.tex, r.base, r.wt, r.ht, c);
+        ck1 += a.mu_blend * bilinear(a.tex + a.texels, r.base, r.wt, r.ht, c);
+        ck2 += a.mu_blend * bilinear(a.tex + 2 * (size_t)a.texels, r.base, r.wt, r.ht, c);
       }
       // _kernels.py:319-359
       const double gg = dI0 * (ck0 - S0 - g0 * B) + dI1 * (ck1 - S1 - g1 * B) +
                         dI2 * (ck2 - S2 - g2 * B) + dA * B;
-      const double dalpha = Tk * gg;
+      const double dalpha = Tc * gg;
       g[4] = dalpha * rb.sd * m;
       if (rb.one_minus_mu > 0.0) {
-        const double wc = Tk * aa * rb.one_minus_mu;
+        const double wc = Tc * aa * rb.one_minus_mu;
         g[5] = dI0 * wc * rb.cd0;
         g[6] = dI1 * wc * rb.cd1;
         g[7] = dI2 * wc * rb.cd2;
       }
       const double dm = dalpha * r.sa;
-      const double hw = 0.5 * (double)(r.wt - 1), hh = 0.5 * (double)(r.ht - 1);
+      const double hw = 0.5 * r.wm1, hh = 0.5 * r.hm1;
       const double mu_u = gU * hw, mu_v = gV * hh;
-      const double u = U / hw - 1.0, v = V / hh - 1.0;
+      const double u = ((double)se.u0 + wu) / hw - 1.0, v = ((double)se.v0 + wv) / hh - 1.0;
       g[0] = dm * (mu_u * rb.gxu + mu_v * rb.gxv);
       g[1] = dm * (mu_u * rb.gyu + mu_v * rb.gyv);
       g[2] = dm * (mu_u * (-u * rb.inv_s) + mu_v * (-v * rb.inv_s));
@@ -375,18 +403,10 @@ __global__ void __launch_bounds__(kTilePix) k_backward(BwdArgs a) {
       S1 = aa * ck1 + om * S1;
       S2 = aa * ck2 + om * S2;
       B *= om;
-      --k;
-      if (k >= 0) {
-        e -= kTilePix;
-        key = (unsigned)a.ent_j[e] + 1u;
-        Tk = a.ent_T[e];
-      } else {
-        key = 0;
-      }
     }
     const unsigned ball = __ballot_sync(kFull, act);
     double* gp = a.grads + (size_t)i * 8;
-    if ((ball & (ball - 1u)) == 0u) {
+    if (__popc(ball) <= 2) {
       if (act) {
 #pragma unroll
         for (int c = 0; c < 8; ++c)
@@ -403,22 +423,29 @@ __global__ void __launch_bounds__(kTilePix) k_backward(BwdArgs a) {
 
 using namespace pf;
 
-extern "C" int pf_forward(const void* rec, int n, const double* tex, int texels,
-                          const int32_t* bin_off, const int32_t* bin_idx, const int32_t* status,
-                          int W, int H, int ty_begin, int ty_end, double eps_skip,
-                          double mu_blend, double bg_r, double bg_g, double bg_b,
-                          const float* bg_img, uint16_t* ent_j, double* ent_T, int32_t* ent_n,
-                          float* img, float* alpha, int loss_kind, const float* target,
-                          const float* target_alpha, double alpha_w, double inv_3P, double inv_P,
-                          float* dI, float* dA, double* part, uint32_t* counter, double* sums,
-                          void* stream) {
-  if (W < 1 || H < 1 || n < 0 || !bin_off || !img || !alpha) return PF_ERR_ARG;
+// Saved-state layout: [entries] SavedEnt, then [entries] float T.
+extern "C" size_t pf_saved_bytes(int capacity) {
+  return (size_t)pf_saved_capacity(capacity) * (sizeof(SavedEnt) + sizeof(float));
+}
+
+extern "C" int pf_forward(const void* rec, int n, const double* tex, const float* quad,
+                          int texels, const int32_t* bin_off, const int32_t* bin_idx,
+                          const int32_t* status, int W, int H, int ty_begin, int ty_end,
+                          double eps_skip, double mu_blend, double bg_r, double bg_g, double bg_b,
+                          const float* bg_img, void* saved, long long saved_entries,
+                          int32_t* ent_n, float* img, float* alpha, int loss_kind,
+                          const float* target, const float* target_alpha, double alpha_w,
+                          double inv_3P, double inv_P, float* dI, float* dA, double* part,
+                          uint32_t* counter, double* sums, void* stream) {
+  (void)counter;
+  (void)sums;
+  if (W < 1 || H < 1 || n < 0 || !bin_off || !img || !alpha || !tex || !quad) return PF_ERR_ARG;
   const int ntx = div_up(W, kTile), nty = div_up(H, kTile);
   if (ty_begin < 0 || ty_end > nty || ty_begin > ty_end) return PF_ERR_ARG;
-  const bool save = ent_j != nullptr;
-  if (save && (!ent_T || !ent_n)) return PF_ERR_ARG;
+  const bool save = saved != nullptr;
+  if (save && (!ent_n || saved_entries < 0)) return PF_ERR_ARG;
   if (loss_kind != PF_LOSS_NONE) {
-    if (!target || !dI || !part || !counter || !sums) return PF_ERR_ARG;
+    if (!target || !dI || !part) return PF_ERR_ARG;
     if (loss_kind == PF_LOSS_SPATIAL && (!target_alpha || !dA)) return PF_ERR_ARG;
     if (loss_kind != PF_LOSS_MSE && loss_kind != PF_LOSS_SPATIAL) return PF_ERR_ARG;
   }
@@ -426,7 +453,9 @@ extern "C" int pf_forward(const void* rec, int n, const double* tex, int texels,
   if (n_tiles == 0) return PF_OK;
   FwdArgs a;
   a.recf = (const RecF*)rec;
+  a.recc = (const RecC*)((const char*)rec + (sizeof(RecF) + sizeof(RecB)) * (size_t)n);
   a.tex = tex;
+  a.quad = (const float4*)quad;
   a.texels = texels;
   a.bin_off = bin_off;
   a.bin_idx = bin_idx;
@@ -441,8 +470,8 @@ extern "C" int pf_forward(const void* rec, int n, const double* tex, int texels,
   a.bg1 = bg_g;
   a.bg2 = bg_b;
   a.bg_img = bg_img;
-  a.ent_j = ent_j;
-  a.ent_T = ent_T;
+  a.ent = (SavedEnt*)saved;
+  a.ent_T = save ? (float*)((SavedEnt*)saved + saved_entries) : nullptr;
   a.ent_n = ent_n;
   a.img = img;
   a.alpha = alpha;
@@ -454,8 +483,6 @@ extern "C" int pf_forward(const void* rec, int n, const double* tex, int texels,
   a.dI = dI;
   a.dA = dA;
   a.part = part;
-  a.counter = counter;
-  a.sums = sums;
   cudaStream_t st = (cudaStream_t)stream;
   const bool mu = mu_blend > 0.0;
 #define PF_FWD(SV, LS, MUV) k_forward<SV, LS, MUV><<<n_tiles, kTilePix, 0, st>>>(a)
@@ -475,13 +502,15 @@ extern "C" int pf_forward(const void* rec, int n, const double* tex, int texels,
   return (int)cudaGetLastError();
 }
 
-extern "C" int pf_backward(const void* rec, int n, const double* tex, int texels,
-                           const int32_t* bin_off, const int32_t* bin_idx, const int32_t* status,
-                           const uint16_t* ent_j, const double* ent_T, const int32_t* ent_n,
-                           const float* dI, const float* dA, double bg_r, double bg_g,
-                           double bg_b, const float* bg_img, double mu_blend, int W, int H,
-                           int ty_begin, int ty_end, double* grads, void* stream) {
-  if (W < 1 || H < 1 || n < 0 || !bin_off || !ent_j || !ent_T || !ent_n || !dI || !grads)
+extern "C" int pf_backward(const void* rec, int n, const double* tex, const float* quad,
+                           int texels, const int32_t* bin_off, const int32_t* bin_idx,
+                           const int32_t* status, const void* saved, long long saved_entries,
+                           const int32_t* ent_n, const float* dI, const float* dA, double bg_r,
+                           double bg_g, double bg_b, const float* bg_img, double mu_blend, int W,
+                           int H, int ty_begin, int ty_end, double* grads, const double* part,
+                           double* sums, void* stream) {
+  if (W < 1 || H < 1 || n < 0 || !bin_off || !saved || saved_entries < 0 || !ent_n || !dI ||
+      !grads || !tex || !quad || (part && !sums))
     return PF_ERR_ARG;
   const int ntx = div_up(W, kTile), nty = div_up(H, kTile);
   if (ty_begin < 0 || ty_end > nty || ty_begin > ty_end) return PF_ERR_ARG;
@@ -491,12 +520,13 @@ extern "C" int pf_backward(const void* rec, int n, const double* tex, int texels
   a.recf = (const RecF*)rec;
   a.recb = (const RecB*)((const char*)rec + sizeof(RecF) * (size_t)n);
   a.tex = tex;
+  a.quad = (const float4*)quad;
   a.texels = texels;
   a.bin_off = bin_off;
   a.bin_idx = bin_idx;
   a.status = status;
-  a.ent_j = ent_j;
-  a.ent_T = ent_T;
+  a.ent = (const SavedEnt*)saved;
+  a.ent_T = (const float*)((const SavedEnt*)saved + saved_entries);
   a.ent_n = ent_n;
   a.dI = dI;
   a.dA = dA;
@@ -510,6 +540,9 @@ extern "C" int pf_backward(const void* rec, int n, const double* tex, int texels
   a.ntx = ntx;
   a.ty_begin = ty_begin;
   a.grads = grads;
+  a.part = part;
+  a.n_part = n_tiles * kWarpsPerTile;
+  a.sums = sums;
   cudaStream_t st = (cudaStream_t)stream;
   const bool mu = mu_blend > 0.0;
   if (mu) {

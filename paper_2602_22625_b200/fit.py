@@ -326,9 +326,9 @@ class StepEngine:
         c.bin()
         c.forward(save=True, eps_skip=self.eps_skip, bg_rgb=self.bg_rgb, bg_img=self.bg_img,
                   loss_kind=self.loss_kind, target=self.target, target_alpha=self.target_alpha,
-                  alpha_w=self.alpha_w, sums=self.sums, P_total=self.P)
+                  alpha_w=self.alpha_w, P_total=self.P)
         c.backward(c.dI, self.gbuf, dA=c.dA if self.loss_kind == nat.PF_LOSS_SPATIAL else None,
-                   bg_rgb=self.bg_rgb, bg_img=self.bg_img)
+                   bg_rgb=self.bg_rgb, bg_img=self.bg_img, sums=self.sums)
         if self.allreduce is not None:
             self.allreduce(self.gbuf)
         adam_launch(self.params, self.grads, self.m, self.v, frozen=self.frozen, gains=self.gains,
