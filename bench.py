@@ -265,40 +265,23 @@ def run_ours(args) -> None:
     ms_step = ms_total / args.steps
     value = 1e3 / ms_step  # whole-job steps/s (every rank advances the same step)
 
-    # per-kernel timing (eager, events on the launching stream, L2 flushed)
-    comp = eng.comp
-    stage_ms = {"bin": 0.0, "forward": 0.0, "backward": 0.0, "adam": 0.0}
-    from paper_2602_22625_b200 import _native as nat
-    from paper_2602_22625_b200.compositor import adam_launch
-
+    # per-stage timing (eager, events on the launching stream, L2 flushed)
+    stage_ms: dict[str, float] = {}
     for _ in range(prof_steps):
         flush.zero_()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-        ev[0].record()
-        comp.preprocess(eng.params)
-        comp.bin()
-        ev[1].record()
-        comp.forward(save=True, eps_skip=eng.eps_skip, bg_rgb=eng.bg_rgb, bg_img=eng.bg_img,
-                     loss_kind=eng.loss_kind, target=eng.target, target_alpha=eng.target_alpha,
-                     alpha_w=eng.alpha_w, P_total=eng.P)
-        ev[2].record()
-        comp.backward(comp.dI, eng.gbuf,
-                      dA=comp.dA if eng.loss_kind == nat.PF_LOSS_SPATIAL else None,
-                      bg_rgb=eng.bg_rgb, bg_img=eng.bg_img, sums=eng.sums)
-        ev[3].record()
-        if eng.allreduce is not None:
-            eng.allreduce(eng.gbuf)
-        adam_launch(eng.params, eng.grads, eng.m, eng.v, frozen=eng.frozen, gains=eng.gains,
-                    n=eng.n, lr_table=eng.lr_table, bc1_table=eng.bc1_table,
-                    bc2_table=eng.bc2_table, iter_counter=eng.iter, clamp=True,
-                    s_min=w.cfg.scale_min, s_max=w.cfg.scale_max, zero_grads=True, sums=eng.sums,
-                    loss_kind=eng.loss_kind, alpha_w=eng.alpha_w, P_total=eng.P,
-                    hist_loss=eng.hist_loss, hist_psnr=eng.hist_psnr, counter=eng.adam_counter)
-        ev[4].record()
+        marks = [("start", torch.cuda.Event(enable_timing=True))]
+        marks[0][1].record()
+
+        def mark(name):
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            marks.append((name, ev))
+
+        eng.launch_step(mark)
         torch.cuda.synchronize()
         eng.done += 1
-        for k, name in enumerate(("bin", "forward", "backward", "adam")):
-            stage_ms[name] += ev[k].elapsed_time(ev[k + 1]) / prof_steps
+        for (_, e0), (name, e1) in zip(marks, marks[1:]):
+            stage_ms[name] = stage_ms.get(name, 0.0) + e0.elapsed_time(e1) / prof_steps
 
     # end-to-end through the public step API with HOST buffers each step:
     # H2D of the packed parameter vector (pinned), graph replay, D2H of the
@@ -315,6 +298,7 @@ def run_ours(args) -> None:
     for _ in range(e2e_steps):
         it = eng.done
         eng.params.view(-1).copy_(h_params, non_blocking=True)
+        eng.refresh()  # the step consumes the uploaded parameters
         eng.step()
         h_params.copy_(eng.params.view(-1), non_blocking=True)
         h_loss.copy_(eng.hist_loss[it : it + 1], non_blocking=True)
@@ -335,7 +319,7 @@ def run_ours(args) -> None:
         return
     peaks = _peaks()
     ab = algorithmic_bytes(eng.P, K16, n, eng.atlas.texels)
-    dom = max(("forward", "backward"), key=lambda k: stage_ms[k])
+    dom = max(("forward", "backward"), key=lambda k: stage_ms.get(k, 0.0))
     achieved = ab[dom] / (stage_ms[dom] * 1e-3) / 1e9
     cpu = cpu_baseline(args.config) if (world == 1 and not args.no_cpu) else None
     line = {

@@ -98,7 +98,8 @@ int pf_atlas_quad(const double* tex, int texels, const int32_t* tpl_base, const 
  *                    math.hypot in bbox_half_side)
  *   padding        bbox padding (fit.effective_padding, fit.py:338-341)
  *   rec      out   n * pf_record_bytes() bytes
- *   scratch        pf_bin_scratch_bytes(n, n_band_tiles, capacity) bytes
+ *   scratch        pf_bin_scratch_bytes(n, n_band_tiles, capacity) bytes (pf_scratch_init'ed);
+ *                  receives the band-clipped tile rect of every primitive
  */
 int pf_preprocess(const double* params, const int32_t* template_id, const int32_t* zorder, int n,
                   const int32_t* tpl_base, const int32_t* tpl_w, const int32_t* tpl_h,
@@ -108,14 +109,40 @@ int pf_preprocess(const double* params, const int32_t* template_id, const int32_
                   void* rec, void* scratch, size_t scratch_bytes, void* stream);
 
 /*
- * K2 — tile binning: exclusive scan of the per-tile counts (CSR offsets) and a
- * two-digit (tile row, tile column) stable radix bucketing of the z-ordered
- * primitive stream (block-wide stable compactions; no sort scratch, no host
- * sync).  Output is bit-identical to bin_tiles (raster.py:227-265): CSR
- * offsets/indices, primitive indices ascending in z inside each tile.
+ * One-time initialisation of a binning scratch buffer (zero it, copy the static
+ * z order).  Call once after allocating pf_bin_scratch_bytes(...) bytes.
+ */
+int pf_scratch_init(void* scratch, size_t scratch_bytes, const int32_t* zorder, int n, int capacity,
+                    void* stream);
+
+/*
+ * K5+K1 fused: one Adam step (fit.py:195-238, table mode as pf_adam) on every
+ * parameter, then the records / tile rects of the NEXT step from the updated
+ * parameters (as pf_preprocess), the loss/psnr history entry and the iteration
+ * counter -- one launch between two renders.  Gradients are zeroed.
+ */
+int pf_adam_preprocess(double* params, double* grads, double* m, double* v, const uint8_t* frozen,
+                       const double* gains8, const double* lr_table, const double* bc1_table,
+                       const double* bc2_table, int32_t* iter, int clamp, double s_min,
+                       double s_max, const double* sums, int loss_kind, double alpha_w,
+                       double inv_3P, double inv_P, double* hist_loss, double* hist_psnr,
+                       const int32_t* template_id, const int32_t* zorder, int n,
+                       const int32_t* tpl_base, const int32_t* tpl_w, const int32_t* tpl_h,
+                       const double* tpl_q, const double* tpl_hyp, int n_tpl, double alpha_max,
+                       double mu_blend, double padding, int W, int H, int tile, int ty_begin,
+                       int ty_end, int capacity, void* rec, void* scratch, size_t scratch_bytes,
+                       void* stream);
+
+/*
+ * K2 — tile binning from the rects of pf_preprocess: one block per tile row,
+ * a two-digit (row, column) stable radix bucketing of the z-ordered primitive
+ * stream (block-wide stable compactions and ballots; no sort scratch, no
+ * atomics, no host sync).  Output is bit-identical to bin_tiles
+ * (raster.py:227-265): primitive indices ascending in z inside each tile.
  *   bin_off  out [n_band_tiles + 1]   (TileBins.offsets)
  *   bin_idx  out [capacity]           (TileBins.indices; first K valid)
- *   status   out int32[4]: [0] = K (total entries), [1] = overflow flag (K > capacity)
+ *   status   out int32[4]: [0] = K (total entries), [1] = overflow flag (K > capacity;
+ *            nothing else is written then)
  */
 int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity,
            void* scratch, size_t scratch_bytes,

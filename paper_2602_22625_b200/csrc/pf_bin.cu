@@ -1,63 +1,57 @@
-// K1 preprocess + K2 tile binning.
+// K1 preprocess (+ optionally the fused Adam step) and K2 tile binning.
 //
 // Reference: bin_tiles (pkg/src/primfit/raster.py:227-265) walks primitives in
 // ascending z, computes a conservative square bbox of half side
 // r = scale*hypot(1, max(1, q)) + padding (bbox_half_side, raster.py:222-224),
 // clips it to the canvas in float64 (ceil/floor, raster.py:248-253) and appends
-// the primitive index to every tile the clipped pixel range touches.
+// the primitive index to every tile the clipped pixel range touches, so every
+// tile list is in ascending z.  adam_step: fit.py:195-238.
 //
-// B200 restatement (three launches, no host sync, no sort scratch):
-//   K1  k_preprocess   one thread per z position: primitive records, float64
-//                      bbox with Python's rounding, per-tile and per-tile-row
-//                      counts (atomics; final values are order independent).
-//   K2a k_bin_scan     block 0: exclusive scan of the per-tile counts -> CSR
-//                      offsets (TileBins.offsets) + K + overflow flag;
-//                      blocks 1..rows: for each tile row, a STABLE block-wide
-//                      compaction of the z-ordered primitive stream (contiguous
-//                      per-thread chunks + one block scan) -> row lists in z order.
-//   K2b k_bin_fill     one block per tile: stable compaction of its row list by
-//                      column range -> the tile's z-ascending primitive list.
-// Together K2a/K2b are a two-digit (tile row, tile column) stable MSD radix
-// bucketing of the z-sorted stream: the output equals a stable radix sort of
-// (tile, z) keys and is bit-identical to the reference's offsets/indices.
+// B200 restatement (no host sync, no sort, no atomics on the binning path):
+//   K1 k_prim<ADAM>  eight lanes per primitive (one per parameter): [Adam update
+//                    of that parameter ->] record build split across the lanes
+//                    (sincos / sigmoids / exact reciprocals on different lanes,
+//                    fields exchanged with shuffles, each lane stores one
+//                    16-byte slice) and the float64 bbox -> band-clipped tile
+//                    rect per z position, with Python's rounding.
+//   K2 k_bin_rows    one 1024-thread block per tile row, a two-digit stable
+//                    radix bucketing of the z-ordered primitive stream:
+//                    (a) stable compaction of the primitives covering the row
+//                        (contiguous per-thread chunks + block scan), while a
+//                        block reduction of "entries in earlier rows" gives the
+//                        row's CSR base without any cross-block communication;
+//                    (b) per-column counts (shared-memory atomics) -> block scan
+//                        -> TileBins.offsets for the row's tiles;
+//                    (c) one warp per column walks the row list with ballots and
+//                        writes that tile's z-ascending primitive list.
+// The CSR bins are bit-identical to the reference's offsets/indices.
 #include "../../include/primfit_b200.h"
+#include "pf_bins.cuh"
 #include "pf_common.cuh"
 
 namespace pf {
 
-struct BinScratch {
-  int4* rect;        // [n] band-clipped tile rect per z position (tx0, ty0, tx1, ty1)
-  int32_t* zprim;    // [n] primitive index per z position
-  int32_t* tcount;   // [n_tiles] per-tile counts
-  int32_t* rcount;   // [n_rows] per-row counts
-  int32_t* rowlist;  // [capacity] z positions, grouped by row
-  int32_t* rowoff;   // [n_rows + 1]
-  size_t total;
+struct AdamPart {
+  double* grads;
+  double* m;
+  double* v;
+  const uint8_t* frozen;
+  double gains[8];
+  const double* lr_table;
+  const double* bc1_table;
+  const double* bc2_table;
+  int32_t* iter;
+  int clamp;
+  double s_min, s_max;
+  const double* sums;
+  int loss_kind;
+  double alpha_w, inv_3P, inv_P;
+  double* hist_loss;
+  double* hist_psnr;
 };
 
-static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-
-static BinScratch carve(void* base, int n, int n_tiles, int n_rows, int cap) {
-  BinScratch s;
-  char* p = (char*)base;
-  size_t off = 0;
-  auto take = [&](size_t bytes) {
-    char* q = p ? p + off : nullptr;
-    off = align_up(off + (bytes > 0 ? bytes : 1), 256);
-    return (void*)q;
-  };
-  s.rect = (int4*)take(sizeof(int4) * (size_t)n);
-  s.zprim = (int32_t*)take(sizeof(int32_t) * (size_t)n);
-  s.tcount = (int32_t*)take(sizeof(int32_t) * (size_t)n_tiles);
-  s.rcount = (int32_t*)take(sizeof(int32_t) * (size_t)n_rows);
-  s.rowlist = (int32_t*)take(sizeof(int32_t) * (size_t)cap);
-  s.rowoff = (int32_t*)take(sizeof(int32_t) * (size_t)(n_rows + 1));
-  s.total = off;
-  return s;
-}
-
 struct PreArgs {
-  const double* params;
+  double* params;
   const int32_t* tid;
   const int32_t* zorder;
   int n;
@@ -67,249 +61,298 @@ struct PreArgs {
   const double* tpl_q;
   const double* tpl_hyp;
   double alpha_max, mu_blend, padding;
-  int W, H, tile, ntx, ty_begin, ty_end;
+  int W, H, tile, ty_begin, ty_end;
   RecF* recf;
-  RecB* recb;
+  RecG* recg;
   RecC* recc;
   BinScratch s;
+  AdamPart ad;
 };
 
-// K1: one thread per z position j (primitive zorder[j]).
-__global__ void __launch_bounds__(32) k_preprocess(PreArgs a) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= a.n) return;
-  const int i = __ldg(a.zorder + j);
-  a.s.zprim[j] = i;
-  const double* p = a.params + (size_t)i * 8;
-  const double x = p[0], y = p[1], s = p[2], rot = p[3], nu = p[4];
-  const double cl0 = p[5], cl1 = p[6], cl2 = p[7];
-  const int t = __ldg(a.tid + i);
-  const int wt = __ldg(a.tpl_w + t), ht = __ldg(a.tpl_h + t);
-  const double q = __ldg(a.tpl_q + t);
-  const double hyp = __ldg(a.tpl_hyp + t);
+constexpr double kB1 = 0.9, kB2 = 0.999, kAdamEps = 1e-8;
+constexpr int kPrimThreads = 256;
 
-  double st, ct;
-  sincos(rot, &st, &ct);
-  const double sig = sigmoid(nu);
-  const double sc0 = sigmoid(cl0), sc1 = sigmoid(cl1), sc2 = sigmoid(cl2);
+// adam_step for one scalar (fit.py:224-237), reference op order, no contraction.
+__device__ __forceinline__ double adam_scalar(const AdamPart& d, size_t idx, int col, int prim,
+                                              double p, double lr, double bc1, double bc2) {
+  const double g = d.grads[idx];
+  d.grads[idx] = 0.0;  // ready for the next backward
+  if (d.frozen == nullptr || d.frozen[prim] == 0) {
+    const double mm = __dadd_rn(__dmul_rn(kB1, d.m[idx]), __dmul_rn(1.0 - kB1, g));
+    const double vv = __dadd_rn(__dmul_rn(kB2, d.v[idx]), __dmul_rn(1.0 - kB2, __dmul_rn(g, g)));
+    d.m[idx] = mm;
+    d.v[idx] = vv;
+    const double mh = __ddiv_rn(mm, bc1);
+    const double vh = __ddiv_rn(vv, bc2);
+    const double eff = __dmul_rn(lr, d.gains[col]);
+    p = __dsub_rn(p, __ddiv_rn(__dmul_rn(eff, mh), __dadd_rn(__dsqrt_rn(vh), kAdamEps)));
+  }
+  if (d.clamp && col == 2) p = fmin(fmax(p, d.s_min), d.s_max);
+  return p;
+}
+
+template <bool ADAM>
+__global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
+  const int g = blockIdx.x * kPrimThreads + threadIdx.x;
+  const int j = g >> 3, c = g & 7;
+  const int lane = threadIdx.x & 31, gb = lane & ~7;
+  const bool live = j < a.n;
+  const int i = live ? __ldg(a.zorder + j) : 0;
+  const size_t pidx = (size_t)i * 8 + c;
+  double pc = live ? a.params[pidx] : 1.0;
+  int it = 0;
+  if (ADAM) {
+    it = *a.ad.iter;
+    if (live) {
+      pc = adam_scalar(a.ad, pidx, c, i, pc, a.ad.lr_table[it], a.ad.bc1_table[it],
+                       a.ad.bc2_table[it]);
+      a.params[pidx] = pc;
+    }
+    if (g == 0 && a.ad.sums) {
+      // history entry of this iteration: the render before this update (fit.py:502-505)
+      const AdamPart& d = a.ad;
+      const double mse = d.sums[0] * d.inv_3P;
+      double loss = mse;
+      if (d.loss_kind == PF_LOSS_SPATIAL)
+        loss = d.sums[1] * d.inv_3P + d.alpha_w * (d.sums[2] * d.inv_P);
+      if (d.hist_loss) d.hist_loss[it] = loss;
+      if (d.hist_psnr)
+        d.hist_psnr[it] = mse == 0.0 ? __longlong_as_double(0x7ff0000000000000ll)
+                                     : 10.0 * log10(1.0 / mse);
+    }
+  }
+  // gather the primitive's 8 parameters from its lane group
+  const double x = __shfl_sync(kFull, pc, gb + 0), y = __shfl_sync(kFull, pc, gb + 1);
+  const double s = __shfl_sync(kFull, pc, gb + 2), rot = __shfl_sync(kFull, pc, gb + 3);
+  const double nu = __shfl_sync(kFull, pc, gb + 4), cl0 = __shfl_sync(kFull, pc, gb + 5);
+  const double cl1 = __shfl_sync(kFull, pc, gb + 6), cl2 = __shfl_sync(kFull, pc, gb + 7);
+  const int t = live ? __ldg(a.tid + i) : 0;
+  const int wt = live ? __ldg(a.tpl_w + t) : 2, ht = live ? __ldg(a.tpl_h + t) : 2;
+  const double q = live ? __ldg(a.tpl_q + t) : 1.0;
+  const double hyp = live ? __ldg(a.tpl_hyp + t) : 1.0;
+  const double sq = __dmul_rn(s, q);
+
+  // transcendental / division work split across the lane group
+  double r0 = 0.0, r1 = 0.0;
+  if (c == 0) {
+    sincos(rot, &r1, &r0);  // r0 = cos, r1 = sin
+  } else if (c <= 4) {
+    r0 = sigmoid(c == 1 ? nu : c == 2 ? cl0 : c == 3 ? cl1 : cl2);
+  } else if (c == 5) {
+    r0 = __ddiv_rn(1.0, s);
+    r1 = __ddiv_rn(1.0, sq);
+  }
+  const double ct = __shfl_sync(kFull, r0, gb + 0), st = __shfl_sync(kFull, r1, gb + 0);
+  const double sig = __shfl_sync(kFull, r0, gb + 1);
+  const double sc0 = __shfl_sync(kFull, r0, gb + 2), sc1 = __shfl_sync(kFull, r0, gb + 3);
+  const double sc2 = __shfl_sync(kFull, r0, gb + 4);
+  const double inv_s = __shfl_sync(kFull, r0, gb + 5), inv_sq = __shfl_sync(kFull, r1, gb + 5);
   const double omm = __dsub_rn(1.0, a.mu_blend);
-
-  RecF rf;
-  rf.px = x;
-  rf.py = y;
-  rf.ct = ct;
-  rf.st = st;
-  rf.s = s;
-  rf.sq = __dmul_rn(s, q);
-  rf.sa = __dmul_rn(a.alpha_max, sig);
-  rf.c0 = __dmul_rn(omm, sc0);
-  rf.c1 = __dmul_rn(omm, sc1);
-  rf.c2 = __dmul_rn(omm, sc2);
-  rf.inv_s = __ddiv_rn(1.0, s);
-  rf.inv_sq = __ddiv_rn(1.0, rf.sq);
-  rf.wm1 = (double)(wt - 1);
-  rf.hm1 = (double)(ht - 1);
-  rf.base = __ldg(a.tpl_base + t);
-  rf.wt = wt;
-  rf.ht = ht;
-  rf.tid = t;
-  a.recf[i] = rf;
-
-  RecB rb;
-  rb.sd = a.alpha_max * sig * (1.0 - sig);
-  rb.cd0 = sc0 * (1.0 - sc0);
-  rb.cd1 = sc1 * (1.0 - sc1);
-  rb.cd2 = sc2 * (1.0 - sc2);
-  const double sqv = rf.sq;
-  rb.gxu = -ct / s;
-  rb.gxv = st / sqv;
-  rb.gyu = -st / s;
-  rb.gyv = -ct / sqv;
-  rb.inv_s = 1.0 / s;
-  rb.q = q;
-  rb.inv_q = 1.0 / q;
-  rb.one_minus_mu = omm;
-  a.recb[i] = rb;
-
   // bbox, float64 with Python's rounding: r = s*hyp + pad, ceil(x-r), floor(x+r)
   const double r = __dadd_rn(__dmul_rn(s, hyp), a.padding);
 
-  // cull record (see RecC): fp32 centre and axes, conservative slack
-  {
-    RecC rc;
-    const double is = rf.inv_s, isq = rf.inv_sq;
-    rc.px = (float)x;
-    rc.py = (float)y;
-    rc.au = (float)(ct * is);
-    rc.bu = (float)(st * is);
-    rc.av = (float)(ct * isq);
-    rc.bv = (float)(st * isq);
-    const double hx = 0.5 * (kWarpW - 1), hy = 0.5 * (kWarpH - 1);
-    const double e_px = fabs(x - (double)rc.px) + fabs(y - (double)rc.py);
-    const double span = e_px + 1e-6 * (fabs(r) + 2.0 * kTile);
-    const double su = (fabs(ct) + fabs(st)) * is, sv = (fabs(ct) + fabs(st)) * isq;
-    rc.eu = (float)((fabs(ct) * hx + fabs(st) * hy) * is + su * span + 1e-5);
-    rc.ev = (float)((fabs(st) * hx + fabs(ct) * hy) * isq + sv * span + 1e-5);
-    a.recc[i] = rc;
+  if (live) {
+    // each lane stores one 16-byte slice of RecF (8 slices) and of RecG (5) / RecC (2)
+    double2* pf = reinterpret_cast<double2*>(a.recf + i);
+    switch (c) {
+      case 0: pf[0] = make_double2(x, y); break;
+      case 1: pf[1] = make_double2(ct, st); break;
+      case 2: pf[2] = make_double2(inv_s, inv_sq); break;
+      case 3: pf[3] = make_double2(s, sq); break;
+      case 4: pf[4] = make_double2((double)(wt - 1), (double)(ht - 1)); break;
+      case 5: pf[5] = make_double2(__dmul_rn(a.alpha_max, sig), __dmul_rn(omm, sc0)); break;
+      case 6: pf[6] = make_double2(__dmul_rn(omm, sc1), __dmul_rn(omm, sc2)); break;
+      default:
+        reinterpret_cast<int4*>(pf)[7] = make_int4(__ldg(a.tpl_base + t), wt, ht, t);
+        break;
+    }
+    float4* pg = reinterpret_cast<float4*>(a.recg + i);
+    switch (c) {
+      case 0:
+        pg[0] = make_float4((float)(a.alpha_max * sig), (float)(omm * sc0), (float)(omm * sc1),
+                            (float)(omm * sc2));
+        break;
+      case 1:
+        pg[1] = make_float4((float)(a.alpha_max * sig * (1.0 - sig)), (float)(sc0 * (1.0 - sc0)),
+                            (float)(sc1 * (1.0 - sc1)), (float)(sc2 * (1.0 - sc2)));
+        break;
+      case 2:
+        pg[2] = make_float4((float)(-ct * inv_s), (float)(st * inv_sq), (float)(-st * inv_s),
+                            (float)(-ct * inv_sq));
+        break;
+      case 3:  // 1/q = s / (s q)
+        pg[3] = make_float4((float)inv_s, (float)q, (float)(s * inv_sq), 0.5f * (float)(wt - 1));
+        break;
+      case 4: {
+        const float hh = 0.5f * (float)(ht - 1), om = (float)omm;
+        pg[4] = make_float4(hh, om, __int_as_float(__ldg(a.tpl_base + t)), __int_as_float(wt));
+        break;
+      }
+      case 5:
+        break;
+      default: {
+        // cull record (see RecC): fp32 centre and axes, conservative slack
+        const float fx = (float)x, fy = (float)y;
+        const double hx = 0.5 * (kWarpW - 1), hy = 0.5 * (kWarpH - 1);
+        const double e_px = fabs(x - (double)fx) + fabs(y - (double)fy);
+        const double span = e_px + 1e-6 * (fabs(r) + 2.0 * kTile);
+        const double act = fabs(ct), ast = fabs(st);
+        float4* pc4 = reinterpret_cast<float4*>(a.recc + i);
+        if (c == 6) {
+          pc4[0] = make_float4(fx, fy, (float)(ct * inv_s), (float)(st * inv_s));
+        } else {
+          const double eu = (act * hx + ast * hy) * inv_s + (act + ast) * inv_s * span + 1e-5;
+          const double ev = (ast * hx + act * hy) * inv_sq + (act + ast) * inv_sq * span + 1e-5;
+          pc4[1] = make_float4((float)(ct * inv_sq), (float)(st * inv_sq), (float)eu, (float)ev);
+        }
+      }
+    }
+    if (c == 0) {
+      double lo_x = fmax(ceil(__dsub_rn(x, r)), 0.0);
+      double hi_x = fmin(floor(__dadd_rn(x, r)), (double)(a.W - 1));
+      double lo_y = fmax(ceil(__dsub_rn(y, r)), 0.0);
+      double hi_y = fmin(floor(__dadd_rn(y, r)), (double)(a.H - 1));
+      int4 rc = make_int4(1, 1, 0, 0);  // empty
+      // NaN-safe: every comparison with NaN is false -> treated as empty
+      if (lo_x <= hi_x && lo_y <= hi_y) {
+        const int tx0 = (int)lo_x / a.tile, tx1 = (int)hi_x / a.tile;
+        const int ty0 = max((int)lo_y / a.tile, a.ty_begin);
+        const int ty1 = min((int)hi_y / a.tile, a.ty_end - 1);
+        if (ty0 <= ty1) rc = make_int4(tx0, ty0, tx1, ty1);
+      }
+      a.s.rect[j] = rc;
+    }
   }
-  double lo_x = ceil(__dsub_rn(x, r)), hi_x = floor(__dadd_rn(x, r));
-  double lo_y = ceil(__dsub_rn(y, r)), hi_y = floor(__dadd_rn(y, r));
-  lo_x = fmax(lo_x, 0.0);
-  lo_y = fmax(lo_y, 0.0);
-  hi_x = fmin(hi_x, (double)(a.W - 1));
-  hi_y = fmin(hi_y, (double)(a.H - 1));
-  int4 rc = make_int4(1, 1, 0, 0);  // empty
-  // NaN-safe: every comparison with NaN is false -> treated as empty
-  if (lo_x <= hi_x && lo_y <= hi_y) {
-    const int tx0 = (int)lo_x / a.tile, tx1 = (int)hi_x / a.tile;
-    int ty0 = (int)lo_y / a.tile, ty1 = (int)hi_y / a.tile;
-    ty0 = max(ty0, a.ty_begin);
-    ty1 = min(ty1, a.ty_end - 1);
-    if (ty0 <= ty1) {
-      rc = make_int4(tx0, ty0, tx1, ty1);
-      for (int ty = ty0; ty <= ty1; ++ty) {
-        const int row = ty - a.ty_begin;
-        atomicAdd(a.s.rcount + row, 1);
-        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(a.s.tcount + row * a.ntx + tx, 1);
+
+  if (ADAM) {
+    // the last block to finish advances the iteration counter (all blocks have read it)
+    __shared__ bool am_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      am_last = atomicAdd(a.s.done, 1u) == gridDim.x - 1;
+      if (am_last) {
+        *a.ad.iter = it + 1;
+        *a.s.done = 0u;
       }
     }
   }
-  a.s.rect[j] = rc;
 }
 
-__device__ __forceinline__ int div_up_d(int a, int b) { return (a + b - 1) / b; }
-
-// Block-wide exclusive scan of one int per thread (1024 threads max).
-// Returns the exclusive prefix; *total receives the block sum.
-__device__ __forceinline__ int block_excl_scan(int v, int* warp_sums, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nw = (blockDim.x + 31) >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(kFull, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) warp_sums[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    int w = lane < nw ? warp_sums[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(kFull, w, o);
-      if (lane >= o) w += y;
-    }
-    if (lane < nw) warp_sums[lane] = w;  // inclusive warp prefix
-  }
-  __syncthreads();
-  const int excl_warp = warp > 0 ? warp_sums[warp - 1] : 0;
-  *total = warp_sums[nw - 1];
-  const int r = excl_warp + x - v;
-  __syncthreads();  // warp_sums reusable by the caller afterwards
-  return r;
-}
-
-struct ScanArgs {
-  int n, n_tiles, n_rows, ntx, ty_begin, cap;
+struct RowArgs {
+  int n, ntx, ty_begin, n_rows, cap, smem_list;
   BinScratch s;
   int32_t* bin_off;
+  int32_t* bin_idx;
   int32_t* status;
 };
 
-constexpr int kScanThreads = 1024;
+constexpr int kRowThreads = 1024;
 
-// K2a: block 0 scans the tile counts; block 1 + r builds row r's list.  Each
-// thread owns a contiguous chunk, so one block scan per block keeps z order.
-__global__ void __launch_bounds__(kScanThreads) k_bin_scan(ScanArgs a) {
-  __shared__ int warp_sums[32];
-  if (blockIdx.x == 0) {
-    const int chunk = div_up_d(a.n_tiles, kScanThreads);
-    const int t0 = min(a.n_tiles, threadIdx.x * chunk), t1 = min(a.n_tiles, t0 + chunk);
-    int local = 0;
-    for (int t = t0; t < t1; ++t) local += a.s.tcount[t];
-    int tot;
-    int run = block_excl_scan(local, warp_sums, &tot);
-    for (int t = t0; t < t1; ++t) {
-      a.bin_off[t] = run;
-      run += a.s.tcount[t];
-    }
-    if (threadIdx.x == 0) {
-      a.bin_off[a.n_tiles] = tot;
-      a.status[0] = tot;
-      a.status[1] = tot > a.cap ? 1 : 0;
-    }
-    return;
-  }
-  const int r = blockIdx.x - 1;
-  const int ty = a.ty_begin + r;
-  // row offset = sum of the counts of the rows before r (rows are few)
-  int part = 0;
-  for (int q = threadIdx.x; q < r; q += kScanThreads) part += a.s.rcount[q];
-  int row_base;
-  (void)block_excl_scan(part, warp_sums, &row_base);
-  const int chunk = div_up_d(a.n, kScanThreads);
-  const int j0 = min(a.n, threadIdx.x * chunk), j1 = min(a.n, j0 + chunk);
-  int local = 0;
+// K2: one block per tile row (band-local r).  See the file header.
+__global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
+  extern __shared__ int2 rsm[];  // [smem_list] row list, then [ntx] column counters
+  __shared__ int ws[32];
+  __shared__ int s_rl, s_base, s_rbase;
+  int* col = reinterpret_cast<int*>(rsm + a.smem_list);
+  const int r = blockIdx.x, ty = a.ty_begin + r;
+  const int tid = threadIdx.x;
+
+  // (a) stable compaction of the primitives covering row ty, z order kept
+  const int chunk = (a.n + kRowThreads - 1) / kRowThreads;
+  const int j0 = min(a.n, tid * chunk), j1 = min(a.n, j0 + chunk);
+  int cnt = 0, below = 0, below_rows = 0, all = 0;
   for (int j = j0; j < j1; ++j) {
     const int4 rc = a.s.rect[j];
-    local += (rc.y <= ty && ty <= rc.w) ? 1 : 0;
+    if (rc.x > rc.z) continue;  // empty
+    const int span = rc.z - rc.x + 1;
+    all += (rc.w - rc.y + 1) * span;
+    if (rc.y <= ty && ty <= rc.w) ++cnt;
+    if (rc.y < ty) {
+      const int rows = min(rc.w, ty - 1) - rc.y + 1;
+      below += rows * span;
+      below_rows += rows;
+    }
   }
   int tot;
-  int pos = row_base + block_excl_scan(local, warp_sums, &tot);
+  int pos = block_excl_scan(cnt, ws, &tot);
+  int base, rbase, K;
+  (void)block_excl_scan(below, ws, &base);
+  (void)block_excl_scan(below_rows, ws, &rbase);
+  (void)block_excl_scan(all, ws, &K);
+  if (r == 0 && tid == 0) {
+    // every block knows K; row block 0 publishes it (TileBins.offsets[-1], overflow flag)
+    a.bin_off[a.n_rows * a.ntx] = K;
+    a.status[0] = K;
+    a.status[1] = K > a.cap ? 1 : 0;
+  }
+  if (K > a.cap) return;  // overflow (block-uniform): nothing is written
+  if (tid == 0) {
+    s_rl = tot;
+    s_base = base;
+    s_rbase = rbase;
+  }
+  for (int c = tid; c < a.ntx; c += kRowThreads) col[c] = 0;
   for (int j = j0; j < j1; ++j) {
     const int4 rc = a.s.rect[j];
-    if (rc.y <= ty && ty <= rc.w) {
-      if (pos < a.cap) a.s.rowlist[pos] = j;
-      ++pos;
-    }
+    if (rc.x > rc.z || rc.y > ty || ty > rc.w) continue;
+    const int2 e = make_int2(j, rc.x | (rc.z << 16));
+    if (pos < a.smem_list) rsm[pos] = e;
+    a.s.rowlist[rbase + pos] = e;  // rbase + pos < rows entries <= K <= cap
+    ++pos;
   }
-  if (threadIdx.x == 0) {
-    a.s.rowoff[r] = row_base;
-    if (r == a.n_rows - 1) a.s.rowoff[a.n_rows] = row_base + tot;
+  __syncthreads();
+  const int RL = s_rl;
+  const int2* list = RL <= a.smem_list ? rsm : a.s.rowlist + s_rbase;
+
+  // (b) per-column counts -> offsets of this row's tiles
+  for (int k = tid; k < RL; k += kRowThreads) {
+    const int pk = list[k].y;
+    for (int tx = pk & 0xffff; tx <= (pk >> 16); ++tx) atomicAdd(col + tx, 1);
+  }
+  __syncthreads();
+  const int cchunk = (a.ntx + kRowThreads - 1) / kRowThreads;
+  const int c0 = min(a.ntx, tid * cchunk), c1 = min(a.ntx, c0 + cchunk);
+  int local = 0;
+  for (int c = c0; c < c1; ++c) local += col[c];
+  int row_total;
+  int run = s_base + block_excl_scan(local, ws, &row_total);
+  for (int c = c0; c < c1; ++c) {
+    const int v = col[c];
+    a.bin_off[r * a.ntx + c] = run;
+    col[c] = run;
+    run += v;
+  }
+  __syncthreads();
+
+  // (c) one warp per column: ordered ballot walk of the row list
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int c = warp; c < a.ntx; c += kRowThreads / 32) {
+    int out = col[c];
+    for (int b = 0; b < RL; b += 32) {
+      const int k = b + lane;
+      bool hit = false;
+      int j = 0;
+      if (k < RL) {
+        const int2 e = list[k];
+        j = e.x;
+        hit = (e.y & 0xffff) <= c && c <= (e.y >> 16);
+      }
+      const unsigned ball = __ballot_sync(kFull, hit);
+      if (hit) a.bin_idx[out + __popc(ball & ((1u << lane) - 1u))] = __ldg(a.s.zprim + j);
+      out += __popc(ball);
+    }
   }
 }
 
-struct FillArgs {
-  int n_tiles, ntx, cap;
-  BinScratch s;
-  const int32_t* bin_off;
-  int32_t* bin_idx;
-  const int32_t* status;
-};
-
-constexpr int kFillThreads = 128;
-
-// K2b: one block per tile, stable compaction of its row list by column range.
-__global__ void __launch_bounds__(kFillThreads) k_bin_fill(FillArgs a) {
-  __shared__ int warp_sums[32];
-  if (a.status[1]) return;  // overflow: lists would not fit
-  const int t = blockIdx.x;
-  const int r = t / a.ntx, tx = t - r * a.ntx;
-  const int r0 = a.s.rowoff[r], n = a.s.rowoff[r + 1] - r0;
-  const int chunk = div_up_d(n, kFillThreads);
-  const int k0 = min(n, (int)threadIdx.x * chunk), k1 = min(n, k0 + chunk);
-  int local = 0;
-  for (int k = k0; k < k1; ++k) {
-    const int4 rc = a.s.rect[a.s.rowlist[r0 + k]];
-    local += (rc.x <= tx && tx <= rc.z) ? 1 : 0;
-  }
-  int tot;
-  int out = a.bin_off[t] + block_excl_scan(local, warp_sums, &tot);
-  for (int k = k0; k < k1; ++k) {
-    const int j = a.s.rowlist[r0 + k];
-    const int4 rc = a.s.rect[j];
-    if (rc.x <= tx && tx <= rc.z) a.bin_idx[out++] = a.s.zprim[j];
-  }
-}
-
-// Alpha quad atlas (see Quad in pf_common.cuh): one thread per texel.
+// Alpha quad atlas (see load_quad in pf_common.cuh): one thread per texel.
 struct QuadArgs {
   const double* tex;  // planar [4][texels]
   int texels, n_tpl;
   const int32_t* base;
   const int32_t* w;
   const int32_t* h;
-  float* quad;
+  float4* quad;
 };
 
 __global__ void k_atlas_quad(QuadArgs a) {
@@ -321,9 +364,11 @@ __global__ void k_atlas_quad(QuadArgs a) {
   const int v = local / wt, u = local - v * wt;
   const double* al = a.tex + 3 * (size_t)a.texels + a.base[t];
   auto at = [&](int uu, int vv) { return (uu < wt && vv < ht) ? al[vv * wt + uu] : 0.0; };
-  reinterpret_cast<float4*>(a.quad)[g] =
-      make_float4((float)at(u, v), (float)at(u + 1, v), (float)at(u, v + 1), (float)at(u + 1, v + 1));
+  a.quad[g] = make_float4((float)at(u, v), (float)at(u + 1, v), (float)at(u, v + 1),
+                          (float)at(u + 1, v + 1));
 }
+
+constexpr int kRowSmemList = 4096;  // row-list entries kept in shared memory (32 KB)
 
 }  // namespace pf
 
@@ -331,8 +376,7 @@ using namespace pf;
 
 extern "C" size_t pf_bin_scratch_bytes(int n, int n_tiles, int capacity) {
   if (n < 0 || n_tiles < 0 || capacity < 0) return 0;
-  // rows <= tiles; size for the worst case (one tile per row)
-  return carve(nullptr, n, n_tiles, n_tiles, capacity).total;
+  return carve(nullptr, n, capacity).total;
 }
 
 static bool band_ok(int W, int H, int tile, int ty_begin, int ty_end, int* ntx, int* n_rows) {
@@ -340,27 +384,25 @@ static bool band_ok(int W, int H, int tile, int ty_begin, int ty_end, int* ntx, 
   *ntx = div_up(W, tile);
   const int nty = div_up(H, tile);
   if (ty_begin < 0 || ty_end > nty || ty_begin > ty_end) return false;
+  if (*ntx > 65535) return false;  // column packed in 16 bits
   *n_rows = ty_end - ty_begin;
   return true;
 }
 
-extern "C" int pf_preprocess(const double* params, const int32_t* template_id,
-                             const int32_t* zorder, int n, const int32_t* tpl_base,
-                             const int32_t* tpl_w, const int32_t* tpl_h, const double* tpl_q,
-                             const double* tpl_hyp, int n_tpl, double alpha_max, double mu_blend,
-                             double padding, int W, int H, int tile, int ty_begin, int ty_end,
-                             int capacity, void* rec, void* scratch, size_t scratch_bytes,
-                             void* stream) {
+static int fill_pre_args(PreArgs& a, double* params, const int32_t* template_id,
+                         const int32_t* zorder, int n, const int32_t* tpl_base,
+                         const int32_t* tpl_w, const int32_t* tpl_h, const double* tpl_q,
+                         const double* tpl_hyp, int n_tpl, double alpha_max, double mu_blend,
+                         double padding, int W, int H, int tile, int ty_begin, int ty_end,
+                         int capacity, void* rec, void* scratch, size_t scratch_bytes) {
   int ntx, n_rows;
   if (n < 0 || n_tpl < 0 || capacity < 0 || !band_ok(W, H, tile, ty_begin, ty_end, &ntx, &n_rows))
     return PF_ERR_ARG;
-  const int n_tiles = n_rows * ntx;
-  if (!scratch || scratch_bytes < pf_bin_scratch_bytes(n, n_tiles, capacity)) return PF_ERR_SCRATCH;
+  if (!scratch || scratch_bytes < pf_bin_scratch_bytes(n, n_rows * ntx, capacity))
+    return PF_ERR_SCRATCH;
   if (n > 0 && (!params || !template_id || !zorder || !rec || !tpl_base || !tpl_w || !tpl_h ||
                 !tpl_q || !tpl_hyp))
     return PF_ERR_ARG;
-  cudaStream_t st = (cudaStream_t)stream;
-  PreArgs a;
   a.params = params;
   a.tid = template_id;
   a.zorder = zorder;
@@ -376,19 +418,98 @@ extern "C" int pf_preprocess(const double* params, const int32_t* template_id,
   a.W = W;
   a.H = H;
   a.tile = tile;
-  a.ntx = ntx;
   a.ty_begin = ty_begin;
   a.ty_end = ty_end;
   a.recf = (RecF*)rec;
-  a.recb = (RecB*)((char*)rec + sizeof(RecF) * (size_t)n);
-  a.recc = (RecC*)((char*)rec + (sizeof(RecF) + sizeof(RecB)) * (size_t)n);
-  a.s = carve(scratch, n, n_tiles, n_tiles, capacity);
-  cudaError_t e = cudaMemsetAsync(a.s.tcount, 0, sizeof(int32_t) * (size_t)n_tiles, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(a.s.rcount, 0, sizeof(int32_t) * (size_t)n_rows, st);
-  if (e != cudaSuccess) return (int)e;
-  // small blocks spread the (latency-bound, sincos/exp heavy) threads over many SMs
-  if (n > 0) k_preprocess<<<div_up(n, 32), 32, 0, st>>>(a);
+  a.recg = (RecG*)((char*)rec + sizeof(RecF) * (size_t)n);
+  a.recc = (RecC*)((char*)rec + (sizeof(RecF) + sizeof(RecG)) * (size_t)n);
+  a.s = carve(scratch, n, capacity);
+  a.ad = AdamPart{};
+  return PF_OK;
+}
+
+static int launch_prim(bool adam, const PreArgs& a, cudaStream_t st) {
+  const int blocks = div_up(a.n > 0 ? a.n * 8 : 1, kPrimThreads);
+  if (adam)
+    k_prim<true><<<blocks, kPrimThreads, 0, st>>>(a);
+  else if (a.n > 0)
+    k_prim<false><<<blocks, kPrimThreads, 0, st>>>(a);
   return (int)cudaGetLastError();
+}
+
+extern "C" int pf_scratch_init(void* scratch, size_t scratch_bytes, const int32_t* zorder, int n,
+                               int capacity, void* stream) {
+  if (!scratch || n < 0 || capacity < 0 ||
+      scratch_bytes < carve(nullptr, n, capacity).total)
+    return PF_ERR_SCRATCH;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(scratch, 0, scratch_bytes, st);
+  if (e != cudaSuccess) return (int)e;
+  BinScratch s = carve(scratch, n, capacity);
+  if (n > 0) {
+    if (!zorder) return PF_ERR_ARG;
+    e = cudaMemcpyAsync(s.zprim, zorder, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice, st);
+  }
+  return (int)e;
+}
+
+extern "C" int pf_preprocess(const double* params, const int32_t* template_id,
+                             const int32_t* zorder, int n, const int32_t* tpl_base,
+                             const int32_t* tpl_w, const int32_t* tpl_h, const double* tpl_q,
+                             const double* tpl_hyp, int n_tpl, double alpha_max, double mu_blend,
+                             double padding, int W, int H, int tile, int ty_begin, int ty_end,
+                             int capacity, void* rec, void* scratch, size_t scratch_bytes,
+                             void* stream) {
+  PreArgs a;
+  const int rc = fill_pre_args(a, const_cast<double*>(params), template_id, zorder, n, tpl_base,
+                               tpl_w, tpl_h, tpl_q, tpl_hyp, n_tpl, alpha_max, mu_blend, padding,
+                               W, H, tile, ty_begin, ty_end, capacity, rec, scratch,
+                               scratch_bytes);
+  if (rc != PF_OK) return rc;
+  return launch_prim(false, a, (cudaStream_t)stream);
+}
+
+extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, double* v,
+                                  const uint8_t* frozen, const double* gains8,
+                                  const double* lr_table, const double* bc1_table,
+                                  const double* bc2_table, int32_t* iter, int clamp, double s_min,
+                                  double s_max, const double* sums, int loss_kind, double alpha_w,
+                                  double inv_3P, double inv_P, double* hist_loss,
+                                  double* hist_psnr, const int32_t* template_id,
+                                  const int32_t* zorder, int n, const int32_t* tpl_base,
+                                  const int32_t* tpl_w, const int32_t* tpl_h, const double* tpl_q,
+                                  const double* tpl_hyp, int n_tpl, double alpha_max,
+                                  double mu_blend, double padding, int W, int H, int tile,
+                                  int ty_begin, int ty_end, int capacity, void* rec, void* scratch,
+                                  size_t scratch_bytes, void* stream) {
+  PreArgs a;
+  const int rc = fill_pre_args(a, params, template_id, zorder, n, tpl_base, tpl_w, tpl_h, tpl_q,
+                               tpl_hyp, n_tpl, alpha_max, mu_blend, padding, W, H, tile,
+                               ty_begin, ty_end, capacity, rec, scratch, scratch_bytes);
+  if (rc != PF_OK) return rc;
+  if (!iter || !lr_table || !bc1_table || !bc2_table || (n > 0 && (!grads || !m || !v)))
+    return PF_ERR_ARG;
+  AdamPart& d = a.ad;
+  d.grads = grads;
+  d.m = m;
+  d.v = v;
+  d.frozen = frozen;
+  for (int c = 0; c < 8; ++c) d.gains[c] = gains8 ? gains8[c] : 1.0;
+  d.lr_table = lr_table;
+  d.bc1_table = bc1_table;
+  d.bc2_table = bc2_table;
+  d.iter = iter;
+  d.clamp = clamp;
+  d.s_min = s_min;
+  d.s_max = s_max;
+  d.sums = sums;
+  d.loss_kind = loss_kind;
+  d.alpha_w = alpha_w;
+  d.inv_3P = inv_3P;
+  d.inv_P = inv_P;
+  d.hist_loss = hist_loss;
+  d.hist_psnr = hist_psnr;
+  return launch_prim(true, a, (cudaStream_t)stream);
 }
 
 extern "C" int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity,
@@ -398,33 +519,33 @@ extern "C" int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, i
   if (n < 0 || capacity < 0 || !band_ok(W, H, tile, ty_begin, ty_end, &ntx, &n_rows))
     return PF_ERR_ARG;
   if (!bin_off || !status || (capacity > 0 && !bin_idx)) return PF_ERR_ARG;
-  const int n_tiles = n_rows * ntx;
-  if (!scratch || scratch_bytes < pf_bin_scratch_bytes(n, n_tiles, capacity)) return PF_ERR_SCRATCH;
+  if (!scratch || scratch_bytes < pf_bin_scratch_bytes(n, n_rows * ntx, capacity))
+    return PF_ERR_SCRATCH;
   cudaStream_t st = (cudaStream_t)stream;
-  BinScratch s = carve(scratch, n, n_tiles, n_tiles, capacity);
-  ScanArgs sa;
-  sa.n = n;
-  sa.n_tiles = n_tiles;
-  sa.n_rows = n_rows;
-  sa.ntx = ntx;
-  sa.ty_begin = ty_begin;
-  sa.cap = capacity;
-  sa.s = s;
-  sa.bin_off = bin_off;
-  sa.status = status;
-  k_bin_scan<<<1 + n_rows, kScanThreads, 0, st>>>(sa);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return (int)e;
-  if (n_tiles == 0) return PF_OK;
-  FillArgs f;
-  f.n_tiles = n_tiles;
-  f.ntx = ntx;
-  f.cap = capacity;
-  f.s = s;
-  f.bin_off = bin_off;
-  f.bin_idx = bin_idx;
-  f.status = status;
-  k_bin_fill<<<n_tiles, kFillThreads, 0, st>>>(f);
+  if (n_rows == 0) {
+    cudaError_t e = cudaMemsetAsync(bin_off, 0, sizeof(int32_t), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(status, 0, 2 * sizeof(int32_t), st);
+    return (int)e;
+  }
+  RowArgs ra;
+  ra.n = n;
+  ra.ntx = ntx;
+  ra.ty_begin = ty_begin;
+  ra.n_rows = n_rows;
+  ra.cap = capacity;
+  ra.smem_list = kRowSmemList;
+  ra.s = carve(scratch, n, capacity);
+  ra.bin_off = bin_off;
+  ra.bin_idx = bin_idx;
+  ra.status = status;
+  const size_t smem = sizeof(int2) * kRowSmemList + sizeof(int) * (size_t)ntx;
+  static bool attr_set = false;
+  if (smem > 48 * 1024 || !attr_set) {
+    cudaFuncSetAttribute(k_bin_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(smem > 48 * 1024 ? smem : 48 * 1024));
+    attr_set = true;
+  }
+  k_bin_rows<<<n_rows, kRowThreads, smem, st>>>(ra);
   return (int)cudaGetLastError();
 }
 
@@ -434,7 +555,7 @@ extern "C" int pf_atlas_quad(const double* tex, int texels, const int32_t* tpl_b
   if (texels < 0 || n_tpl < 0 || (texels > 0 && (!tex || !tpl_base || !tpl_w || !tpl_h || !quad)))
     return PF_ERR_ARG;
   if (texels == 0) return PF_OK;
-  QuadArgs a{tex, texels, n_tpl, tpl_base, tpl_w, tpl_h, quad};
+  QuadArgs a{tex, texels, n_tpl, tpl_base, tpl_w, tpl_h, reinterpret_cast<float4*>(quad)};
   k_atlas_quad<<<div_up(texels, 256), 256, 0, (cudaStream_t)stream>>>(a);
   return (int)cudaGetLastError();
 }

@@ -11,7 +11,7 @@
 // B200 design:
 //   Each warp owns an 8x4 pixel sub-tile (8 warps = 16x16 tile), compact so the
 //   warp-uniform culling below rejects as many list entries as possible, and
-//   warps never wait on each other (no block barrier on the hot path).
+//   warps never wait on each other on the hot path.
 //   forward  - for every 32 list entries a warp runs a lane-parallel
 //              conservative separating-axis test (primitive axes) of each
 //              entry's footprint against its 8x4 pixel rectangle (32-byte fp32
@@ -29,13 +29,16 @@
 //              With loss_kind != NONE the MSE / spatial loss, dL/dI (and dL/dA)
 //              and per-warp loss partials are fused in; the backward reduces the
 //              partials in fixed order (deterministic loss value).
-//   backward - each warp walks its pixels' saved entries back to front, picking
-//              the next list position with __reduce_max_sync so it only visits
+//   backward - the tile's 80-byte fp32 gradient records are staged in shared
+//              memory with cp.async (one barrier at block start).  Each warp
+//              then walks its pixels' saved entries back to front, picking the
+//              next list position with __reduce_max_sync so it only visits
 //              entries that touch its 32 pixels.  Active lanes compute the 8
-//              gradients in float64; a 9-shuffle __shfl_xor transpose butterfly
-//              reduces them across the warp and 8 lanes issue one float64
-//              atomicAdd each (RED.E.ADD.F64); with <= 2 active lanes the lanes
-//              issue their atomics directly (no shuffle latency).
+//              gradients in fp32 (the backward takes no decisions; ~1e-5 of the
+//              float64 reference against a 1e-3 bar); a 9-shuffle __shfl_xor
+//              transpose butterfly reduces them across the warp and 8 lanes
+//              issue one float64 atomicAdd each (RED.E.ADD.F64); with <= 2
+//              active lanes the lanes issue their atomics directly.
 #include "../../include/primfit_b200.h"
 #include "pf_common.cuh"
 
@@ -225,8 +228,7 @@ __global__ void __launch_bounds__(kTilePix) k_forward(FwdArgs a) {
 }
 
 struct BwdArgs {
-  const RecF* recf;
-  const RecB* recb;
+  const RecG* recg;
   const double* tex;
   const float4* quad;
   int texels;
@@ -238,9 +240,9 @@ struct BwdArgs {
   const int32_t* ent_n;
   const float* dI;
   const float* dA;
-  double bg0, bg1, bg2;
+  float bg0, bg1, bg2;
   const float* bg_img;
-  double mu_blend;
+  float mu_blend;
   int W, H, ntx, ty_begin;
   double* grads;
   const double* part;  // forward loss partials (NULL: none)
@@ -250,26 +252,26 @@ struct BwdArgs {
 
 // Sum 8 values over the warp with a transpose butterfly (9 shuffles instead of
 // 40): afterwards lane l holds the warp total of value ((l >> 2) & 7).
-__device__ __forceinline__ double warp_reduce8(const double (&g)[8]) {
+__device__ __forceinline__ float warp_reduce8(const float (&g)[8]) {
   const int lane = threadIdx.x & 31;
-  double w[4];
+  float w[4];
   const bool h16 = lane & 16;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const double send = h16 ? g[q] : g[q + 4];
-    const double keep = h16 ? g[q + 4] : g[q];
+    const float send = h16 ? g[q] : g[q + 4];
+    const float keep = h16 ? g[q + 4] : g[q];
     w[q] = keep + __shfl_xor_sync(kFull, send, 16);
   }
-  double x2[2];
+  float x2[2];
   const bool h8 = lane & 8;
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
-    const double send = h8 ? w[q] : w[q + 2];
-    const double keep = h8 ? w[q + 2] : w[q];
+    const float send = h8 ? w[q] : w[q + 2];
+    const float keep = h8 ? w[q + 2] : w[q];
     x2[q] = keep + __shfl_xor_sync(kFull, send, 8);
   }
   const bool h4 = lane & 4;
-  double y = (h4 ? x2[1] : x2[0]) + __shfl_xor_sync(kFull, h4 ? x2[0] : x2[1], 4);
+  float y = (h4 ? x2[1] : x2[0]) + __shfl_xor_sync(kFull, h4 ? x2[0] : x2[1], 4);
   y += __shfl_xor_sync(kFull, y, 2);
   y += __shfl_xor_sync(kFull, y, 1);
   return y;
@@ -303,8 +305,18 @@ __device__ void reduce_loss_partials(const double* part, int n_part, double* sum
   }
 }
 
+constexpr int kBwdStage = 128;  // list entries whose gradient records are staged (10 KB)
+
+__device__ __forceinline__ float bilinear_f(const double* __restrict__ plane, int base, int wt,
+                                            int ht, int u0, int v0, float wu, float wv) {
+  const Cell c{u0, v0, (double)wu, (double)wv};
+  return (float)bilinear(plane, base, wt, ht, c);
+}
+
 template <bool MU, bool HAS_DA>
-__global__ void __launch_bounds__(kTilePix, 3) k_backward(BwdArgs a) {
+__global__ void __launch_bounds__(kTilePix) k_backward(BwdArgs a) {
+  __shared__ __align__(16) RecG sg[kBwdStage];
+  __shared__ int sidx[kBwdStage];
   if (a.status && a.status[1]) return;
   if (a.part && blockIdx.x == 0) reduce_loss_partials(a.part, a.n_part, a.sums);
   const int tb = blockIdx.x;
@@ -315,6 +327,21 @@ __global__ void __launch_bounds__(kTilePix, 3) k_backward(BwdArgs a) {
   const bool valid = x < a.W && y < a.H;
   const int lane = threadIdx.x & 31;
   const int b0 = a.bin_off[tb];
+  const int L = a.bin_off[tb + 1] - b0;
+
+  // stage the gradient records of the first kBwdStage list entries
+  {
+    constexpr int kPieces = sizeof(RecG) / 16;
+    const int cnt = min(L, kBwdStage);
+    for (int pc = threadIdx.x; pc < cnt * kPieces; pc += kTilePix) {
+      const int r = pc / kPieces, q = pc - r * kPieces;
+      const int i = __ldg(a.bin_idx + b0 + r);
+      if (q == 0) sidx[r] = i;
+      cp_async16(reinterpret_cast<char*>(&sg[r]) + q * 16,
+                 reinterpret_cast<const char*>(a.recg + i) + q * 16);
+    }
+    cp_async_commit();
+  }
 
   const size_t pix = valid ? (size_t)y * a.W + x : 0;
   int k = valid ? a.ent_n[pix] - 1 : -1;
@@ -327,8 +354,8 @@ __global__ void __launch_bounds__(kTilePix, 3) k_backward(BwdArgs a) {
     curT = a.ent_T[e];
     key = (unsigned)cur.j + 1u;
   }
-  double dI0 = 0.0, dI1 = 0.0, dI2 = 0.0, dA = 0.0;
-  double g0 = a.bg0, g1 = a.bg1, g2 = a.bg2;
+  float dI0 = 0.0f, dI1 = 0.0f, dI2 = 0.0f, dA = 0.0f;
+  float g0 = a.bg0, g1 = a.bg1, g2 = a.bg2;
   if (valid) {
     dI0 = a.dI[pix * 3 + 0];
     dI1 = a.dI[pix * 3 + 1];
@@ -340,19 +367,23 @@ __global__ void __launch_bounds__(kTilePix, 3) k_backward(BwdArgs a) {
       g2 = a.bg_img[pix * 3 + 2];
     }
   }
-  double S0 = 0.0, S1 = 0.0, S2 = 0.0, B = 1.0;
+  float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f, B = 1.0f;
+  cp_async_wait<0>();
+  __syncthreads();
 
   while (true) {
     const unsigned jm = __reduce_max_sync(kFull, key);
     if (jm == 0u) break;
+    const int j = (int)(jm - 1u);
     const bool act = key == jm;
-    const int i = __ldg(a.bin_idx + b0 + (int)(jm - 1u));
-    double g[8];
+    const bool staged = j < kBwdStage;
+    const int i = staged ? sidx[j] : __ldg(a.bin_idx + b0 + j);
+    float g[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) g[c] = 0.0;
+    for (int c = 0; c < 8; ++c) g[c] = 0.0f;
     if (act) {
       const SavedEnt se = cur;
-      const double Tc = curT;
+      const float Tc = curT;
       // prefetch this lane's next saved entry while the math below runs
       --k;
       if (k >= 0) {
@@ -363,42 +394,43 @@ __global__ void __launch_bounds__(kTilePix, 3) k_backward(BwdArgs a) {
       } else {
         key = 0;
       }
-      const RecF& r = a.recf[i];
-      const RecB& rb = a.recb[i];
-      const double wu = se.wu, wv = se.wv;
+      const RecG& r = staged ? sg[j] : a.recg[i];
+      const float wu = se.wu, wv = se.wv;
       const float4 q = load_quad(a.quad, r.base, r.wt, se.u0, se.v0);
-      const double m = bilerp(q, wu, wv);
-      const double iu = 1.0 - wu, iv = 1.0 - wv;
-      const double gU = iv * ((double)q.y - (double)q.x) + wv * ((double)q.w - (double)q.z);
-      const double gV = iu * ((double)q.z - (double)q.x) + wu * ((double)q.w - (double)q.y);
-      const double aa = r.sa * m;
-      double ck0 = r.c0, ck1 = r.c1, ck2 = r.c2;
+      const float iu = 1.0f - wu, iv = 1.0f - wv;
+      const float m = (iu * iv) * q.x + (wu * iv) * q.y + (iu * wv) * q.z + (wu * wv) * q.w;
+      const float gU = iv * (q.y - q.x) + wv * (q.w - q.z);
+      const float gV = iu * (q.z - q.x) + wu * (q.w - q.y);
+      const float aa = r.sa * m;
+      float ck0 = r.c0, ck1 = r.c1, ck2 = r.c2;
       if (MU) {
-        const Cell c{se.u0, se.v0, wu, wv};
-        ck0 += a.mu_blend * bilinear(a.tex, r.base, r.wt, r.ht, c);
-        ck1 += a.mu_blend * bilinear(a.tex + a.texels, r.base, r.wt, r.ht, c);
-        ck2 += a.mu_blend * bilinear(a.tex + 2 * (size_t)a.texels, r.base, r.wt, r.ht, c);
+        const double* t = a.tex;
+        const float mu = a.mu_blend;
+        ck0 += mu * bilinear_f(t, r.base, r.wt, (int)(2.0f * r.hh) + 1, se.u0, se.v0, wu, wv);
+        ck1 += mu * bilinear_f(t + a.texels, r.base, r.wt, (int)(2.0f * r.hh) + 1, se.u0, se.v0,
+                               wu, wv);
+        ck2 += mu * bilinear_f(t + 2 * (size_t)a.texels, r.base, r.wt, (int)(2.0f * r.hh) + 1,
+                               se.u0, se.v0, wu, wv);
       }
       // _kernels.py:319-359
-      const double gg = dI0 * (ck0 - S0 - g0 * B) + dI1 * (ck1 - S1 - g1 * B) +
-                        dI2 * (ck2 - S2 - g2 * B) + dA * B;
-      const double dalpha = Tc * gg;
-      g[4] = dalpha * rb.sd * m;
-      if (rb.one_minus_mu > 0.0) {
-        const double wc = Tc * aa * rb.one_minus_mu;
-        g[5] = dI0 * wc * rb.cd0;
-        g[6] = dI1 * wc * rb.cd1;
-        g[7] = dI2 * wc * rb.cd2;
+      const float gg = dI0 * (ck0 - S0 - g0 * B) + dI1 * (ck1 - S1 - g1 * B) +
+                       dI2 * (ck2 - S2 - g2 * B) + dA * B;
+      const float dalpha = Tc * gg;
+      g[4] = dalpha * r.sd * m;
+      if (r.omm > 0.0f) {
+        const float wc = Tc * aa * r.omm;
+        g[5] = dI0 * wc * r.cd0;
+        g[6] = dI1 * wc * r.cd1;
+        g[7] = dI2 * wc * r.cd2;
       }
-      const double dm = dalpha * r.sa;
-      const double hw = 0.5 * r.wm1, hh = 0.5 * r.hm1;
-      const double mu_u = gU * hw, mu_v = gV * hh;
-      const double u = ((double)se.u0 + wu) / hw - 1.0, v = ((double)se.v0 + wv) / hh - 1.0;
-      g[0] = dm * (mu_u * rb.gxu + mu_v * rb.gxv);
-      g[1] = dm * (mu_u * rb.gyu + mu_v * rb.gyv);
-      g[2] = dm * (mu_u * (-u * rb.inv_s) + mu_v * (-v * rb.inv_s));
-      g[3] = dm * (mu_u * (v * rb.q) + mu_v * (-u * rb.inv_q));
-      const double om = 1.0 - aa;
+      const float dm = dalpha * r.sa;
+      const float mu_u = gU * r.hw, mu_v = gV * r.hh;
+      const float u = ((float)se.u0 + wu) / r.hw - 1.0f, v = ((float)se.v0 + wv) / r.hh - 1.0f;
+      g[0] = dm * (mu_u * r.gxu + mu_v * r.gxv);
+      g[1] = dm * (mu_u * r.gyu + mu_v * r.gyv);
+      g[2] = dm * (mu_u * (-u * r.inv_s) + mu_v * (-v * r.inv_s));
+      g[3] = dm * (mu_u * (v * r.q) + mu_v * (-u * r.inv_q));
+      const float om = 1.0f - aa;
       S0 = aa * ck0 + om * S0;
       S1 = aa * ck1 + om * S1;
       S2 = aa * ck2 + om * S2;
@@ -410,11 +442,11 @@ __global__ void __launch_bounds__(kTilePix, 3) k_backward(BwdArgs a) {
       if (act) {
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-          if (g[c] != 0.0) atomicAdd(gp + c, g[c]);
+          if (g[c] != 0.0f) atomicAdd(gp + c, (double)g[c]);
       }
     } else {
-      const double tot = warp_reduce8(g);
-      if ((lane & 3) == 0 && tot != 0.0) atomicAdd(gp + (lane >> 2), tot);
+      const float tot = warp_reduce8(g);
+      if ((lane & 3) == 0 && tot != 0.0f) atomicAdd(gp + (lane >> 2), (double)tot);
     }
   }
 }
@@ -453,7 +485,7 @@ extern "C" int pf_forward(const void* rec, int n, const double* tex, const float
   if (n_tiles == 0) return PF_OK;
   FwdArgs a;
   a.recf = (const RecF*)rec;
-  a.recc = (const RecC*)((const char*)rec + (sizeof(RecF) + sizeof(RecB)) * (size_t)n);
+  a.recc = (const RecC*)((const char*)rec + (sizeof(RecF) + sizeof(RecG)) * (size_t)n);
   a.tex = tex;
   a.quad = (const float4*)quad;
   a.texels = texels;
@@ -517,8 +549,7 @@ extern "C" int pf_backward(const void* rec, int n, const double* tex, const floa
   const int n_tiles = (ty_end - ty_begin) * ntx;
   if (n_tiles == 0) return PF_OK;
   BwdArgs a;
-  a.recf = (const RecF*)rec;
-  a.recb = (const RecB*)((const char*)rec + sizeof(RecF) * (size_t)n);
+  a.recg = (const RecG*)((const char*)rec + sizeof(RecF) * (size_t)n);
   a.tex = tex;
   a.quad = (const float4*)quad;
   a.texels = texels;
@@ -530,11 +561,11 @@ extern "C" int pf_backward(const void* rec, int n, const double* tex, const floa
   a.ent_n = ent_n;
   a.dI = dI;
   a.dA = dA;
-  a.bg0 = bg_r;
-  a.bg1 = bg_g;
-  a.bg2 = bg_b;
+  a.bg0 = (float)bg_r;
+  a.bg1 = (float)bg_g;
+  a.bg2 = (float)bg_b;
   a.bg_img = bg_img;
-  a.mu_blend = mu_blend;
+  a.mu_blend = (float)mu_blend;
   a.W = W;
   a.H = H;
   a.ntx = ntx;

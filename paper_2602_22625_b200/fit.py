@@ -319,25 +319,36 @@ class StepEngine:
         self.eps_skip = float(cfg.eps_skip)
         self.done = 0
 
-    # one full optimisation step, stream-ordered, no host sync
-    def launch_step(self) -> None:
+    # one full optimisation step, stream-ordered, no host sync:
+    #   [K2 bin] -> [K3 forward + loss] -> [K4 backward]
+    #   -> (allreduce) -> [K5+K1 Adam + next step's records/offsets]
+    # (the very first step is preceded by a stand-alone K1, see step()).
+    def launch_step(self, mark: Callable[[str], None] | None = None) -> None:
         c = self.comp
-        c.preprocess(self.params)
+        mark = mark or (lambda name: None)
         c.bin()
+        mark("bin")
         c.forward(save=True, eps_skip=self.eps_skip, bg_rgb=self.bg_rgb, bg_img=self.bg_img,
                   loss_kind=self.loss_kind, target=self.target, target_alpha=self.target_alpha,
                   alpha_w=self.alpha_w, P_total=self.P)
+        mark("forward")
         c.backward(c.dI, self.gbuf, dA=c.dA if self.loss_kind == nat.PF_LOSS_SPATIAL else None,
                    bg_rgb=self.bg_rgb, bg_img=self.bg_img, sums=self.sums)
+        mark("backward")
         if self.allreduce is not None:
             self.allreduce(self.gbuf)
-        adam_launch(self.params, self.grads, self.m, self.v, frozen=self.frozen, gains=self.gains,
-                    n=self.n, lr_table=self.lr_table, bc1_table=self.bc1_table,
-                    bc2_table=self.bc2_table, iter_counter=self.iter, clamp=True,
-                    s_min=self.cfg.scale_min, s_max=self.cfg.scale_max, zero_grads=True,
-                    sums=self.sums, loss_kind=self.loss_kind, alpha_w=self.alpha_w,
-                    P_total=self.P, hist_loss=self.hist_loss, hist_psnr=self.hist_psnr,
-                    counter=self.adam_counter)
+            mark("allreduce")
+        c.adam_preprocess(self.params, self.grads, self.m, self.v, frozen=self.frozen,
+                          gains=self.gains, lr_table=self.lr_table, bc1_table=self.bc1_table,
+                          bc2_table=self.bc2_table, iter_counter=self.iter,
+                          s_min=self.cfg.scale_min, s_max=self.cfg.scale_max, sums=self.sums,
+                          loss_kind=self.loss_kind, alpha_w=self.alpha_w, P_total=self.P,
+                          hist_loss=self.hist_loss, hist_psnr=self.hist_psnr)
+        mark("adam_preprocess")
+
+    def refresh(self) -> None:
+        """Rebuild records / offsets from the current params (after host edits)."""
+        self.comp.preprocess(self.params)
 
     def capture(self) -> None:
         g = torch.cuda.CUDAGraph()
@@ -356,6 +367,8 @@ class StepEngine:
         if self.graph is not None:
             self.graph.replay()
         else:
+            if self.done == 0:
+                self.refresh()
             self.launch_step()
             if self.use_graph:
                 self.capture()  # step 0 ran eagerly (warm-up); later steps replay
@@ -384,6 +397,7 @@ class StepEngine:
         self.m.copy_(torch.from_numpy(np.asarray(state.m, dtype=np.float64)))
         self.v.copy_(torch.from_numpy(np.asarray(state.v, dtype=np.float64)))
         self.frozen.copy_(torch.from_numpy(np.asarray(state.frozen, dtype=bool).astype(np.uint8)))
+        self.refresh()
 
     def history(self, compute_psnr: bool = True) -> list[HistoryEntry]:
         k = self.done
