@@ -184,11 +184,12 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
         pg[3] = make_float4((float)inv_s, (float)q, (float)(s * inv_sq), 0.5f * (float)(wt - 1));
         break;
       case 4: {
-        const float hh = 0.5f * (float)(ht - 1), om = (float)omm;
-        pg[4] = make_float4(hh, om, __int_as_float(__ldg(a.tpl_base + t)), __int_as_float(wt));
+        const double hw = 0.5 * (double)(wt - 1), hh = 0.5 * (double)(ht - 1);
+        pg[4] = make_float4((float)hh, (float)(1.0 / hw), (float)(1.0 / hh), (float)omm);
         break;
       }
       case 5:
+        reinterpret_cast<int4*>(pg)[5] = make_int4(__ldg(a.tpl_base + t), wt, ht, 0);
         break;
       default: {
         // cull record (see RecC): fp32 centre and axes, conservative slack

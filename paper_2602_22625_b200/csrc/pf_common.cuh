@@ -41,10 +41,10 @@ struct __align__(16) RecG {
   float sd, cd0, cd1, cd2;    // alpha_max*sig*(1-sig), sc*(1-sc)
   float gxu, gxv, gyu, gyv;   // -ct/s, st/(s q), -st/s, -ct/(s q)
   float inv_s, q, inv_q, hw;  // 1/s, aspect, 1/aspect, 0.5 (wt - 1)
-  float hh, omm;              // 0.5 (ht - 1), 1 - mu_blend
-  int32_t base, wt;           // template atlas slot
+  float hh, inv_hw, inv_hh, omm;  // 0.5 (ht - 1), 1/hw, 1/hh, 1 - mu_blend
+  int32_t base, wt, ht, pad;  // template atlas slot
 };
-static_assert(sizeof(RecG) == 80, "RecG must be 80 bytes");
+static_assert(sizeof(RecG) == 96, "RecG must be 96 bytes");
 
 // Cull record (32 bytes, fp32): just what the warp-level footprint test needs,
 // so testing 32 list entries costs two 16-byte loads per lane.
@@ -60,15 +60,48 @@ static_assert(sizeof(RecC) == 32, "RecC must be 32 bytes");
 // Warp sub-tile shape (8 warps cover a 16x16 tile) -- used by the cull record.
 constexpr int kWarpW = 8, kWarpH = 4;
 
-// Saved forward entry (16 bytes, one 128-bit store / load): list position j,
-// texel cell (u0, v0) and fp32 bilinear weights.  The entry's incoming
-// transmittance T (the reference's Tbuf) is kept in a parallel fp32 array.
+// Saved forward entry (16 bytes, one 128-bit store / load): list position j
+// (16 bits), texel cell u0, v0 (16 bits each), bilinear weights wu, wv as
+// 24-bit fixed point (2^-24 = fp32 resolution on [0, 1)) and the incoming
+// transmittance T (the reference's Tbuf, _kernels.py:294-297) as fp32:
+//   w0 = j | u0 << 16,  w1 = v0 | wu[23:8] << 16,  w2 = wu[7:0] | wv << 8,  w3 = T
 struct __align__(16) SavedEnt {
-  uint16_t j;
-  int16_t u0, v0;
-  uint16_t pad;
-  float wu, wv;
+  uint32_t w0, w1, w2;
+  float T;
 };
+
+__device__ __forceinline__ uint32_t to_fix24(double w) {
+  const double q = w * 16777216.0 + 0.5;
+  return (uint32_t)(q >= 16777215.0 ? 16777215.0 : (q < 0.0 ? 0.0 : q));
+}
+
+__device__ __forceinline__ SavedEnt pack_saved(int j, int u0, int v0, double wu, double wv,
+                                              double T) {
+  const uint32_t qu = to_fix24(wu), qv = to_fix24(wv);
+  SavedEnt s;
+  s.w0 = (uint32_t)(j & 0xffff) | ((uint32_t)(u0 & 0xffff) << 16);
+  s.w1 = (uint32_t)(v0 & 0xffff) | ((qu >> 8) << 16);
+  s.w2 = (qu & 0xffu) | (qv << 8);
+  s.T = (float)T;
+  return s;
+}
+
+struct SavedView {
+  int j, u0, v0;
+  float wu, wv, T;
+};
+
+__device__ __forceinline__ SavedView unpack_saved(const SavedEnt& s) {
+  SavedView v;
+  v.j = (int)(s.w0 & 0xffffu);
+  v.u0 = (int)(int16_t)(s.w0 >> 16);
+  v.v0 = (int)(int16_t)(s.w1 & 0xffffu);
+  const uint32_t qu = ((s.w1 >> 16) << 8) | (s.w2 & 0xffu);
+  v.wu = (float)qu * (1.0f / 16777216.0f);
+  v.wv = (float)(s.w2 >> 8) * (1.0f / 16777216.0f);
+  v.T = s.T;
+  return v;
+}
 static_assert(sizeof(SavedEnt) == 16, "SavedEnt must be 16 bytes");
 
 // Stable two-branch logistic, _kernels.py:27-32.

@@ -22,14 +22,14 @@
 //              load, no bounds checks; the eps decision is re-taken on the
 //              float64 plane when within rounding).  T and C are float64.
 //              Saved state: per contributing (pixel, entry) one 16-byte record
-//              (list position, texel cell, bilinear weights) plus its incoming
-//              T (the reference's Tbuf) in a parallel fp32 array, at slot
+//              (list position, texel cell, unorm16 bilinear weights, incoming
+//              T = the reference's Tbuf, _kernels.py:294-297) at slot
 //              256*bin_off[t] + k*256 + pixel (k = the pixel's contribution
 //              ordinal): single pass, coalesced within a warp.
 //              With loss_kind != NONE the MSE / spatial loss, dL/dI (and dL/dA)
 //              and per-warp loss partials are fused in; the backward reduces the
 //              partials in fixed order (deterministic loss value).
-//   backward - the tile's 80-byte fp32 gradient records are staged in shared
+//   backward - the tile's 96-byte fp32 gradient records are staged in shared
 //              memory with cp.async (one barrier at block start).  Each warp
 //              then walks its pixels' saved entries back to front, picking the
 //              next list position with __reduce_max_sync so it only visits
@@ -83,7 +83,6 @@ struct FwdArgs {
   double bg0, bg1, bg2;
   const float* bg_img;
   SavedEnt* ent;
-  float* ent_T;
   int32_t* ent_n;
   float* img;
   float* alpha;
@@ -146,16 +145,7 @@ __global__ void __launch_bounds__(kTilePix) k_forward(FwdArgs a) {
         cb += a.mu_blend * bilinear(a.tex + 2 * (size_t)a.texels, r.base, r.wt, r.ht, c);
       }
       if (SAVE) {
-        SavedEnt s;
-        s.j = (uint16_t)(sub + bit);
-        s.u0 = (int16_t)c.u0;
-        s.v0 = (int16_t)c.v0;
-        s.pad = 0;
-        s.wu = (float)c.wu;
-        s.wv = (float)c.wv;
-        const size_t e = e0 + (size_t)nsave * kTilePix;
-        a.ent[e] = s;
-        a.ent_T[e] = (float)T;
+        a.ent[e0 + (size_t)nsave * kTilePix] = pack_saved(sub + bit, c.u0, c.v0, c.wu, c.wv, T);
         ++nsave;
       }
       const double Ta = T * aa;
@@ -236,7 +226,6 @@ struct BwdArgs {
   const int32_t* bin_idx;
   const int32_t* status;
   const SavedEnt* ent;
-  const float* ent_T;
   const int32_t* ent_n;
   const float* dI;
   const float* dA;
@@ -305,7 +294,7 @@ __device__ void reduce_loss_partials(const double* part, int n_part, double* sum
   }
 }
 
-constexpr int kBwdStage = 128;  // list entries whose gradient records are staged (10 KB)
+constexpr int kBwdStage = 128;  // list entries whose gradient records are staged (12 KB)
 
 __device__ __forceinline__ float bilinear_f(const double* __restrict__ plane, int base, int wt,
                                             int ht, int u0, int v0, float wu, float wv) {
@@ -348,11 +337,9 @@ __global__ void __launch_bounds__(kTilePix) k_backward(BwdArgs a) {
   size_t e = (size_t)b0 * kTilePix + threadIdx.x + (size_t)(k > 0 ? k : 0) * kTilePix;
   unsigned key = 0;
   SavedEnt cur{};
-  float curT = 0.0f;
   if (k >= 0) {
     cur = a.ent[e];
-    curT = a.ent_T[e];
-    key = (unsigned)cur.j + 1u;
+    key = (cur.w0 & 0xffffu) + 1u;
   }
   float dI0 = 0.0f, dI1 = 0.0f, dI2 = 0.0f, dA = 0.0f;
   float g0 = a.bg0, g1 = a.bg1, g2 = a.bg2;
@@ -382,19 +369,22 @@ __global__ void __launch_bounds__(kTilePix) k_backward(BwdArgs a) {
 #pragma unroll
     for (int c = 0; c < 8; ++c) g[c] = 0.0f;
     if (act) {
-      const SavedEnt se = cur;
-      const float Tc = curT;
+      const SavedView se = unpack_saved(cur);
+      const float Tc = se.T;
       // prefetch this lane's next saved entry while the math below runs
       --k;
       if (k >= 0) {
         e -= kTilePix;
         cur = a.ent[e];
-        curT = a.ent_T[e];
-        key = (unsigned)cur.j + 1u;
+        key = (cur.w0 & 0xffffu) + 1u;
       } else {
         key = 0;
       }
-      const RecG& r = staged ? sg[j] : a.recg[i];
+      RecG r;
+      if (staged)
+        r = sg[j];
+      else
+        r = a.recg[i];
       const float wu = se.wu, wv = se.wv;
       const float4 q = load_quad(a.quad, r.base, r.wt, se.u0, se.v0);
       const float iu = 1.0f - wu, iv = 1.0f - wv;
@@ -406,11 +396,9 @@ __global__ void __launch_bounds__(kTilePix) k_backward(BwdArgs a) {
       if (MU) {
         const double* t = a.tex;
         const float mu = a.mu_blend;
-        ck0 += mu * bilinear_f(t, r.base, r.wt, (int)(2.0f * r.hh) + 1, se.u0, se.v0, wu, wv);
-        ck1 += mu * bilinear_f(t + a.texels, r.base, r.wt, (int)(2.0f * r.hh) + 1, se.u0, se.v0,
-                               wu, wv);
-        ck2 += mu * bilinear_f(t + 2 * (size_t)a.texels, r.base, r.wt, (int)(2.0f * r.hh) + 1,
-                               se.u0, se.v0, wu, wv);
+        ck0 += mu * bilinear_f(t, r.base, r.wt, r.ht, se.u0, se.v0, wu, wv);
+        ck1 += mu * bilinear_f(t + a.texels, r.base, r.wt, r.ht, se.u0, se.v0, wu, wv);
+        ck2 += mu * bilinear_f(t + 2 * (size_t)a.texels, r.base, r.wt, r.ht, se.u0, se.v0, wu, wv);
       }
       // _kernels.py:319-359
       const float gg = dI0 * (ck0 - S0 - g0 * B) + dI1 * (ck1 - S1 - g1 * B) +
@@ -425,7 +413,8 @@ __global__ void __launch_bounds__(kTilePix) k_backward(BwdArgs a) {
       }
       const float dm = dalpha * r.sa;
       const float mu_u = gU * r.hw, mu_v = gV * r.hh;
-      const float u = ((float)se.u0 + wu) / r.hw - 1.0f, v = ((float)se.v0 + wv) / r.hh - 1.0f;
+      const float u = ((float)se.u0 + wu) * r.inv_hw - 1.0f;
+      const float v = ((float)se.v0 + wv) * r.inv_hh - 1.0f;
       g[0] = dm * (mu_u * r.gxu + mu_v * r.gxv);
       g[1] = dm * (mu_u * r.gyu + mu_v * r.gyv);
       g[2] = dm * (mu_u * (-u * r.inv_s) + mu_v * (-v * r.inv_s));
@@ -455,9 +444,9 @@ __global__ void __launch_bounds__(kTilePix) k_backward(BwdArgs a) {
 
 using namespace pf;
 
-// Saved-state layout: [entries] SavedEnt, then [entries] float T.
+// Saved-state layout: [entries] SavedEnt (16 B).
 extern "C" size_t pf_saved_bytes(int capacity) {
-  return (size_t)pf_saved_capacity(capacity) * (sizeof(SavedEnt) + sizeof(float));
+  return (size_t)pf_saved_capacity(capacity) * sizeof(SavedEnt);
 }
 
 extern "C" int pf_forward(const void* rec, int n, const double* tex, const float* quad,
@@ -503,7 +492,6 @@ extern "C" int pf_forward(const void* rec, int n, const double* tex, const float
   a.bg2 = bg_b;
   a.bg_img = bg_img;
   a.ent = (SavedEnt*)saved;
-  a.ent_T = save ? (float*)((SavedEnt*)saved + saved_entries) : nullptr;
   a.ent_n = ent_n;
   a.img = img;
   a.alpha = alpha;
@@ -557,7 +545,6 @@ extern "C" int pf_backward(const void* rec, int n, const double* tex, const floa
   a.bin_idx = bin_idx;
   a.status = status;
   a.ent = (const SavedEnt*)saved;
-  a.ent_T = (const float*)((const SavedEnt*)saved + saved_entries);
   a.ent_n = ent_n;
   a.dI = dI;
   a.dA = dA;
