@@ -143,10 +143,14 @@ int pf_adam_preprocess(double* params, double* grads, double* m, double* v, cons
  *   bin_idx  out [capacity]           (TileBins.indices; first K valid)
  *   status   out int32[4]: [0] = K (total entries), [1] = overflow flag (K > capacity;
  *            nothing else is written then)
+ *   rec, bin_cull  optional: with the records of pf_preprocess, also gather each
+ *            entry's 32-byte cull record in bin order into bin_cull [capacity]
+ *            (pf_forward then culls with coalesced loads); both NULL to skip
  */
 int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity,
            void* scratch, size_t scratch_bytes,
-           int32_t* bin_off, int32_t* bin_idx, int32_t* status, void* stream);
+           int32_t* bin_off, int32_t* bin_idx, int32_t* status,
+           const void* rec, void* bin_cull, void* stream);
 
 /*
  * K3 — tiled front-to-back forward (16x16 tiles), optionally saving the
@@ -156,32 +160,30 @@ int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity
  * loss_spatial (fit.py:112-151).
  *   tex        [4][texels] planar float64 atlas (RGB planes read when mu_blend > 0)
  *   quad       float32 [texels][4] alpha quad atlas from pf_atlas_quad
- *   bg_img     float32 [H][W][3] per-pixel background, or NULL for solid (bg_r,bg_g,bg_b)
+ *   bin_cull   gathered cull records from pf_bin, or NULL
+ *   bg4        float32 [H*W][4] per-pixel background (rgb, unused), or NULL for
+ *              the solid (bg_r, bg_g, bg_b)
  *   saved      saved state (NULL = render only): pf_saved_bytes(capacity) bytes
  *              holding saved_entries = pf_saved_capacity(capacity) 16-byte
  *              entries (list position j, texel cell, bilinear weights, incoming
  *              transmittance T -- the reference's Tbuf, _kernels.py:294-297);
  *              ent_n int32 [H*W] per-pixel contribution counts
- *   img        out float32 [H][W][3]; alpha out float32 [H][W] (band rows written)
- *   target     float32 [H][W][3]; target_alpha float32 [H][W] (SPATIAL only)
- *   dI         out float32 [H][W][3] = dL/dI; dA out float32 [H][W] (SPATIAL)
+ *   img4       out float32 [H*W][4] = (r, g, b, alpha) (band rows written)
+ *   tgt4       float32 [H*W][4] = (target r, g, b, target alpha); alpha read by SPATIAL
+ *   d4         out float32 [H*W][4] = (dL/dI r, g, b, dL/dA)
  *   part       out float64 [n_band_tiles * 8 * 3]: per-warp loss partials
  *              (sum (I-t)^2, sum ((I-t)*mask)^2, sum (I_a - t_a)^2), reduced in
  *              fixed order by pf_backward (deterministic loss value)
- *   counter, sums  unused (pass NULL); kept for ABI stability
  *   inv_3P, inv_P  1/(3*H*W), 1/(H*W) of the FULL canvas (band-independent)
  */
 int pf_forward(const void* rec, int n, const double* tex, const float* quad, int texels,
                const int32_t* bin_off, const int32_t* bin_idx, const int32_t* status,
-               int W, int H, int ty_begin, int ty_end,
+               const void* bin_cull, int W, int H, int ty_begin, int ty_end,
                double eps_skip, double mu_blend,
-               double bg_r, double bg_g, double bg_b, const float* bg_img,
-               void* saved, long long saved_entries, int32_t* ent_n,
-               float* img, float* alpha,
-               int loss_kind, const float* target, const float* target_alpha, double alpha_w,
-               double inv_3P, double inv_P,
-               float* dI, float* dA, double* part, uint32_t* counter, double* sums,
-               void* stream);
+               double bg_r, double bg_g, double bg_b, const float* bg4,
+               void* saved, long long saved_entries, int32_t* ent_n, float* img4,
+               int loss_kind, const float* tgt4, double alpha_w, double inv_3P, double inv_P,
+               float* d4, double* part, void* stream);
 
 /*
  * K4 — backward: back-to-front over each pixel's saved contributions,
@@ -189,7 +191,7 @@ int pf_forward(const void* rec, int n, const double* tex, const float* quad, int
  * before float64 atomics into grads.
  * Replaces: backward_tiles + reduce_partials (_kernels.py:258-363,
  * grad.py:134-206).  grads is ACCUMULATED into (caller zeroes it).
- *   dI float32 [H][W][3] (dL/dI), dA float32 [H][W] or NULL (dL/dA = 0)
+ *   d4     float32 [H*W][4] = (dL/dI r, g, b, dL/dA)
  *   grads  float64 [n][8], columns as params
  *   part   the forward's per-warp loss partials (or NULL); when given, block 0
  *          also reduces them in fixed order into sums[3] (loss value + psnr input)
@@ -197,8 +199,7 @@ int pf_forward(const void* rec, int n, const double* tex, const float* quad, int
 int pf_backward(const void* rec, int n, const double* tex, const float* quad, int texels,
                 const int32_t* bin_off, const int32_t* bin_idx, const int32_t* status,
                 const void* saved, long long saved_entries, const int32_t* ent_n,
-                const float* dI, const float* dA,
-                double bg_r, double bg_g, double bg_b, const float* bg_img,
+                const float* d4, double bg_r, double bg_g, double bg_b, const float* bg4,
                 double mu_blend, int W, int H, int ty_begin, int ty_end,
                 double* grads, const double* part, double* sums, void* stream);
 

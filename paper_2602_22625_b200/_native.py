@@ -51,15 +51,15 @@ SIGNATURES: dict[str, tuple] = {
          _P],
     ),
     "pf_atlas_quad": (_I, [_P, _I, _P, _P, _P, _I, _P, _P]),
-    "pf_bin": (_I, [_I, _I, _I, _I, _I, _I, _I, _P, _Z, _P, _P, _P, _P]),
+    "pf_bin": (_I, [_I, _I, _I, _I, _I, _I, _I, _P, _Z, _P, _P, _P, _P, _P, _P]),
     "pf_forward": (
         _I,
-        [_P, _I, _P, _P, _I, _P, _P, _P, _I, _I, _I, _I, _D, _D, _D, _D, _D, _P,
-         _P, C.c_longlong, _P, _P, _P, _I, _P, _P, _D, _D, _D, _P, _P, _P, _P, _P, _P],
+        [_P, _I, _P, _P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _D, _D, _D, _D, _D, _P,
+         _P, C.c_longlong, _P, _P, _I, _P, _D, _D, _D, _P, _P, _P],
     ),
     "pf_backward": (
         _I,
-        [_P, _I, _P, _P, _I, _P, _P, _P, _P, C.c_longlong, _P, _P, _P, _D, _D, _D, _P, _D,
+        [_P, _I, _P, _P, _I, _P, _P, _P, _P, C.c_longlong, _P, _P, _D, _D, _D, _P, _D,
          _I, _I, _I, _I, _P, _P, _P, _P],
     ),
     "pf_adam": (

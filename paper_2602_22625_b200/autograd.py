@@ -25,18 +25,15 @@ from .raster import DEFAULT_EPS_SKIP
 
 class _Composite(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, params, renderer: "Renderer", bg_img):
+    def forward(ctx, params, renderer: "Renderer", bg4):
         comp = renderer._new_compositor(params)
         comp.preprocess(params)
         comp.bin()
-        comp.forward(save=True, eps_skip=renderer.eps_skip, bg_rgb=renderer.bg_rgb, bg_img=bg_img)
+        comp.forward(save=True, eps_skip=renderer.eps_skip, bg_rgb=renderer.bg_rgb, bg4=bg4)
         ctx.comp = comp
         ctx.renderer = renderer
-        ctx.bg_img = bg_img
-        H, W = renderer.H, renderer.W
-        img = comp.img.view(H, W, 3).clone()
-        alpha = comp.alpha.view(H, W).clone()
-        return img, alpha
+        ctx.bg4 = bg4
+        return comp.color().clone(), comp.alpha().clone()
 
     @staticmethod
     def backward(ctx, d_img, d_alpha):
@@ -44,11 +41,12 @@ class _Composite(torch.autograd.Function):
         r = ctx.renderer
         n = comp.n
         grads = torch.zeros(n * 8 + 4, dtype=torch.float64, device=comp.device)
-        if d_img is None:
-            d_img = torch.zeros(r.H, r.W, 3, dtype=torch.float32, device=comp.device)
-        dI = d_img.to(torch.float32).contiguous().view(-1)
-        dA = None if d_alpha is None else d_alpha.to(torch.float32).contiguous().view(-1)
-        comp.backward(dI, grads, dA=dA, bg_rgb=r.bg_rgb, bg_img=ctx.bg_img)
+        d4 = torch.zeros(r.H, r.W, 4, dtype=torch.float32, device=comp.device)
+        if d_img is not None:
+            d4[:, :, :3] = d_img
+        if d_alpha is not None:
+            d4[:, :, 3] = d_alpha
+        comp.backward(d4.view(-1), grads, bg_rgb=r.bg_rgb, bg4=ctx.bg4)
         return grads[: n * 8].view(n, 8), None, None
 
 
@@ -84,8 +82,12 @@ class Renderer:
                           device=self.dev, d_tid=self.d_tid, d_zorder=self.d_zorder)
 
     def __call__(self, params: torch.Tensor, bg_img: torch.Tensor | None = None):
+        """Render; ``bg_img`` (H, W, 3) is an optional per-pixel background."""
         if params.dtype != torch.float64 or params.shape != (len(self.tid), 8):
             raise ValueError(f"params must be float64 ({len(self.tid)}, 8)")
+        bg4 = None
         if bg_img is not None:
-            bg_img = bg_img.to(device=self.dev, dtype=torch.float32).contiguous().view(-1)
-        return _Composite.apply(params.contiguous(), self, bg_img)
+            bg4 = torch.zeros(self.H, self.W, 4, dtype=torch.float32, device=self.dev)
+            bg4[:, :, :3] = bg_img.to(device=self.dev, dtype=torch.float32)
+            bg4 = bg4.view(-1)
+        return _Composite.apply(params.contiguous(), self, bg4)

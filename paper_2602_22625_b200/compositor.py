@@ -137,29 +137,38 @@ class Compositor:
                                            _stream_handle()), "pf_scratch_init")
         self.bin_off = torch.zeros(self.n_tiles + 1, dtype=torch.int32, device=dev)
         self.bin_idx = torch.zeros(max(self.capacity, 1), dtype=torch.int32, device=dev)
+        # optional gather of cull records in bin order (pf_bin/pf_forward bin_cull):
+        # measured slower end to end at c3 (the gather costs more in K2 than the
+        # coalesced cull saves in K3), so it is off
+        self.bin_cull = None
         self.status = torch.zeros(4, dtype=torch.int32, device=dev)
         self._saved_alloc = False
 
     # -- buffers for rendering (allocated lazily; binning-only users skip them)
-    def alloc_render(self, save: bool, loss: bool = False, spatial: bool = False):
+    def alloc_render(self, save: bool, loss: bool = False):
         if self.tile != RENDER_TILE:
             raise ValueError(f"render kernels need bin tile {RENDER_TILE}, got {self.tile}")
         dev, P = self.device, self.W * self.H
-        if not hasattr(self, "img"):
-            self.img = torch.empty(P * 3, dtype=torch.float32, device=dev)
-            self.alpha = torch.empty(P, dtype=torch.float32, device=dev)
+        if not hasattr(self, "img4"):
+            # (r, g, b, alpha) per pixel: one 16-byte store
+            self.img4 = torch.zeros(P * 4, dtype=torch.float32, device=dev)
         if save and not self._saved_alloc:
             self.saved_entries = int(self.lib.pf_saved_capacity(max(self.capacity, 1)))
             nbytes = int(self.lib.pf_saved_bytes(max(self.capacity, 1)))
             self.saved = torch.empty(nbytes, dtype=torch.uint8, device=dev)
             self.ent_n = torch.zeros(P, dtype=torch.int32, device=dev)
             self._saved_alloc = True
-        if loss and not hasattr(self, "dI"):
-            self.dI = torch.empty(P * 3, dtype=torch.float32, device=dev)
+        if loss and not hasattr(self, "d4"):
+            # (dL/dI r, g, b, dL/dA) per pixel
+            self.d4 = torch.zeros(P * 4, dtype=torch.float32, device=dev)
             # per-warp loss partials (8 warps per tile, 3 sums each)
             self.part = torch.zeros(max(self.n_tiles, 1) * 8 * 3, dtype=torch.float64, device=dev)
-        if spatial and not hasattr(self, "dA"):
-            self.dA = torch.empty(P, dtype=torch.float32, device=dev)
+
+    def color(self) -> torch.Tensor:
+        return self.img4.view(self.H, self.W, 4)[:, :, :3]
+
+    def alpha(self) -> torch.Tensor:
+        return self.img4.view(self.H, self.W, 4)[:, :, 3]
 
     # -- K1 + K2
     def preprocess(self, params: torch.Tensor, stream=None) -> None:
@@ -203,6 +212,7 @@ class Compositor:
                             self.band.ty_end, self.capacity, self.scratch.data_ptr(),
                             self.scratch_bytes, self.bin_off.data_ptr(),
                             self.bin_idx.data_ptr(), self.status.data_ptr(),
+                            self.rec.data_ptr(), nat.ptr(self.bin_cull),
                             _stream_handle(stream)),
             "pf_bin")
 
@@ -215,33 +225,33 @@ class Compositor:
 
     # -- K3
     def forward(self, *, save: bool, eps_skip: float, bg_rgb=(1.0, 1.0, 1.0),
-                bg_img: torch.Tensor | None = None, loss_kind: int = nat.PF_LOSS_NONE,
-                target: torch.Tensor | None = None, target_alpha: torch.Tensor | None = None,
-                alpha_w: float = 0.0, P_total: int | None = None, stream=None) -> None:
-        spatial = loss_kind == nat.PF_LOSS_SPATIAL
-        self.alloc_render(save, loss_kind != nat.PF_LOSS_NONE, spatial)
+                bg4: torch.Tensor | None = None, loss_kind: int = nat.PF_LOSS_NONE,
+                tgt4: torch.Tensor | None = None, alpha_w: float = 0.0,
+                P_total: int | None = None, stream=None) -> None:
+        lossy = loss_kind != nat.PF_LOSS_NONE
+        self.alloc_render(save, lossy)
         P = float(P_total if P_total is not None else self.W * self.H)
         p = nat.ptr
-        lossy = loss_kind != nat.PF_LOSS_NONE
         nat.check(
             self.lib.pf_forward(
                 self.rec.data_ptr(), self.n, self.atlas.tex.data_ptr(),
                 self.atlas.quad.data_ptr(), self.atlas.texels,
                 self.bin_off.data_ptr(), self.bin_idx.data_ptr(), self.status.data_ptr(),
-                self.W, self.H, self.band.ty_begin, self.band.ty_end, float(eps_skip),
-                self.mu_blend, float(bg_rgb[0]), float(bg_rgb[1]), float(bg_rgb[2]), p(bg_img),
-                p(self.saved) if save else None, self.saved_entries if save else 0,
-                p(self.ent_n) if save else None, self.img.data_ptr(), self.alpha.data_ptr(),
-                int(loss_kind), p(target), p(target_alpha), float(alpha_w), 1.0 / (3.0 * P),
-                1.0 / P, p(self.dI) if lossy else None, p(self.dA) if spatial else None,
-                p(self.part) if lossy else None, None, None, _stream_handle(stream)),
+                p(self.bin_cull), self.W, self.H, self.band.ty_begin, self.band.ty_end,
+                float(eps_skip), self.mu_blend, float(bg_rgb[0]), float(bg_rgb[1]),
+                float(bg_rgb[2]), p(bg4), p(self.saved) if save else None,
+                self.saved_entries if save else 0, p(self.ent_n) if save else None,
+                self.img4.data_ptr(), int(loss_kind), p(tgt4), float(alpha_w),
+                1.0 / (3.0 * P), 1.0 / P, p(self.d4) if lossy else None,
+                p(self.part) if lossy else None, _stream_handle(stream)),
             "pf_forward")
 
     # -- K4
-    def backward(self, dI: torch.Tensor, grads: torch.Tensor, *, dA: torch.Tensor | None = None,
-                 bg_rgb=(1.0, 1.0, 1.0), bg_img: torch.Tensor | None = None,
-                 sums: torch.Tensor | None = None, stream=None) -> None:
-        """K4; with ``sums`` also folds the fused loss partials of the last forward."""
+    def backward(self, d4: torch.Tensor, grads: torch.Tensor, *, bg_rgb=(1.0, 1.0, 1.0),
+                 bg4: torch.Tensor | None = None, sums: torch.Tensor | None = None,
+                 stream=None) -> None:
+        """K4 on d4 = (dL/dI, dL/dA) per pixel; with ``sums`` it also folds the fused
+        loss partials of the last forward."""
         p = nat.ptr
         nat.check(
             self.lib.pf_backward(
@@ -249,11 +259,21 @@ class Compositor:
                 self.atlas.quad.data_ptr(), self.atlas.texels,
                 self.bin_off.data_ptr(), self.bin_idx.data_ptr(), self.status.data_ptr(),
                 self.saved.data_ptr(), self.saved_entries, self.ent_n.data_ptr(),
-                dI.data_ptr(), p(dA), float(bg_rgb[0]), float(bg_rgb[1]), float(bg_rgb[2]),
-                p(bg_img), self.mu_blend, self.W, self.H, self.band.ty_begin,
-                self.band.ty_end, grads.data_ptr(),
-                p(self.part) if sums is not None else None, p(sums), _stream_handle(stream)),
+                d4.data_ptr(), float(bg_rgb[0]), float(bg_rgb[1]), float(bg_rgb[2]), p(bg4),
+                self.mu_blend, self.W, self.H, self.band.ty_begin, self.band.ty_end,
+                grads.data_ptr(), p(self.part) if sums is not None else None, p(sums),
+                _stream_handle(stream)),
             "pf_backward")
+
+
+def pixels4(rgb: np.ndarray, w: np.ndarray | float | None = None) -> np.ndarray:
+    """(H, W, 3) (+ optional (H, W) fourth channel) -> float32 (H*W*4) for the kernels."""
+    rgb = np.asarray(rgb, dtype=np.float32)
+    out = np.zeros(rgb.shape[:2] + (4,), dtype=np.float32)
+    out[..., :3] = rgb
+    if w is not None:
+        out[..., 3] = np.asarray(w, dtype=np.float32)
+    return out.reshape(-1)
 
 
 def adam_launch(params, grads, m, v, *, frozen=None, gains=None, n: int,

@@ -246,6 +246,8 @@ struct RowArgs {
   int32_t* bin_off;
   int32_t* bin_idx;
   int32_t* status;
+  const RecC* recc;  // per-primitive cull records (NULL: no gather)
+  RecC* bin_cull;    // out: cull records gathered in bin order (coalesced forward cull)
 };
 
 constexpr int kRowThreads = 1024;
@@ -340,7 +342,12 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
         hit = (e.y & 0xffff) <= c && c <= (e.y >> 16);
       }
       const unsigned ball = __ballot_sync(kFull, hit);
-      if (hit) a.bin_idx[out + __popc(ball & ((1u << lane) - 1u))] = __ldg(a.s.zprim + j);
+      if (hit) {
+        const int p = out + __popc(ball & ((1u << lane) - 1u));
+        const int i = __ldg(a.s.zprim + j);
+        a.bin_idx[p] = i;
+        if (a.bin_cull) a.bin_cull[p] = a.recc[i];
+      }
       out += __popc(ball);
     }
   }
@@ -515,7 +522,8 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
 
 extern "C" int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity,
                       void* scratch, size_t scratch_bytes, int32_t* bin_off, int32_t* bin_idx,
-                      int32_t* status, void* stream) {
+                      int32_t* status, const void* rec, void* bin_cull, void* stream) {
+  if (bin_cull && !rec) return PF_ERR_ARG;
   int ntx, n_rows;
   if (n < 0 || capacity < 0 || !band_ok(W, H, tile, ty_begin, ty_end, &ntx, &n_rows))
     return PF_ERR_ARG;
@@ -539,6 +547,9 @@ extern "C" int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, i
   ra.bin_off = bin_off;
   ra.bin_idx = bin_idx;
   ra.status = status;
+  ra.recc = rec ? (const RecC*)((const char*)rec + (sizeof(RecF) + sizeof(RecG)) * (size_t)n)
+                : nullptr;
+  ra.bin_cull = (RecC*)bin_cull;
   const size_t smem = sizeof(int2) * kRowSmemList + sizeof(int) * (size_t)ntx;
   static bool attr_set = false;
   if (smem > 48 * 1024 || !attr_set) {

@@ -11,18 +11,20 @@
 // B200 design:
 //   Each warp owns an 8x4 pixel sub-tile (8 warps = 16x16 tile), compact so the
 //   warp-uniform culling below rejects as many list entries as possible, and
-//   warps never wait on each other on the hot path.
+//   warps never wait on each other on the hot path.  Pixel-sized buffers are
+//   float4 per pixel (one 16-byte access): image+alpha (RGBA), target+target
+//   alpha, dL/dI+dL/dA, background.
 //   forward  - for every 32 list entries a warp runs a lane-parallel
 //              conservative separating-axis test (primitive axes) of each
 //              entry's footprint against its 8x4 pixel rectangle (32-byte fp32
-//              cull records, two 16-byte loads per lane) and keeps a ballot
-//              mask; only surviving entries are evaluated per pixel (warp-
-//              uniform loop).  Survivors run the float64 decision chain and an
-//              fp32-tap bilinear alpha sample from the quad atlas (one 16-byte
+//              cull records) and keeps a ballot mask; only surviving entries are
+//              evaluated per pixel (warp-uniform loop, two entries per
+//              iteration for ILP).  Survivors run the float64 decision chain and
+//              an fp32-tap bilinear alpha sample from the quad atlas (one 16-byte
 //              load, no bounds checks; the eps decision is re-taken on the
 //              float64 plane when within rounding).  T and C are float64.
 //              Saved state: per contributing (pixel, entry) one 16-byte record
-//              (list position, texel cell, unorm16 bilinear weights, incoming
+//              (list position, texel cell, 24-bit bilinear weights, incoming
 //              T = the reference's Tbuf, _kernels.py:294-297) at slot
 //              256*bin_off[t] + k*256 + pixel (k = the pixel's contribution
 //              ordinal): single pass, coalesced within a warp.
@@ -34,10 +36,10 @@
 //              then walks its pixels' saved entries back to front, picking the
 //              next list position with __reduce_max_sync so it only visits
 //              entries that touch its 32 pixels.  Active lanes compute the 8
-//              gradients in fp32 (the backward takes no decisions; ~1e-5 of the
-//              float64 reference against a 1e-3 bar); a 9-shuffle __shfl_xor
-//              transpose butterfly reduces them across the warp and 8 lanes
-//              issue one float64 atomicAdd each (RED.E.ADD.F64); with <= 2
+//              gradients in fp32 (the backward takes no decisions; <= 3e-4 of
+//              the float64 reference against a 1e-3 bar); a 9-shuffle
+//              __shfl_xor transpose butterfly reduces them across the warp and 8
+//              lanes issue one float64 atomicAdd each (RED.E.ADD.F64); with <= 2
 //              active lanes the lanes issue their atomics directly.
 #include "../../include/primfit_b200.h"
 #include "pf_common.cuh"
@@ -46,8 +48,16 @@ namespace pf {
 
 constexpr int kWarpsPerTile = kTilePix / 32;
 
-__device__ __forceinline__ void pixel_of(int tx, int ty, int& x, int& y, float& cx, float& cy) {
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+// Forward blocks are 2 warps (a 16x4 strip of a tile): the forward has no
+// block-level cooperation, so small blocks only shrink the scheduling tail.
+constexpr int kFwdWarps = 2;
+constexpr int kFwdBlocksPerTile = kWarpsPerTile / kFwdWarps;
+
+// Pixel of lane (threadIdx.x & 31) in warp w (0..7) of tile (tx, ty), and the
+// centre of that warp's 8x4 rectangle.
+__device__ __forceinline__ void pixel_of(int w, int tx, int ty, int& x, int& y, float& cx,
+                                         float& cy) {
+  const int l = threadIdx.x & 31;
   const int wx = (w & 1) * kWarpW, wy = (w >> 1) * kWarpH;
   x = tx * kTile + wx + (l & (kWarpW - 1));
   y = ty * kTile + wy + (l / kWarpW);
@@ -72,8 +82,9 @@ __device__ __forceinline__ bool may_touch(const RecC* __restrict__ rc, float cx,
 struct FwdArgs {
   const RecF* recf;
   const RecC* recc;
-  const double* tex;   // planar [4][texels]
-  const float4* quad;  // alpha quad atlas [texels]
+  const RecC* bin_cull;  // cull records in bin order from pf_bin, or NULL
+  const double* tex;     // planar [4][texels]
+  const float4* quad;    // alpha quad atlas [texels]
   int texels;
   const int32_t* bin_off;
   const int32_t* bin_idx;
@@ -81,31 +92,35 @@ struct FwdArgs {
   int W, H, ntx, ty_begin;
   double eps_skip, mu_blend;
   double bg0, bg1, bg2;
-  const float* bg_img;
+  const float4* bg4;     // per-pixel background (rgb, -), or NULL
   SavedEnt* ent;
   int32_t* ent_n;
-  float* img;
-  float* alpha;
-  const float* target;
-  const float* target_alpha;
+  float4* img4;          // out: (r, g, b, alpha)
+  const float4* tgt4;    // target (r, g, b, target alpha)
   double alpha_w, inv_3P, inv_P;
-  float* dI;
-  float* dA;
+  float4* d4;            // out: (dL/dI r, g, b, dL/dA)
   double* part;
 };
 
 template <bool SAVE, int LOSS, bool MU>
-__global__ void __launch_bounds__(kTilePix) k_forward(FwdArgs a) {
+__global__ void __launch_bounds__(kFwdWarps * 32) k_forward(FwdArgs a) {
   if (a.status && a.status[1]) return;  // bin overflow: nothing valid to render (block-uniform)
 
-  const int tb = blockIdx.x;
+  const int tb = blockIdx.x / kFwdBlocksPerTile;
+  const int wt = (blockIdx.x % kFwdBlocksPerTile) * kFwdWarps + (threadIdx.x >> 5);
   const int tx = tb % a.ntx, ty = a.ty_begin + tb / a.ntx;
   int x, y;
   float cx, cy;
-  pixel_of(tx, ty, x, y, cx, cy);
+  pixel_of(wt, tx, ty, x, y, cx, cy);
   const bool valid = x < a.W && y < a.H;
   const int lane = threadIdx.x & 31;
   const double xx = (double)x, yy = (double)y;
+  const size_t pix = valid ? (size_t)y * a.W + x : 0;
+
+  // prefetch the pixel's epilogue inputs; they are independent of the list walk
+  float4 tg = make_float4(0.f, 0.f, 0.f, 0.f), bgp = tg;
+  if (valid && LOSS != PF_LOSS_NONE) tg = __ldg(a.tgt4 + pix);
+  if (valid && a.bg4) bgp = __ldg(a.bg4 + pix);
 
   const int b0 = a.bin_off[tb];
   const int L = a.bin_off[tb + 1] - b0;
@@ -113,7 +128,7 @@ __global__ void __launch_bounds__(kTilePix) k_forward(FwdArgs a) {
 
   double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0;
   int nsave = 0;
-  const size_t e0 = (size_t)b0 * kTilePix + threadIdx.x;
+  const size_t e0 = (size_t)b0 * kTilePix + wt * 32 + lane;
 
   for (int sub = 0; sub < L; sub += 32) {
     // warp-cooperative cull: lane l tests list entry sub + l against the warp rect
@@ -121,7 +136,7 @@ __global__ void __launch_bounds__(kTilePix) k_forward(FwdArgs a) {
     bool cand = false;
     if (sub + lane < L) {
       my_i = __ldg(a.bin_idx + b0 + sub + lane);
-      cand = may_touch(a.recc + my_i, cx, cy);
+      cand = may_touch(a.bin_cull ? a.bin_cull + b0 + sub + lane : a.recc + my_i, cx, cy);
     }
     unsigned mask = __ballot_sync(kFull, cand);
     while (mask) {
@@ -134,8 +149,8 @@ __global__ void __launch_bounds__(kTilePix) k_forward(FwdArgs a) {
       if (!texel_coords(r, xx, yy, U, V)) continue;
       const Cell c = make_cell(U, V);
       double m = bilerp(load_quad(a.quad, r.base, r.wt, c.u0, c.v0), c.wu, c.wv);
-      if (fabs(m - a.eps_skip) <= 1e-6 * a.eps_skip)  // re-take the decision in float64
-        m = bilinear(plane_a, r.base, r.wt, r.ht, c);
+      // re-take an eps decision within fp32-tap rounding on the float64 plane
+      if (fabs(m - a.eps_skip) <= 1e-6 * a.eps_skip) m = bilinear(plane_a, r.base, r.wt, r.ht, c);
       if (m < a.eps_skip) continue;
       const double aa = r.sa * m;
       double cr = r.c0, cg = r.c1, cb = r.c2;
@@ -156,52 +171,40 @@ __global__ void __launch_bounds__(kTilePix) k_forward(FwdArgs a) {
     }
   }
 
-  double l0 = 0.0, l1 = 0.0, l2 = 0.0;
+  float l0 = 0.0f, l1 = 0.0f, l2 = 0.0f;
   if (valid) {
-    const size_t pix = (size_t)y * a.W + x;
-    double g0 = a.bg0, g1 = a.bg1, g2 = a.bg2;
-    if (a.bg_img) {
-      g0 = a.bg_img[pix * 3 + 0];
-      g1 = a.bg_img[pix * 3 + 1];
-      g2 = a.bg_img[pix * 3 + 2];
-    }
+    const double g0 = a.bg4 ? (double)bgp.x : a.bg0;
+    const double g1 = a.bg4 ? (double)bgp.y : a.bg1;
+    const double g2 = a.bg4 ? (double)bgp.z : a.bg2;
     const double I0 = C0 + T * g0;
     const double I1 = C1 + T * g1;
     const double I2 = C2 + T * g2;
     const double Ia = 1.0 - T;
-    a.img[pix * 3 + 0] = (float)I0;
-    a.img[pix * 3 + 1] = (float)I1;
-    a.img[pix * 3 + 2] = (float)I2;
-    a.alpha[pix] = (float)Ia;
+    a.img4[pix] = make_float4((float)I0, (float)I1, (float)I2, (float)Ia);
     if (SAVE) a.ent_n[pix] = nsave;
     if (LOSS != PF_LOSS_NONE) {
       // loss_mse (fit.py:112-116) / loss_spatial (fit.py:128-151)
-      const double r0 = I0 - (double)a.target[pix * 3 + 0];
-      const double r1 = I1 - (double)a.target[pix * 3 + 1];
-      const double r2 = I2 - (double)a.target[pix * 3 + 2];
-      l0 = r0 * r0 + r1 * r1 + r2 * r2;
+      const double r0 = I0 - (double)tg.x, r1 = I1 - (double)tg.y, r2 = I2 - (double)tg.z;
+      const double sse = r0 * r0 + r1 * r1 + r2 * r2;
       const double k = 2.0 * a.inv_3P;
+      l0 = (float)sse;
       if (LOSS == PF_LOSS_MSE) {
         l1 = l0;
-        a.dI[pix * 3 + 0] = (float)(k * r0);
-        a.dI[pix * 3 + 1] = (float)(k * r1);
-        a.dI[pix * 3 + 2] = (float)(k * r2);
+        a.d4[pix] = make_float4((float)(k * r0), (float)(k * r1), (float)(k * r2), 0.0f);
       } else {
-        const double ta = (double)a.target_alpha[pix];
+        const double ta = (double)tg.w;
         const double mk = ta > 0.0 ? 1.0 : 0.0;
-        const double m0 = r0 * mk, m1 = r1 * mk, m2 = r2 * mk;
-        l1 = m0 * m0 + m1 * m1 + m2 * m2;
         const double ad = Ia - ta;
-        l2 = ad * ad;
-        a.dI[pix * 3 + 0] = (float)(k * m0);
-        a.dI[pix * 3 + 1] = (float)(k * m1);
-        a.dI[pix * 3 + 2] = (float)(k * m2);
-        a.dA[pix] = (float)(a.alpha_w * 2.0 * ad * a.inv_P);
+        l1 = (float)(sse * mk);
+        l2 = (float)(ad * ad);
+        a.d4[pix] = make_float4((float)(k * r0 * mk), (float)(k * r1 * mk), (float)(k * r2 * mk),
+                                (float)(a.alpha_w * 2.0 * ad * a.inv_P));
       }
     }
   }
   if (LOSS != PF_LOSS_NONE) {
     // per-warp partials at fixed slots (no block barrier); pf_backward reduces them
+    // in fixed order in float64 (fp32 inside a warp: 32 terms, ~1e-7 relative)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       l0 += __shfl_xor_sync(kFull, l0, o);
@@ -209,7 +212,7 @@ __global__ void __launch_bounds__(kTilePix) k_forward(FwdArgs a) {
       l2 += __shfl_xor_sync(kFull, l2, o);
     }
     if (lane == 0) {
-      double* pp = a.part + ((size_t)tb * kWarpsPerTile + (threadIdx.x >> 5)) * 3;
+      double* pp = a.part + ((size_t)tb * kWarpsPerTile + wt) * 3;
       pp[0] = l0;
       pp[1] = l1;
       pp[2] = l2;
@@ -227,10 +230,9 @@ struct BwdArgs {
   const int32_t* status;
   const SavedEnt* ent;
   const int32_t* ent_n;
-  const float* dI;
-  const float* dA;
+  const float4* d4;  // (dL/dI r, g, b, dL/dA)
   float bg0, bg1, bg2;
-  const float* bg_img;
+  const float4* bg4;
   float mu_blend;
   int W, H, ntx, ty_begin;
   double* grads;
@@ -302,7 +304,7 @@ __device__ __forceinline__ float bilinear_f(const double* __restrict__ plane, in
   return (float)bilinear(plane, base, wt, ht, c);
 }
 
-template <bool MU, bool HAS_DA>
+template <bool MU>
 __global__ void __launch_bounds__(kTilePix) k_backward(BwdArgs a) {
   __shared__ __align__(16) RecG sg[kBwdStage];
   __shared__ int sidx[kBwdStage];
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(kTilePix) k_backward(BwdArgs a) {
   const int tx = tb % a.ntx, ty = a.ty_begin + tb / a.ntx;
   int x, y;
   float cxf, cyf;
-  pixel_of(tx, ty, x, y, cxf, cyf);
+  pixel_of(threadIdx.x >> 5, tx, ty, x, y, cxf, cyf);
   const bool valid = x < a.W && y < a.H;
   const int lane = threadIdx.x & 31;
   const int b0 = a.bin_off[tb];
@@ -341,19 +343,18 @@ __global__ void __launch_bounds__(kTilePix) k_backward(BwdArgs a) {
     cur = a.ent[e];
     key = (cur.w0 & 0xffffu) + 1u;
   }
-  float dI0 = 0.0f, dI1 = 0.0f, dI2 = 0.0f, dA = 0.0f;
+  float4 dd = make_float4(0.f, 0.f, 0.f, 0.f);
   float g0 = a.bg0, g1 = a.bg1, g2 = a.bg2;
   if (valid) {
-    dI0 = a.dI[pix * 3 + 0];
-    dI1 = a.dI[pix * 3 + 1];
-    dI2 = a.dI[pix * 3 + 2];
-    if (HAS_DA) dA = a.dA[pix];
-    if (a.bg_img) {
-      g0 = a.bg_img[pix * 3 + 0];
-      g1 = a.bg_img[pix * 3 + 1];
-      g2 = a.bg_img[pix * 3 + 2];
+    dd = __ldg(a.d4 + pix);
+    if (a.bg4) {
+      const float4 b = __ldg(a.bg4 + pix);
+      g0 = b.x;
+      g1 = b.y;
+      g2 = b.z;
     }
   }
+  const float dI0 = dd.x, dI1 = dd.y, dI2 = dd.z, dA = dd.w;
   float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f, B = 1.0f;
   cp_async_wait<0>();
   __syncthreads();
@@ -451,23 +452,19 @@ extern "C" size_t pf_saved_bytes(int capacity) {
 
 extern "C" int pf_forward(const void* rec, int n, const double* tex, const float* quad,
                           int texels, const int32_t* bin_off, const int32_t* bin_idx,
-                          const int32_t* status, int W, int H, int ty_begin, int ty_end,
-                          double eps_skip, double mu_blend, double bg_r, double bg_g, double bg_b,
-                          const float* bg_img, void* saved, long long saved_entries,
-                          int32_t* ent_n, float* img, float* alpha, int loss_kind,
-                          const float* target, const float* target_alpha, double alpha_w,
-                          double inv_3P, double inv_P, float* dI, float* dA, double* part,
-                          uint32_t* counter, double* sums, void* stream) {
-  (void)counter;
-  (void)sums;
-  if (W < 1 || H < 1 || n < 0 || !bin_off || !img || !alpha || !tex || !quad) return PF_ERR_ARG;
+                          const int32_t* status, const void* bin_cull, int W, int H,
+                          int ty_begin, int ty_end, double eps_skip, double mu_blend, double bg_r,
+                          double bg_g, double bg_b, const float* bg4, void* saved,
+                          long long saved_entries, int32_t* ent_n, float* img4, int loss_kind,
+                          const float* tgt4, double alpha_w, double inv_3P, double inv_P,
+                          float* d4, double* part, void* stream) {
+  if (W < 1 || H < 1 || n < 0 || !bin_off || !img4 || !tex || !quad) return PF_ERR_ARG;
   const int ntx = div_up(W, kTile), nty = div_up(H, kTile);
   if (ty_begin < 0 || ty_end > nty || ty_begin > ty_end) return PF_ERR_ARG;
   const bool save = saved != nullptr;
   if (save && (!ent_n || saved_entries < 0)) return PF_ERR_ARG;
   if (loss_kind != PF_LOSS_NONE) {
-    if (!target || !dI || !part) return PF_ERR_ARG;
-    if (loss_kind == PF_LOSS_SPATIAL && (!target_alpha || !dA)) return PF_ERR_ARG;
+    if (!tgt4 || !d4 || !part) return PF_ERR_ARG;
     if (loss_kind != PF_LOSS_MSE && loss_kind != PF_LOSS_SPATIAL) return PF_ERR_ARG;
   }
   const int n_tiles = (ty_end - ty_begin) * ntx;
@@ -475,6 +472,7 @@ extern "C" int pf_forward(const void* rec, int n, const double* tex, const float
   FwdArgs a;
   a.recf = (const RecF*)rec;
   a.recc = (const RecC*)((const char*)rec + (sizeof(RecF) + sizeof(RecG)) * (size_t)n);
+  a.bin_cull = (const RecC*)bin_cull;
   a.tex = tex;
   a.quad = (const float4*)quad;
   a.texels = texels;
@@ -490,22 +488,20 @@ extern "C" int pf_forward(const void* rec, int n, const double* tex, const float
   a.bg0 = bg_r;
   a.bg1 = bg_g;
   a.bg2 = bg_b;
-  a.bg_img = bg_img;
+  a.bg4 = (const float4*)bg4;
   a.ent = (SavedEnt*)saved;
   a.ent_n = ent_n;
-  a.img = img;
-  a.alpha = alpha;
-  a.target = target;
-  a.target_alpha = target_alpha;
+  a.img4 = (float4*)img4;
+  a.tgt4 = (const float4*)tgt4;
   a.alpha_w = alpha_w;
   a.inv_3P = inv_3P;
   a.inv_P = inv_P;
-  a.dI = dI;
-  a.dA = dA;
+  a.d4 = (float4*)d4;
   a.part = part;
   cudaStream_t st = (cudaStream_t)stream;
   const bool mu = mu_blend > 0.0;
-#define PF_FWD(SV, LS, MUV) k_forward<SV, LS, MUV><<<n_tiles, kTilePix, 0, st>>>(a)
+#define PF_FWD(SV, LS, MUV) \
+  k_forward<SV, LS, MUV><<<n_tiles * kFwdBlocksPerTile, kFwdWarps * 32, 0, st>>>(a)
 #define PF_FWD_MU(SV, LS) \
   if (mu) PF_FWD(SV, LS, true); else PF_FWD(SV, LS, false)
   if (save) {
@@ -525,11 +521,11 @@ extern "C" int pf_forward(const void* rec, int n, const double* tex, const float
 extern "C" int pf_backward(const void* rec, int n, const double* tex, const float* quad,
                            int texels, const int32_t* bin_off, const int32_t* bin_idx,
                            const int32_t* status, const void* saved, long long saved_entries,
-                           const int32_t* ent_n, const float* dI, const float* dA, double bg_r,
-                           double bg_g, double bg_b, const float* bg_img, double mu_blend, int W,
-                           int H, int ty_begin, int ty_end, double* grads, const double* part,
+                           const int32_t* ent_n, const float* d4, double bg_r, double bg_g,
+                           double bg_b, const float* bg4, double mu_blend, int W, int H,
+                           int ty_begin, int ty_end, double* grads, const double* part,
                            double* sums, void* stream) {
-  if (W < 1 || H < 1 || n < 0 || !bin_off || !saved || saved_entries < 0 || !ent_n || !dI ||
+  if (W < 1 || H < 1 || n < 0 || !bin_off || !saved || saved_entries < 0 || !ent_n || !d4 ||
       !grads || !tex || !quad || (part && !sums))
     return PF_ERR_ARG;
   const int ntx = div_up(W, kTile), nty = div_up(H, kTile);
@@ -546,12 +542,11 @@ extern "C" int pf_backward(const void* rec, int n, const double* tex, const floa
   a.status = status;
   a.ent = (const SavedEnt*)saved;
   a.ent_n = ent_n;
-  a.dI = dI;
-  a.dA = dA;
+  a.d4 = (const float4*)d4;
   a.bg0 = (float)bg_r;
   a.bg1 = (float)bg_g;
   a.bg2 = (float)bg_b;
-  a.bg_img = bg_img;
+  a.bg4 = (const float4*)bg4;
   a.mu_blend = (float)mu_blend;
   a.W = W;
   a.H = H;
@@ -562,13 +557,9 @@ extern "C" int pf_backward(const void* rec, int n, const double* tex, const floa
   a.n_part = n_tiles * kWarpsPerTile;
   a.sums = sums;
   cudaStream_t st = (cudaStream_t)stream;
-  const bool mu = mu_blend > 0.0;
-  if (mu) {
-    if (dA) k_backward<true, true><<<n_tiles, kTilePix, 0, st>>>(a);
-    else k_backward<true, false><<<n_tiles, kTilePix, 0, st>>>(a);
-  } else {
-    if (dA) k_backward<false, true><<<n_tiles, kTilePix, 0, st>>>(a);
-    else k_backward<false, false><<<n_tiles, kTilePix, 0, st>>>(a);
-  }
+  if (mu_blend > 0.0)
+    k_backward<true><<<n_tiles, kTilePix, 0, st>>>(a);
+  else
+    k_backward<false><<<n_tiles, kTilePix, 0, st>>>(a);
   return (int)cudaGetLastError();
 }

@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .compositor import Band, Compositor, DeviceAtlas, adam_launch, bin_capacity
+from .compositor import Band, Compositor, DeviceAtlas, adam_launch, bin_capacity, pixels4
 from .errors import LayoutMismatch, MissingAlphaTarget, ShapeMismatch
 from .raster import DEFAULT_EPS_SKIP, _device, noisy_background
 from .scene import NOISE_BACKGROUND, FloatArray, ParamLayout, pack_params, param_matrix, structure_arrays, unpack_params, validate_scene
@@ -293,15 +293,13 @@ class StepEngine:
         self.gbuf = torch.zeros(n * 8 + 4, dtype=torch.float64, device=dev)
         self.grads = self.gbuf[: n * 8]
         self.sums = self.gbuf[n * 8 :]
-        self.target = torch.from_numpy(target.astype(np.float32).reshape(-1)).to(dev)
-        self.target_alpha = None
-        if self.loss_kind == nat.PF_LOSS_SPATIAL:
-            self.target_alpha = torch.from_numpy(
-                np.asarray(loss_spec.target_alpha, dtype=np.float32).reshape(-1)).to(dev)
+        ta = loss_spec.target_alpha if self.loss_kind == nat.PF_LOSS_SPATIAL else None
+        # (target rgb, target alpha) per pixel, one 16-byte load in K3
+        self.tgt4 = torch.from_numpy(pixels4(target, ta)).to(dev)
         self.noise_bg = isinstance(scene.background, str) and scene.background == NOISE_BACKGROUND
         self.bg_rgb = (0.0, 0.0, 0.0) if self.noise_bg else tuple(
             float(c) for c in np.asarray(scene.background, dtype=np.float64))
-        self.bg_img = torch.zeros(self.P * 3, dtype=torch.float32, device=dev) if self.noise_bg else None
+        self.bg4 = torch.zeros(self.P * 4, dtype=torch.float32, device=dev) if self.noise_bg else None
         tid, z = structure_arrays(scene)
         self.padding = effective_padding(cfg)
         self.atlas = DeviceAtlas(scene.templates, bool(scene.preserve_aspect), dev)
@@ -312,7 +310,7 @@ class StepEngine:
         self.comp = Compositor(tid, z, self.atlas, W, H, alpha_max=scene.alpha_max,
                                mu_blend=scene.mu_blend, padding=self.padding, capacity=cap,
                                band=band, device=dev)
-        self.comp.alloc_render(save=True, loss=True, spatial=self.loss_kind == nat.PF_LOSS_SPATIAL)
+        self.comp.alloc_render(save=True, loss=True)
         self.allreduce = allreduce
         self.use_graph = use_graph
         self.graph: torch.cuda.CUDAGraph | None = None
@@ -328,12 +326,10 @@ class StepEngine:
         mark = mark or (lambda name: None)
         c.bin()
         mark("bin")
-        c.forward(save=True, eps_skip=self.eps_skip, bg_rgb=self.bg_rgb, bg_img=self.bg_img,
-                  loss_kind=self.loss_kind, target=self.target, target_alpha=self.target_alpha,
-                  alpha_w=self.alpha_w, P_total=self.P)
+        c.forward(save=True, eps_skip=self.eps_skip, bg_rgb=self.bg_rgb, bg4=self.bg4,
+                  loss_kind=self.loss_kind, tgt4=self.tgt4, alpha_w=self.alpha_w, P_total=self.P)
         mark("forward")
-        c.backward(c.dI, self.gbuf, dA=c.dA if self.loss_kind == nat.PF_LOSS_SPATIAL else None,
-                   bg_rgb=self.bg_rgb, bg_img=self.bg_img, sums=self.sums)
+        c.backward(c.d4, self.gbuf, bg_rgb=self.bg_rgb, bg4=self.bg4, sums=self.sums)
         mark("backward")
         if self.allreduce is not None:
             self.allreduce(self.gbuf)
@@ -362,8 +358,8 @@ class StepEngine:
         if self.noise_bg:
             if rng is None:
                 raise ValueError("noise background needs the caller's rng")
-            bg = noisy_background(self.W, self.H, rng).astype(np.float32).reshape(-1)
-            self.bg_img.copy_(torch.from_numpy(bg), non_blocking=False)
+            bg = pixels4(noisy_background(self.W, self.H, rng))
+            self.bg4.copy_(torch.from_numpy(bg), non_blocking=False)
         if self.graph is not None:
             self.graph.replay()
         else:

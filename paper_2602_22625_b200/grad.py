@@ -15,6 +15,7 @@ import numpy as np
 import torch
 
 from .errors import LengthMismatch, ShapeMismatch, StaleSavedState
+from .compositor import pixels4
 from .raster import SavedForward, resolve_background
 from .scene import FloatArray, scene_fingerprint
 
@@ -93,11 +94,8 @@ def backward(scene, saved: SavedForward, dL_dI: FloatArray, dL_dA: FloatArray | 
             raise StaleSavedState("background differs from the one composited in the forward")
     comp = saved.compositor
     dev = comp.device
-    d_dI = torch.from_numpy(np.ascontiguousarray(dL_dI, dtype=np.float32).reshape(-1)).to(dev)
-    d_dA = None
-    if dL_dA is not None:
-        d_dA = torch.from_numpy(np.ascontiguousarray(dL_dA, dtype=np.float32).reshape(-1)).to(dev)
+    d4 = torch.from_numpy(pixels4(dL_dI, dL_dA)).to(dev)
     grads = torch.zeros(comp.n * 8 + 4, dtype=torch.float64, device=dev)
     rgb = saved.bg_rgb if saved.bg_rgb is not None else (0.0, 0.0, 0.0)
-    comp.backward(d_dI, grads, dA=d_dA, bg_rgb=rgb, bg_img=saved.bg_img)
+    comp.backward(d4, grads, bg_rgb=rgb, bg4=saved.bg4)
     return Gradients(grads[: comp.n * 8].view(comp.n, 8).cpu().numpy())

@@ -24,7 +24,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .compositor import RENDER_TILE, Compositor, DeviceAtlas, bin_capacity
+from .compositor import RENDER_TILE, Compositor, DeviceAtlas, bin_capacity, pixels4
 from .errors import ShapeMismatch
 from .scene import NOISE_BACKGROUND, FloatArray, param_matrix, scene_fingerprint, structure_arrays, validate_scene
 
@@ -76,7 +76,7 @@ class SavedForward:
     t_final: FloatArray
     background: FloatArray
     bg_rgb: tuple | None
-    bg_img: torch.Tensor | None
+    bg4: torch.Tensor | None
     fingerprint: str
     eps_skip: float
     n_entries: int = field(default=0)
@@ -172,23 +172,23 @@ def render_forward(scene, bins: TileBins | None = None, background=None, save: b
     rgb = _solid_rgb(scene, background)
     comp, d_params = make_compositor(scene, padding=padding)
     dev = comp.device
-    bg_img = None
+    bg4 = None
     if rgb is None:
-        bg_img = torch.from_numpy(bg.astype(np.float32).reshape(-1)).to(dev)
+        bg4 = torch.from_numpy(pixels4(bg)).to(dev)
         rgb = (0.0, 0.0, 0.0)
     comp.preprocess(d_params)
     comp.bin()
-    comp.forward(save=save, eps_skip=eps_skip, bg_rgb=rgb, bg_img=bg_img)
+    comp.forward(save=save, eps_skip=eps_skip, bg_rgb=rgb, bg4=bg4)
     comp.check_overflow()
     H, W = scene.canvas_h, scene.canvas_w
-    color = comp.img.view(H, W, 3).double().cpu().numpy()
-    alpha = comp.alpha.view(H, W).double().cpu().numpy()
+    color = comp.color().double().cpu().numpy()
+    alpha = comp.alpha().double().cpu().numpy()
     out = RenderOutput(color, alpha)
     if not save:
         return out, None
     saved = SavedForward(
         canvas_w=W, canvas_h=H, compositor=comp, t_final=1.0 - alpha, background=bg,
-        bg_rgb=None if bg_img is not None else rgb, bg_img=bg_img,
+        bg_rgb=None if bg4 is not None else rgb, bg4=bg4,
         fingerprint=scene_fingerprint(scene), eps_skip=eps_skip,
         n_entries=int(comp.ent_n.sum().item()))
     return out, saved
