@@ -42,10 +42,13 @@ def algorithmic_bytes(P: int, K16: int, N: int, atlas_texels: int) -> dict:
     """B_step = 68 P + 12 K16 + 288 N + 16 * texels (fp32 model)."""
     A = 16 * atlas_texels
     return {
-        "step": 68 * P + 12 * K16 + 288 * N + A,
+        "total": 68 * P + 12 * K16 + 288 * N + A,
         # per-kernel split of the same model (DESIGN.md §5)
         "forward": 48 * P + 4 * K16 + A,
         "backward": 20 * P + 4 * K16 + 32 * N,
+        # K34 fused render+loss+backward: target in, per-entry index + records,
+        # atlas taps (the contribution stack never leaves the SM)
+        "step": 16 * P + 4 * K16 + 256 * N + A,
         "bin": 4 * K16 + 32 * N,
         "adam": 224 * N,
     }
@@ -319,7 +322,7 @@ def run_ours(args) -> None:
         return
     peaks = _peaks()
     ab = algorithmic_bytes(eng.P, K16, n, eng.atlas.texels)
-    dom = max(("forward", "backward"), key=lambda k: stage_ms.get(k, 0.0))
+    dom = max(("forward", "backward", "step"), key=lambda k: stage_ms.get(k, 0.0))
     achieved = ab[dom] / (stage_ms[dom] * 1e-3) / 1e9
     cpu = cpu_baseline(args.config) if (world == 1 and not args.no_cpu) else None
     line = {
@@ -334,7 +337,7 @@ def run_ours(args) -> None:
                      "frac": achieved / peaks["hbm_gbs"], "traffic": None,
                      "peak_src": peaks["src"], "algorithmic_bytes": ab[dom],
                      "kernel_ms": stage_ms[dom],
-                     "step_frac": ab["step"] * value / 1e9 / peaks["hbm_gbs"]},
+                     "step_frac": ab["total"] * value / 1e9 / peaks["hbm_gbs"]},
         "stage_ms": stage_ms,
         "e2e": {"value": 1e3 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": n * 8 * 8,
                 "d2h_bytes_per_step": n * 8 * 8 + 8},

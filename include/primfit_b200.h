@@ -120,11 +120,14 @@ int pf_scratch_init(void* scratch, size_t scratch_bytes, const int32_t* zorder, 
  * parameter, then the records / tile rects of the NEXT step from the updated
  * parameters (as pf_preprocess), the loss/psnr history entry and the iteration
  * counter -- one launch between two renders.  Gradients are zeroed.
+ *   sums   loss sums of this step (read), or -- with part != NULL -- written
+ *          from a fixed-order two-level fold of pf_fit_step's n_part partials
  */
 int pf_adam_preprocess(double* params, double* grads, double* m, double* v, const uint8_t* frozen,
                        const double* gains8, const double* lr_table, const double* bc1_table,
                        const double* bc2_table, int32_t* iter, int clamp, double s_min,
-                       double s_max, const double* sums, int loss_kind, double alpha_w,
+                       double s_max, double* sums, const double* part, int n_part,
+                       int loss_kind, double alpha_w,
                        double inv_3P, double inv_P, double* hist_loss, double* hist_psnr,
                        const int32_t* template_id, const int32_t* zorder, int n,
                        const int32_t* tpl_base, const int32_t* tpl_w, const int32_t* tpl_h,
@@ -202,6 +205,31 @@ int pf_backward(const void* rec, int n, const double* tex, const float* quad, in
                 const float* d4, double bg_r, double bg_g, double bg_b, const float* bg4,
                 double mu_blend, int W, int H, int ty_begin, int ty_end,
                 double* grads, const double* part, double* sums, void* stream);
+
+/*
+ * K34 — the fit step's render -> loss -> backward in one kernel (mu_blend == 0).
+ * Replaces: the run_loop body render_forward(save=True) -> evaluate_loss ->
+ * backward (fit.py:486-492; raster.py:290-363, fit.py:112-151, grad.py:134-187).
+ * Same decisions, compositing, loss and gradients as pf_forward(save, loss) +
+ * pf_backward, but the per-pixel contribution stack stays in shared memory
+ * (depth >= 2 spills to `spill`) and dL/dI never leaves registers.
+ *   spill   device scratch of pf_step_spill_bytes(capacity) bytes
+ *   img4    optional out float32 [H*W][4] (r, g, b, alpha); NULL skips it
+ *   part    out float64 [n_band_tiles * 8][3] per-warp loss partials (sum (I-t)^2,
+ *           sum ((I-t)*mask)^2, sum (I_a-t_a)^2); fold them with pf_fold_loss or
+ *           pass them to pf_adam_preprocess
+ *   grads   float64 [n][8] accumulated into (zeroed by pf_adam_preprocess)
+ */
+size_t pf_step_spill_bytes(int capacity);
+int pf_fit_step(const void* rec, int n, const double* tex, const float* quad, int texels,
+                const int32_t* bin_off, const int32_t* bin_idx, const int32_t* status,
+                int W, int H, int ty_begin, int ty_end, double eps_skip,
+                double bg_r, double bg_g, double bg_b, const float* bg4,
+                int loss_kind, const float* tgt4, double alpha_w, double inv_3P, double inv_P,
+                void* spill, float* img4, double* part, double* grads, void* stream);
+
+/* Fixed-order fold of n_part partial triples into sums[3] (deterministic). */
+int pf_fold_loss(const double* part, int n_part, double* sums, void* stream);
 
 /*
  * K5 — fused Adam step (+ loss/psnr history, + gradient zeroing for the next step).

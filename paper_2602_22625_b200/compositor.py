@@ -186,8 +186,9 @@ class Compositor:
 
     def adam_preprocess(self, params, grads, m, v, *, frozen, gains, lr_table, bc1_table,
                         bc2_table, iter_counter, s_min, s_max, sums, loss_kind, alpha_w, P_total,
-                        hist_loss, hist_psnr, stream=None) -> None:
-        """K5+K1 fused: Adam on every parameter, then the next step's records + offsets."""
+                        hist_loss, hist_psnr, part=None, stream=None) -> None:
+        """K5+K1 fused: Adam on every parameter, then the next step's records + offsets.
+        With ``part`` (pf_fit_step's loss partials) the loss sums are folded here."""
         a = self.atlas
         g8 = (C.c_double * 8)(*[float(g) for g in gains])
         P = float(P_total)
@@ -196,7 +197,7 @@ class Compositor:
                 params.data_ptr(), grads.data_ptr(), m.data_ptr(), v.data_ptr(), nat.ptr(frozen),
                 C.addressof(g8), lr_table.data_ptr(), bc1_table.data_ptr(), bc2_table.data_ptr(),
                 iter_counter.data_ptr(), 1, float(s_min), float(s_max), nat.ptr(sums),
-                int(loss_kind), float(alpha_w), 1.0 / (3.0 * P), 1.0 / P, nat.ptr(hist_loss),
+                nat.ptr(part), self.n_part if part is not None else 0, int(loss_kind), float(alpha_w), 1.0 / (3.0 * P), 1.0 / P, nat.ptr(hist_loss),
                 nat.ptr(hist_psnr), self.d_tid.data_ptr(), self.d_zorder.data_ptr(), self.n,
                 a.d_base.data_ptr(), a.d_w.data_ptr(), a.d_h.data_ptr(), a.d_q.data_ptr(),
                 a.d_hyp.data_ptr(), a.n_templates, self.alpha_max, self.mu_blend, self.padding,
@@ -245,6 +246,49 @@ class Compositor:
                 1.0 / (3.0 * P), 1.0 / P, p(self.d4) if lossy else None,
                 p(self.part) if lossy else None, _stream_handle(stream)),
             "pf_forward")
+
+    # -- K34 (fit step: forward + loss + backward in one kernel)
+    def fit_step(self, grads: torch.Tensor, sums: torch.Tensor | None, *, eps_skip: float,
+                 bg_rgb=(1.0, 1.0, 1.0), bg4: torch.Tensor | None = None,
+                 loss_kind: int = nat.PF_LOSS_MSE, tgt4: torch.Tensor, alpha_w: float = 0.0,
+                 P_total: int | None = None, image: bool = False, stream=None) -> None:
+        if self.mu_blend > 0.0:
+            raise ValueError("pf_fit_step needs mu_blend == 0; use forward + backward")
+        if self.tile != RENDER_TILE:
+            raise ValueError(f"render kernels need bin tile {RENDER_TILE}, got {self.tile}")
+        dev, P = self.device, self.W * self.H
+        if not hasattr(self, "spill"):
+            nbytes = int(self.lib.pf_step_spill_bytes(max(self.capacity, 1)))
+            self.spill = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            if not hasattr(self, "part"):
+                self.part = torch.zeros(max(self.n_tiles, 1) * 8 * 3, dtype=torch.float64,
+                                        device=dev)
+        if image and not hasattr(self, "img4"):
+            self.img4 = torch.zeros(P * 4, dtype=torch.float32, device=dev)
+        Pt = float(P_total if P_total is not None else P)
+        p = nat.ptr
+        nat.check(
+            self.lib.pf_fit_step(
+                self.rec.data_ptr(), self.n, self.atlas.tex.data_ptr(),
+                self.atlas.quad.data_ptr(), self.atlas.texels,
+                self.bin_off.data_ptr(), self.bin_idx.data_ptr(), self.status.data_ptr(),
+                self.W, self.H, self.band.ty_begin, self.band.ty_end, float(eps_skip),
+                float(bg_rgb[0]), float(bg_rgb[1]), float(bg_rgb[2]), p(bg4), int(loss_kind),
+                tgt4.data_ptr(), float(alpha_w), 1.0 / (3.0 * Pt), 1.0 / Pt,
+                self.spill.data_ptr(), p(self.img4) if image else None, self.part.data_ptr(),
+                grads.data_ptr(), _stream_handle(stream)),
+            "pf_fit_step")
+        if sums is not None:
+            self.fold_loss(sums, stream)
+
+    @property
+    def n_part(self) -> int:
+        """Loss partial triples per launch (8 warps per band tile)."""
+        return self.n_tiles * 8
+
+    def fold_loss(self, sums: torch.Tensor, stream=None) -> None:
+        nat.check(self.lib.pf_fold_loss(self.part.data_ptr(), self.n_part, sums.data_ptr(),
+                                        _stream_handle(stream)), "pf_fold_loss")
 
     # -- K4
     def backward(self, d4: torch.Tensor, grads: torch.Tensor, *, bg_rgb=(1.0, 1.0, 1.0),

@@ -43,7 +43,9 @@ struct AdamPart {
   int32_t* iter;
   int clamp;
   double s_min, s_max;
-  const double* sums;
+  double* sums;          // loss sums (read, or written by the fold below)
+  const double* part;    // per-warp loss partials of pf_fit_step to fold here, or NULL
+  int n_part;
   int loss_kind;
   double alpha_w, inv_3P, inv_P;
   double* hist_loss;
@@ -108,17 +110,34 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
                        a.ad.bc2_table[it]);
       a.params[pidx] = pc;
     }
-    if (g == 0 && a.ad.sums) {
-      // history entry of this iteration: the render before this update (fit.py:502-505)
-      const AdamPart& d = a.ad;
-      const double mse = d.sums[0] * d.inv_3P;
-      double loss = mse;
-      if (d.loss_kind == PF_LOSS_SPATIAL)
-        loss = d.sums[1] * d.inv_3P + d.alpha_w * (d.sums[2] * d.inv_P);
-      if (d.hist_loss) d.hist_loss[it] = loss;
-      if (d.hist_psnr)
-        d.hist_psnr[it] = mse == 0.0 ? __longlong_as_double(0x7ff0000000000000ll)
-                                     : 10.0 * log10(1.0 / mse);
+    if (a.ad.part) {
+      // first level of the fixed-order loss fold: this block's chunk of partials
+      __shared__ double fr[kPrimThreads / 32][3];
+      const int chunk = (a.ad.n_part + gridDim.x - 1) / gridDim.x;
+      const int beg = blockIdx.x * chunk, end = min(beg + chunk, a.ad.n_part);
+      double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+      for (int k = beg + threadIdx.x; k < end; k += kPrimThreads) {
+        v0 += __ldcg(a.ad.part + 3 * k + 0);
+        v1 += __ldcg(a.ad.part + 3 * k + 1);
+        v2 += __ldcg(a.ad.part + 3 * k + 2);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        v0 += __shfl_xor_sync(kFull, v0, o);
+        v1 += __shfl_xor_sync(kFull, v1, o);
+        v2 += __shfl_xor_sync(kFull, v2, o);
+      }
+      if (lane == 0) {
+        fr[threadIdx.x >> 5][0] = v0;
+        fr[threadIdx.x >> 5][1] = v1;
+        fr[threadIdx.x >> 5][2] = v2;
+      }
+      __syncthreads();
+      if (threadIdx.x < 3) {
+        double t = 0.0;
+        for (int w = 0; w < kPrimThreads / 32; ++w) t += fr[w][threadIdx.x];
+        a.s.fold[blockIdx.x * 3 + threadIdx.x] = t;
+      }
     }
   }
   // gather the primitive's 8 parameters from its lane group
@@ -232,7 +251,48 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
     if (threadIdx.x == 0) {
       __threadfence();
       am_last = atomicAdd(a.s.done, 1u) == gridDim.x - 1;
-      if (am_last) {
+    }
+    __syncthreads();
+    if (am_last && threadIdx.x < 32) {
+      __threadfence();
+      const AdamPart& d = a.ad;
+      bool have = d.sums != nullptr;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      if (d.part) {
+        // second level: the per-block folds, lane-strided then a fixed xor tree
+        for (int b = lane; b < (int)gridDim.x; b += 32) {
+          s0 += __ldcg(a.s.fold + 3 * b + 0);
+          s1 += __ldcg(a.s.fold + 3 * b + 1);
+          s2 += __ldcg(a.s.fold + 3 * b + 2);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          s0 += __shfl_xor_sync(kFull, s0, o);
+          s1 += __shfl_xor_sync(kFull, s1, o);
+          s2 += __shfl_xor_sync(kFull, s2, o);
+        }
+        if (d.sums && lane == 0) {
+          d.sums[0] = s0;
+          d.sums[1] = s1;
+          d.sums[2] = s2;
+        }
+        have = true;
+      } else if (have) {
+        s0 = __ldcg(d.sums + 0);
+        s1 = __ldcg(d.sums + 1);
+        s2 = __ldcg(d.sums + 2);
+      }
+      if (lane == 0) {
+        if (have) {
+          // history entry of this iteration: the render before this update (fit.py:502-505)
+          const double mse = s0 * d.inv_3P;
+          double loss = mse;
+          if (d.loss_kind == PF_LOSS_SPATIAL) loss = s1 * d.inv_3P + d.alpha_w * (s2 * d.inv_P);
+          if (d.hist_loss) d.hist_loss[it] = loss;
+          if (d.hist_psnr)
+            d.hist_psnr[it] = mse == 0.0 ? __longlong_as_double(0x7ff0000000000000ll)
+                                         : 10.0 * log10(1.0 / mse);
+        }
         *a.ad.iter = it + 1;
         *a.s.done = 0u;
       }
@@ -481,7 +541,8 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
                                   const uint8_t* frozen, const double* gains8,
                                   const double* lr_table, const double* bc1_table,
                                   const double* bc2_table, int32_t* iter, int clamp, double s_min,
-                                  double s_max, const double* sums, int loss_kind, double alpha_w,
+                                  double s_max, double* sums, const double* part, int n_part,
+                                  int loss_kind, double alpha_w,
                                   double inv_3P, double inv_P, double* hist_loss,
                                   double* hist_psnr, const int32_t* template_id,
                                   const int32_t* zorder, int n, const int32_t* tpl_base,
@@ -510,7 +571,10 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
   d.clamp = clamp;
   d.s_min = s_min;
   d.s_max = s_max;
+  if (part && n_part < 0) return PF_ERR_ARG;
   d.sums = sums;
+  d.part = part;
+  d.n_part = part ? n_part : 0;
   d.loss_kind = loss_kind;
   d.alpha_w = alpha_w;
   d.inv_3P = inv_3P;

@@ -10,6 +10,7 @@ struct BinScratch {
   int32_t* zprim;    // [n] primitive index per z position (static, set by pf_scratch_init)
   int2* rowlist;     // [capacity] per-row z-ordered lists: (z position, tx0 | tx1 << 16)
   uint32_t* done;    // [4] last-block ticket
+  double* fold;      // [prim blocks][3] per-block loss-partial folds (pf_adam_preprocess)
   size_t total;
 };
 
@@ -28,6 +29,7 @@ static inline BinScratch carve(void* base, int n, int cap) {
   s.zprim = (int32_t*)take(sizeof(int32_t) * (size_t)n);
   s.rowlist = (int2*)take(sizeof(int2) * (size_t)cap);
   s.done = (uint32_t*)take(sizeof(uint32_t) * 4);
+  s.fold = (double*)take(sizeof(double) * 3 * (size_t)((8 * (size_t)n + 255) / 256 + 1));
   s.total = off;
   return s;
 }

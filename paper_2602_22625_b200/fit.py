@@ -15,6 +15,8 @@ schedule lookup in K5).
 
 from __future__ import annotations
 
+import os
+
 import csv
 import math
 from collections.abc import Callable
@@ -310,7 +312,11 @@ class StepEngine:
         self.comp = Compositor(tid, z, self.atlas, W, H, alpha_max=scene.alpha_max,
                                mu_blend=scene.mu_blend, padding=self.padding, capacity=cap,
                                band=band, device=dev)
-        self.comp.alloc_render(save=True, loss=True)
+        # K34 (one kernel for render -> loss -> backward) whenever colour does not
+        # come from the texture; PF_TWO_KERNEL=1 forces K3 + K4 (A/B checks)
+        self.fused = scene.mu_blend == 0.0 and os.environ.get("PF_TWO_KERNEL", "0") != "1"
+        if not self.fused:
+            self.comp.alloc_render(save=True, loss=True)
         self.allreduce = allreduce
         self.use_graph = use_graph
         self.graph: torch.cuda.CUDAGraph | None = None
@@ -326,11 +332,21 @@ class StepEngine:
         mark = mark or (lambda name: None)
         c.bin()
         mark("bin")
-        c.forward(save=True, eps_skip=self.eps_skip, bg_rgb=self.bg_rgb, bg4=self.bg4,
-                  loss_kind=self.loss_kind, tgt4=self.tgt4, alpha_w=self.alpha_w, P_total=self.P)
-        mark("forward")
-        c.backward(c.d4, self.gbuf, bg_rgb=self.bg_rgb, bg4=self.bg4, sums=self.sums)
-        mark("backward")
+        fold_in_adam = self.fused and self.allreduce is None
+        if self.fused:
+            # one rank: the loss partials are folded inside the Adam launch; with an
+            # allreduce they are folded first so the sums travel with the grads
+            c.fit_step(self.gbuf, None if fold_in_adam else self.sums, eps_skip=self.eps_skip,
+                       bg_rgb=self.bg_rgb, bg4=self.bg4, loss_kind=self.loss_kind,
+                       tgt4=self.tgt4, alpha_w=self.alpha_w, P_total=self.P)
+            mark("step")
+        else:
+            c.forward(save=True, eps_skip=self.eps_skip, bg_rgb=self.bg_rgb, bg4=self.bg4,
+                      loss_kind=self.loss_kind, tgt4=self.tgt4, alpha_w=self.alpha_w,
+                      P_total=self.P)
+            mark("forward")
+            c.backward(c.d4, self.gbuf, bg_rgb=self.bg_rgb, bg4=self.bg4, sums=self.sums)
+            mark("backward")
         if self.allreduce is not None:
             self.allreduce(self.gbuf)
             mark("allreduce")
@@ -339,7 +355,8 @@ class StepEngine:
                           bc2_table=self.bc2_table, iter_counter=self.iter,
                           s_min=self.cfg.scale_min, s_max=self.cfg.scale_max, sums=self.sums,
                           loss_kind=self.loss_kind, alpha_w=self.alpha_w, P_total=self.P,
-                          hist_loss=self.hist_loss, hist_psnr=self.hist_psnr)
+                          hist_loss=self.hist_loss, hist_psnr=self.hist_psnr,
+                          part=c.part if fold_in_adam else None)
         mark("adam_preprocess")
 
     def refresh(self) -> None:

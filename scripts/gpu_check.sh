@@ -11,7 +11,7 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
      --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/ncu_bench.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on \
-     -k regex:"k_forward|k_backward|k_bin_rows|k_prim" -s 30 -c 8 \
+     -k regex:"k_step|k_forward|k_backward|k_bin_rows|k_prim" -s 30 -c 8 \
      -o gpurun_out/prof_full -f python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/ncu_full.log 2>&1
   ls -la gpurun_out/*.ncu-rep 2>/dev/null
 fi

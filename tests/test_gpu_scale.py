@@ -131,3 +131,109 @@ def test_autograd_function_matches_api(torch_cuda):
     g = grad.backward(sc, saved, dI)
     ok, err = grad_close(params.grad.cpu().numpy(), g.data)
     assert ok, err
+
+
+def _fused_grads(eng, image=True):
+    """One K2 + K34 launch on the engine's current parameters (no Adam)."""
+    eng.refresh()
+    c = eng.comp
+    c.bin()
+    eng.gbuf.zero_()
+    c.fit_step(eng.gbuf, eng.sums, eps_skip=eng.eps_skip, bg_rgb=eng.bg_rgb, bg4=eng.bg4,
+               loss_kind=eng.loss_kind, tgt4=eng.tgt4, alpha_w=eng.alpha_w, P_total=eng.P,
+               image=image)
+    c.check_overflow()
+    return (eng.grads.view(-1, 8).cpu().numpy(), eng.sums.cpu().numpy(),
+            c.color().double().cpu().numpy(), c.alpha().double().cpu().numpy())
+
+
+@pytest.mark.parametrize("name", ["c1", "c3", "c4"])
+def test_fused_step_matches_oracle(torch_cuda, oracle, name):
+    """K34 (render -> loss -> backward in one kernel) against the oracle's
+    render_forward + loss + backward on the same perturbed mid-fit state."""
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.fit import StepEngine, effective_padding
+
+    w = synth.make_workload(name)
+    sc = w.scene
+    rng = np.random.default_rng(7)
+    for p in sc.primitives:
+        p.x += float(rng.uniform(-0.5, 0.5))
+        p.y += float(rng.uniform(-0.5, 0.5))
+        p.opacity_logit = float(rng.uniform(-2.0, 3.0))
+    eng = StepEngine(sc, w.cfg, w.loss, 1, use_graph=False)
+    assert eng.fused
+    g, sums, color, alpha = _fused_grads(eng)
+    pk = oracle.Packed(sc)
+    off, idx = oracle.bin_tiles(pk, 32, effective_padding(w.cfg))
+    img, a_ref, sv = oracle.render_forward(pk, off, idx, 32, oracle.background(sc), True,
+                                           w.cfg.eps_skip)
+    ok, err = fwd_close(color, img)
+    assert ok, f"{name} fused colour rel err {err}"
+    ok, err = fwd_close(alpha, a_ref)
+    assert ok, f"{name} fused alpha rel err {err}"
+    P = img.shape[0] * img.shape[1]
+    diff = img - w.target
+    if w.loss.kind == "mse":
+        dI, dA = 2.0 * diff / diff.size, None
+        np.testing.assert_allclose(sums[0] / (3 * P), np.mean(diff**2), rtol=1e-5)
+    else:
+        ta = np.asarray(w.loss.target_alpha, dtype=np.float64)
+        mk = (ta > 0).astype(np.float64)
+        dI = 2.0 * diff * mk[..., None] / diff.size
+        dA = w.loss.alpha_w * 2.0 * (a_ref - ta) / P
+        np.testing.assert_allclose(sums[1], np.sum((diff * mk[..., None]) ** 2), rtol=1e-5)
+        np.testing.assert_allclose(sums[2], np.sum((a_ref - ta) ** 2), rtol=1e-5, atol=1e-9)
+    g_ref = oracle.backward(pk, sv, dI, dA)
+    ok, err = grad_close(g, g_ref)
+    assert ok, f"{name} fused grad rel err {err}"
+
+
+def test_fused_step_equals_two_kernel_path(torch_cuda, monkeypatch):
+    """K34 vs K3 + K4 over a graph-replayed rollout: same loss history and
+    parameters (both backwards are fp32 with the same operation order)."""
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.fit import StepEngine
+
+    w = synth.make_workload("c1")
+    w.cfg.num_iterations = 6
+    a = StepEngine(w.scene, w.cfg, w.loss, 6)
+    monkeypatch.setenv("PF_TWO_KERNEL", "1")
+    b = StepEngine(w.scene, w.cfg, w.loss, 6)
+    assert a.fused and not b.fused
+    a.run(6)
+    b.run(6)
+    np.testing.assert_allclose([h.loss for h in a.history()], [h.loss for h in b.history()],
+                               rtol=1e-6)
+    # Adam amplifies round-off-level gradient differences (atomic order) into
+    # +-lr steps on near-zero components: bar as in the oracle rollout test
+    close = np.isclose(a.params_host(), b.params_host(), rtol=1e-4, atol=1e-6)
+    assert close.mean() > 0.99, close.mean()
+
+
+def test_fused_step_deep_stack_spill(torch_cuda, oracle):
+    """Pixels with more than 4 contributions exercise the HBM spill of K34's
+    shared-memory stack: many overlapping primitives on a small canvas."""
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.fit import StepEngine, effective_padding
+
+    w = synth.make_workload("c1")
+    sc = w.scene
+    rng = np.random.default_rng(3)
+    for p in sc.primitives:  # pile everything into the centre
+        p.x = 128.0 + float(rng.uniform(-20, 20))
+        p.y = 128.0 + float(rng.uniform(-20, 20))
+        p.opacity_logit = -3.0  # low alpha: long lists before T runs out
+    eng = StepEngine(sc, w.cfg, w.loss, 1, use_graph=False)
+    g, sums, color, alpha = _fused_grads(eng)
+    pk = oracle.Packed(sc)
+    off, idx = oracle.bin_tiles(pk, 32, effective_padding(w.cfg))
+    img, a_ref, sv = oracle.render_forward(pk, off, idx, 32, oracle.background(sc), True,
+                                           w.cfg.eps_skip)
+    assert np.diff(sv["offsets"]).max() > 8  # the spill path is taken
+    ok, err = fwd_close(color, img)
+    assert ok, err
+    dI = 2.0 * (img - w.target) / img.size
+    g_ref = oracle.backward(pk, sv, dI, None)
+    ok, err = grad_close(g, g_ref)
+    assert ok, f"spill grad rel err {err}"
