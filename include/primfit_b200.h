@@ -96,6 +96,8 @@ int pf_atlas_quad(const double* tex, int texels, const int32_t* tpl_base, const 
  *                    preserve_aspect, else 1.0; raster.py:88-91)
  *   tpl_hyp  [n_tpl] hypot(1, max(1, q)) (host-computed, bit-identical to
  *                    math.hypot in bbox_half_side)
+ *   tpl_pbase [n_tpl] base of each template in the padded alpha plane of
+ *                    pf_atlas_pad (used by pf_fit_step's records), or NULL
  *   padding        bbox padding (fit.effective_padding, fit.py:338-341)
  *   rec      out   n * pf_record_bytes() bytes
  *   scratch        pf_bin_scratch_bytes(n, n_band_tiles, capacity) bytes (pf_scratch_init'ed);
@@ -103,8 +105,8 @@ int pf_atlas_quad(const double* tex, int texels, const int32_t* tpl_base, const 
  */
 int pf_preprocess(const double* params, const int32_t* template_id, const int32_t* zorder, int n,
                   const int32_t* tpl_base, const int32_t* tpl_w, const int32_t* tpl_h,
-                  const double* tpl_q, const double* tpl_hyp, int n_tpl,
-                  double alpha_max, double mu_blend, double padding,
+                  const double* tpl_q, const double* tpl_hyp, const int32_t* tpl_pbase,
+                  int n_tpl, double alpha_max, double mu_blend, double padding,
                   int W, int H, int tile, int ty_begin, int ty_end, int capacity,
                   void* rec, void* scratch, size_t scratch_bytes, void* stream);
 
@@ -131,7 +133,8 @@ int pf_adam_preprocess(double* params, double* grads, double* m, double* v, cons
                        double inv_3P, double inv_P, double* hist_loss, double* hist_psnr,
                        const int32_t* template_id, const int32_t* zorder, int n,
                        const int32_t* tpl_base, const int32_t* tpl_w, const int32_t* tpl_h,
-                       const double* tpl_q, const double* tpl_hyp, int n_tpl, double alpha_max,
+                       const double* tpl_q, const double* tpl_hyp, const int32_t* tpl_pbase,
+                       int n_tpl, double alpha_max,
                        double mu_blend, double padding, int W, int H, int tile, int ty_begin,
                        int ty_end, int capacity, void* rec, void* scratch, size_t scratch_bytes,
                        void* stream);
@@ -146,14 +149,17 @@ int pf_adam_preprocess(double* params, double* grads, double* m, double* v, cons
  *   bin_idx  out [capacity]           (TileBins.indices; first K valid)
  *   status   out int32[4]: [0] = K (total entries), [1] = overflow flag (K > capacity;
  *            nothing else is written then)
- *   rec, bin_cull  optional: with the records of pf_preprocess, also gather each
- *            entry's 32-byte cull record in bin order into bin_cull [capacity]
- *            (pf_forward then culls with coalesced loads); both NULL to skip
+ *   tile_classes  optional int32 [16 + 16 * n_band_tiles] (NULL to skip): the
+ *            tiles grouped by cost class (list length / 4, capped at 15) for
+ *            pf_fit_step's longest-first schedule -- [0..16) counts (accumulated:
+ *            zero before the first pf_bin; pf_fit_step re-zeroes them), then one
+ *            list of band tile indices per class.  Order inside a class is not
+ *            deterministic; it only steers scheduling.
  */
 int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity,
            void* scratch, size_t scratch_bytes,
            int32_t* bin_off, int32_t* bin_idx, int32_t* status,
-           const void* rec, void* bin_cull, void* stream);
+           int32_t* tile_classes, void* stream);
 
 /*
  * K3 — tiled front-to-back forward (16x16 tiles), optionally saving the
@@ -163,7 +169,6 @@ int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity
  * loss_spatial (fit.py:112-151).
  *   tex        [4][texels] planar float64 atlas (RGB planes read when mu_blend > 0)
  *   quad       float32 [texels][4] alpha quad atlas from pf_atlas_quad
- *   bin_cull   gathered cull records from pf_bin, or NULL
  *   bg4        float32 [H*W][4] per-pixel background (rgb, unused), or NULL for
  *              the solid (bg_r, bg_g, bg_b)
  *   saved      saved state (NULL = render only): pf_saved_bytes(capacity) bytes
@@ -181,7 +186,7 @@ int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity
  */
 int pf_forward(const void* rec, int n, const double* tex, const float* quad, int texels,
                const int32_t* bin_off, const int32_t* bin_idx, const int32_t* status,
-               const void* bin_cull, int W, int H, int ty_begin, int ty_end,
+               int W, int H, int ty_begin, int ty_end,
                double eps_skip, double mu_blend,
                double bg_r, double bg_g, double bg_b, const float* bg4,
                void* saved, long long saved_entries, int32_t* ent_n, float* img4,
@@ -207,26 +212,44 @@ int pf_backward(const void* rec, int n, const double* tex, const float* quad, in
                 double* grads, const double* part, double* sums, void* stream);
 
 /*
- * K34 — the fit step's render -> loss -> backward in one kernel (mu_blend == 0).
- * Replaces: the run_loop body render_forward(save=True) -> evaluate_loss ->
- * backward (fit.py:486-492; raster.py:290-363, fit.py:112-151, grad.py:134-187).
- * Same decisions, compositing, loss and gradients as pf_forward(save, loss) +
- * pf_backward, but the per-pixel contribution stack stays in shared memory
- * (depth >= 2 spills to `spill`) and dL/dI never leaves registers.
+ * Zero-padded fp32 alpha plane for pf_fit_step: template t occupies
+ * (tpl_w[t] + 1) x (tpl_h[t] + 1) texels from tpl_pbase[t] (row stride w + 1);
+ * the extra column / row are the reference's zero padding (_kernels.py:35-40).
+ * apad out: float32 [pad_texels]; pad_texels >= sum (w+1)(h+1), a multiple of 4.
+ */
+int pf_atlas_pad(const double* tex, int texels, const int32_t* tpl_base, const int32_t* tpl_pbase,
+                 const int32_t* tpl_w, const int32_t* tpl_h, int n_tpl, int pad_texels,
+                 float* apad, void* stream);
+
+/*
+ * K34 — the fit step's render -> loss -> backward in one persistent kernel
+ * (mu_blend == 0).  Replaces: the run_loop body render_forward(save=True) ->
+ * evaluate_loss -> backward (fit.py:486-492; raster.py:290-363, fit.py:112-151,
+ * grad.py:134-187).  Same decisions, compositing, loss and gradients as
+ * pf_forward(save, loss) + pf_backward, but the padded alpha atlas and the
+ * tile's records live in shared memory, the per-pixel contribution stack stays
+ * on chip (depth >= 2 spills to `spill`) and dL/dI never leaves registers.
+ *   apad    padded alpha plane from pf_atlas_pad (pad_texels floats)
+ *   apad64  the same plane as float64 (pad_texels doubles), or NULL; staged in
+ *           shared memory when it fits (no fp32->fp64 conversions on the hot path)
  *   spill   device scratch of pf_step_spill_bytes(capacity) bytes
  *   img4    optional out float32 [H*W][4] (r, g, b, alpha); NULL skips it
  *   part    out float64 [n_band_tiles * 8][3] per-warp loss partials (sum (I-t)^2,
  *           sum ((I-t)*mask)^2, sum (I_a-t_a)^2); fold them with pf_fold_loss or
  *           pass them to pf_adam_preprocess
  *   grads   float64 [n][8] accumulated into (zeroed by pf_adam_preprocess)
+ *   counters uint32[2] zeroed once at allocation (tile ticket; self-resetting)
+ *   tile_classes  pf_bin's tile classes of this band (longest-first schedule; the
+ *           counts are re-zeroed for the next pf_bin), or NULL (tile order)
  */
 size_t pf_step_spill_bytes(int capacity);
-int pf_fit_step(const void* rec, int n, const double* tex, const float* quad, int texels,
-                const int32_t* bin_off, const int32_t* bin_idx, const int32_t* status,
+int pf_fit_step(const void* rec, int n, const double* tex, const float* apad,
+                const double* apad64, int pad_texels, int texels, const int32_t* bin_off, const int32_t* bin_idx, const int32_t* status,
                 int W, int H, int ty_begin, int ty_end, double eps_skip,
                 double bg_r, double bg_g, double bg_b, const float* bg4,
                 int loss_kind, const float* tgt4, double alpha_w, double inv_3P, double inv_P,
-                void* spill, float* img4, double* part, double* grads, void* stream);
+                void* spill, float* img4, double* part, double* grads, uint32_t* counters,
+                const int32_t* tile_classes, void* stream);
 
 /* Fixed-order fold of n_part partial triples into sums[3] (deterministic). */
 int pf_fold_loss(const double* part, int n_part, double* sums, void* stream);

@@ -40,28 +40,29 @@ SIGNATURES: dict[str, tuple] = {
     "pf_saved_bytes": (_Z, [_I]),
     "pf_preprocess": (
         _I,
-        [_P, _P, _P, _I, _P, _P, _P, _P, _P, _I, _D, _D, _D, _I, _I, _I, _I, _I, _I, _P, _P, _Z,
-         _P],
+        [_P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _I, _D, _D, _D, _I, _I, _I, _I, _I, _I, _P, _P,
+         _Z, _P],
     ),
     "pf_scratch_init": (_I, [_P, _Z, _P, _I, _I, _P]),
     "pf_adam_preprocess": (
         _I,
         [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _D, _D, _P, _P, _I, _I, _D, _D, _D, _P,
-         _P, _P, _P, _I, _P, _P, _P, _P, _P, _I, _D, _D, _D, _I, _I, _I, _I, _I, _I, _P, _P,
-         _Z, _P],
+         _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _I, _D, _D, _D, _I, _I, _I, _I, _I, _I, _P,
+         _P, _Z, _P],
     ),
     "pf_atlas_quad": (_I, [_P, _I, _P, _P, _P, _I, _P, _P]),
-    "pf_bin": (_I, [_I, _I, _I, _I, _I, _I, _I, _P, _Z, _P, _P, _P, _P, _P, _P]),
+    "pf_atlas_pad": (_I, [_P, _I, _P, _P, _P, _P, _I, _I, _P, _P]),
+    "pf_bin": (_I, [_I, _I, _I, _I, _I, _I, _I, _P, _Z, _P, _P, _P, _P, _P]),
     "pf_forward": (
         _I,
-        [_P, _I, _P, _P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _D, _D, _D, _D, _D, _P,
+        [_P, _I, _P, _P, _I, _P, _P, _P, _I, _I, _I, _I, _D, _D, _D, _D, _D, _P,
          _P, C.c_longlong, _P, _P, _I, _P, _D, _D, _D, _P, _P, _P],
     ),
     "pf_step_spill_bytes": (_Z, [_I]),
     "pf_fit_step": (
         _I,
-        [_P, _I, _P, _P, _I, _P, _P, _P, _I, _I, _I, _I, _D, _D, _D, _D, _P, _I, _P, _D, _D, _D,
-         _P, _P, _P, _P, _P],
+        [_P, _I, _P, _P, _P, _I, _I, _P, _P, _P, _I, _I, _I, _I, _D, _D, _D, _D, _P, _I, _P, _D,
+         _D, _D, _P, _P, _P, _P, _P, _P, _P],
     ),
     "pf_fold_loss": (_I, [_P, _I, _P, _P]),
     "pf_backward": (

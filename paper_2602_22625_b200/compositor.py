@@ -71,12 +71,30 @@ class DeviceAtlas:
         self.d_hyp = torch.from_numpy(self.hyp).to(dev)
         # alpha quad atlas (four bilinear taps per texel, zero padded), built on device
         self.quad = torch.zeros(max(self.texels, 1) * 4, dtype=torch.float32, device=dev)
+        # zero-padded fp32 alpha plane ((w+1) x (h+1) per template) for pf_fit_step
+        psz = (self.tw.astype(np.int64) + 1) * (self.th.astype(np.int64) + 1)
+        self.pbase = np.concatenate(([0], np.cumsum(psz)))[:-1].astype(np.int32)
+        self.pad_texels = int(-(-max(int(psz.sum()), 1) // 4) * 4)
+        self.d_pbase = torch.from_numpy(self.pbase).to(dev)
+        self.apad = torch.zeros(self.pad_texels, dtype=torch.float32, device=dev)
+        self.apad64 = torch.zeros(self.pad_texels, dtype=torch.float64, device=dev)
         if self.texels:
             lib = nat.load()
             nat.check(lib.pf_atlas_quad(self.tex.data_ptr(), self.texels, self.d_base.data_ptr(),
                                         self.d_w.data_ptr(), self.d_h.data_ptr(),
                                         self.n_templates, self.quad.data_ptr(),
                                         _stream_handle()), "pf_atlas_quad")
+            nat.check(lib.pf_atlas_pad(self.tex.data_ptr(), self.texels, self.d_base.data_ptr(),
+                                       self.d_pbase.data_ptr(), self.d_w.data_ptr(),
+                                       self.d_h.data_ptr(), self.n_templates, self.pad_texels,
+                                       self.apad.data_ptr(), _stream_handle()), "pf_atlas_pad")
+            # float64 copy of the padded plane (exact: built from the float64 atlas)
+            pad64 = np.zeros(self.pad_texels, dtype=np.float64)
+            for a_, pb, w_, h_ in zip(rgbas, self.pbase, self.tw, self.th):
+                blk = np.zeros((h_ + 1, w_ + 1), dtype=np.float64)
+                blk[:h_, :w_] = a_[:, :, 3]
+                pad64[pb : pb + blk.size] = blk.reshape(-1)
+            self.apad64.copy_(torch.from_numpy(pad64))
 
 
 def bin_capacity(scales: np.ndarray, tids: np.ndarray, hyp: np.ndarray, padding: float,
@@ -137,12 +155,17 @@ class Compositor:
                                            _stream_handle()), "pf_scratch_init")
         self.bin_off = torch.zeros(self.n_tiles + 1, dtype=torch.int32, device=dev)
         self.bin_idx = torch.zeros(max(self.capacity, 1), dtype=torch.int32, device=dev)
-        # optional gather of cull records in bin order (pf_bin/pf_forward bin_cull):
-        # measured slower end to end at c3 (the gather costs more in K2 than the
-        # coalesced cull saves in K3), so it is off
-        self.bin_cull = None
+        # tile cost classes for pf_fit_step's longest-first schedule (fused path only)
+        self.tile_classes = None
         self.status = torch.zeros(4, dtype=torch.int32, device=dev)
         self._saved_alloc = False
+
+    def enable_step_schedule(self) -> None:
+        """Have pf_bin emit tile cost classes for pf_fit_step's longest-first
+        schedule (call before the first bin() of a fused fit loop)."""
+        if self.tile_classes is None:
+            self.tile_classes = torch.zeros(16 * (1 + max(self.n_tiles, 1)), dtype=torch.int32,
+                                            device=self.device)
 
     # -- buffers for rendering (allocated lazily; binning-only users skip them)
     def alloc_render(self, save: bool, loss: bool = False):
@@ -177,10 +200,10 @@ class Compositor:
             self.lib.pf_preprocess(
                 params.data_ptr(), self.d_tid.data_ptr(), self.d_zorder.data_ptr(), self.n,
                 a.d_base.data_ptr(), a.d_w.data_ptr(), a.d_h.data_ptr(), a.d_q.data_ptr(),
-                a.d_hyp.data_ptr(), a.n_templates, self.alpha_max, self.mu_blend, self.padding,
-                self.W, self.H, self.tile, self.band.ty_begin, self.band.ty_end, self.capacity,
-                self.rec.data_ptr(), self.scratch.data_ptr(), self.scratch_bytes,
-                _stream_handle(stream)),
+                a.d_hyp.data_ptr(), a.d_pbase.data_ptr(), a.n_templates, self.alpha_max,
+                self.mu_blend, self.padding, self.W, self.H, self.tile, self.band.ty_begin,
+                self.band.ty_end, self.capacity, self.rec.data_ptr(), self.scratch.data_ptr(),
+                self.scratch_bytes, _stream_handle(stream)),
             "pf_preprocess")
         return st
 
@@ -200,10 +223,10 @@ class Compositor:
                 nat.ptr(part), self.n_part if part is not None else 0, int(loss_kind), float(alpha_w), 1.0 / (3.0 * P), 1.0 / P, nat.ptr(hist_loss),
                 nat.ptr(hist_psnr), self.d_tid.data_ptr(), self.d_zorder.data_ptr(), self.n,
                 a.d_base.data_ptr(), a.d_w.data_ptr(), a.d_h.data_ptr(), a.d_q.data_ptr(),
-                a.d_hyp.data_ptr(), a.n_templates, self.alpha_max, self.mu_blend, self.padding,
-                self.W, self.H, self.tile, self.band.ty_begin, self.band.ty_end, self.capacity,
-                self.rec.data_ptr(), self.scratch.data_ptr(), self.scratch_bytes,
-                _stream_handle(stream)),
+                a.d_hyp.data_ptr(), a.d_pbase.data_ptr(), a.n_templates, self.alpha_max,
+                self.mu_blend, self.padding, self.W, self.H, self.tile, self.band.ty_begin,
+                self.band.ty_end, self.capacity, self.rec.data_ptr(), self.scratch.data_ptr(),
+                self.scratch_bytes, _stream_handle(stream)),
             "pf_adam_preprocess")
 
     def bin(self, stream=None) -> None:
@@ -213,8 +236,7 @@ class Compositor:
                             self.band.ty_end, self.capacity, self.scratch.data_ptr(),
                             self.scratch_bytes, self.bin_off.data_ptr(),
                             self.bin_idx.data_ptr(), self.status.data_ptr(),
-                            self.rec.data_ptr(), nat.ptr(self.bin_cull),
-                            _stream_handle(stream)),
+                            nat.ptr(self.tile_classes), _stream_handle(stream)),
             "pf_bin")
 
     def check_overflow(self) -> int:
@@ -238,7 +260,7 @@ class Compositor:
                 self.rec.data_ptr(), self.n, self.atlas.tex.data_ptr(),
                 self.atlas.quad.data_ptr(), self.atlas.texels,
                 self.bin_off.data_ptr(), self.bin_idx.data_ptr(), self.status.data_ptr(),
-                p(self.bin_cull), self.W, self.H, self.band.ty_begin, self.band.ty_end,
+                self.W, self.H, self.band.ty_begin, self.band.ty_end,
                 float(eps_skip), self.mu_blend, float(bg_rgb[0]), float(bg_rgb[1]),
                 float(bg_rgb[2]), p(bg4), p(self.saved) if save else None,
                 self.saved_entries if save else 0, p(self.ent_n) if save else None,
@@ -260,6 +282,7 @@ class Compositor:
         if not hasattr(self, "spill"):
             nbytes = int(self.lib.pf_step_spill_bytes(max(self.capacity, 1)))
             self.spill = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            self.step_ctr = torch.zeros(2, dtype=torch.int32, device=dev)
             if not hasattr(self, "part"):
                 self.part = torch.zeros(max(self.n_tiles, 1) * 8 * 3, dtype=torch.float64,
                                         device=dev)
@@ -270,20 +293,22 @@ class Compositor:
         nat.check(
             self.lib.pf_fit_step(
                 self.rec.data_ptr(), self.n, self.atlas.tex.data_ptr(),
-                self.atlas.quad.data_ptr(), self.atlas.texels,
+                self.atlas.apad.data_ptr(), self.atlas.apad64.data_ptr(), self.atlas.pad_texels,
+                self.atlas.texels,
                 self.bin_off.data_ptr(), self.bin_idx.data_ptr(), self.status.data_ptr(),
                 self.W, self.H, self.band.ty_begin, self.band.ty_end, float(eps_skip),
                 float(bg_rgb[0]), float(bg_rgb[1]), float(bg_rgb[2]), p(bg4), int(loss_kind),
                 tgt4.data_ptr(), float(alpha_w), 1.0 / (3.0 * Pt), 1.0 / Pt,
                 self.spill.data_ptr(), p(self.img4) if image else None, self.part.data_ptr(),
-                grads.data_ptr(), _stream_handle(stream)),
+                grads.data_ptr(), self.step_ctr.data_ptr(), nat.ptr(self.tile_classes),
+                _stream_handle(stream)),
             "pf_fit_step")
         if sums is not None:
             self.fold_loss(sums, stream)
 
     @property
     def n_part(self) -> int:
-        """Loss partial triples per launch (8 warps per band tile)."""
+        """Loss partial triples per pf_fit_step launch (one per warp: 8 per band tile)."""
         return self.n_tiles * 8
 
     def fold_loss(self, sums: torch.Tensor, stream=None) -> None:

@@ -141,8 +141,8 @@ extern "C" int pf_adam(double* params, double* grads, double* m, double* v, cons
   return (int)cudaGetLastError();
 }
 
-extern "C" int pf_abi_version(void) { return 1; }
-extern "C" size_t pf_record_bytes(void) { return sizeof(RecF) + sizeof(RecG) + sizeof(RecC); }
+extern "C" int pf_abi_version(void) { return 2; }
+extern "C" size_t pf_record_bytes(void) { return sizeof(RecF) + sizeof(RecG) + sizeof(RecC) + sizeof(RecS); }
 extern "C" int pf_render_tile(void) { return kTile; }
 extern "C" long long pf_saved_capacity(int capacity) {
   return (long long)capacity * (long long)kTilePix;

@@ -67,6 +67,8 @@ struct PreArgs {
   RecF* recf;
   RecG* recg;
   RecC* recc;
+  RecS* recs;
+  const int32_t* tpl_pbase;  // padded-atlas base per template (RecS)
   BinScratch s;
   AdamPart ad;
 };
@@ -227,6 +229,52 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
         }
       }
     }
+    {
+      // step record (RecS, pf_common.cuh): affine texel map + gradient coefficients
+      const double hw = 0.5 * (double)(wt - 1), hh = 0.5 * (double)(ht - 1);
+      const double au = hw * ct * inv_s, bu = hw * st * inv_s;
+      const double cu = hw * (1.0 - (ct * x + st * y) * inv_s);
+      const double av = -hh * st * inv_sq, bv = hh * ct * inv_sq;
+      const double cv = hh * (1.0 + (st * x - ct * y) * inv_sq);
+      double2* ps = reinterpret_cast<double2*>(a.recs + i);
+      float4* ps4 = reinterpret_cast<float4*>(a.recs + i);
+      const double sa_d = __dmul_rn(a.alpha_max, sig);
+      switch (c) {
+        case 0: ps[0] = make_double2(au, bu); break;
+        case 1: ps[1] = make_double2(cu, av); break;
+        case 2: ps[2] = make_double2(bv, cv); break;
+        case 3: ps[3] = make_double2(sa_d, __dmul_rn(omm, sc0)); break;
+        case 4: ps[4] = make_double2(__dmul_rn(omm, sc1), __dmul_rn(omm, sc2)); break;
+        case 5: ps[5] = make_double2((double)(wt - 1), (double)(ht - 1)); break;
+        case 6: {
+          // guard band of the affine U, V: >= 1e4 x their error bound
+          const double du = 1e-11 * (fabs(au) * a.W + fabs(bu) * a.H + fabs(cu) + (wt - 1) + 1.0);
+          const double dv = 1e-11 * (fabs(av) * a.W + fabs(bv) * a.H + fabs(cv) + (ht - 1) + 1.0);
+          ps[6] = make_double2(fmax(du, dv), 0.0);
+          break;
+        }
+        default:
+          reinterpret_cast<int4*>(ps4)[7] =
+              make_int4(a.tpl_pbase ? __ldg(a.tpl_pbase + t) : 0, wt + 1, i, 0);
+          break;
+      }
+      switch (c) {
+        case 0:
+          ps4[8] = make_float4((float)(a.alpha_max * sig * (1.0 - sig)), (float)(sc0 * (1.0 - sc0)),
+                               (float)(sc1 * (1.0 - sc1)), (float)(sc2 * (1.0 - sc2)));
+          break;
+        case 1:
+          ps4[9] = make_float4((float)(-ct * inv_s), (float)(st * inv_sq), (float)(-st * inv_s),
+                               (float)(-ct * inv_sq));
+          break;
+        case 2: ps4[10] = make_float4((float)inv_s, (float)q, (float)(s * inv_sq), (float)hw); break;
+        case 3: ps4[11] = make_float4((float)hh, (float)omm, (float)sa_d, 0.0f); break;
+        case 4:
+          ps4[12] = make_float4((float)(omm * sc0), (float)(omm * sc1), (float)(omm * sc2), 0.0f);
+          break;
+        default: break;
+      }
+    }
     if (c == 0) {
       double lo_x = fmax(ceil(__dsub_rn(x, r)), 0.0);
       double hi_x = fmin(floor(__dadd_rn(x, r)), (double)(a.W - 1));
@@ -306,8 +354,8 @@ struct RowArgs {
   int32_t* bin_off;
   int32_t* bin_idx;
   int32_t* status;
-  const RecC* recc;  // per-primitive cull records (NULL: no gather)
-  RecC* bin_cull;    // out: cull records gathered in bin order (coalesced forward cull)
+  int32_t* classes;  // optional tile cost classes (see kTileClasses), or NULL
+  int n_tiles;
 };
 
 constexpr int kRowThreads = 1024;
@@ -317,7 +365,9 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
   extern __shared__ int2 rsm[];  // [smem_list] row list, then [ntx] column counters
   __shared__ int ws[32];
   __shared__ int s_rl, s_base, s_rbase;
+  __shared__ int s_ccnt[kTileClasses], s_cbase[kTileClasses];
   int* col = reinterpret_cast<int*>(rsm + a.smem_list);
+  int* ccls = col + a.ntx;  // per-column tile class | rank within the block << 8
   const int r = blockIdx.x, ty = a.ty_begin + r;
   const int tid = threadIdx.x;
 
@@ -356,6 +406,7 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
     s_rbase = rbase;
   }
   for (int c = tid; c < a.ntx; c += kRowThreads) col[c] = 0;
+  if (tid < kTileClasses) s_ccnt[tid] = 0;
   for (int j = j0; j < j1; ++j) {
     const int4 rc = a.s.rect[j];
     if (rc.x > rc.z || rc.y > ty || ty > rc.w) continue;
@@ -385,8 +436,23 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
     a.bin_off[r * a.ntx + c] = run;
     col[c] = run;
     run += v;
+    if (a.classes) {
+      // longest-first schedule for pf_fit_step: tile -> class list of its length
+      const int cl = tile_class(v);
+      const int rank = atomicAdd(&s_ccnt[cl], 1);
+      ccls[c] = cl | (rank << 8);
+    }
   }
   __syncthreads();
+  if (a.classes) {
+    if (tid < kTileClasses) s_cbase[tid] = s_ccnt[tid] ? atomicAdd(a.classes + tid, s_ccnt[tid]) : 0;
+    __syncthreads();
+    for (int c = c0; c < c1; ++c) {
+      const int cl = ccls[c] & 0xff, rank = ccls[c] >> 8;
+      const int pos = s_cbase[cl] + rank;
+      if (pos < a.n_tiles) a.classes[kTileClasses + cl * a.n_tiles + pos] = r * a.ntx + c;
+    }
+  }
 
   // (c) one warp per column: ordered ballot walk of the row list
   const int lane = tid & 31, warp = tid >> 5;
@@ -406,7 +472,6 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
         const int p = out + __popc(ball & ((1u << lane) - 1u));
         const int i = __ldg(a.s.zprim + j);
         a.bin_idx[p] = i;
-        if (a.bin_cull) a.bin_cull[p] = a.recc[i];
       }
       out += __popc(ball);
     }
@@ -436,6 +501,31 @@ __global__ void k_atlas_quad(QuadArgs a) {
                           (float)at(u + 1, v + 1));
 }
 
+// Zero-padded fp32 alpha plane (RecS.pbase / wp): template t occupies
+// (wt + 1) x (ht + 1) texels from pbase[t]; the extra column and row are the
+// reference's zero padding (_kernels.py:35-40), so a bilinear sample with the
+// cell inside the box needs no bounds checks.
+struct PadArgs {
+  const double* tex;
+  int texels, n_tpl, pad_texels;
+  const int32_t* base;
+  const int32_t* pbase;
+  const int32_t* w;
+  const int32_t* h;
+  float* apad;
+};
+
+__global__ void k_atlas_pad(PadArgs a) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= a.pad_texels) return;
+  int t = 0;
+  while (t + 1 < a.n_tpl && a.pbase[t + 1] <= g) ++t;
+  const int wt = a.w[t], ht = a.h[t], local = g - a.pbase[t];
+  const int v = local / (wt + 1), u = local - v * (wt + 1);
+  const double* al = a.tex + 3 * (size_t)a.texels + a.base[t];
+  a.apad[g] = (t < a.n_tpl && u < wt && v < ht) ? (float)al[v * wt + u] : 0.0f;
+}
+
 constexpr int kRowSmemList = 4096;  // row-list entries kept in shared memory (32 KB)
 
 }  // namespace pf
@@ -460,9 +550,10 @@ static bool band_ok(int W, int H, int tile, int ty_begin, int ty_end, int* ntx, 
 static int fill_pre_args(PreArgs& a, double* params, const int32_t* template_id,
                          const int32_t* zorder, int n, const int32_t* tpl_base,
                          const int32_t* tpl_w, const int32_t* tpl_h, const double* tpl_q,
-                         const double* tpl_hyp, int n_tpl, double alpha_max, double mu_blend,
-                         double padding, int W, int H, int tile, int ty_begin, int ty_end,
-                         int capacity, void* rec, void* scratch, size_t scratch_bytes) {
+                         const double* tpl_hyp, const int32_t* tpl_pbase, int n_tpl,
+                         double alpha_max, double mu_blend, double padding, int W, int H,
+                         int tile, int ty_begin, int ty_end, int capacity, void* rec,
+                         void* scratch, size_t scratch_bytes) {
   int ntx, n_rows;
   if (n < 0 || n_tpl < 0 || capacity < 0 || !band_ok(W, H, tile, ty_begin, ty_end, &ntx, &n_rows))
     return PF_ERR_ARG;
@@ -491,6 +582,8 @@ static int fill_pre_args(PreArgs& a, double* params, const int32_t* template_id,
   a.recf = (RecF*)rec;
   a.recg = (RecG*)((char*)rec + sizeof(RecF) * (size_t)n);
   a.recc = (RecC*)((char*)rec + (sizeof(RecF) + sizeof(RecG)) * (size_t)n);
+  a.recs = (RecS*)((char*)rec + (sizeof(RecF) + sizeof(RecG) + sizeof(RecC)) * (size_t)n);
+  a.tpl_pbase = tpl_pbase;
   a.s = carve(scratch, n, capacity);
   a.ad = AdamPart{};
   return PF_OK;
@@ -524,13 +617,14 @@ extern "C" int pf_scratch_init(void* scratch, size_t scratch_bytes, const int32_
 extern "C" int pf_preprocess(const double* params, const int32_t* template_id,
                              const int32_t* zorder, int n, const int32_t* tpl_base,
                              const int32_t* tpl_w, const int32_t* tpl_h, const double* tpl_q,
-                             const double* tpl_hyp, int n_tpl, double alpha_max, double mu_blend,
-                             double padding, int W, int H, int tile, int ty_begin, int ty_end,
-                             int capacity, void* rec, void* scratch, size_t scratch_bytes,
-                             void* stream) {
+                             const double* tpl_hyp, const int32_t* tpl_pbase, int n_tpl,
+                             double alpha_max, double mu_blend, double padding, int W, int H,
+                             int tile, int ty_begin, int ty_end, int capacity, void* rec,
+                             void* scratch, size_t scratch_bytes, void* stream) {
   PreArgs a;
   const int rc = fill_pre_args(a, const_cast<double*>(params), template_id, zorder, n, tpl_base,
-                               tpl_w, tpl_h, tpl_q, tpl_hyp, n_tpl, alpha_max, mu_blend, padding,
+                               tpl_w, tpl_h, tpl_q, tpl_hyp, tpl_pbase, n_tpl, alpha_max,
+                               mu_blend, padding,
                                W, H, tile, ty_begin, ty_end, capacity, rec, scratch,
                                scratch_bytes);
   if (rc != PF_OK) return rc;
@@ -547,13 +641,14 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
                                   double* hist_psnr, const int32_t* template_id,
                                   const int32_t* zorder, int n, const int32_t* tpl_base,
                                   const int32_t* tpl_w, const int32_t* tpl_h, const double* tpl_q,
-                                  const double* tpl_hyp, int n_tpl, double alpha_max,
-                                  double mu_blend, double padding, int W, int H, int tile,
+                                  const double* tpl_hyp, const int32_t* tpl_pbase, int n_tpl,
+                                  double alpha_max, double mu_blend, double padding, int W, int H,
+                                  int tile,
                                   int ty_begin, int ty_end, int capacity, void* rec, void* scratch,
                                   size_t scratch_bytes, void* stream) {
   PreArgs a;
   const int rc = fill_pre_args(a, params, template_id, zorder, n, tpl_base, tpl_w, tpl_h, tpl_q,
-                               tpl_hyp, n_tpl, alpha_max, mu_blend, padding, W, H, tile,
+                               tpl_hyp, tpl_pbase, n_tpl, alpha_max, mu_blend, padding, W, H, tile,
                                ty_begin, ty_end, capacity, rec, scratch, scratch_bytes);
   if (rc != PF_OK) return rc;
   if (!iter || !lr_table || !bc1_table || !bc2_table || (n > 0 && (!grads || !m || !v)))
@@ -586,8 +681,7 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
 
 extern "C" int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity,
                       void* scratch, size_t scratch_bytes, int32_t* bin_off, int32_t* bin_idx,
-                      int32_t* status, const void* rec, void* bin_cull, void* stream) {
-  if (bin_cull && !rec) return PF_ERR_ARG;
+                      int32_t* status, int32_t* tile_classes, void* stream) {
   int ntx, n_rows;
   if (n < 0 || capacity < 0 || !band_ok(W, H, tile, ty_begin, ty_end, &ntx, &n_rows))
     return PF_ERR_ARG;
@@ -611,10 +705,9 @@ extern "C" int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, i
   ra.bin_off = bin_off;
   ra.bin_idx = bin_idx;
   ra.status = status;
-  ra.recc = rec ? (const RecC*)((const char*)rec + (sizeof(RecF) + sizeof(RecG)) * (size_t)n)
-                : nullptr;
-  ra.bin_cull = (RecC*)bin_cull;
-  const size_t smem = sizeof(int2) * kRowSmemList + sizeof(int) * (size_t)ntx;
+  ra.classes = tile_classes;
+  ra.n_tiles = n_rows * ntx;
+  const size_t smem = sizeof(int2) * kRowSmemList + 2 * sizeof(int) * (size_t)ntx;
   static bool attr_set = false;
   if (smem > 48 * 1024 || !attr_set) {
     cudaFuncSetAttribute(k_bin_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -633,5 +726,17 @@ extern "C" int pf_atlas_quad(const double* tex, int texels, const int32_t* tpl_b
   if (texels == 0) return PF_OK;
   QuadArgs a{tex, texels, n_tpl, tpl_base, tpl_w, tpl_h, reinterpret_cast<float4*>(quad)};
   k_atlas_quad<<<div_up(texels, 256), 256, 0, (cudaStream_t)stream>>>(a);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int pf_atlas_pad(const double* tex, int texels, const int32_t* tpl_base,
+                            const int32_t* tpl_pbase, const int32_t* tpl_w, const int32_t* tpl_h,
+                            int n_tpl, int pad_texels, float* apad, void* stream) {
+  if (texels < 0 || n_tpl < 0 || pad_texels < 0 ||
+      (pad_texels > 0 && (!tex || !tpl_base || !tpl_pbase || !tpl_w || !tpl_h || !apad)))
+    return PF_ERR_ARG;
+  if (pad_texels == 0 || n_tpl == 0) return PF_OK;
+  PadArgs a{tex, texels, n_tpl, pad_texels, tpl_base, tpl_pbase, tpl_w, tpl_h, apad};
+  k_atlas_pad<<<div_up(pad_texels, 256), 256, 0, (cudaStream_t)stream>>>(a);
   return (int)cudaGetLastError();
 }

@@ -57,6 +57,40 @@ struct __align__(16) RecC {
 };
 static_assert(sizeof(RecC) == 32, "RecC must be 32 bytes");
 
+// Step record (208 bytes): everything pf_fit_step reads per list entry, staged
+// in shared memory once per tile by TMA bulk copies.
+//   forward  texel coordinates as one affine map per axis,
+//              U = au*x + bu*y + cu,  V = av*x + bv*y + cv   (float64, 2 DFMA each)
+//            -- the reference's per-pair chain (_kernels.py:106-114) folded into
+//            per-primitive coefficients.  They differ from the reference's U, V
+//            by < 1e-10 texel; `delta` (>= 1e4 x that bound) is the guard band:
+//            a pair whose U or V lies within delta of a box edge re-takes the
+//            inside test with the reference's exact op order (texel_coords on
+//            RecF), so every inside/outside decision matches the reference.
+//            Opacity / colours in float64 for the compositing (no conversions on
+//            the hot path); pbase/wp address the zero-padded alpha plane.
+//   backward fp32 gradient coefficients (as RecG) and gidx = the row of grads.
+struct __align__(16) RecS {
+  double au, bu, cu, av, bv, cv;
+  double sa, c0, c1, c2;        // alpha_max*sig, (1-mu)*sigmoid(c)
+  double wm1, hm1;              // wt - 1, ht - 1
+  double delta, pad_d;          // guard band of the affine U, V (texels)
+  int32_t pbase, wp;            // padded-atlas base, padded row stride (wt + 1)
+  int32_t gidx, pad_i;          // primitive index (row of params / grads)
+  float sd, cd0, cd1, cd2;      // alpha_max*sig*(1-sig), sc*(1-sc)
+  float gxu, gxv, gyu, gyv;     // -ct/s, st/(s q), -st/s, -ct/(s q)
+  float inv_s, q, inv_q, hw;    // 1/s, aspect, 1/aspect, 0.5 (wt - 1)
+  float hh, omm, saf, pad_f;    // 0.5 (ht - 1), 1 - mu_blend, (float)sa
+  float c0f, c1f, c2f, pad_g;   // (float)c
+};
+static_assert(sizeof(RecS) == 208, "RecS must be 208 bytes");
+
+// Tile cost classes for pf_fit_step's longest-first schedule: class of a tile
+// = min(kTileClasses - 1, list length / 4).  pf_bin's optional tile_classes
+// buffer: int32 [kTileClasses] counts, then [kTileClasses][n_tiles] tile lists.
+constexpr int kTileClasses = 16;
+__host__ __device__ inline int tile_class(int L) { return L / 4 < kTileClasses - 1 ? L / 4 : kTileClasses - 1; }
+
 // Warp sub-tile shape (8 warps cover a 16x16 tile) -- used by the cull record.
 constexpr int kWarpW = 8, kWarpH = 4;
 

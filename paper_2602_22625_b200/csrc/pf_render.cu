@@ -82,7 +82,6 @@ __device__ __forceinline__ bool may_touch(const RecC* __restrict__ rc, float cx,
 struct FwdArgs {
   const RecF* recf;
   const RecC* recc;
-  const RecC* bin_cull;  // cull records in bin order from pf_bin, or NULL
   const double* tex;     // planar [4][texels]
   const float4* quad;    // alpha quad atlas [texels]
   int texels;
@@ -136,7 +135,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_forward(FwdArgs a) {
     bool cand = false;
     if (sub + lane < L) {
       my_i = __ldg(a.bin_idx + b0 + sub + lane);
-      cand = may_touch(a.bin_cull ? a.bin_cull + b0 + sub + lane : a.recc + my_i, cx, cy);
+      cand = may_touch(a.recc + my_i, cx, cy);
     }
     unsigned mask = __ballot_sync(kFull, cand);
     while (mask) {
@@ -452,7 +451,7 @@ extern "C" size_t pf_saved_bytes(int capacity) {
 
 extern "C" int pf_forward(const void* rec, int n, const double* tex, const float* quad,
                           int texels, const int32_t* bin_off, const int32_t* bin_idx,
-                          const int32_t* status, const void* bin_cull, int W, int H,
+                          const int32_t* status, int W, int H,
                           int ty_begin, int ty_end, double eps_skip, double mu_blend, double bg_r,
                           double bg_g, double bg_b, const float* bg4, void* saved,
                           long long saved_entries, int32_t* ent_n, float* img4, int loss_kind,
@@ -472,7 +471,6 @@ extern "C" int pf_forward(const void* rec, int n, const double* tex, const float
   FwdArgs a;
   a.recf = (const RecF*)rec;
   a.recc = (const RecC*)((const char*)rec + (sizeof(RecF) + sizeof(RecG)) * (size_t)n);
-  a.bin_cull = (const RecC*)bin_cull;
   a.tex = tex;
   a.quad = (const float4*)quad;
   a.texels = texels;

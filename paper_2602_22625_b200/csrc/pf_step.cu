@@ -1,4 +1,4 @@
-// K34: the fit step's render -> loss -> backward as ONE kernel.
+// K34: the fit step's render -> loss -> backward as ONE persistent kernel.
 //
 // Reference: the loop body of run_loop (pkg/src/primfit/fit.py:486-492):
 //   out, saved = render_forward(scene, bins, bg, save=True)   raster.py:290-363
@@ -7,27 +7,31 @@
 // Both losses the fit uses (MSE, spatial) are pixel-local: dL/dI and dL/dA of
 // a pixel depend only on that pixel's colour and alpha.  So the thread that
 // composites a pixel already holds everything its backward needs, and the
-// saved contribution lists never have to leave the SM:
+// saved contribution lists never leave the SM.
 //
-//   forward phase  - identical decisions and float64 compositing to
-//                    k_forward (pf_render.cu); each contributing (pixel, entry)
-//                    pushes a 32-byte record (list position, primitive, incoming
-//                    T, mask m, dm/dU, dm/dV, u, v) into a per-thread shared-memory
-//                    stack (kStepKS deep; deeper entries spill to HBM at a slot
-//                    unique to (tile, depth, pixel) -- 0.5% of pixels at c3);
-//   loss           - pixel-local loss, dL/dI, dL/dA in registers; per-warp fp32
-//                    partials; the last block to finish (atomic ticket) folds all
-//                    partials into sums[] in fixed order (deterministic);
-//   backward phase - the same back-to-front warp walk as k_backward (list
-//                    position picked with __reduce_max_sync) over the stack, with
-//                    the tile's fp32 gradient records staged in shared memory by
-//                    cp.async during the forward phase; warp transpose-butterfly
-//                    reduction and float64 RED atomics into grads.
-//
-// Versus K3 + K4 this removes the saved-entry, ent_n and dL/dI round trips
-// through L2/HBM, the backward kernel's whole dependent prologue and the
-// backward's atlas re-fetch (m, dm/dU, dm/dV are stored, not re-sampled).
+// Layout per block (persistent, one CTA per SM slot, tiles from an atomic ticket):
+//   shared  zero-padded fp32 alpha plane of the whole atlas (loaded once per
+//           block; 36 KB at c3), the tile's step records (RecS, 160 B) and cull
+//           records (RecC, 32 B) staged by cp.async in chunks of kS2Stage list
+//           entries, and a per-thread contribution stack kS2KS deep (deeper
+//           entries spill to HBM at a slot unique to (tile, depth, pixel)).
+//   forward  per warp (8x4 pixels): lane-parallel footprint cull of 32 list
+//           entries, then per surviving entry the affine float64 texel map
+//           (2 DFMA per axis; the reference's exact op order re-runs only inside
+//           a guard band around the box edges / the eps threshold), 4 shared
+//           taps, float64 bilinear, eps test, float64 compositing (T, C) --
+//           identical decisions to _kernels.py:183-255 -- and a 32-byte stack
+//           push (list position, incoming T, m, dm/dU, dm/dV, u, v).
+//   loss     pixel-local loss, dL/dI, dL/dA in registers; per-tile partial sums
+//           written at a fixed slot (the fold in pf_adam_preprocess is fixed-order,
+//           so the loss value is deterministic).
+//   backward the same back-to-front warp walk as k_backward (list position picked
+//           with __reduce_max_sync) over the stack, records from shared memory;
+//           warp transpose-butterfly reduction and float64 RED atomics into grads.
 // mu_blend > 0 (colour from the texture) keeps the two-kernel path.
+#include <cstdlib>
+#include <type_traits>
+
 #include "../../include/primfit_b200.h"
 #include "pf_common.cuh"
 
@@ -35,63 +39,110 @@ namespace pf {
 
 namespace {
 
-constexpr int kStepWarps = 2;                           // 64-thread blocks (a 16x4 strip)
-constexpr int kStepBlocksPerTile = (kTilePix / 32) / kStepWarps;
-constexpr int kStepKS = 2;                              // stack depth in shared memory
+constexpr int kCW = kTilePix / 32;                      // consumer warps per group (one tile)
+constexpr int kStage = 32;                              // list entries staged per tile
+constexpr int kNBuf = 2;                                // stage buffers per group (ring)
+constexpr int kKS = 5;                                  // contribution-stack depth in smem
+constexpr uint32_t kEntBytes = sizeof(RecS) + sizeof(RecC);
+// one stage buffer: kStage RecS + kStage RecC + the tile's target (+ background) pixels
+constexpr size_t kBufRec = (size_t)kStage * kEntBytes;
+constexpr size_t kBufPix = (size_t)kTilePix * sizeof(float4);
+constexpr size_t kStackLevel = (size_t)kTilePix * (sizeof(float4) + sizeof(float));
+__host__ __device__ constexpr size_t buf_bytes(bool bg) { return kBufRec + kBufPix * (bg ? 2 : 1); }
+// per group: kNBuf stage buffers + a kKS-deep contribution stack per consumer thread
+__host__ __device__ constexpr size_t group_bytes(bool bg) {
+  return kNBuf * buf_bytes(bg) + kKS * kStackLevel;
+}
 
 struct StepArgs {
   const RecF* recf;
-  const RecG* recg;
+  const RecS* recs;
   const RecC* recc;
   const double* tex;
-  const float4* quad;
+  const float* apad;     // zero-padded fp32 alpha plane (global copy)
+  const double* apad64;  // the same plane in float64 (shared-memory copy source)
+  int pad_texels;
   int texels;
   const int32_t* bin_off;
   const int32_t* bin_idx;
   const int32_t* status;
-  int W, H, ntx, ty_begin;
+  int W, H, ntx, ty_begin, n_tiles;
   double eps_skip;
+  double eps_band;       // eps re-check band (see warp_tile)
   double bg0, bg1, bg2;
   const float4* bg4;
   float4* img4;          // optional (r, g, b, alpha)
   const float4* tgt4;
   double alpha_w, inv_3P, inv_P;
-  double* part;
-  float4* spill;         // [slot][2] for stack depth >= kStepKS
+  double* part;          // [n_tiles * 8][3] per-warp loss partials
+  float4* spill;         // [slot][2] for stack depth >= kKS
   double* grads;
+  unsigned* ctr;         // [2]: tile ticket, finished producers (self-resetting)
+  int sched_lazy;        // 1: fetch the next ticket only once a ring slot is free
+  const int32_t* classes;  // pf_bin's tile classes (counts + lists) or NULL: tile = ticket
+  int32_t* classes_rw;
+  unsigned long long* prof;  // diagnostics (PF_STEP_PROF=1): [warp slot][6], else NULL
 };
 
-__device__ __forceinline__ void step_pixel(int w, int tx, int ty, int& x, int& y, float& cx,
-                                           float& cy) {
-  const int l = threadIdx.x & 31;
-  const int wx = (w & 1) * kWarpW, wy = (w >> 1) * kWarpH;
-  x = tx * kTile + wx + (l & (kWarpW - 1));
-  y = ty * kTile + wy + (l / kWarpW);
-  cx = (float)(tx * kTile + wx) + 0.5f * (kWarpW - 1);
-  cy = (float)(ty * kTile + wy) + 0.5f * (kWarpH - 1);
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
-__device__ __forceinline__ bool step_may_touch(const RecC* __restrict__ rc, float cx, float cy) {
-  const float4 a = __ldg(reinterpret_cast<const float4*>(rc));
-  const float4 b = __ldg(reinterpret_cast<const float4*>(rc) + 1);
-  const float dx = cx - a.x, dy = cy - a.y;
-  const float uc = a.z * dx + a.w * dy;
-  const float vc = b.x * dy - b.y * dx;
-  const bool out_u = fabsf(uc) > 1.0f + b.z + 1e-5f * fabsf(uc);
-  const bool out_v = fabsf(vc) > 1.0f + b.w + 1e-5f * fabsf(vc);
+// ---- mbarrier / bulk-copy primitives (PTX)
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "PF_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
+      " @!p bra PF_WAIT_%=;\n}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(su32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// wait with an explicit back-off (the waiting warp leaves the issue slots alone)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity, unsigned ns) {
+  while (!mbar_try(b, parity)) __nanosleep(ns);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ bool cull_touch(const RecC& rc, float cx, float cy) {
+  const float dx = cx - rc.px, dy = cy - rc.py;
+  const float uc = rc.au * dx + rc.bu * dy;
+  const float vc = rc.av * dy - rc.bv * dx;
+  const bool out_u = fabsf(uc) > 1.0f + rc.eu + 1e-5f * fabsf(uc);
+  const bool out_v = fabsf(vc) > 1.0f + rc.ev + 1e-5f * fabsf(vc);
   return !(out_u || out_v);
-}
-
-// texel_coords (pf_common.cuh) that also hands back the normalised (u, v).
-__device__ __forceinline__ bool texel_coords_uv(const RecF& r, double xx, double yy, double& U,
-                                                double& V, double& u, double& v) {
-  const double dx = __dsub_rn(xx, r.px);
-  const double dy = __dsub_rn(yy, r.py);
-  u = div_rn(__dadd_rn(__dmul_rn(r.ct, dx), __dmul_rn(r.st, dy)), r.s, r.inv_s);
-  v = div_rn(__dadd_rn(__dmul_rn(-r.st, dx), __dmul_rn(r.ct, dy)), r.sq, r.inv_sq);
-  U = __dmul_rn(__dmul_rn(__dadd_rn(u, 1.0), 0.5), r.wm1);
-  V = __dmul_rn(__dmul_rn(__dadd_rn(v, 1.0), 0.5), r.hm1);
-  return !(U < 0.0 || U > r.wm1 || V < 0.0 || V > r.hm1);
 }
 
 __device__ __forceinline__ float step_reduce8(const float (&g)[8]) {
@@ -119,72 +170,145 @@ __device__ __forceinline__ float step_reduce8(const float (&g)[8]) {
   return y;
 }
 
-}  // namespace
+// fp32 -> fp64 on the integer ALU for a non-negative finite float (alpha taps
+// are in [0, 1]); denormals flush to 0.  Keeps F2F off the (quarter-rate)
+// conversion pipe, which bounds this kernel otherwise.
+__device__ __forceinline__ double f32_to_f64_alu(uint32_t b) {
+  const uint32_t hi = (b >> 3) + 0x38000000u, lo = b << 29;
+  return (b & 0x7f800000u) ? __hiloint2double((int)hi, (int)lo) : 0.0;
+}
 
-template <int LOSS>
-__global__ void __launch_bounds__(kStepWarps * 32) k_step(StepArgs a) {
-  __shared__ float4 stA[kStepKS][kStepWarps * 32];  // (j, i, T, m)
-  __shared__ float4 stB[kStepKS][kStepWarps * 32];  // (dm/dU, dm/dV, u, v)
+// Padded alpha atlas access, float64 result: shared fp64 copy (LDS.64),
+// shared fp32 copy, or the global fp32 plane.
+struct AtlasS64 {
+  uint32_t base;
+  __device__ __forceinline__ double operator()(int i) const {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(base + 8u * (uint32_t)i));
+    return v;
+  }
+};
+struct AtlasS32 {
+  uint32_t base;
+  __device__ __forceinline__ double operator()(int i) const {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(base + 4u * (uint32_t)i));
+    return f32_to_f64_alu(v);
+  }
+};
+struct AtlasG32 {
+  const uint32_t* p;
+  __device__ __forceinline__ double operator()(int i) const { return f32_to_f64_alu(__ldg(p + i)); }
+};
 
-  const int st_ovf = a.status[1];
-  const int tb = blockIdx.x / kStepBlocksPerTile;
-  const int b0 = a.bin_off[tb];
-  const int L = a.bin_off[tb + 1] - b0;
-  if (st_ovf) return;  // bin overflow (grid-uniform): lists are not valid
+// floor(U) and U - floor(U) for 0 <= U < 2^31 with two DADDs (round-down add of
+// 1.5 * 2^52 leaves floor(U) in the low mantissa bits) -- no conversion pipe.
+__device__ __forceinline__ void cell_of(double U, int& u0, double& wu) {
+  constexpr double kMagic = 6755399441055744.0;
+  const double t = __dadd_rd(U, kMagic);
+  u0 = __double2loint(t);
+  wu = U - (t - kMagic);
+}
 
-  const int t = threadIdx.x;
-  const int lane = t & 31;
-  const int wt = (blockIdx.x % kStepBlocksPerTile) * kStepWarps + (t >> 5);
-  const int tx = tb % a.ntx, ty = a.ty_begin + tb / a.ntx;
-  int x, y;
-  float cx, cy;
-  step_pixel(wt, tx, ty, x, y, cx, cy);
+// Record access for one tile: staged (shared) entries, plus -- for lists longer
+// than kStage, a rare case -- the remaining entries straight from HBM/L2.
+struct StagedRecs {
+  const RecS* s;
+  const RecC* c;
+  __device__ __forceinline__ const RecS& rec(int j) const { return s[j]; }
+  __device__ __forceinline__ const RecC& cull(int j) const { return c[j]; }
+};
+struct MixedRecs {
+  const RecS* s;
+  const RecC* c;
+  const RecS* gs;
+  const RecC* gc;
+  const int32_t* idx;  // bin_idx + b0
+  __device__ __forceinline__ const RecS& rec(int j) const {
+    return j < kStage ? s[j] : gs[__ldg(idx + j)];
+  }
+  __device__ __forceinline__ const RecC& cull(int j) const {
+    return j < kStage ? c[j] : gc[__ldg(idx + j)];
+  }
+};
+
+// One consumer warp's share (8x4 pixels) of one tile: forward, loss, backward.
+template <int LOSS, typename RECS, typename ATL>
+__device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, const ATL& atl,
+                                          const float4* tgs, const float4* bgs, float4* stA,
+                                          float* stB, int tile, int b0, int L, int txy, int w) {
+  const int lane = threadIdx.x & 31;
+  const int ct = w * 32 + lane;  // consumer thread (pixel) index within the tile
+  const int tx = txy & 0xffff, ty = txy >> 16;
+  const int wx = (w & 1) * kWarpW, wy = (w >> 1) * kWarpH;
+  const int x = tx * kTile + wx + (lane & (kWarpW - 1));
+  const int y = ty * kTile + wy + (lane / kWarpW);
+  const float cx = (float)(tx * kTile + wx) + 0.5f * (kWarpW - 1);
+  const float cy = (float)(ty * kTile + wy) + 0.5f * (kWarpH - 1);
   const bool valid = x < a.W && y < a.H;
   const double xx = (double)x, yy = (double)y;
   const size_t pix = valid ? (size_t)y * a.W + x : 0;
-  const size_t slot0 = (size_t)b0 * kTilePix + wt * 32 + lane;
-
-  float4 tg = make_float4(0.f, 0.f, 0.f, 0.f), bgp = tg;
-  if (valid) tg = __ldg(a.tgt4 + pix);
-  if (valid && a.bg4) bgp = __ldg(a.bg4 + pix);
-
-  // ---- forward phase (k_forward semantics, _kernels.py:183-255)
+  const size_t slot0 = (size_t)b0 * kTilePix + ct;
+  const int tp_ = (wy + lane / kWarpW) * kTile + wx + (lane & (kWarpW - 1));  // pixel in tile
   const double* plane_a = a.tex + 3 * (size_t)a.texels;
+
+  // ---- forward (k_forward semantics, _kernels.py:183-255)
   double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0;
   int ns = 0;
   for (int sub = 0; sub < L; sub += 32) {
-    int my_i = 0;
-    bool cand = false;
-    if (sub + lane < L) {
-      my_i = __ldg(a.bin_idx + b0 + sub + lane);
-      cand = step_may_touch(a.recc + my_i, cx, cy);
-    }
+    const int jl = sub + lane;
+    const bool cand = jl < L && cull_touch(R.cull(jl), cx, cy);
     unsigned mask = __ballot_sync(kFull, cand);
+    if (!valid) mask = 0u;  // divergent only in a partial last tile row / column
     while (mask) {
       const int bit = __ffs(mask) - 1;
       mask &= mask - 1;
-      const int i = __shfl_sync(kFull, my_i, bit);
-      if (!valid) continue;
-      const RecF& r = a.recf[i];
-      double U, V, u, v;
-      if (!texel_coords_uv(r, xx, yy, U, V, u, v)) continue;
-      const Cell c = make_cell(U, V);
-      const float4 q = load_quad(a.quad, r.base, r.wt, c.u0, c.v0);
-      double m = bilerp(q, c.wu, c.wv);
-      if (fabs(m - a.eps_skip) <= 1e-6 * a.eps_skip) m = bilinear(plane_a, r.base, r.wt, r.ht, c);
+      const int j = sub + bit;
+      const RecS& r = R.rec(j);
+      double U = fma(r.au, xx, fma(r.bu, yy, r.cu));
+      double V = fma(r.av, xx, fma(r.bv, yy, r.cv));
+      const double dl = r.delta, wm1 = r.wm1, hm1 = r.hm1;
+      const bool exact = fabs(U) < dl || fabs(U - wm1) < dl || fabs(V) < dl || fabs(V - hm1) < dl;
+      if (exact) {
+        if (!texel_coords(a.recf[r.gidx], xx, yy, U, V)) continue;
+      } else if (!(U >= 0.0 && U <= wm1 && V >= 0.0 && V <= hm1)) {
+        continue;
+      }
+      int u0, v0;
+      double wu, wv;
+      cell_of(U, u0, wu);
+      cell_of(V, v0, wv);
+      int tp = r.pbase + v0 * r.wp + u0;
+      double t00 = atl(tp), t01 = atl(tp + 1), t10 = atl(tp + r.wp), t11 = atl(tp + r.wp + 1);
+      const double l0 = fma(wu, t01 - t00, t00), l1 = fma(wu, t11 - t10, t10);
+      double m = fma(wv, l1 - l0, l0);
+      if (exact || fabs(m - a.eps_skip) <= a.eps_band) {
+        // rare: the reference's exact chain for the decision and the value
+        const RecF& f = a.recf[r.gidx];
+        if (!exact) (void)texel_coords(f, xx, yy, U, V);
+        const Cell c = make_cell(U, V);
+        m = bilinear(plane_a, f.base, f.wt, f.ht, c);
+        wu = c.wu;
+        wv = c.wv;
+        tp = r.pbase + c.v0 * r.wp + c.u0;
+        t00 = atl(tp);
+        t01 = atl(tp + 1);
+        t10 = atl(tp + r.wp);
+        t11 = atl(tp + r.wp + 1);
+      }
       if (m < a.eps_skip) continue;
-      const float wu = (float)c.wu, wv = (float)c.wv;
-      const float gU = (1.0f - wv) * (q.y - q.x) + wv * (q.w - q.z);
-      const float gV = (1.0f - wu) * (q.z - q.x) + wu * (q.w - q.y);
-      const float4 ea = make_float4(__int_as_float(sub + bit), __int_as_float(i), (float)T, (float)m);
-      const float4 eb = make_float4(gU, gV, (float)u, (float)v);
-      if (ns < kStepKS) {
-        stA[ns][t] = ea;
-        stB[ns][t] = eb;
+      // dm/dU, dm/dV (_kernels.py:61-73) -- alpha channel only (Appendix A.3)
+      const double gU = fma(wv, (t11 - t10) - (t01 - t00), t01 - t00);
+      const double gV = fma(wu, (t11 - t01) - (t10 - t00), t10 - t00);
+      const float4 ea = make_float4(__int_as_float(j), (float)T, (float)m, (float)gU);
+      const float eb = (float)gV;
+      if (ns < kKS) {
+        stA[ns * kTilePix + ct] = ea;
+        stB[ns * kTilePix + ct] = eb;
       } else {
-        float4* sp = a.spill + 2 * (slot0 + (size_t)(ns - kStepKS) * kTilePix);
+        float4* sp = a.spill + 2 * (slot0 + (size_t)(ns - kKS) * kTilePix);
         sp[0] = ea;
-        sp[1] = eb;
+        sp[1] = make_float4(eb, 0.f, 0.f, 0.f);
       }
       ++ns;
       const double aa = r.sa * m;
@@ -197,6 +321,8 @@ __global__ void __launch_bounds__(kStepWarps * 32) k_step(StepArgs a) {
   }
 
   // ---- loss (fit.py:112-151), pixel-local
+  const float4 tg = tgs[tp_];
+  const float4 bgp = bgs ? bgs[tp_] : make_float4(0.f, 0.f, 0.f, 0.f);
   const float g0 = a.bg4 ? bgp.x : (float)a.bg0;
   const float g1 = a.bg4 ? bgp.y : (float)a.bg1;
   const float g2 = a.bg4 ? bgp.z : (float)a.bg2;
@@ -236,24 +362,27 @@ __global__ void __launch_bounds__(kStepWarps * 32) k_step(StepArgs a) {
     l2 += __shfl_xor_sync(kFull, l2, o);
   }
   if (lane == 0) {
-    double* pp = a.part + ((size_t)tb * (kTilePix / 32) + wt) * 3;
+    double* pp = a.part + ((size_t)tile * kCW + w) * 3;
     pp[0] = l0;
     pp[1] = l1;
     pp[2] = l2;
   }
-  // ---- backward phase (_kernels.py:258-363), back to front over the stack
+
+  // ---- backward (_kernels.py:258-363), back to front over the stack
   float S0 = 0.f, S1 = 0.f, S2 = 0.f, B = 1.f;
+  const float xf = (float)x, yf = (float)y;
   int k = ns - 1;
-  float4 ea = make_float4(0.f, 0.f, 0.f, 0.f), eb = ea;
+  float4 ea = make_float4(0.f, 0.f, 0.f, 0.f);
+  float eb = 0.f;
   unsigned key = 0;
   auto fetch = [&](int d) {
-    if (d < kStepKS) {
-      ea = stA[d][t];
-      eb = stB[d][t];
+    if (d < kKS) {
+      ea = stA[d * kTilePix + ct];
+      eb = stB[d * kTilePix + ct];
     } else {
-      const float4* sp = a.spill + 2 * (slot0 + (size_t)(d - kStepKS) * kTilePix);
+      const float4* sp = a.spill + 2 * (slot0 + (size_t)(d - kKS) * kTilePix);
       ea = sp[0];
-      eb = sp[1];
+      eb = sp[1].x;
     }
     key = (unsigned)__float_as_int(ea.x) + 1u;
   };
@@ -263,17 +392,21 @@ __global__ void __launch_bounds__(kStepWarps * 32) k_step(StepArgs a) {
     if (jm == 0u) break;
     const bool act = key == jm;
     const unsigned ball = __ballot_sync(kFull, act);
-    const int i = __shfl_sync(kFull, __float_as_int(ea.y), __ffs(ball) - 1);
+    const RecS& r = R.rec((int)jm - 1);
     float g[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) g[c] = 0.0f;
     if (act) {
-      const float Tc = ea.z, m = ea.w, gU = eb.x, gV = eb.y, u = eb.z, v = eb.w;
+      const float Tc = ea.y, m = ea.z, gU = ea.w, gV = eb;
       if (--k >= 0) fetch(k); else key = 0;
-      const RecG r = a.recg[i];
-      const float aa = r.sa * m;
-      const float gg = dI0 * (r.c0 - S0 - g0 * B) + dI1 * (r.c1 - S1 - g1 * B) +
-                       dI2 * (r.c2 - S2 - g2 * B) + dA * B;
+      // normalised template coordinates from the fp32 cull record (gradient-only use)
+      const RecC& cc = R.cull((int)jm - 1);
+      const float dxf = xf - cc.px, dyf = yf - cc.py;
+      const float u = cc.au * dxf + cc.bu * dyf;
+      const float v = cc.av * dyf - cc.bv * dxf;
+      const float aa = r.saf * m;
+      const float gg = dI0 * (r.c0f - S0 - g0 * B) + dI1 * (r.c1f - S1 - g1 * B) +
+                       dI2 * (r.c2f - S2 - g2 * B) + dA * B;
       const float dalpha = Tc * gg;
       g[4] = dalpha * r.sd * m;
       if (r.omm > 0.0f) {
@@ -282,19 +415,19 @@ __global__ void __launch_bounds__(kStepWarps * 32) k_step(StepArgs a) {
         g[6] = dI1 * wc * r.cd1;
         g[7] = dI2 * wc * r.cd2;
       }
-      const float dm = dalpha * r.sa;
+      const float dm = dalpha * r.saf;
       const float mu_u = gU * r.hw, mu_v = gV * r.hh;
       g[0] = dm * (mu_u * r.gxu + mu_v * r.gxv);
       g[1] = dm * (mu_u * r.gyu + mu_v * r.gyv);
       g[2] = dm * (mu_u * (-u * r.inv_s) + mu_v * (-v * r.inv_s));
       g[3] = dm * (mu_u * (v * r.q) + mu_v * (-u * r.inv_q));
       const float om = 1.0f - aa;
-      S0 = aa * r.c0 + om * S0;
-      S1 = aa * r.c1 + om * S1;
-      S2 = aa * r.c2 + om * S2;
+      S0 = aa * r.c0f + om * S0;
+      S1 = aa * r.c1f + om * S1;
+      S2 = aa * r.c2f + om * S2;
       B *= om;
     }
-    double* gp = a.grads + (size_t)i * 8;
+    double* gp = a.grads + (size_t)r.gidx * 8;
     if (__popc(ball) <= 2) {
       if (act) {
 #pragma unroll
@@ -305,6 +438,223 @@ __global__ void __launch_bounds__(kStepWarps * 32) k_step(StepArgs a) {
       const float tot = step_reduce8(g);
       if ((lane & 3) == 0 && tot != 0.0f) atomicAdd(gp + (lane >> 2), (double)tot);
     }
+  }
+}
+
+}  // namespace
+
+// Persistent, warp-specialised.  One CTA per SM; G groups of 9 warps: one
+// producer warp and 8 consumer warps (one 8x4 pixel sub-tile each).
+//   producer  takes a tile ticket, reads the tile's list, then (once the ring
+//             slot is free) TMA bulk-copies the list's step + cull records and
+//             the tile's target (+ background) rows into an nbuf-deep ring of
+//             stage buffers (mbarrier full/empty handshake, expect_tx bytes).
+//   consumers forward -> loss -> backward out of shared memory only; no
+//             block-wide barrier after the prologue, so warps drift freely.
+// The padded alpha atlas is loaded into shared memory once per CTA: float64
+// (ATL == 2) when it fits, else float32 (ATL == 1); ATL == 0 reads the global
+// fp32 plane.
+template <int LOSS, int ATL, int G, bool BG>
+__global__ void __launch_bounds__(G * (kCW + 1) * 32, 1) k_step(StepArgs a) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ __align__(8) uint64_t full[G][kNBuf], empty[G][kNBuf];
+  __shared__ int4 hdr[G][kNBuf];
+
+  const int t = threadIdx.x;
+  if (a.status[1]) {
+    // bin overflow (grid-uniform): lists are not valid; leave clean counters
+    if (blockIdx.x == 0 && a.classes && t < kTileClasses) a.classes_rw[t] = 0;
+    return;
+  }
+  const int lane = t & 31, warp = t >> 5;
+  constexpr bool has_bg = BG;
+  constexpr size_t gbytes = group_bytes(BG), bbytes = buf_bytes(BG);
+  unsigned char* satl = sm + G * gbytes;
+  using Atl = typename std::conditional<
+      ATL == 2, AtlasS64, typename std::conditional<ATL == 1, AtlasS32, AtlasG32>::type>::type;
+  Atl atl;
+  if constexpr (ATL == 0) atl.p = reinterpret_cast<const uint32_t*>(a.apad);
+  else atl.base = su32(satl);
+  if (ATL != 0) {
+    // staggered start: the CTAs do not all hit the same L2 lines at once
+    const int nq = ATL == 2 ? a.pad_texels >> 1 : a.pad_texels >> 2;
+    const float4* src = reinterpret_cast<const float4*>(ATL == 2 ? (const void*)a.apad64
+                                                                 : (const void*)a.apad);
+    float4* dst = reinterpret_cast<float4*>(satl);
+    const int rot = (int)((blockIdx.x * 37u) % (unsigned)max(nq, 1));
+    for (int k = t; k < nq; k += blockDim.x) {
+      int q = k + rot;
+      if (q >= nq) q -= nq;
+      dst[q] = __ldg(src + q);
+    }
+  }
+  if (t < G * kNBuf) {
+    mbar_init(&full[t / kNBuf][t % kNBuf], 1);
+    mbar_init(&empty[t / kNBuf][t % kNBuf], kCW);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+
+  const int g = warp / (kCW + 1), wg = warp % (kCW + 1);
+  unsigned char* gs = sm + g * gbytes;
+  float4* stA = reinterpret_cast<float4*>(gs + kNBuf * bbytes);
+  float* stB = reinterpret_cast<float*>(stA + kKS * kTilePix);
+  auto buf_rec = [&](int b) { return reinterpret_cast<RecS*>(gs + b * bbytes); };
+  auto buf_cull = [&](int b) {
+    return reinterpret_cast<RecC*>(gs + b * bbytes + kStage * sizeof(RecS));
+  };
+  auto buf_tgt = [&](int b) { return reinterpret_cast<float4*>(gs + b * bbytes + kBufRec); };
+  auto buf_bg = [&](int b) {
+    return reinterpret_cast<float4*>(gs + b * bbytes + kBufRec + kBufPix);
+  };
+
+  unsigned long long p_wait = 0, p_work = 0, p_n = 0, p_first = 0, p_t0 = a.prof ? gtimer() : 0;
+  if (wg == kCW) {
+    // ---------------- producer warp
+    // Dynamic schedule: a global ticket t is mapped to a tile through the
+    // per-class tile lists pf_bin wrote (classes by list length, heaviest
+    // first: longest-processing-time order, so the tail of the launch is made
+    // of light tiles).  The next tile's ticket and list are fetched right
+    // after the current tile's copies go out, overlapping the wait for the
+    // next free ring slot.  (a.sched_lazy: fetch only once the slot is free.)
+    int cls_pre = 0;  // lane l < kTileClasses: tiles in classes heaviest..l (inclusive)
+    if (a.classes) {
+      const int c = lane < kTileClasses ? __ldg(a.classes + (kTileClasses - 1 - lane)) : 0;
+      cls_pre = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, cls_pre, o);
+        if (lane >= o) cls_pre += y;
+      }
+    }
+    auto next_tile = [&]() {
+      int t = 0;
+      if (lane == 0) t = (int)atomicAdd(a.ctr, 1u);
+      t = __shfl_sync(kFull, t, 0);
+      if (a.classes && t < a.n_tiles) {
+        const unsigned below = __ballot_sync(kFull, lane < kTileClasses && cls_pre <= t);
+        const int ci = __popc(below);  // rank of the class holding ticket t
+        const int before = __shfl_sync(kFull, cls_pre, max(ci - 1, 0));
+        const int idx = t - (ci > 0 ? before : 0);
+        // (ci == kTileClasses: counts do not cover t -- never with pf_bin's lists)
+        t = ci < kTileClasses
+                ? __ldg(a.classes + kTileClasses + (kTileClasses - 1 - ci) * a.n_tiles + idx)
+                : a.n_tiles;
+      }
+      return t;
+    };
+    int tile = next_tile();
+    int b0 = 0, L = 0, i0 = 0;
+    auto load_list = [&]() {
+      if (tile < a.n_tiles) {
+        b0 = __ldg(a.bin_off + tile);
+        L = __ldg(a.bin_off + tile + 1) - b0;
+        i0 = lane < L ? __ldg(a.bin_idx + b0 + lane) : 0;
+      }
+    };
+    load_list();
+    int buf = 0;
+    uint32_t eph = 0;  // parity of the empty barrier we wait on next, per slot (bit b)
+    for (int k = 0;; ++k) {
+      if (k >= kNBuf) {
+        const unsigned long long c0 = a.prof ? clock64() : 0;
+        mbar_wait_sleep(&empty[g][buf], (eph >> buf) & 1u, 256);
+        if (a.prof) p_wait += clock64() - c0;
+        eph ^= 1u << buf;
+        if (a.sched_lazy && k > 0) {
+          tile = next_tile();
+          load_list();
+        }
+      }
+      if (tile >= a.n_tiles) {
+        int last = 0;
+        if (lane == 0) {
+          hdr[g][buf] = make_int4(-1, 0, 0, 0);
+          mbar_arrive(&full[g][buf]);
+          last = atomicAdd(a.ctr + 1, 1u) == gridDim.x * G - 1;
+        }
+        // the last producer out resets the ticket and (every producer read them
+        // at its start) the class counts for the next step
+        if (__shfl_sync(kFull, last, 0)) {
+          if (lane == 0) {
+            atomicExch(a.ctr, 0u);
+            atomicExch(a.ctr + 1, 0u);
+          }
+          if (a.classes && lane < kTileClasses) a.classes_rw[lane] = 0;
+        }
+        break;
+      }
+      const int nst = min(L, kStage);
+      const int tx = tile % a.ntx, ty = a.ty_begin + tile / a.ntx;
+      const int vw = min(kTile, a.W - tx * kTile);
+      const int vh = min(kTile, a.H - ty * kTile);
+      const uint32_t row_bytes = (uint32_t)vw * sizeof(float4);
+      if (lane == 0) {
+        hdr[g][buf] = make_int4(tile, b0, L, tx | (ty << 16));
+        mbar_arrive_tx(&full[g][buf], (uint32_t)nst * kEntBytes +
+                                          (uint32_t)vh * row_bytes * (has_bg ? 2u : 1u));
+      }
+      __syncwarp();
+      if (lane < nst) {
+        bulk_g2s(buf_rec(buf) + lane, a.recs + i0, sizeof(RecS), &full[g][buf]);
+        bulk_g2s(buf_cull(buf) + lane, a.recc + i0, sizeof(RecC), &full[g][buf]);
+      }
+      if (lane < vh) {
+        const size_t row = (size_t)(ty * kTile + lane) * a.W + (size_t)tx * kTile;
+        bulk_g2s(buf_tgt(buf) + lane * kTile, a.tgt4 + row, row_bytes, &full[g][buf]);
+        if (has_bg) bulk_g2s(buf_bg(buf) + lane * kTile, a.bg4 + row, row_bytes, &full[g][buf]);
+      }
+      buf = buf + 1 == kNBuf ? 0 : buf + 1;
+      if (!a.sched_lazy || k + 1 < kNBuf) {
+        tile = next_tile();
+        load_list();
+      }
+    }
+  } else {
+    // ---------------- consumer warps
+    int buf = 0;
+    uint32_t fph = 0;
+    for (;;) {
+      const unsigned long long c0 = a.prof ? clock64() : 0;
+      mbar_wait_sleep(&full[g][buf], (fph >> buf) & 1u, 64);
+      const unsigned long long c1 = a.prof ? clock64() : 0;
+      if (a.prof) {
+        p_wait += c1 - c0;
+        if (p_n == 0) p_first = c1 - c0;
+      }
+      fph ^= 1u << buf;
+      const int4 h = hdr[g][buf];
+      if (h.x < 0) break;
+      const RecS* rs = buf_rec(buf);
+      const RecC* rc = buf_cull(buf);
+      const float4* tgs = buf_tgt(buf);
+      const float4* bgs = has_bg ? buf_bg(buf) : nullptr;
+      if (h.z <= kStage) {
+        warp_tile<LOSS>(a, StagedRecs{rs, rc}, atl, tgs, bgs, stA, stB, h.x, h.y, h.z, h.w, wg);
+      } else {
+        warp_tile<LOSS>(a, MixedRecs{rs, rc, a.recs, a.recc, a.bin_idx + h.y}, atl, tgs, bgs,
+                        stA, stB, h.x, h.y, h.z, h.w, wg);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[g][buf]);
+      if (a.prof) {
+        const unsigned long long dt = clock64() - c1;
+        p_work += dt;
+        ++p_n;
+        if (lane == 0 && h.x < 65536)
+          a.prof[6 * 148 * 32 + (size_t)h.x * kCW + wg] = dt | ((unsigned long long)(gtimer() & 0xffffffffu) << 32);
+      }
+      buf = buf + 1 == kNBuf ? 0 : buf + 1;
+    }
+  }
+  if (a.prof && lane == 0) {
+    unsigned long long* o = a.prof + ((size_t)blockIdx.x * blockDim.x / 32 + warp) * 6;
+    o[0] = p_wait;
+    o[1] = p_work;
+    o[2] = p_n;
+    o[3] = p_t0;
+    o[4] = gtimer();
+    o[5] = (unsigned long long)(wg == kCW) | (p_first << 1);
   }
 }
 
@@ -353,15 +703,37 @@ extern "C" size_t pf_step_spill_bytes(int capacity) {
   return (size_t)(capacity > 0 ? capacity : 1) * kTilePix * 2 * sizeof(float4);
 }
 
-extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const float* quad,
-                           int texels, const int32_t* bin_off, const int32_t* bin_idx,
-                           const int32_t* status, int W, int H, int ty_begin, int ty_end,
-                           double eps_skip, double bg_r, double bg_g, double bg_b,
-                           const float* bg4, int loss_kind, const float* tgt4, double alpha_w,
-                           double inv_3P, double inv_P, void* spill, float* img4, double* part,
-                           double* grads, void* stream) {
-  if (W < 1 || H < 1 || n < 0 || !bin_off || !bin_idx || !status || !tex || !quad || !tgt4 ||
-      !spill || !part || !grads)
+static unsigned long long* g_prof_buf = nullptr;
+static int g_prof_slots = 0;
+
+// Diagnostics only (not part of the documented ABI): copy the last profiled
+// pf_fit_step's per-warp counters to the host (synchronous).
+extern "C" int pf_step_prof_dump(unsigned long long* host, int max_slots) {
+  if (!g_prof_buf) return 0;
+  const int n = g_prof_slots < max_slots ? g_prof_slots : max_slots;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, g_prof_buf, sizeof(unsigned long long) * 6 * n, cudaMemcpyDeviceToHost);
+  return n;
+}
+
+extern "C" int pf_step_prof_tiles(unsigned long long* host, int n_tiles) {
+  if (!g_prof_buf) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, g_prof_buf + 6 * 148 * 32, sizeof(unsigned long long) * 8 * (size_t)n_tiles,
+             cudaMemcpyDeviceToHost);
+  return n_tiles;
+}
+
+extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const float* apad,
+                           const double* apad64, int pad_texels, int texels, const int32_t* bin_off,
+                           const int32_t* bin_idx, const int32_t* status, int W, int H,
+                           int ty_begin, int ty_end, double eps_skip, double bg_r, double bg_g,
+                           double bg_b, const float* bg4, int loss_kind, const float* tgt4,
+                           double alpha_w, double inv_3P, double inv_P, void* spill, float* img4,
+                           double* part, double* grads, uint32_t* counters,
+                           const int32_t* tile_classes, void* stream) {
+  if (W < 1 || H < 1 || n < 0 || !bin_off || !bin_idx || !status || !tex || !apad || !tgt4 ||
+      !spill || !part || !grads || !counters || pad_texels < 0 || (pad_texels & 3))
     return PF_ERR_ARG;
   if (loss_kind != PF_LOSS_MSE && loss_kind != PF_LOSS_SPATIAL) return PF_ERR_ARG;
   const int ntx = div_up(W, kTile), nty = div_up(H, kTile);
@@ -370,10 +742,12 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   if (n_tiles == 0) return PF_OK;
   StepArgs a;
   a.recf = (const RecF*)rec;
-  a.recg = (const RecG*)((const char*)rec + sizeof(RecF) * (size_t)n);
   a.recc = (const RecC*)((const char*)rec + (sizeof(RecF) + sizeof(RecG)) * (size_t)n);
+  a.recs = (const RecS*)((const char*)rec + (sizeof(RecF) + sizeof(RecG) + sizeof(RecC)) * (size_t)n);
   a.tex = tex;
-  a.quad = (const float4*)quad;
+  a.apad = apad;
+  a.apad64 = apad64;
+  a.pad_texels = pad_texels;
   a.texels = texels;
   a.bin_off = bin_off;
   a.bin_idx = bin_idx;
@@ -382,7 +756,10 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   a.H = H;
   a.ntx = ntx;
   a.ty_begin = ty_begin;
+  a.n_tiles = n_tiles;
   a.eps_skip = eps_skip;
+  // eps re-check band: fp32 taps (<= 6e-8 relative) + affine U, V (<= 1e-10 texel)
+  a.eps_band = 1e-6 * eps_skip + 1e-9;
   a.bg0 = bg_r;
   a.bg1 = bg_g;
   a.bg2 = bg_b;
@@ -395,11 +772,68 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   a.part = part;
   a.spill = (float4*)spill;
   a.grads = grads;
+  a.ctr = counters;
+  a.sched_lazy = getenv("PF_STEP_LAZY") ? 1 : 0;
+  a.classes = getenv("PF_STEP_NOLPT") ? nullptr : tile_classes;
+  a.classes_rw = const_cast<int32_t*>(a.classes);
+  a.prof = nullptr;
+  static unsigned long long* prof_buf = nullptr;
+  if (getenv("PF_STEP_PROF")) {
+    if (!prof_buf) cudaMalloc(&prof_buf, sizeof(unsigned long long) * (6 * 148 * 32 + 65536 * 8));
+    a.prof = prof_buf;
+  }
+  g_prof_buf = prof_buf;
   cudaStream_t st = (cudaStream_t)stream;
-  const int grid = n_tiles * kStepBlocksPerTile;
-  if (loss_kind == PF_LOSS_MSE)
-    k_step<PF_LOSS_MSE><<<grid, kStepWarps * 32, 0, st>>>(a);
-  else
-    k_step<PF_LOSS_SPATIAL><<<grid, kStepWarps * 32, 0, st>>>(a);
+  static int sms = 0, optin = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  const size_t budget = (size_t)optin - 1024;  // static smem (barriers, headers)
+  // groups per CTA (PF_STEP_GROUPS overrides for A/B runs); the atlas goes to
+  // shared memory as float64 when it fits, else float32, else stays global
+  int G = 3;
+  if (const char* e = getenv("PF_STEP_GROUPS")) G = atoi(e) == 2 ? 2 : 3;
+  const bool no64 = getenv("PF_STEP_ATL32") != nullptr;
+  const bool bg = bg4 != nullptr;
+  const size_t gb = group_bytes(bg);
+  const size_t a32 = (size_t)pad_texels * sizeof(float), a64 = 2 * a32;
+  int atl = 0;
+  for (int gg = G; gg >= 2 && atl == 0; --gg) {
+    if (apad64 && !no64 && gg * gb + a64 <= budget) { G = gg; atl = 2; }
+    else if (gg * gb + a32 <= budget) { G = gg; atl = 1; }
+  }
+  const size_t smem = G * gb + (atl == 2 ? a64 : atl == 1 ? a32 : 0);
+  void (*kern)(StepArgs);
+#define PF_PICK3(LS, GG)                                                                 \
+  kern = bg ? (atl == 2 ? k_step<LS, 2, GG, true> : atl == 1 ? k_step<LS, 1, GG, true>      \
+                                                           : k_step<LS, 0, GG, true>)       \
+            : (atl == 2 ? k_step<LS, 2, GG, false> : atl == 1 ? k_step<LS, 1, GG, false>    \
+                                                            : k_step<LS, 0, GG, false>);
+#define PF_PICK(LS)      \
+  if (G == 3) {          \
+    PF_PICK3(LS, 3)      \
+  } else {               \
+    PF_PICK3(LS, 2)      \
+  }
+  if (loss_kind == PF_LOSS_MSE) {
+    PF_PICK(PF_LOSS_MSE)
+  } else {
+    PF_PICK(PF_LOSS_SPATIAL)
+  }
+#undef PF_PICK3
+#undef PF_PICK
+  static void (*last_kern)(StepArgs) = nullptr;
+  static size_t last_smem = 0;
+  if (kern != last_kern || smem != last_smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    last_kern = kern;
+    last_smem = smem;
+  }
+  const int grid = min(sms, max(1, (n_tiles + G - 1) / G));
+  g_prof_slots = grid * G * (kCW + 1);
+  kern<<<grid, G * (kCW + 1) * 32, smem, st>>>(a);
   return (int)cudaGetLastError();
 }

@@ -315,7 +315,9 @@ class StepEngine:
         # K34 (one kernel for render -> loss -> backward) whenever colour does not
         # come from the texture; PF_TWO_KERNEL=1 forces K3 + K4 (A/B checks)
         self.fused = scene.mu_blend == 0.0 and os.environ.get("PF_TWO_KERNEL", "0") != "1"
-        if not self.fused:
+        if self.fused:
+            self.comp.enable_step_schedule()
+        else:
             self.comp.alloc_render(save=True, loss=True)
         self.allreduce = allreduce
         self.use_graph = use_graph
