@@ -87,35 +87,39 @@ int pf_atlas_quad(const double* tex, int texels, const int32_t* tpl_base, const 
                   const int32_t* tpl_h, int n_tpl, float* quad, void* stream);
 
 /*
- * K1 — per-primitive preprocess + bin count.
+ * One-time setup of a binning scratch buffer for a scene structure: zero it,
+ * copy the static z order, and build the static per-primitive structure
+ * (template geometry, z rank) that K1 reads with one load per primitive.
+ *   template_id [n]   PrimitiveParams.template_id (scene.py:70-87)
+ *   zorder      [n]   primitive indices in ascending z (PackedScene.order, raster.py:92)
+ *   tpl_base / tpl_pbase / tpl_w / tpl_h [n_tpl]  atlas base, padded-atlas base
+ *                     (pf_atlas_pad; may be NULL), template width / height
+ *   tpl_q   [n_tpl]   aspect q used for primitives of that template (th/tw when
+ *                     preserve_aspect, else 1.0; raster.py:88-91)
+ *   tpl_hyp [n_tpl]   hypot(1, max(1, q)) (host-computed, bit-identical to
+ *                     math.hypot in bbox_half_side, raster.py:222-224)
+ */
+int pf_scratch_init(void* scratch, size_t scratch_bytes, const int32_t* template_id,
+                    const int32_t* zorder, int n, const int32_t* tpl_base,
+                    const int32_t* tpl_pbase, const int32_t* tpl_w, const int32_t* tpl_h,
+                    const double* tpl_q, const double* tpl_hyp, int n_tpl, int capacity,
+                    void* stream);
+
+/*
+ * K1 — per-primitive preprocess + bin rects.
  * Replaces: the per-pair inline transform/sigmoid math of every numba kernel
  * (_kernels.py:106-123), pack_scene (raster.py:63-96) and the bbox part of
  * bin_tiles (raster.py:246-257, bbox_half_side raster.py:222-224).
- *   zorder   [n]  primitive indices in ascending z (PackedScene.order, raster.py:92)
- *   tpl_q    [n_tpl] aspect q used for primitives of that template (th/tw when
- *                    preserve_aspect, else 1.0; raster.py:88-91)
- *   tpl_hyp  [n_tpl] hypot(1, max(1, q)) (host-computed, bit-identical to
- *                    math.hypot in bbox_half_side)
- *   tpl_pbase [n_tpl] base of each template in the padded alpha plane of
- *                    pf_atlas_pad (used by pf_fit_step's records), or NULL
- *   padding        bbox padding (fit.effective_padding, fit.py:338-341)
+ *   params   float64 [n][8]
+ *   padding  bbox padding (fit.effective_padding, fit.py:338-341)
  *   rec      out   n * pf_record_bytes() bytes
- *   scratch        pf_bin_scratch_bytes(n, n_band_tiles, capacity) bytes (pf_scratch_init'ed);
- *                  receives the band-clipped tile rect of every primitive
+ *   scratch  pf_bin_scratch_bytes(n, n_band_tiles, capacity) bytes, set up by
+ *            pf_scratch_init; receives the band-clipped tile rect of every
+ *            primitive at its z rank
  */
-int pf_preprocess(const double* params, const int32_t* template_id, const int32_t* zorder, int n,
-                  const int32_t* tpl_base, const int32_t* tpl_w, const int32_t* tpl_h,
-                  const double* tpl_q, const double* tpl_hyp, const int32_t* tpl_pbase,
-                  int n_tpl, double alpha_max, double mu_blend, double padding,
+int pf_preprocess(const double* params, int n, double alpha_max, double mu_blend, double padding,
                   int W, int H, int tile, int ty_begin, int ty_end, int capacity,
                   void* rec, void* scratch, size_t scratch_bytes, void* stream);
-
-/*
- * One-time initialisation of a binning scratch buffer (zero it, copy the static
- * z order).  Call once after allocating pf_bin_scratch_bytes(...) bytes.
- */
-int pf_scratch_init(void* scratch, size_t scratch_bytes, const int32_t* zorder, int n, int capacity,
-                    void* stream);
 
 /*
  * K5+K1 fused: one Adam step (fit.py:195-238, table mode as pf_adam) on every
@@ -129,12 +133,8 @@ int pf_adam_preprocess(double* params, double* grads, double* m, double* v, cons
                        const double* gains8, const double* lr_table, const double* bc1_table,
                        const double* bc2_table, int32_t* iter, int clamp, double s_min,
                        double s_max, double* sums, const double* part, int n_part,
-                       int loss_kind, double alpha_w,
-                       double inv_3P, double inv_P, double* hist_loss, double* hist_psnr,
-                       const int32_t* template_id, const int32_t* zorder, int n,
-                       const int32_t* tpl_base, const int32_t* tpl_w, const int32_t* tpl_h,
-                       const double* tpl_q, const double* tpl_hyp, const int32_t* tpl_pbase,
-                       int n_tpl, double alpha_max,
+                       int loss_kind, double alpha_w, double inv_3P, double inv_P,
+                       double* hist_loss, double* hist_psnr, int n, double alpha_max,
                        double mu_blend, double padding, int W, int H, int tile, int ty_begin,
                        int ty_end, int capacity, void* rec, void* scratch, size_t scratch_bytes,
                        void* stream);

@@ -150,8 +150,12 @@ class Compositor:
         self.rec = torch.empty(max(self.n, 1) * rb, dtype=torch.uint8, device=dev)
         self.scratch_bytes = int(self.lib.pf_bin_scratch_bytes(self.n, self.n_tiles, self.capacity))
         self.scratch = torch.zeros(self.scratch_bytes, dtype=torch.uint8, device=dev)
+        a = atlas
         nat.check(self.lib.pf_scratch_init(self.scratch.data_ptr(), self.scratch_bytes,
-                                           self.d_zorder.data_ptr(), self.n, self.capacity,
+                                           self.d_tid.data_ptr(), self.d_zorder.data_ptr(), self.n,
+                                           a.d_base.data_ptr(), a.d_pbase.data_ptr(),
+                                           a.d_w.data_ptr(), a.d_h.data_ptr(), a.d_q.data_ptr(),
+                                           a.d_hyp.data_ptr(), a.n_templates, self.capacity,
                                            _stream_handle()), "pf_scratch_init")
         self.bin_off = torch.zeros(self.n_tiles + 1, dtype=torch.int32, device=dev)
         self.bin_idx = torch.zeros(max(self.capacity, 1), dtype=torch.int32, device=dev)
@@ -195,24 +199,19 @@ class Compositor:
 
     # -- K1 + K2
     def preprocess(self, params: torch.Tensor, stream=None) -> None:
-        a = self.atlas
-        st = nat.check(
+        nat.check(
             self.lib.pf_preprocess(
-                params.data_ptr(), self.d_tid.data_ptr(), self.d_zorder.data_ptr(), self.n,
-                a.d_base.data_ptr(), a.d_w.data_ptr(), a.d_h.data_ptr(), a.d_q.data_ptr(),
-                a.d_hyp.data_ptr(), a.d_pbase.data_ptr(), a.n_templates, self.alpha_max,
-                self.mu_blend, self.padding, self.W, self.H, self.tile, self.band.ty_begin,
-                self.band.ty_end, self.capacity, self.rec.data_ptr(), self.scratch.data_ptr(),
-                self.scratch_bytes, _stream_handle(stream)),
+                params.data_ptr(), self.n, self.alpha_max, self.mu_blend, self.padding, self.W,
+                self.H, self.tile, self.band.ty_begin, self.band.ty_end, self.capacity,
+                self.rec.data_ptr(), self.scratch.data_ptr(), self.scratch_bytes,
+                _stream_handle(stream)),
             "pf_preprocess")
-        return st
 
     def adam_preprocess(self, params, grads, m, v, *, frozen, gains, lr_table, bc1_table,
                         bc2_table, iter_counter, s_min, s_max, sums, loss_kind, alpha_w, P_total,
                         hist_loss, hist_psnr, part=None, stream=None) -> None:
         """K5+K1 fused: Adam on every parameter, then the next step's records + offsets.
         With ``part`` (pf_fit_step's loss partials) the loss sums are folded here."""
-        a = self.atlas
         g8 = (C.c_double * 8)(*[float(g) for g in gains])
         P = float(P_total)
         nat.check(
@@ -220,13 +219,12 @@ class Compositor:
                 params.data_ptr(), grads.data_ptr(), m.data_ptr(), v.data_ptr(), nat.ptr(frozen),
                 C.addressof(g8), lr_table.data_ptr(), bc1_table.data_ptr(), bc2_table.data_ptr(),
                 iter_counter.data_ptr(), 1, float(s_min), float(s_max), nat.ptr(sums),
-                nat.ptr(part), self.n_part if part is not None else 0, int(loss_kind), float(alpha_w), 1.0 / (3.0 * P), 1.0 / P, nat.ptr(hist_loss),
-                nat.ptr(hist_psnr), self.d_tid.data_ptr(), self.d_zorder.data_ptr(), self.n,
-                a.d_base.data_ptr(), a.d_w.data_ptr(), a.d_h.data_ptr(), a.d_q.data_ptr(),
-                a.d_hyp.data_ptr(), a.d_pbase.data_ptr(), a.n_templates, self.alpha_max,
-                self.mu_blend, self.padding, self.W, self.H, self.tile, self.band.ty_begin,
-                self.band.ty_end, self.capacity, self.rec.data_ptr(), self.scratch.data_ptr(),
-                self.scratch_bytes, _stream_handle(stream)),
+                nat.ptr(part), self.n_part if part is not None else 0, int(loss_kind),
+                float(alpha_w), 1.0 / (3.0 * P), 1.0 / P, nat.ptr(hist_loss),
+                nat.ptr(hist_psnr), self.n, self.alpha_max, self.mu_blend, self.padding, self.W,
+                self.H, self.tile, self.band.ty_begin, self.band.ty_end, self.capacity,
+                self.rec.data_ptr(), self.scratch.data_ptr(), self.scratch_bytes,
+                _stream_handle(stream)),
             "pf_adam_preprocess")
 
     def bin(self, stream=None) -> None:

@@ -10,6 +10,8 @@
 // psnr (fit.py:241-247) = 10*log10(1/mse), inf when mse == 0.
 #include <math_constants.h>
 
+#include <cstdlib>
+
 #include "../../include/primfit_b200.h"
 #include "pf_common.cuh"
 
@@ -146,4 +148,40 @@ extern "C" size_t pf_record_bytes(void) { return sizeof(RecF) + sizeof(RecG) + s
 extern "C" int pf_render_tile(void) { return kTile; }
 extern "C" long long pf_saved_capacity(int capacity) {
   return (long long)capacity * (long long)kTilePix;
+}
+
+// Diagnostics timeline buffer (see tl_mark in pf_common.cuh): allocated on the
+// first call when PF_TIMELINE is set in the environment, else NULL.
+static unsigned long long* g_tl = nullptr;
+extern "C" int pf_timeline_reset();
+unsigned long long* pf::pf_timeline_ptr() {
+  static bool checked = false;
+  if (!checked) {
+    checked = true;
+    if (getenv("PF_TIMELINE")) {
+      cudaMalloc(&g_tl, sizeof(unsigned long long) * 64);
+      pf_timeline_reset();
+    }
+  }
+  return g_tl;
+}
+
+extern "C" int pf_timeline_reset() {
+  if (!g_tl) return 0;
+  unsigned long long h[64];
+  for (int k = 0; k < 16; ++k) {
+    h[4 * k] = ~0ull;
+    h[4 * k + 1] = ~0ull;
+    h[4 * k + 2] = 0;
+    h[4 * k + 3] = 0;
+  }
+  cudaMemcpy(g_tl, h, sizeof(h), cudaMemcpyHostToDevice);
+  return 1;
+}
+
+extern "C" int pf_timeline_dump(unsigned long long* host) {
+  if (!g_tl) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, g_tl, sizeof(unsigned long long) * 64, cudaMemcpyDeviceToHost);
+  return 1;
 }

@@ -54,36 +54,30 @@ struct AdamPart {
 
 struct PreArgs {
   double* params;
-  const int32_t* tid;
-  const int32_t* zorder;
   int n;
-  const int32_t* tpl_base;
-  const int32_t* tpl_w;
-  const int32_t* tpl_h;
-  const double* tpl_q;
-  const double* tpl_hyp;
   double alpha_max, mu_blend, padding;
   int W, H, tile, ty_begin, ty_end;
   RecF* recf;
   RecG* recg;
   RecC* recc;
   RecS* recs;
-  const int32_t* tpl_pbase;  // padded-atlas base per template (RecS)
   BinScratch s;
   AdamPart ad;
+  unsigned long long* tl;  // diagnostics timeline or NULL
 };
 
 constexpr double kB1 = 0.9, kB2 = 0.999, kAdamEps = 1e-8;
 constexpr int kPrimThreads = 256;
 
 // adam_step for one scalar (fit.py:224-237), reference op order, no contraction.
-__device__ __forceinline__ double adam_scalar(const AdamPart& d, size_t idx, int col, int prim,
-                                              double p, double lr, double bc1, double bc2) {
-  const double g = d.grads[idx];
-  d.grads[idx] = 0.0;  // ready for the next backward
-  if (d.frozen == nullptr || d.frozen[prim] == 0) {
-    const double mm = __dadd_rn(__dmul_rn(kB1, d.m[idx]), __dmul_rn(1.0 - kB1, g));
-    const double vv = __dadd_rn(__dmul_rn(kB2, d.v[idx]), __dmul_rn(1.0 - kB2, __dmul_rn(g, g)));
+// m, v, frozen are loaded by the caller before the PDL wait (k_step does not
+// touch them); g is this step's gradient.
+__device__ __forceinline__ double adam_scalar(const AdamPart& d, size_t idx, int col, bool live_p,
+                                              double p, double g, double m0, double v0, double lr,
+                                              double bc1, double bc2) {
+  if (live_p) {
+    const double mm = __dadd_rn(__dmul_rn(kB1, m0), __dmul_rn(1.0 - kB1, g));
+    const double vv = __dadd_rn(__dmul_rn(kB2, v0), __dmul_rn(1.0 - kB2, __dmul_rn(g, g)));
     d.m[idx] = mm;
     d.v[idx] = vv;
     const double mh = __ddiv_rn(mm, bc1);
@@ -97,21 +91,40 @@ __device__ __forceinline__ double adam_scalar(const AdamPart& d, size_t idx, int
 
 template <bool ADAM>
 __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
+  tl_mark(a.tl, ADAM ? 2 : 3, 0);
   const int g = blockIdx.x * kPrimThreads + threadIdx.x;
-  const int j = g >> 3, c = g & 7;
+  const int i = g >> 3, c = g & 7;  // primitive, parameter column
   const int lane = threadIdx.x & 31, gb = lane & ~7;
-  const bool live = j < a.n;
-  const int i = live ? __ldg(a.zorder + j) : 0;
+  const bool live = i < a.n;
+  // static structure: one 48-byte record, independent of the parameter loads
+  PrimInfo pi{2, 2, 0, 0, 1.0, 1.0, 0, 0, 0, 0};
+  if (live) {
+    const int4* src = reinterpret_cast<const int4*>(a.s.pinfo + i);
+    const int4 w0 = __ldg(src), w1 = __ldg(src + 1), w2 = __ldg(src + 2);
+    pi.wt = w0.x; pi.ht = w0.y; pi.base = w0.z; pi.pbase = w0.w;
+    pi.q = __hiloint2double(w1.y, w1.x);
+    pi.hyp = __hiloint2double(w1.w, w1.z);
+    pi.zrank = w2.x; pi.tid = w2.y;
+  }
   const size_t pidx = (size_t)i * 8 + c;
   double pc = live ? a.params[pidx] : 1.0;
   int it = 0;
   if (ADAM) {
+    // everything k_step (the predecessor) does not write, before the PDL wait
     it = *a.ad.iter;
+    const double lr = a.ad.lr_table[it], bc1 = a.ad.bc1_table[it], bc2 = a.ad.bc2_table[it];
+    const double m0 = live ? a.ad.m[pidx] : 0.0, v0 = live ? a.ad.v[pidx] : 0.0;
+    const bool live_p = live && (a.ad.frozen == nullptr || a.ad.frozen[i] == 0);
+    pdl_trigger();
+    pdl_wait();
+    tl_mark(a.tl, 2, 1);
     if (live) {
-      pc = adam_scalar(a.ad, pidx, c, i, pc, a.ad.lr_table[it], a.ad.bc1_table[it],
-                       a.ad.bc2_table[it]);
+      const double gr = a.ad.grads[pidx];
+      a.ad.grads[pidx] = 0.0;  // ready for the next backward
+      pc = adam_scalar(a.ad, pidx, c, live_p, pc, gr, m0, v0, lr, bc1, bc2);
       a.params[pidx] = pc;
     }
+    tl_mark(a.tl, 4, 1);
     if (a.ad.part) {
       // first level of the fixed-order loss fold: this block's chunk of partials
       __shared__ double fr[kPrimThreads / 32][3];
@@ -142,15 +155,19 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
       }
     }
   }
+  if (!ADAM) {
+    pdl_wait();  // (records / rects may still be read by a predecessor)
+    tl_mark(a.tl, 3, 1);
+    pdl_trigger();
+  }
+  if (ADAM) tl_mark(a.tl, 5, 1);
   // gather the primitive's 8 parameters from its lane group
   const double x = __shfl_sync(kFull, pc, gb + 0), y = __shfl_sync(kFull, pc, gb + 1);
   const double s = __shfl_sync(kFull, pc, gb + 2), rot = __shfl_sync(kFull, pc, gb + 3);
   const double nu = __shfl_sync(kFull, pc, gb + 4), cl0 = __shfl_sync(kFull, pc, gb + 5);
   const double cl1 = __shfl_sync(kFull, pc, gb + 6), cl2 = __shfl_sync(kFull, pc, gb + 7);
-  const int t = live ? __ldg(a.tid + i) : 0;
-  const int wt = live ? __ldg(a.tpl_w + t) : 2, ht = live ? __ldg(a.tpl_h + t) : 2;
-  const double q = live ? __ldg(a.tpl_q + t) : 1.0;
-  const double hyp = live ? __ldg(a.tpl_hyp + t) : 1.0;
+  const int t = pi.tid, wt = pi.wt, ht = pi.ht;
+  const double q = pi.q, hyp = pi.hyp;
   const double sq = __dmul_rn(s, q);
 
   // transcendental / division work split across the lane group
@@ -184,7 +201,7 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
       case 5: pf[5] = make_double2(__dmul_rn(a.alpha_max, sig), __dmul_rn(omm, sc0)); break;
       case 6: pf[6] = make_double2(__dmul_rn(omm, sc1), __dmul_rn(omm, sc2)); break;
       default:
-        reinterpret_cast<int4*>(pf)[7] = make_int4(__ldg(a.tpl_base + t), wt, ht, t);
+        reinterpret_cast<int4*>(pf)[7] = make_int4(pi.base, wt, ht, t);
         break;
     }
     float4* pg = reinterpret_cast<float4*>(a.recg + i);
@@ -210,7 +227,7 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
         break;
       }
       case 5:
-        reinterpret_cast<int4*>(pg)[5] = make_int4(__ldg(a.tpl_base + t), wt, ht, 0);
+        reinterpret_cast<int4*>(pg)[5] = make_int4(pi.base, wt, ht, 0);
         break;
       default: {
         // cull record (see RecC): fp32 centre and axes, conservative slack
@@ -255,7 +272,7 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
         }
         default:
           reinterpret_cast<int4*>(ps4)[7] =
-              make_int4(a.tpl_pbase ? __ldg(a.tpl_pbase + t) : 0, wt + 1, i, 0);
+              make_int4(pi.pbase, wt + 1, i, 0);
           break;
       }
       switch (c) {
@@ -288,19 +305,21 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
         const int ty1 = min((int)hi_y / a.tile, a.ty_end - 1);
         if (ty0 <= ty1) rc = make_int4(tx0, ty0, tx1, ty1);
       }
-      a.s.rect[j] = rc;
+      a.s.rect[pi.zrank] = rc;
     }
   }
 
   if (ADAM) {
     // the last block to finish advances the iteration counter (all blocks have read it)
     __shared__ bool am_last;
+    tl_mark(a.tl, 6, 1);
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
       am_last = atomicAdd(a.s.done, 1u) == gridDim.x - 1;
     }
     __syncthreads();
+    tl_mark(a.tl, 7, 1);
     if (am_last && threadIdx.x < 32) {
       __threadfence();
       const AdamPart& d = a.ad;
@@ -346,6 +365,7 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
       }
     }
   }
+  tl_mark(a.tl, ADAM ? 2 : 3, 3);
 }
 
 struct RowArgs {
@@ -356,28 +376,42 @@ struct RowArgs {
   int32_t* status;
   int32_t* classes;  // optional tile cost classes (see kTileClasses), or NULL
   int n_tiles;
+  unsigned long long* tl;
 };
 
 constexpr int kRowThreads = 1024;
+constexpr int kRowCache = 8;  // rects per thread kept in registers between the passes
 
-// K2: one block per tile row (band-local r).  See the file header.
+// K2: blocks (r, cb): tile row r, column block cb of gridDim.y.  See the file
+// header.  Every column block of a row redoes (a) (cheap: the rects are in L2)
+// and the column counts of (b); offsets, classes and the ballot walks of (c)
+// cover only its own columns, so a row's work spreads over gridDim.y SMs.
+template <bool CACHE>
 __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
   extern __shared__ int2 rsm[];  // [smem_list] row list, then [ntx] column counters
   __shared__ int ws[32];
+  __shared__ int4 ws4[32];
   __shared__ int s_rl, s_base, s_rbase;
   __shared__ int s_ccnt[kTileClasses], s_cbase[kTileClasses];
   int* col = reinterpret_cast<int*>(rsm + a.smem_list);
   int* ccls = col + a.ntx;  // per-column tile class | rank within the block << 8
   const int r = blockIdx.x, ty = a.ty_begin + r;
+  const int cb = blockIdx.y, ncb = gridDim.y;
+  const int cbeg = (int)((long long)a.ntx * cb / ncb), cend = (int)((long long)a.ntx * (cb + 1) / ncb);
   const int tid = threadIdx.x;
+  tl_mark(a.tl, 0, 0);
+  pdl_wait();     // rects come from K1
+  tl_mark(a.tl, 0, 1);
+  pdl_trigger();  // after the wait: a dependent that starts early sees K1 complete
 
   // (a) stable compaction of the primitives covering row ty, z order kept
   const int chunk = (a.n + kRowThreads - 1) / kRowThreads;
   const int j0 = min(a.n, tid * chunk), j1 = min(a.n, j0 + chunk);
+  int4 rcache[CACHE ? kRowCache : 1];
+  int zcache[CACHE ? kRowCache : 1];
   int cnt = 0, below = 0, below_rows = 0, all = 0;
-  for (int j = j0; j < j1; ++j) {
-    const int4 rc = a.s.rect[j];
-    if (rc.x > rc.z) continue;  // empty
+  auto tally = [&](const int4& rc) {
+    if (rc.x > rc.z) return;  // empty
     const int span = rc.z - rc.x + 1;
     all += (rc.w - rc.y + 1) * span;
     if (rc.y <= ty && ty <= rc.w) ++cnt;
@@ -386,20 +420,36 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
       below += rows * span;
       below_rows += rows;
     }
+  };
+  if (CACHE) {
+    // all loads first (independent), then the tallies
+#pragma unroll
+    for (int k = 0; k < kRowCache; ++k)
+      rcache[k] = j0 + k < j1 ? a.s.rect[j0 + k] : make_int4(1, 1, 0, 0);
+#pragma unroll
+    for (int k = 0; k < kRowCache; ++k) {
+      const int4 rc = rcache[k];
+      zcache[k] = (rc.x <= rc.z && rc.y <= ty && ty <= rc.w) ? __ldg(a.s.zprim + j0 + k) : 0;
+      tally(rc);
+    }
+  } else {
+    for (int j = j0; j < j1; ++j) tally(a.s.rect[j]);
   }
-  int tot;
-  int pos = block_excl_scan(cnt, ws, &tot);
-  int base, rbase, K;
-  (void)block_excl_scan(below, ws, &base);
-  (void)block_excl_scan(below_rows, ws, &rbase);
-  (void)block_excl_scan(all, ws, &K);
-  if (r == 0 && tid == 0) {
-    // every block knows K; row block 0 publishes it (TileBins.offsets[-1], overflow flag)
+  int4 tot4;
+  const int4 ex = block_excl_scan4(make_int4(cnt, below, below_rows, all), ws4, &tot4);
+  const int tot = tot4.x, base = tot4.y, rbase = tot4.z, K = tot4.w;
+  int pos = ex.x;
+  if (r == 0 && cb == 0 && tid == 0) {
+    // every block knows K; block (0, 0) publishes it (TileBins.offsets[-1], overflow flag)
     a.bin_off[a.n_rows * a.ntx] = K;
     a.status[0] = K;
     a.status[1] = K > a.cap ? 1 : 0;
   }
-  if (K > a.cap) return;  // overflow (block-uniform): nothing is written
+  tl_mark(a.tl, 8, 1);
+  if (K > a.cap) {  // overflow (grid-uniform): nothing is written
+    tl_mark(a.tl, 0, 3);
+    return;
+  }
   if (tid == 0) {
     s_rl = tot;
     s_base = base;
@@ -407,19 +457,34 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
   }
   for (int c = tid; c < a.ntx; c += kRowThreads) col[c] = 0;
   if (tid < kTileClasses) s_ccnt[tid] = 0;
-  for (int j = j0; j < j1; ++j) {
-    const int4 rc = a.s.rect[j];
-    if (rc.x > rc.z || rc.y > ty || ty > rc.w) continue;
-    const int2 e = make_int2(j, rc.x | (rc.z << 16));
+  // long rows spill the list to HBM (every column block writes the same values)
+  const bool spill_list = tot > a.smem_list;
+  auto put = [&](int i, const int4& rc) {
+    // (primitive index, column span): the list order is the z order
+    const int2 e = make_int2(i, rc.x | (rc.z << 16));
     if (pos < a.smem_list) rsm[pos] = e;
-    a.s.rowlist[rbase + pos] = e;  // rbase + pos < rows entries <= K <= cap
+    if (spill_list) a.s.rowlist[rbase + pos] = e;  // rbase + pos < rows entries <= K <= cap
     ++pos;
+  };
+  if (CACHE) {
+#pragma unroll
+    for (int k = 0; k < kRowCache; ++k) {
+      const int4 rc = rcache[k];
+      if (rc.x <= rc.z && rc.y <= ty && ty <= rc.w) put(zcache[k], rc);
+    }
+  } else {
+    for (int j = j0; j < j1; ++j) {
+      const int4 rc = a.s.rect[j];
+      if (rc.x > rc.z || rc.y > ty || ty > rc.w) continue;
+      put(__ldg(a.s.zprim + j), rc);
+    }
   }
   __syncthreads();
   const int RL = s_rl;
   const int2* list = RL <= a.smem_list ? rsm : a.s.rowlist + s_rbase;
 
-  // (b) per-column counts -> offsets of this row's tiles
+  tl_mark(a.tl, 9, 1);
+  // (b) per-column counts (all columns) -> offsets of this block's tiles
   for (int k = tid; k < RL; k += kRowThreads) {
     const int pk = list[k].y;
     for (int tx = pk & 0xffff; tx <= (pk >> 16); ++tx) atomicAdd(col + tx, 1);
@@ -433,30 +498,33 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
   int run = s_base + block_excl_scan(local, ws, &row_total);
   for (int c = c0; c < c1; ++c) {
     const int v = col[c];
-    a.bin_off[r * a.ntx + c] = run;
     col[c] = run;
-    run += v;
-    if (a.classes) {
-      // longest-first schedule for pf_fit_step: tile -> class list of its length
-      const int cl = tile_class(v);
-      const int rank = atomicAdd(&s_ccnt[cl], 1);
-      ccls[c] = cl | (rank << 8);
+    if (c >= cbeg && c < cend) {
+      a.bin_off[r * a.ntx + c] = run;
+      if (a.classes) {
+        // longest-first schedule for pf_fit_step: tile -> class list of its length
+        const int cl = tile_class(v);
+        const int rank = atomicAdd(&s_ccnt[cl], 1);
+        ccls[c] = cl | (rank << 8);
+      }
     }
+    run += v;
   }
   __syncthreads();
   if (a.classes) {
     if (tid < kTileClasses) s_cbase[tid] = s_ccnt[tid] ? atomicAdd(a.classes + tid, s_ccnt[tid]) : 0;
     __syncthreads();
-    for (int c = c0; c < c1; ++c) {
+    for (int c = max(c0, cbeg); c < min(c1, cend); ++c) {
       const int cl = ccls[c] & 0xff, rank = ccls[c] >> 8;
-      const int pos = s_cbase[cl] + rank;
-      if (pos < a.n_tiles) a.classes[kTileClasses + cl * a.n_tiles + pos] = r * a.ntx + c;
+      const int p = s_cbase[cl] + rank;
+      if (p < a.n_tiles) a.classes[kTileClasses + cl * a.n_tiles + p] = r * a.ntx + c;
     }
   }
 
-  // (c) one warp per column: ordered ballot walk of the row list
+  tl_mark(a.tl, 10, 1);
+  // (c) one warp per column of this block: ordered ballot walk of the row list
   const int lane = tid & 31, warp = tid >> 5;
-  for (int c = warp; c < a.ntx; c += kRowThreads / 32) {
+  for (int c = cbeg + warp; c < cend; c += kRowThreads / 32) {
     int out = col[c];
     for (int b = 0; b < RL; b += 32) {
       const int k = b + lane;
@@ -468,14 +536,11 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
         hit = (e.y & 0xffff) <= c && c <= (e.y >> 16);
       }
       const unsigned ball = __ballot_sync(kFull, hit);
-      if (hit) {
-        const int p = out + __popc(ball & ((1u << lane) - 1u));
-        const int i = __ldg(a.s.zprim + j);
-        a.bin_idx[p] = i;
-      }
+      if (hit) a.bin_idx[out + __popc(ball & ((1u << lane) - 1u))] = j;
       out += __popc(ball);
     }
   }
+  tl_mark(a.tl, 0, 3);
 }
 
 // Alpha quad atlas (see load_quad in pf_common.cuh): one thread per texel.
@@ -547,30 +612,17 @@ static bool band_ok(int W, int H, int tile, int ty_begin, int ty_end, int* ntx, 
   return true;
 }
 
-static int fill_pre_args(PreArgs& a, double* params, const int32_t* template_id,
-                         const int32_t* zorder, int n, const int32_t* tpl_base,
-                         const int32_t* tpl_w, const int32_t* tpl_h, const double* tpl_q,
-                         const double* tpl_hyp, const int32_t* tpl_pbase, int n_tpl,
-                         double alpha_max, double mu_blend, double padding, int W, int H,
-                         int tile, int ty_begin, int ty_end, int capacity, void* rec,
-                         void* scratch, size_t scratch_bytes) {
+static int fill_pre_args(PreArgs& a, double* params, int n, double alpha_max, double mu_blend,
+                         double padding, int W, int H, int tile, int ty_begin, int ty_end,
+                         int capacity, void* rec, void* scratch, size_t scratch_bytes) {
   int ntx, n_rows;
-  if (n < 0 || n_tpl < 0 || capacity < 0 || !band_ok(W, H, tile, ty_begin, ty_end, &ntx, &n_rows))
+  if (n < 0 || capacity < 0 || !band_ok(W, H, tile, ty_begin, ty_end, &ntx, &n_rows))
     return PF_ERR_ARG;
   if (!scratch || scratch_bytes < pf_bin_scratch_bytes(n, n_rows * ntx, capacity))
     return PF_ERR_SCRATCH;
-  if (n > 0 && (!params || !template_id || !zorder || !rec || !tpl_base || !tpl_w || !tpl_h ||
-                !tpl_q || !tpl_hyp))
-    return PF_ERR_ARG;
+  if (n > 0 && (!params || !rec)) return PF_ERR_ARG;
   a.params = params;
-  a.tid = template_id;
-  a.zorder = zorder;
   a.n = n;
-  a.tpl_base = tpl_base;
-  a.tpl_w = tpl_w;
-  a.tpl_h = tpl_h;
-  a.tpl_q = tpl_q;
-  a.tpl_hyp = tpl_hyp;
   a.alpha_max = alpha_max;
   a.mu_blend = mu_blend;
   a.padding = padding;
@@ -583,24 +635,58 @@ static int fill_pre_args(PreArgs& a, double* params, const int32_t* template_id,
   a.recg = (RecG*)((char*)rec + sizeof(RecF) * (size_t)n);
   a.recc = (RecC*)((char*)rec + (sizeof(RecF) + sizeof(RecG)) * (size_t)n);
   a.recs = (RecS*)((char*)rec + (sizeof(RecF) + sizeof(RecG) + sizeof(RecC)) * (size_t)n);
-  a.tpl_pbase = tpl_pbase;
   a.s = carve(scratch, n, capacity);
   a.ad = AdamPart{};
+  a.tl = pf_timeline_ptr();
   return PF_OK;
 }
 
 static int launch_prim(bool adam, const PreArgs& a, cudaStream_t st) {
   const int blocks = div_up(a.n > 0 ? a.n * 8 : 1, kPrimThreads);
-  if (adam)
-    k_prim<true><<<blocks, kPrimThreads, 0, st>>>(a);
-  else if (a.n > 0)
-    k_prim<false><<<blocks, kPrimThreads, 0, st>>>(a);
+  if (adam) return (int)launch_pdl(k_prim<true>, blocks, kPrimThreads, 0, st, a);
+  if (a.n > 0) return (int)launch_pdl(k_prim<false>, blocks, kPrimThreads, 0, st, a);
   return (int)cudaGetLastError();
 }
 
-extern "C" int pf_scratch_init(void* scratch, size_t scratch_bytes, const int32_t* zorder, int n,
-                               int capacity, void* stream) {
-  if (!scratch || n < 0 || capacity < 0 ||
+// One-time static structure: pinfo[zorder[j]] = {template geometry, z rank j}.
+struct InfoArgs {
+  const int32_t* tid;
+  const int32_t* zorder;
+  int n, n_tpl;
+  const int32_t* base;
+  const int32_t* pbase;
+  const int32_t* w;
+  const int32_t* h;
+  const double* q;
+  const double* hyp;
+  PrimInfo* pinfo;
+};
+
+__global__ void k_pinfo(InfoArgs a) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.n) return;
+  const int i = a.zorder[j];
+  const int t = a.tid[i];
+  PrimInfo p;
+  const bool ok = t >= 0 && t < a.n_tpl;
+  p.wt = ok ? a.w[t] : 2;
+  p.ht = ok ? a.h[t] : 2;
+  p.base = ok ? a.base[t] : 0;
+  p.pbase = ok && a.pbase ? a.pbase[t] : 0;
+  p.q = ok ? a.q[t] : 1.0;
+  p.hyp = ok ? a.hyp[t] : 1.0;
+  p.zrank = j;
+  p.tid = t;
+  p.pad0 = p.pad1 = 0;
+  a.pinfo[i] = p;
+}
+
+extern "C" int pf_scratch_init(void* scratch, size_t scratch_bytes, const int32_t* template_id,
+                               const int32_t* zorder, int n, const int32_t* tpl_base,
+                               const int32_t* tpl_pbase, const int32_t* tpl_w,
+                               const int32_t* tpl_h, const double* tpl_q, const double* tpl_hyp,
+                               int n_tpl, int capacity, void* stream) {
+  if (!scratch || n < 0 || capacity < 0 || n_tpl < 0 ||
       scratch_bytes < carve(nullptr, n, capacity).total)
     return PF_ERR_SCRATCH;
   cudaStream_t st = (cudaStream_t)stream;
@@ -608,23 +694,24 @@ extern "C" int pf_scratch_init(void* scratch, size_t scratch_bytes, const int32_
   if (e != cudaSuccess) return (int)e;
   BinScratch s = carve(scratch, n, capacity);
   if (n > 0) {
-    if (!zorder) return PF_ERR_ARG;
+    if (!zorder || !template_id || !tpl_base || !tpl_w || !tpl_h || !tpl_q || !tpl_hyp)
+      return PF_ERR_ARG;
     e = cudaMemcpyAsync(s.zprim, zorder, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return (int)e;
+    InfoArgs ia{template_id, zorder, n, n_tpl, tpl_base, tpl_pbase, tpl_w, tpl_h, tpl_q, tpl_hyp,
+                s.pinfo};
+    k_pinfo<<<div_up(n, 256), 256, 0, st>>>(ia);
+    e = cudaGetLastError();
   }
   return (int)e;
 }
 
-extern "C" int pf_preprocess(const double* params, const int32_t* template_id,
-                             const int32_t* zorder, int n, const int32_t* tpl_base,
-                             const int32_t* tpl_w, const int32_t* tpl_h, const double* tpl_q,
-                             const double* tpl_hyp, const int32_t* tpl_pbase, int n_tpl,
-                             double alpha_max, double mu_blend, double padding, int W, int H,
-                             int tile, int ty_begin, int ty_end, int capacity, void* rec,
-                             void* scratch, size_t scratch_bytes, void* stream) {
+extern "C" int pf_preprocess(const double* params, int n, double alpha_max, double mu_blend,
+                             double padding, int W, int H, int tile, int ty_begin, int ty_end,
+                             int capacity, void* rec, void* scratch, size_t scratch_bytes,
+                             void* stream) {
   PreArgs a;
-  const int rc = fill_pre_args(a, const_cast<double*>(params), template_id, zorder, n, tpl_base,
-                               tpl_w, tpl_h, tpl_q, tpl_hyp, tpl_pbase, n_tpl, alpha_max,
-                               mu_blend, padding,
+  const int rc = fill_pre_args(a, const_cast<double*>(params), n, alpha_max, mu_blend, padding,
                                W, H, tile, ty_begin, ty_end, capacity, rec, scratch,
                                scratch_bytes);
   if (rc != PF_OK) return rc;
@@ -636,20 +723,14 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
                                   const double* lr_table, const double* bc1_table,
                                   const double* bc2_table, int32_t* iter, int clamp, double s_min,
                                   double s_max, double* sums, const double* part, int n_part,
-                                  int loss_kind, double alpha_w,
-                                  double inv_3P, double inv_P, double* hist_loss,
-                                  double* hist_psnr, const int32_t* template_id,
-                                  const int32_t* zorder, int n, const int32_t* tpl_base,
-                                  const int32_t* tpl_w, const int32_t* tpl_h, const double* tpl_q,
-                                  const double* tpl_hyp, const int32_t* tpl_pbase, int n_tpl,
-                                  double alpha_max, double mu_blend, double padding, int W, int H,
-                                  int tile,
+                                  int loss_kind, double alpha_w, double inv_3P, double inv_P,
+                                  double* hist_loss, double* hist_psnr, int n, double alpha_max,
+                                  double mu_blend, double padding, int W, int H, int tile,
                                   int ty_begin, int ty_end, int capacity, void* rec, void* scratch,
                                   size_t scratch_bytes, void* stream) {
   PreArgs a;
-  const int rc = fill_pre_args(a, params, template_id, zorder, n, tpl_base, tpl_w, tpl_h, tpl_q,
-                               tpl_hyp, tpl_pbase, n_tpl, alpha_max, mu_blend, padding, W, H, tile,
-                               ty_begin, ty_end, capacity, rec, scratch, scratch_bytes);
+  const int rc = fill_pre_args(a, params, n, alpha_max, mu_blend, padding, W, H, tile, ty_begin,
+                               ty_end, capacity, rec, scratch, scratch_bytes);
   if (rc != PF_OK) return rc;
   if (!iter || !lr_table || !bc1_table || !bc2_table || (n > 0 && (!grads || !m || !v)))
     return PF_ERR_ARG;
@@ -707,15 +788,27 @@ extern "C" int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, i
   ra.status = status;
   ra.classes = tile_classes;
   ra.n_tiles = n_rows * ntx;
+  ra.tl = pf_timeline_ptr();
   const size_t smem = sizeof(int2) * kRowSmemList + 2 * sizeof(int) * (size_t)ntx;
-  static bool attr_set = false;
-  if (smem > 48 * 1024 || !attr_set) {
-    cudaFuncSetAttribute(k_bin_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const bool cache = (n + kRowThreads - 1) / kRowThreads <= kRowCache;
+  void (*kern)(RowArgs) = cache ? k_bin_rows<true> : k_bin_rows<false>;
+  static size_t attr_smem[2] = {0, 0};
+  if (smem > attr_smem[cache]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(smem > 48 * 1024 ? smem : 48 * 1024));
-    attr_set = true;
+    attr_smem[cache] = smem;
   }
-  k_bin_rows<<<n_rows, kRowThreads, smem, st>>>(ra);
-  return (int)cudaGetLastError();
+  // column blocks per row: as many as fit in one wave (1024-thread blocks, one
+  // per SM with the register cache), >= 16 columns each
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int ncb = (cache ? 1 : 2) * sms / n_rows;
+  ncb = max(1, min(ncb, ntx / 16));
+  return (int)launch_pdl2(kern, dim3(n_rows, ncb), kRowThreads, smem, st, ra);
 }
 
 extern "C" int pf_atlas_quad(const double* tex, int texels, const int32_t* tpl_base,

@@ -5,9 +5,19 @@
 
 namespace pf {
 
+// Static per-primitive structure (template geometry, z rank), built once by
+// pf_scratch_init so that K1 has no dependent loads before its math.
+struct __align__(16) PrimInfo {
+  int32_t wt, ht, base, pbase;  // template size, atlas base, padded-atlas base
+  double q, hyp;                // v-axis aspect, bbox factor hypot(1, max(1, q))
+  int32_t zrank, tid, pad0, pad1;
+};
+static_assert(sizeof(PrimInfo) == 48, "PrimInfo must be 48 bytes");
+
 struct BinScratch {
   int4* rect;        // [n] band-clipped tile rect per z position (tx0, ty0, tx1, ty1)
   int32_t* zprim;    // [n] primitive index per z position (static, set by pf_scratch_init)
+  PrimInfo* pinfo;   // [n] static per-primitive structure (pf_scratch_init)
   int2* rowlist;     // [capacity] per-row z-ordered lists: (z position, tx0 | tx1 << 16)
   uint32_t* done;    // [4] last-block ticket
   double* fold;      // [prim blocks][3] per-block loss-partial folds (pf_adam_preprocess)
@@ -27,6 +37,7 @@ static inline BinScratch carve(void* base, int n, int cap) {
   };
   s.rect = (int4*)take(sizeof(int4) * (size_t)n);
   s.zprim = (int32_t*)take(sizeof(int32_t) * (size_t)n);
+  s.pinfo = (PrimInfo*)take(sizeof(PrimInfo) * (size_t)n);
   s.rowlist = (int2*)take(sizeof(int2) * (size_t)cap);
   s.done = (uint32_t*)take(sizeof(uint32_t) * 4);
   s.fold = (double*)take(sizeof(double) * 3 * (size_t)((8 * (size_t)n + 255) / 256 + 1));
@@ -61,6 +72,47 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_sums, int* total
   *total = warp_sums[nw - 1];
   const int r = excl_warp + x - v;
   __syncthreads();  // warp_sums reusable by the caller afterwards
+  return r;
+}
+
+// Block-wide exclusive scan of four ints per thread at once (one barrier pass).
+__device__ __forceinline__ int4 block_excl_scan4(int4 v, int4* warp_sums, int4* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  int4 x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y0 = __shfl_up_sync(kFull, x.x, o), y1 = __shfl_up_sync(kFull, x.y, o);
+    const int y2 = __shfl_up_sync(kFull, x.z, o), y3 = __shfl_up_sync(kFull, x.w, o);
+    if (lane >= o) {
+      x.x += y0;
+      x.y += y1;
+      x.z += y2;
+      x.w += y3;
+    }
+  }
+  if (lane == 31) warp_sums[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int4 w = lane < nw ? warp_sums[lane] : make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y0 = __shfl_up_sync(kFull, w.x, o), y1 = __shfl_up_sync(kFull, w.y, o);
+      const int y2 = __shfl_up_sync(kFull, w.z, o), y3 = __shfl_up_sync(kFull, w.w, o);
+      if (lane >= o) {
+        w.x += y0;
+        w.y += y1;
+        w.z += y2;
+        w.w += y3;
+      }
+    }
+    if (lane < nw) warp_sums[lane] = w;  // inclusive warp prefix
+  }
+  __syncthreads();
+  const int4 ew = warp > 0 ? warp_sums[warp - 1] : make_int4(0, 0, 0, 0);
+  *total = warp_sums[nw - 1];
+  const int4 r = make_int4(ew.x + x.x - v.x, ew.y + x.y - v.y, ew.z + x.z - v.z, ew.w + x.w - v.w);
+  __syncthreads();
   return r;
 }
 

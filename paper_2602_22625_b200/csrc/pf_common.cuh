@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace pf {
@@ -250,5 +251,54 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 inline int div_up(int a, int b) { return (a + b - 1) / b; }
+
+// Programmatic dependent launch (PDL): kernels of the fit step are launched
+// with programmatic stream serialization, so a kernel's blocks may start while
+// its predecessor drains.  Rules: (1) before pdl_wait() a kernel reads nothing
+// its predecessor writes and writes nothing its predecessor reads; (2) every
+// path calls pdl_wait() before exiting; (3) a kernel whose dependent reads
+// data from EARLIER kernels before its own wait triggers only after its wait
+// (then "dependent launched" implies "everything before me completed").
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Diagnostics timeline (PF_TIMELINE=1 builds the pointer; NULL otherwise):
+// per kernel slot k, [4k] = min block start, [4k+1] = min PDL-wait return,
+// [4k+2] = max PDL-wait return, [4k+3] = max block end (globaltimer ns).
+__device__ __forceinline__ unsigned long long gtime_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void tl_mark(unsigned long long* tl, int slot, int what) {
+  if (tl == nullptr || (threadIdx.x & (what == 3 ? 31 : 0xffffffff)) != 0) return;
+  const unsigned long long t = gtime_ns();
+  if (what == 0 || what == 1) atomicMin(tl + 4 * slot + what, t);
+  if (what == 1 || what == 3) atomicMax(tl + 4 * slot + (what == 1 ? 2 : 3), t);
+}
+unsigned long long* pf_timeline_ptr();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl2(void (*kern)(KArgs...), dim3 grid, int block, size_t smem,
+                               cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  return launch_pdl2(kern, dim3((unsigned)grid), block, smem, st, std::forward<Args>(args)...);
+}
 
 }  // namespace pf

@@ -82,6 +82,7 @@ struct StepArgs {
   const int32_t* classes;  // pf_bin's tile classes (counts + lists) or NULL: tile = ticket
   int32_t* classes_rw;
   unsigned long long* prof;  // diagnostics (PF_STEP_PROF=1): [warp slot][6], else NULL
+  unsigned long long* tl;    // diagnostics timeline or NULL
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -103,15 +104,6 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 __device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
                : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "PF_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
-      " @!p bra PF_WAIT_%=;\n}" ::"r"(su32(b)),
-      "r"(parity)
-      : "memory");
 }
 __device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
   uint32_t ok;
@@ -460,12 +452,8 @@ __global__ void __launch_bounds__(G * (kCW + 1) * 32, 1) k_step(StepArgs a) {
   __shared__ __align__(8) uint64_t full[G][kNBuf], empty[G][kNBuf];
   __shared__ int4 hdr[G][kNBuf];
 
+  tl_mark(a.tl, 1, 0);
   const int t = threadIdx.x;
-  if (a.status[1]) {
-    // bin overflow (grid-uniform): lists are not valid; leave clean counters
-    if (blockIdx.x == 0 && a.classes && t < kTileClasses) a.classes_rw[t] = 0;
-    return;
-  }
   const int lane = t & 31, warp = t >> 5;
   constexpr bool has_bg = BG;
   constexpr size_t gbytes = group_bytes(BG), bbytes = buf_bytes(BG);
@@ -493,7 +481,18 @@ __global__ void __launch_bounds__(G * (kCW + 1) * 32, 1) k_step(StepArgs a) {
     mbar_init(&empty[t / kNBuf][t % kNBuf], kCW);
   }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  pdl_wait();  // bins, classes and records of this step are complete from here on
+  tl_mark(a.tl, 1, 1);
+  // after the wait (so a dependent that starts early knows K2 -- and by induction
+  // the previous Adam step -- has completed): the Adam kernel may start loading
+  // its inputs that this kernel does not write
+  pdl_trigger();
   __syncthreads();
+  if (a.status[1]) {
+    // bin overflow (grid-uniform): lists are not valid; leave clean counters
+    if (blockIdx.x == 0 && a.classes && t < kTileClasses) a.classes_rw[t] = 0;
+    return;
+  }
 
   const int g = warp / (kCW + 1), wg = warp % (kCW + 1);
   unsigned char* gs = sm + g * gbytes;
@@ -558,7 +557,7 @@ __global__ void __launch_bounds__(G * (kCW + 1) * 32, 1) k_step(StepArgs a) {
     for (int k = 0;; ++k) {
       if (k >= kNBuf) {
         const unsigned long long c0 = a.prof ? clock64() : 0;
-        mbar_wait_sleep(&empty[g][buf], (eph >> buf) & 1u, 256);
+        mbar_wait_sleep(&empty[g][buf], (eph >> buf) & 1u, 500);
         if (a.prof) p_wait += clock64() - c0;
         eph ^= 1u << buf;
         if (a.sched_lazy && k > 0) {
@@ -616,7 +615,7 @@ __global__ void __launch_bounds__(G * (kCW + 1) * 32, 1) k_step(StepArgs a) {
     uint32_t fph = 0;
     for (;;) {
       const unsigned long long c0 = a.prof ? clock64() : 0;
-      mbar_wait_sleep(&full[g][buf], (fph >> buf) & 1u, 64);
+      mbar_wait_sleep(&full[g][buf], (fph >> buf) & 1u, 200);
       const unsigned long long c1 = a.prof ? clock64() : 0;
       if (a.prof) {
         p_wait += c1 - c0;
@@ -647,6 +646,7 @@ __global__ void __launch_bounds__(G * (kCW + 1) * 32, 1) k_step(StepArgs a) {
       buf = buf + 1 == kNBuf ? 0 : buf + 1;
     }
   }
+  tl_mark(a.tl, 1, 3);
   if (a.prof && lane == 0) {
     unsigned long long* o = a.prof + ((size_t)blockIdx.x * blockDim.x / 32 + warp) * 6;
     o[0] = p_wait;
@@ -777,6 +777,7 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   a.classes = getenv("PF_STEP_NOLPT") ? nullptr : tile_classes;
   a.classes_rw = const_cast<int32_t*>(a.classes);
   a.prof = nullptr;
+  a.tl = pf_timeline_ptr();
   static unsigned long long* prof_buf = nullptr;
   if (getenv("PF_STEP_PROF")) {
     if (!prof_buf) cudaMalloc(&prof_buf, sizeof(unsigned long long) * (6 * 148 * 32 + 65536 * 8));
@@ -834,6 +835,5 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   }
   const int grid = min(sms, max(1, (n_tiles + G - 1) / G));
   g_prof_slots = grid * G * (kCW + 1);
-  kern<<<grid, G * (kCW + 1) * 32, smem, st>>>(a);
-  return (int)cudaGetLastError();
+  return (int)launch_pdl(kern, grid, G * (kCW + 1) * 32, smem, st, a);
 }
