@@ -292,7 +292,8 @@ def run_ours(args) -> None:
     n = eng.n
     h_params = torch.empty(n * 8, dtype=torch.float64, pin_memory=True)
     h_params.copy_(eng.params.view(-1).cpu())
-    h_loss = torch.empty(1, dtype=torch.float64, pin_memory=True)
+    nb = eng.adam_blocks
+    h_loss = torch.empty(nb * 3, dtype=torch.float64, pin_memory=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -304,7 +305,7 @@ def run_ours(args) -> None:
         eng.refresh()  # the step consumes the uploaded parameters
         eng.step()
         h_params.copy_(eng.params.view(-1), non_blocking=True)
-        h_loss.copy_(eng.hist_loss[it : it + 1], non_blocking=True)
+        h_loss.copy_(eng.hist_part[it * nb * 3 : (it + 1) * nb * 3], non_blocking=True)
         torch.cuda.current_stream().synchronize()
     e_end.record()
     torch.cuda.synchronize()
@@ -340,7 +341,7 @@ def run_ours(args) -> None:
                      "step_frac": ab["total"] * value / 1e9 / peaks["hbm_gbs"]},
         "stage_ms": stage_ms,
         "e2e": {"value": 1e3 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": n * 8 * 8,
-                "d2h_bytes_per_step": n * 8 * 8 + 8},
+                "d2h_bytes_per_step": n * 8 * 8 + nb * 3 * 8},
         "gpu_launches": (nodes * args.steps) if nodes else None,
         "kernels_per_step": nodes,
         "clocks": clk,

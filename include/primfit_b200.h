@@ -122,22 +122,27 @@ int pf_preprocess(const double* params, int n, double alpha_max, double mu_blend
                   void* rec, void* scratch, size_t scratch_bytes, void* stream);
 
 /*
- * K5+K1 fused: one Adam step (fit.py:195-238, table mode as pf_adam) on every
- * parameter, then the records / tile rects of the NEXT step from the updated
- * parameters (as pf_preprocess), the loss/psnr history entry and the iteration
- * counter -- one launch between two renders.  Gradients are zeroed.
- *   sums   loss sums of this step (read), or -- with part != NULL -- written
- *          from a fixed-order two-level fold of pf_fit_step's n_part partials
+ * K5+K1 fused: one Adam step (fit.py:195-238) on every parameter, then the
+ * records / tile rects of the NEXT step from the updated parameters (as
+ * pf_preprocess) -- one launch between two renders.  Gradients are zeroed.
+ * The learning rate and bias corrections come from host tables indexed by the
+ * iteration counter kept in `scratch` (zeroed by pf_scratch_init; the Adam
+ * launch marks the iteration done and the next pf_bin advances the counter).
+ *   sums       this step's loss sums (after a cross-rank allreduce), or NULL
+ *   part       pf_fit_step's n_part per-warp loss partials, or NULL
+ *   hist_part  [iterations][pf_adam_blocks(n)][3] float64: this step's loss sums
+ *              per launch block (fixed-order fold of `part`, or `sums` in block
+ *              0 and zeros elsewhere); summing the blocks in order gives the
+ *              HistoryEntry loss of the iteration (fit.py:502-505), or NULL
  */
+int pf_adam_blocks(int n);
 int pf_adam_preprocess(double* params, double* grads, double* m, double* v, const uint8_t* frozen,
                        const double* gains8, const double* lr_table, const double* bc1_table,
-                       const double* bc2_table, int32_t* iter, int clamp, double s_min,
-                       double s_max, double* sums, const double* part, int n_part,
-                       int loss_kind, double alpha_w, double inv_3P, double inv_P,
-                       double* hist_loss, double* hist_psnr, int n, double alpha_max,
-                       double mu_blend, double padding, int W, int H, int tile, int ty_begin,
-                       int ty_end, int capacity, void* rec, void* scratch, size_t scratch_bytes,
-                       void* stream);
+                       const double* bc2_table, int clamp, double s_min, double s_max,
+                       const double* sums, const double* part, int n_part, double* hist_part,
+                       int n, double alpha_max, double mu_blend, double padding, int W, int H,
+                       int tile, int ty_begin, int ty_end, int capacity, void* rec, void* scratch,
+                       size_t scratch_bytes, void* stream);
 
 /*
  * K2 — tile binning from the rects of pf_preprocess: one block per tile row,

@@ -208,24 +208,26 @@ class Compositor:
             "pf_preprocess")
 
     def adam_preprocess(self, params, grads, m, v, *, frozen, gains, lr_table, bc1_table,
-                        bc2_table, iter_counter, s_min, s_max, sums, loss_kind, alpha_w, P_total,
-                        hist_loss, hist_psnr, part=None, stream=None) -> None:
-        """K5+K1 fused: Adam on every parameter, then the next step's records + offsets.
-        With ``part`` (pf_fit_step's loss partials) the loss sums are folded here."""
+                        bc2_table, s_min, s_max, sums=None, part=None, hist_part=None,
+                        stream=None) -> None:
+        """K5+K1 fused: Adam on every parameter, then the next step's records + rects.
+        ``part``: pf_fit_step's loss partials (folded per block into ``hist_part``);
+        ``sums``: already reduced loss sums (multi-rank path)."""
         g8 = (C.c_double * 8)(*[float(g) for g in gains])
-        P = float(P_total)
         nat.check(
             self.lib.pf_adam_preprocess(
                 params.data_ptr(), grads.data_ptr(), m.data_ptr(), v.data_ptr(), nat.ptr(frozen),
                 C.addressof(g8), lr_table.data_ptr(), bc1_table.data_ptr(), bc2_table.data_ptr(),
-                iter_counter.data_ptr(), 1, float(s_min), float(s_max), nat.ptr(sums),
-                nat.ptr(part), self.n_part if part is not None else 0, int(loss_kind),
-                float(alpha_w), 1.0 / (3.0 * P), 1.0 / P, nat.ptr(hist_loss),
-                nat.ptr(hist_psnr), self.n, self.alpha_max, self.mu_blend, self.padding, self.W,
-                self.H, self.tile, self.band.ty_begin, self.band.ty_end, self.capacity,
-                self.rec.data_ptr(), self.scratch.data_ptr(), self.scratch_bytes,
-                _stream_handle(stream)),
+                1, float(s_min), float(s_max), nat.ptr(sums), nat.ptr(part),
+                self.n_part if part is not None else 0, nat.ptr(hist_part), self.n,
+                self.alpha_max, self.mu_blend, self.padding, self.W, self.H, self.tile,
+                self.band.ty_begin, self.band.ty_end, self.capacity, self.rec.data_ptr(),
+                self.scratch.data_ptr(), self.scratch_bytes, _stream_handle(stream)),
             "pf_adam_preprocess")
+
+    @property
+    def adam_blocks(self) -> int:
+        return int(self.lib.pf_adam_blocks(self.n))
 
     def bin(self, stream=None) -> None:
         """K2: CSR tile bins (z-ascending lists) from the rects of the last K1."""

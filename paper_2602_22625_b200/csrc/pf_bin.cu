@@ -40,16 +40,12 @@ struct AdamPart {
   const double* lr_table;
   const double* bc1_table;
   const double* bc2_table;
-  int32_t* iter;
   int clamp;
   double s_min, s_max;
-  double* sums;          // loss sums (read, or written by the fold below)
+  const double* sums;    // loss sums of this step (after an allreduce), or NULL
   const double* part;    // per-warp loss partials of pf_fit_step to fold here, or NULL
   int n_part;
-  int loss_kind;
-  double alpha_w, inv_3P, inv_P;
-  double* hist_loss;
-  double* hist_psnr;
+  double* hist_part;     // [iterations][gridDim.x][3] per-block loss sums (history)
 };
 
 struct PreArgs {
@@ -109,51 +105,34 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
   const size_t pidx = (size_t)i * 8 + c;
   double pc = live ? a.params[pidx] : 1.0;
   int it = 0;
+  double fv0 = 0.0, fv1 = 0.0, fv2 = 0.0;  // loss-fold partial sums of this thread
   if (ADAM) {
     // everything k_step (the predecessor) does not write, before the PDL wait
-    it = *a.ad.iter;
+    it = (int)a.s.done[1];  // advanced by K2 of the next step (see k_bin_rows)
     const double lr = a.ad.lr_table[it], bc1 = a.ad.bc1_table[it], bc2 = a.ad.bc2_table[it];
     const double m0 = live ? a.ad.m[pidx] : 0.0, v0 = live ? a.ad.v[pidx] : 0.0;
     const bool live_p = live && (a.ad.frozen == nullptr || a.ad.frozen[i] == 0);
     pdl_trigger();
     pdl_wait();
     tl_mark(a.tl, 2, 1);
+    // this step's gradient and (first fold level) this block's chunk of k_step's
+    // loss partials: both loads in flight before any math
+    const double gr = live ? a.ad.grads[pidx] : 0.0;
+    if (a.ad.part) {
+      const int chunk = (a.ad.n_part + gridDim.x - 1) / gridDim.x;
+      const int beg = blockIdx.x * chunk, end = min(beg + chunk, a.ad.n_part);
+      for (int k = beg + threadIdx.x; k < end; k += kPrimThreads) {
+        fv0 += __ldcg(a.ad.part + 3 * k + 0);
+        fv1 += __ldcg(a.ad.part + 3 * k + 1);
+        fv2 += __ldcg(a.ad.part + 3 * k + 2);
+      }
+    }
     if (live) {
-      const double gr = a.ad.grads[pidx];
       a.ad.grads[pidx] = 0.0;  // ready for the next backward
       pc = adam_scalar(a.ad, pidx, c, live_p, pc, gr, m0, v0, lr, bc1, bc2);
       a.params[pidx] = pc;
     }
     tl_mark(a.tl, 4, 1);
-    if (a.ad.part) {
-      // first level of the fixed-order loss fold: this block's chunk of partials
-      __shared__ double fr[kPrimThreads / 32][3];
-      const int chunk = (a.ad.n_part + gridDim.x - 1) / gridDim.x;
-      const int beg = blockIdx.x * chunk, end = min(beg + chunk, a.ad.n_part);
-      double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-      for (int k = beg + threadIdx.x; k < end; k += kPrimThreads) {
-        v0 += __ldcg(a.ad.part + 3 * k + 0);
-        v1 += __ldcg(a.ad.part + 3 * k + 1);
-        v2 += __ldcg(a.ad.part + 3 * k + 2);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        v0 += __shfl_xor_sync(kFull, v0, o);
-        v1 += __shfl_xor_sync(kFull, v1, o);
-        v2 += __shfl_xor_sync(kFull, v2, o);
-      }
-      if (lane == 0) {
-        fr[threadIdx.x >> 5][0] = v0;
-        fr[threadIdx.x >> 5][1] = v1;
-        fr[threadIdx.x >> 5][2] = v2;
-      }
-      __syncthreads();
-      if (threadIdx.x < 3) {
-        double t = 0.0;
-        for (int w = 0; w < kPrimThreads / 32; ++w) t += fr[w][threadIdx.x];
-        a.s.fold[blockIdx.x * 3 + threadIdx.x] = t;
-      }
-    }
   }
   if (!ADAM) {
     pdl_wait();  // (records / rects may still be read by a predecessor)
@@ -310,60 +289,36 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
   }
 
   if (ADAM) {
-    // the last block to finish advances the iteration counter (all blocks have read it)
-    __shared__ bool am_last;
+    // this block's loss sums of the step (fixed-order fold of its chunk of
+    // k_step's partials, or the allreduced sums from block 0) go to the history
+    // buffer; the host folds the blocks in order (deterministic).  Block 0 marks
+    // the iteration done: K2 of the next step advances the counter.
+    __shared__ double fr[kPrimThreads / 32][3];
     tl_mark(a.tl, 6, 1);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      am_last = atomicAdd(a.s.done, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    tl_mark(a.tl, 7, 1);
-    if (am_last && threadIdx.x < 32) {
-      __threadfence();
-      const AdamPart& d = a.ad;
-      bool have = d.sums != nullptr;
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-      if (d.part) {
-        // second level: the per-block folds, lane-strided then a fixed xor tree
-        for (int b = lane; b < (int)gridDim.x; b += 32) {
-          s0 += __ldcg(a.s.fold + 3 * b + 0);
-          s1 += __ldcg(a.s.fold + 3 * b + 1);
-          s2 += __ldcg(a.s.fold + 3 * b + 2);
-        }
+    if (a.ad.part) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          s0 += __shfl_xor_sync(kFull, s0, o);
-          s1 += __shfl_xor_sync(kFull, s1, o);
-          s2 += __shfl_xor_sync(kFull, s2, o);
-        }
-        if (d.sums && lane == 0) {
-          d.sums[0] = s0;
-          d.sums[1] = s1;
-          d.sums[2] = s2;
-        }
-        have = true;
-      } else if (have) {
-        s0 = __ldcg(d.sums + 0);
-        s1 = __ldcg(d.sums + 1);
-        s2 = __ldcg(d.sums + 2);
+      for (int o = 16; o > 0; o >>= 1) {
+        fv0 += __shfl_xor_sync(kFull, fv0, o);
+        fv1 += __shfl_xor_sync(kFull, fv1, o);
+        fv2 += __shfl_xor_sync(kFull, fv2, o);
       }
       if (lane == 0) {
-        if (have) {
-          // history entry of this iteration: the render before this update (fit.py:502-505)
-          const double mse = s0 * d.inv_3P;
-          double loss = mse;
-          if (d.loss_kind == PF_LOSS_SPATIAL) loss = s1 * d.inv_3P + d.alpha_w * (s2 * d.inv_P);
-          if (d.hist_loss) d.hist_loss[it] = loss;
-          if (d.hist_psnr)
-            d.hist_psnr[it] = mse == 0.0 ? __longlong_as_double(0x7ff0000000000000ll)
-                                         : 10.0 * log10(1.0 / mse);
-        }
-        *a.ad.iter = it + 1;
-        *a.s.done = 0u;
+        fr[threadIdx.x >> 5][0] = fv0;
+        fr[threadIdx.x >> 5][1] = fv1;
+        fr[threadIdx.x >> 5][2] = fv2;
       }
+      __syncthreads();
     }
+    if (threadIdx.x < 3 && a.ad.hist_part) {
+      double tsum = 0.0;
+      if (a.ad.part) {
+        for (int w = 0; w < kPrimThreads / 32; ++w) tsum += fr[w][threadIdx.x];
+      } else if (a.ad.sums && blockIdx.x == 0) {
+        tsum = a.ad.sums[threadIdx.x];
+      }
+      a.ad.hist_part[((size_t)it * gridDim.x + blockIdx.x) * 3 + threadIdx.x] = tsum;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.s.done[2] = 1u;
   }
   tl_mark(a.tl, ADAM ? 2 : 3, 3);
 }
@@ -403,6 +358,11 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
   pdl_wait();     // rects come from K1
   tl_mark(a.tl, 0, 1);
   pdl_trigger();  // after the wait: a dependent that starts early sees K1 complete
+  if (r == 0 && cb == 0 && tid == 0 && a.s.done[2]) {
+    // the Adam step before this binning is complete: advance the iteration counter
+    a.s.done[1] += 1u;
+    a.s.done[2] = 0u;
+  }
 
   // (a) stable compaction of the primitives covering row ty, z order kept
   const int chunk = (a.n + kRowThreads - 1) / kRowThreads;
@@ -718,22 +678,24 @@ extern "C" int pf_preprocess(const double* params, int n, double alpha_max, doub
   return launch_prim(false, a, (cudaStream_t)stream);
 }
 
+extern "C" int pf_adam_blocks(int n) { return div_up(n > 0 ? n * 8 : 1, kPrimThreads); }
+
 extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, double* v,
                                   const uint8_t* frozen, const double* gains8,
                                   const double* lr_table, const double* bc1_table,
-                                  const double* bc2_table, int32_t* iter, int clamp, double s_min,
-                                  double s_max, double* sums, const double* part, int n_part,
-                                  int loss_kind, double alpha_w, double inv_3P, double inv_P,
-                                  double* hist_loss, double* hist_psnr, int n, double alpha_max,
-                                  double mu_blend, double padding, int W, int H, int tile,
-                                  int ty_begin, int ty_end, int capacity, void* rec, void* scratch,
+                                  const double* bc2_table, int clamp, double s_min, double s_max,
+                                  const double* sums, const double* part, int n_part,
+                                  double* hist_part, int n, double alpha_max, double mu_blend,
+                                  double padding, int W, int H, int tile, int ty_begin,
+                                  int ty_end, int capacity, void* rec, void* scratch,
                                   size_t scratch_bytes, void* stream) {
   PreArgs a;
   const int rc = fill_pre_args(a, params, n, alpha_max, mu_blend, padding, W, H, tile, ty_begin,
                                ty_end, capacity, rec, scratch, scratch_bytes);
   if (rc != PF_OK) return rc;
-  if (!iter || !lr_table || !bc1_table || !bc2_table || (n > 0 && (!grads || !m || !v)))
+  if (!lr_table || !bc1_table || !bc2_table || (n > 0 && (!grads || !m || !v)))
     return PF_ERR_ARG;
+  if (part && n_part < 0) return PF_ERR_ARG;
   AdamPart& d = a.ad;
   d.grads = grads;
   d.m = m;
@@ -743,20 +705,13 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
   d.lr_table = lr_table;
   d.bc1_table = bc1_table;
   d.bc2_table = bc2_table;
-  d.iter = iter;
   d.clamp = clamp;
   d.s_min = s_min;
   d.s_max = s_max;
-  if (part && n_part < 0) return PF_ERR_ARG;
   d.sums = sums;
   d.part = part;
   d.n_part = part ? n_part : 0;
-  d.loss_kind = loss_kind;
-  d.alpha_w = alpha_w;
-  d.inv_3P = inv_3P;
-  d.inv_P = inv_P;
-  d.hist_loss = hist_loss;
-  d.hist_psnr = hist_psnr;
+  d.hist_part = hist_part;
   return launch_prim(true, a, (cudaStream_t)stream);
 }
 

@@ -288,10 +288,6 @@ class StepEngine:
         self.lr_table = torch.tensor(self.lr_host, dtype=torch.float64, device=dev)
         self.bc1_table = torch.tensor(bc1, dtype=torch.float64, device=dev)
         self.bc2_table = torch.tensor(bc2, dtype=torch.float64, device=dev)
-        self.iter = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.adam_counter = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.hist_loss = torch.zeros(max(self.total, 1), dtype=torch.float64, device=dev)
-        self.hist_psnr = torch.zeros(max(self.total, 1), dtype=torch.float64, device=dev)
         self.gbuf = torch.zeros(n * 8 + 4, dtype=torch.float64, device=dev)
         self.grads = self.gbuf[: n * 8]
         self.sums = self.gbuf[n * 8 :]
@@ -319,6 +315,10 @@ class StepEngine:
             self.comp.enable_step_schedule()
         else:
             self.comp.alloc_render(save=True, loss=True)
+        # per-iteration loss sums per Adam block (history; folded in order on the host)
+        self.adam_blocks = self.comp.adam_blocks
+        self.hist_part = torch.zeros(max(self.total, 1) * self.adam_blocks * 3, dtype=torch.float64,
+                                     device=dev)
         self.allreduce = allreduce
         self.use_graph = use_graph
         self.graph: torch.cuda.CUDAGraph | None = None
@@ -354,11 +354,9 @@ class StepEngine:
             mark("allreduce")
         c.adam_preprocess(self.params, self.grads, self.m, self.v, frozen=self.frozen,
                           gains=self.gains, lr_table=self.lr_table, bc1_table=self.bc1_table,
-                          bc2_table=self.bc2_table, iter_counter=self.iter,
-                          s_min=self.cfg.scale_min, s_max=self.cfg.scale_max, sums=self.sums,
-                          loss_kind=self.loss_kind, alpha_w=self.alpha_w, P_total=self.P,
-                          hist_loss=self.hist_loss, hist_psnr=self.hist_psnr,
-                          part=c.part if fold_in_adam else None)
+                          bc2_table=self.bc2_table, s_min=self.cfg.scale_min,
+                          s_max=self.cfg.scale_max, sums=None if fold_in_adam else self.sums,
+                          part=c.part if fold_in_adam else None, hist_part=self.hist_part)
         mark("adam_preprocess")
 
     def refresh(self) -> None:
@@ -414,10 +412,30 @@ class StepEngine:
         self.frozen.copy_(torch.from_numpy(np.asarray(state.frozen, dtype=bool).astype(np.uint8)))
         self.refresh()
 
+    def loss_psnr(self, sums: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+        """History values from per-iteration loss sums [k][3] (fit.py:112-151, 241-247)."""
+        inv_3P, inv_P = 1.0 / (3.0 * self.P), 1.0 / self.P
+        mse = sums[:, 0] * inv_3P
+        if self.loss_kind == nat.PF_LOSS_SPATIAL:
+            loss = sums[:, 1] * inv_3P + self.alpha_w * (sums[:, 2] * inv_P)
+        else:
+            loss = mse
+        with np.errstate(divide="ignore"):
+            ps = np.where(mse == 0.0, np.inf, 10.0 * np.log10(1.0 / np.where(mse == 0.0, 1.0, mse)))
+        return loss, ps
+
+    def iteration_sums(self, part: np.ndarray) -> np.ndarray:
+        """Fixed-order fold of hist_part blocks: [k][blocks][3] -> [k][3]."""
+        part = part.reshape(-1, self.adam_blocks, 3)
+        out = np.zeros((part.shape[0], 3), dtype=np.float64)
+        for b in range(self.adam_blocks):
+            out += part[:, b, :]
+        return out
+
     def history(self, compute_psnr: bool = True) -> list[HistoryEntry]:
         k = self.done
-        loss = self.hist_loss[:k].cpu().numpy()
-        ps = self.hist_psnr[:k].cpu().numpy()
+        part = self.hist_part[: k * self.adam_blocks * 3].cpu().numpy()
+        loss, ps = self.loss_psnr(self.iteration_sums(part))
         return [HistoryEntry(i, float(loss[i]), float(ps[i]) if compute_psnr else math.nan,
                              self.lr_host[i], 0) for i in range(k)]
 
