@@ -193,21 +193,19 @@ def _config(name: str, w) -> dict:
             "l2": "flushed (256 MiB write) before every timed step"}
 
 
-def graph_kernel_count(graph) -> int | None:
-    try:
-        from cuda.bindings import runtime as rt
-
-        g = graph.raw_cuda_graph()
-        err, nodes, num = rt.cudaGraphGetNodes(g, 0)
-        err, nodes, num = rt.cudaGraphGetNodes(g, num)
-        kinds = 0
-        for nd in nodes:
-            e, t = rt.cudaGraphNodeGetType(nd)
-            if t == rt.cudaGraphNodeType.cudaGraphNodeTypeKernel:
-                kinds += 1
-        return kinds
-    except Exception:
-        return None
+def ncu_traffic(kernel_prefix: str) -> float | None:
+    """dram bytes (read + write) per launch of the named kernel from the committed
+    ncu --set full summary under profiles/ (newest file), or None."""
+    files = sorted((ROOT / "profiles").glob("*ncu_kernels*.json"))
+    for f in reversed(files):
+        try:
+            d = json.loads(f.read_text())
+        except (OSError, ValueError):
+            continue
+        for name, v in d.items():
+            if kernel_prefix in name and "dram_traffic_bytes" in v:
+                return float(v["dram_traffic_bytes"])
+    return None
 
 
 def run_ours(args) -> None:
@@ -316,7 +314,7 @@ def run_ours(args) -> None:
     e2e_ms = float(t.item())
     eng.check()
 
-    nodes = graph_kernel_count(eng.graph) if eng.graph is not None else None
+    nodes = eng.kernels_per_step
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -335,7 +333,9 @@ def run_ours(args) -> None:
                    "K16": K16, "band": [band.ty_begin, band.ty_end]},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved,
                      "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                     "frac": achieved / peaks["hbm_gbs"],
+                     "traffic": ncu_traffic({"step": "k_step", "forward": "k_forward",
+                                             "backward": "k_backward"}[dom]),
                      "peak_src": peaks["src"], "algorithmic_bytes": ab[dom],
                      "kernel_ms": stage_ms[dom],
                      "step_frac": ab["total"] * value / 1e9 / peaks["hbm_gbs"]},

@@ -163,6 +163,7 @@ class Compositor:
         self.tile_classes = None
         self.status = torch.zeros(4, dtype=torch.int32, device=dev)
         self._saved_alloc = False
+        self.launches = 0  # kernels launched through this object (one per stage call)
 
     def enable_step_schedule(self) -> None:
         """Have pf_bin emit tile cost classes for pf_fit_step's longest-first
@@ -206,6 +207,7 @@ class Compositor:
                 self.rec.data_ptr(), self.scratch.data_ptr(), self.scratch_bytes,
                 _stream_handle(stream)),
             "pf_preprocess")
+        self.launches += 1
 
     def adam_preprocess(self, params, grads, m, v, *, frozen, gains, lr_table, bc1_table,
                         bc2_table, s_min, s_max, sums=None, part=None, hist_part=None,
@@ -224,6 +226,7 @@ class Compositor:
                 self.band.ty_begin, self.band.ty_end, self.capacity, self.rec.data_ptr(),
                 self.scratch.data_ptr(), self.scratch_bytes, _stream_handle(stream)),
             "pf_adam_preprocess")
+        self.launches += 1
 
     @property
     def adam_blocks(self) -> int:
@@ -238,6 +241,7 @@ class Compositor:
                             self.bin_idx.data_ptr(), self.status.data_ptr(),
                             nat.ptr(self.tile_classes), _stream_handle(stream)),
             "pf_bin")
+        self.launches += 1
 
     def check_overflow(self) -> int:
         """Synchronising read of K; raises BinOverflow when capacity was exceeded."""
@@ -268,6 +272,7 @@ class Compositor:
                 1.0 / (3.0 * P), 1.0 / P, p(self.d4) if lossy else None,
                 p(self.part) if lossy else None, _stream_handle(stream)),
             "pf_forward")
+        self.launches += 1
 
     # -- K34 (fit step: forward + loss + backward in one kernel)
     def fit_step(self, grads: torch.Tensor, sums: torch.Tensor | None, *, eps_skip: float,
@@ -303,6 +308,7 @@ class Compositor:
                 grads.data_ptr(), self.step_ctr.data_ptr(), nat.ptr(self.tile_classes),
                 _stream_handle(stream)),
             "pf_fit_step")
+        self.launches += 1
         if sums is not None:
             self.fold_loss(sums, stream)
 
@@ -314,6 +320,7 @@ class Compositor:
     def fold_loss(self, sums: torch.Tensor, stream=None) -> None:
         nat.check(self.lib.pf_fold_loss(self.part.data_ptr(), self.n_part, sums.data_ptr(),
                                         _stream_handle(stream)), "pf_fold_loss")
+        self.launches += 1
 
     # -- K4
     def backward(self, d4: torch.Tensor, grads: torch.Tensor, *, bg_rgb=(1.0, 1.0, 1.0),
@@ -333,6 +340,7 @@ class Compositor:
                 grads.data_ptr(), p(self.part) if sums is not None else None, p(sums),
                 _stream_handle(stream)),
             "pf_backward")
+        self.launches += 1
 
 
 def pixels4(rgb: np.ndarray, w: np.ndarray | float | None = None) -> np.ndarray:

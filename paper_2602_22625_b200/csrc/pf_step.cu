@@ -245,7 +245,11 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
   const double* plane_a = a.tex + 3 * (size_t)a.texels;
 
   // ---- forward (k_forward semantics, _kernels.py:183-255)
-  double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0;
+  // compositing state in fp32: ~1e-7 relative on the image against the 1e-5 bar
+  // (every decision was taken in float64 above it)
+  // alpha = 1 - T is accumulated as sum T*a (all terms positive: relative
+  // accuracy also where T is close to 1)
+  float T = 1.0f, Aacc = 0.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
   int ns = 0;
   for (int sub = 0; sub < L; sub += 32) {
     const int jl = sub + lane;
@@ -292,7 +296,8 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
       // dm/dU, dm/dV (_kernels.py:61-73) -- alpha channel only (Appendix A.3)
       const double gU = fma(wv, (t11 - t10) - (t01 - t00), t01 - t00);
       const double gV = fma(wu, (t11 - t01) - (t10 - t00), t10 - t00);
-      const float4 ea = make_float4(__int_as_float(j), (float)T, (float)m, (float)gU);
+      const float mf = (float)m;
+      const float4 ea = make_float4(__int_as_float(j), T, mf, (float)gU);
       const float eb = (float)gV;
       if (ns < kKS) {
         stA[ns * kTilePix + ct] = ea;
@@ -303,12 +308,13 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
         sp[1] = make_float4(eb, 0.f, 0.f, 0.f);
       }
       ++ns;
-      const double aa = r.sa * m;
-      const double Ta = T * aa;
-      C0 += Ta * r.c0;
-      C1 += Ta * r.c1;
-      C2 += Ta * r.c2;
-      T *= 1.0 - aa;
+      const float aa = r.saf * mf;
+      const float Ta = T * aa;
+      C0 += Ta * r.c0f;
+      C1 += Ta * r.c1f;
+      C2 += Ta * r.c2f;
+      Aacc += Ta;
+      T *= 1.0f - aa;
     }
   }
 
@@ -321,10 +327,10 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
   float dI0 = 0.f, dI1 = 0.f, dI2 = 0.f, dA = 0.f;
   float l0 = 0.f, l1 = 0.f, l2 = 0.f;
   if (valid) {
-    const double I0 = C0 + T * (a.bg4 ? (double)bgp.x : a.bg0);
-    const double I1 = C1 + T * (a.bg4 ? (double)bgp.y : a.bg1);
-    const double I2 = C2 + T * (a.bg4 ? (double)bgp.z : a.bg2);
-    const double Ia = 1.0 - T;
+    const double I0 = (double)C0 + (double)T * (a.bg4 ? (double)bgp.x : a.bg0);
+    const double I1 = (double)C1 + (double)T * (a.bg4 ? (double)bgp.y : a.bg1);
+    const double I2 = (double)C2 + (double)T * (a.bg4 ? (double)bgp.z : a.bg2);
+    const double Ia = (double)Aacc;
     if (a.img4) a.img4[pix] = make_float4((float)I0, (float)I1, (float)I2, (float)Ia);
     const double r0 = I0 - (double)tg.x, r1 = I1 - (double)tg.y, r2 = I2 - (double)tg.z;
     const double sse = r0 * r0 + r1 * r1 + r2 * r2;

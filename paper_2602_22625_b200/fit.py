@@ -324,6 +324,7 @@ class StepEngine:
         self.graph: torch.cuda.CUDAGraph | None = None
         self.eps_skip = float(cfg.eps_skip)
         self.done = 0
+        self.kernels_per_step: int | None = None
 
     # one full optimisation step, stream-ordered, no host sync:
     #   [K2 bin] -> [K3 forward + loss] -> [K4 backward]
@@ -365,8 +366,10 @@ class StepEngine:
 
     def capture(self) -> None:
         g = torch.cuda.CUDAGraph()
+        before = self.comp.launches
         with torch.cuda.graph(g):
             self.launch_step()
+        self.kernels_per_step = self.comp.launches - before  # this package's kernels only
         self.graph = g
 
     def step(self, rng: np.random.Generator | None = None) -> None:
