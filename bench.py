@@ -284,29 +284,28 @@ def run_ours(args) -> None:
         for (_, e0), (name, e1) in zip(marks, marks[1:]):
             stage_ms[name] = stage_ms.get(name, 0.0) + e0.elapsed_time(e1) / prof_steps
 
-    # end-to-end through the public step API with HOST buffers each step:
-    # H2D of the packed parameter vector (pinned), graph replay, D2H of the
-    # updated vector + the step's loss.
+    # end-to-end through the public step API with HOST buffers each step: one
+    # graph per step = H2D of the packed parameter vector (pinned), preprocess,
+    # bin, fit step, Adam, D2H of the updated vector + the step's loss sums, then
+    # a host synchronisation (the host holds the step's result before the next).
     n = eng.n
     h_params = torch.empty(n * 8, dtype=torch.float64, pin_memory=True)
     h_params.copy_(eng.params.view(-1).cpu())
     nb = eng.adam_blocks
     h_loss = torch.empty(nb * 3, dtype=torch.float64, pin_memory=True)
+    eng.capture_host_step(h_params, h_loss)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_start.record()
     for _ in range(e2e_steps):
-        it = eng.done
-        eng.params.view(-1).copy_(h_params, non_blocking=True)
-        eng.refresh()  # the step consumes the uploaded parameters
-        eng.step()
-        h_params.copy_(eng.params.view(-1), non_blocking=True)
-        h_loss.copy_(eng.hist_part[it * nb * 3 : (it + 1) * nb * 3], non_blocking=True)
+        eng.host_step()
         torch.cuda.current_stream().synchronize()
+        loss_host = float(h_loss.numpy()[0::3].sum())  # the step's loss sum, on the host
     e_end.record()
     torch.cuda.synchronize()
+    assert np.isfinite(loss_host)
     e2e_ms = e_start.elapsed_time(e_end) / e2e_steps
     t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
     if world > 1:

@@ -134,13 +134,15 @@ int pf_preprocess(const double* params, int n, double alpha_max, double mu_blend
  *              per launch block (fixed-order fold of `part`, or `sums` in block
  *              0 and zeros elsewhere); summing the blocks in order gives the
  *              HistoryEntry loss of the iteration (fit.py:502-505), or NULL
+ *   last_part  [pf_adam_blocks(n)][3]: the same sums of the latest step only (a
+ *              fixed address a per-step host read can use), or NULL
  */
 int pf_adam_blocks(int n);
 int pf_adam_preprocess(double* params, double* grads, double* m, double* v, const uint8_t* frozen,
                        const double* gains8, const double* lr_table, const double* bc1_table,
                        const double* bc2_table, int clamp, double s_min, double s_max,
                        const double* sums, const double* part, int n_part, double* hist_part,
-                       int n, double alpha_max, double mu_blend, double padding, int W, int H,
+                       double* last_part, int n, double alpha_max, double mu_blend, double padding, int W, int H,
                        int tile, int ty_begin, int ty_end, int capacity, void* rec, void* scratch,
                        size_t scratch_bytes, void* stream);
 

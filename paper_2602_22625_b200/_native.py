@@ -43,8 +43,8 @@ SIGNATURES: dict[str, tuple] = {
     "pf_adam_blocks": (_I, [_I]),
     "pf_adam_preprocess": (
         _I,
-        [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _D, _D, _P, _P, _I, _P, _I, _D, _D, _D, _I, _I,
-         _I, _I, _I, _I, _P, _P, _Z, _P],
+        [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _D, _D, _P, _P, _I, _P, _P, _I, _D, _D, _D, _I,
+         _I, _I, _I, _I, _I, _P, _P, _Z, _P],
     ),
     "pf_atlas_quad": (_I, [_P, _I, _P, _P, _P, _I, _P, _P]),
     "pf_atlas_pad": (_I, [_P, _I, _P, _P, _P, _P, _I, _I, _P, _P]),

@@ -211,7 +211,7 @@ class Compositor:
 
     def adam_preprocess(self, params, grads, m, v, *, frozen, gains, lr_table, bc1_table,
                         bc2_table, s_min, s_max, sums=None, part=None, hist_part=None,
-                        stream=None) -> None:
+                        last_part=None, stream=None) -> None:
         """K5+K1 fused: Adam on every parameter, then the next step's records + rects.
         ``part``: pf_fit_step's loss partials (folded per block into ``hist_part``);
         ``sums``: already reduced loss sums (multi-rank path)."""
@@ -221,7 +221,8 @@ class Compositor:
                 params.data_ptr(), grads.data_ptr(), m.data_ptr(), v.data_ptr(), nat.ptr(frozen),
                 C.addressof(g8), lr_table.data_ptr(), bc1_table.data_ptr(), bc2_table.data_ptr(),
                 1, float(s_min), float(s_max), nat.ptr(sums), nat.ptr(part),
-                self.n_part if part is not None else 0, nat.ptr(hist_part), self.n,
+                self.n_part if part is not None else 0, nat.ptr(hist_part), nat.ptr(last_part),
+                self.n,
                 self.alpha_max, self.mu_blend, self.padding, self.W, self.H, self.tile,
                 self.band.ty_begin, self.band.ty_end, self.capacity, self.rec.data_ptr(),
                 self.scratch.data_ptr(), self.scratch_bytes, _stream_handle(stream)),

@@ -46,6 +46,7 @@ struct AdamPart {
   const double* part;    // per-warp loss partials of pf_fit_step to fold here, or NULL
   int n_part;
   double* hist_part;     // [iterations][gridDim.x][3] per-block loss sums (history)
+  double* last_part;     // [gridDim.x][3] the same for the latest step only, or NULL
 };
 
 struct PreArgs {
@@ -317,6 +318,7 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
         tsum = a.ad.sums[threadIdx.x];
       }
       a.ad.hist_part[((size_t)it * gridDim.x + blockIdx.x) * 3 + threadIdx.x] = tsum;
+      if (a.ad.last_part) a.ad.last_part[blockIdx.x * 3 + threadIdx.x] = tsum;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) a.s.done[2] = 1u;
   }
@@ -685,7 +687,8 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
                                   const double* lr_table, const double* bc1_table,
                                   const double* bc2_table, int clamp, double s_min, double s_max,
                                   const double* sums, const double* part, int n_part,
-                                  double* hist_part, int n, double alpha_max, double mu_blend,
+                                  double* hist_part, double* last_part, int n, double alpha_max,
+                                  double mu_blend,
                                   double padding, int W, int H, int tile, int ty_begin,
                                   int ty_end, int capacity, void* rec, void* scratch,
                                   size_t scratch_bytes, void* stream) {
@@ -712,6 +715,7 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
   d.part = part;
   d.n_part = part ? n_part : 0;
   d.hist_part = hist_part;
+  d.last_part = last_part;
   return launch_prim(true, a, (cudaStream_t)stream);
 }
 

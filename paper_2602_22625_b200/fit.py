@@ -319,6 +319,7 @@ class StepEngine:
         self.adam_blocks = self.comp.adam_blocks
         self.hist_part = torch.zeros(max(self.total, 1) * self.adam_blocks * 3, dtype=torch.float64,
                                      device=dev)
+        self.last_part = torch.zeros(self.adam_blocks * 3, dtype=torch.float64, device=dev)
         self.allreduce = allreduce
         self.use_graph = use_graph
         self.graph: torch.cuda.CUDAGraph | None = None
@@ -357,7 +358,8 @@ class StepEngine:
                           gains=self.gains, lr_table=self.lr_table, bc1_table=self.bc1_table,
                           bc2_table=self.bc2_table, s_min=self.cfg.scale_min,
                           s_max=self.cfg.scale_max, sums=None if fold_in_adam else self.sums,
-                          part=c.part if fold_in_adam else None, hist_part=self.hist_part)
+                          part=c.part if fold_in_adam else None, hist_part=self.hist_part,
+                          last_part=self.last_part)
         mark("adam_preprocess")
 
     def refresh(self) -> None:
@@ -371,6 +373,28 @@ class StepEngine:
             self.launch_step()
         self.kernels_per_step = self.comp.launches - before  # this package's kernels only
         self.graph = g
+
+    def capture_host_step(self, h_params: torch.Tensor, h_loss: torch.Tensor) -> None:
+        """One CUDA graph for a step driven through HOST buffers: H2D of the packed
+        parameter vector (pinned ``h_params``), preprocess, bin, fit step, Adam,
+        D2H of the updated vector and of the step's loss sums (``h_loss``, pinned,
+        adam_blocks * 3 doubles).  Replay with host_step()."""
+        if self.graph is None and self.done == 0:
+            raise RuntimeError("run one step() first (eager warm-up + capture)")
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.params.view(-1).copy_(h_params, non_blocking=True)
+            self.refresh()
+            self.launch_step()
+            h_params.copy_(self.params.view(-1), non_blocking=True)
+            h_loss.copy_(self.last_part, non_blocking=True)
+        self.host_graph = g
+
+    def host_step(self) -> None:
+        if self.done >= self.total:
+            raise ValueError(f"iteration {self.done} outside [0, {self.total})")
+        self.host_graph.replay()
+        self.done += 1
 
     def step(self, rng: np.random.Generator | None = None) -> None:
         if self.done >= self.total:
