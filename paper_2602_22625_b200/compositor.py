@@ -169,8 +169,9 @@ class Compositor:
         """Have pf_bin emit tile cost classes for pf_fit_step's longest-first
         schedule (call before the first bin() of a fused fit loop)."""
         if self.tile_classes is None:
-            self.tile_classes = torch.zeros(16 * (1 + max(self.n_tiles, 1)), dtype=torch.int32,
-                                            device=self.device)
+            # counts, per-class tile lists, measured tile costs
+            self.tile_classes = torch.zeros(16 * (1 + max(self.n_tiles, 1)) + max(self.n_tiles, 1),
+                                            dtype=torch.int32, device=self.device)
 
     # -- buffers for rendering (allocated lazily; binning-only users skip them)
     def alloc_render(self, save: bool, loss: bool = False):

@@ -366,6 +366,13 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
     a.s.done[2] = 0u;
   }
 
+  // measured cost of this thread's column tile (first column of its chunk; read
+  // early so the load overlaps the scan)
+  const int cchunk = (a.ntx + kRowThreads - 1) / kRowThreads;
+  const int c0 = min(a.ntx, tid * cchunk), c1 = min(a.ntx, c0 + cchunk);
+  int32_t* cost_row = a.classes ? a.classes + kTileClasses * (1 + a.n_tiles) + r * a.ntx : nullptr;
+  const int cost0 = (cost_row && c0 < c1 && c0 >= cbeg && c0 < cend) ? cost_row[c0] : 0;
+
   // (a) stable compaction of the primitives covering row ty, z order kept
   const int chunk = (a.n + kRowThreads - 1) / kRowThreads;
   const int j0 = min(a.n, tid * chunk), j1 = min(a.n, j0 + chunk);
@@ -452,8 +459,6 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
     for (int tx = pk & 0xffff; tx <= (pk >> 16); ++tx) atomicAdd(col + tx, 1);
   }
   __syncthreads();
-  const int cchunk = (a.ntx + kRowThreads - 1) / kRowThreads;
-  const int c0 = min(a.ntx, tid * cchunk), c1 = min(a.ntx, c0 + cchunk);
   int local = 0;
   for (int c = c0; c < c1; ++c) local += col[c];
   int row_total;
@@ -464,8 +469,11 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
     if (c >= cbeg && c < cend) {
       a.bin_off[r * a.ntx + c] = run;
       if (a.classes) {
-        // longest-first schedule for pf_fit_step: tile -> class list of its length
-        const int cl = tile_class(v);
+        // longest-first schedule for pf_fit_step: tile -> class list of its cost
+        // (measured by the previous fit step; its list length before that)
+        const int w = c == c0 ? cost0 : cost_row[c];
+        cost_row[c] = 0;
+        const int cl = tile_class(w > 0 ? w : v);
         const int rank = atomicAdd(&s_ccnt[cl], 1);
         ccls[c] = cl | (rank << 8);
       }

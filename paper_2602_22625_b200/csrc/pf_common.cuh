@@ -86,9 +86,12 @@ struct __align__(16) RecS {
 };
 static_assert(sizeof(RecS) == 208, "RecS must be 208 bytes");
 
-// Tile cost classes for pf_fit_step's longest-first schedule: class of a tile
-// = min(kTileClasses - 1, list length / 4).  pf_bin's optional tile_classes
-// buffer: int32 [kTileClasses] counts, then [kTileClasses][n_tiles] tile lists.
+// Tile cost classes for pf_fit_step's longest-first schedule.  pf_bin's
+// optional tile_classes buffer: int32 [kTileClasses] counts, then
+// [kTileClasses][n_tiles] tile lists, then [n_tiles] tile costs measured by the
+// previous pf_fit_step (its rects' candidate + backward-step counts, max over
+// the tile; 0 = unknown).  Class = cost / 4, or list length / 4 when the cost is
+// unknown, capped at kTileClasses - 1.
 constexpr int kTileClasses = 16;
 __host__ __device__ inline int tile_class(int L) { return L / 4 < kTileClasses - 1 ? L / 4 : kTileClasses - 1; }
 

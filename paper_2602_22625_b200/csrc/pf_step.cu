@@ -81,6 +81,7 @@ struct StepArgs {
   int sched_lazy;        // 1: fetch the next ticket only once a ring slot is free
   const int32_t* classes;  // pf_bin's tile classes (counts + lists) or NULL: tile = ticket
   int32_t* classes_rw;
+  int32_t* tile_cost;      // [n_tiles] measured work of each tile (next step's classes)
   unsigned long long* prof;  // diagnostics (PF_STEP_PROF=1): [warp slot][6], else NULL
   unsigned long long* tl;    // diagnostics timeline or NULL
 };
@@ -251,10 +252,12 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
   // accuracy also where T is close to 1)
   float T = 1.0f, Aacc = 0.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
   int ns = 0;
+  int work = 2;  // this rect's work units (candidates + 2 x backward steps): tile cost
   for (int sub = 0; sub < L; sub += 32) {
     const int jl = sub + lane;
     const bool cand = jl < L && cull_touch(R.cull(jl), cx, cy);
     unsigned mask = __ballot_sync(kFull, cand);
+    work += __popc(mask);
     if (!valid) mask = 0u;  // divergent only in a partial last tile row / column
     while (mask) {
       const int bit = __ffs(mask) - 1;
@@ -388,6 +391,7 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
   while (true) {
     const unsigned jm = __reduce_max_sync(kFull, key);
     if (jm == 0u) break;
+    work += 2;
     const bool act = key == jm;
     const unsigned ball = __ballot_sync(kFull, act);
     const RecS& r = R.rec((int)jm - 1);
@@ -437,6 +441,8 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
       if ((lane & 3) == 0 && tot != 0.0f) atomicAdd(gp + (lane >> 2), (double)tot);
     }
   }
+  // the tile's cost for the next step's longest-first schedule: max over its rects
+  if (a.tile_cost && lane == 0) atomicMax(a.tile_cost + tile, work);
 }
 
 }  // namespace
@@ -782,6 +788,8 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   a.sched_lazy = getenv("PF_STEP_LAZY") ? 1 : 0;
   a.classes = getenv("PF_STEP_NOLPT") ? nullptr : tile_classes;
   a.classes_rw = const_cast<int32_t*>(a.classes);
+  a.tile_cost = tile_classes ? const_cast<int32_t*>(tile_classes) + kTileClasses * (1 + n_tiles)
+                             : nullptr;
   a.prof = nullptr;
   a.tl = pf_timeline_ptr();
   static unsigned long long* prof_buf = nullptr;
