@@ -156,12 +156,13 @@ int pf_adam_preprocess(double* params, double* grads, double* m, double* v, cons
  *   bin_idx  out [capacity]           (TileBins.indices; first K valid)
  *   status   out int32[4]: [0] = K (total entries), [1] = overflow flag (K > capacity;
  *            nothing else is written then)
- *   tile_classes  optional int32 [16 + 17 * n_band_tiles] (NULL to skip): the
+ *   tile_classes  optional int32 [16 + 65 * n_band_tiles] (NULL to skip): the
  *            band tiles grouped by cost class for pf_fit_step's longest-first
  *            schedule -- [0..16) counts (accumulated: zero before the first
- *            pf_bin; pf_fit_step re-zeroes them), one list of tile indices per
- *            class, then the per-tile costs pf_fit_step measured (consumed and
- *            cleared here; the list length stands in until a first fit step).
+ *            pf_bin; pf_fit_step re-zeroes them), one list of int4 tile entries
+ *            (tile, list offset, list length, tx | ty << 16) per class, then the
+ *            per-tile costs pf_fit_step measured (consumed and cleared here; the
+ *            list length stands in until a first fit step).
  *            Order inside a class is not deterministic; it only steers scheduling.
  */
 int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity,

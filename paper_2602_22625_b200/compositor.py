@@ -170,8 +170,9 @@ class Compositor:
         schedule (call before the first bin() of a fused fit loop)."""
         if self.tile_classes is None:
             # counts, per-class tile lists, measured tile costs
-            self.tile_classes = torch.zeros(16 * (1 + max(self.n_tiles, 1)) + max(self.n_tiles, 1),
-                                            dtype=torch.int32, device=self.device)
+            nt = max(self.n_tiles, 1)
+            self.tile_classes = torch.zeros(16 + 16 * 4 * nt + nt, dtype=torch.int32,
+                                            device=self.device)
 
     # -- buffers for rendering (allocated lazily; binning-only users skip them)
     def alloc_render(self, save: bool, loss: bool = False):

@@ -352,6 +352,7 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
   __shared__ int s_ccnt[kTileClasses], s_cbase[kTileClasses];
   int* col = reinterpret_cast<int*>(rsm + a.smem_list);
   int* ccls = col + a.ntx;  // per-column tile class | rank within the block << 8
+  int* ccnt = ccls + a.ntx;  // per-column tile list length
   const int r = blockIdx.x, ty = a.ty_begin + r;
   const int cb = blockIdx.y, ncb = gridDim.y;
   const int cbeg = (int)((long long)a.ntx * cb / ncb), cend = (int)((long long)a.ntx * (cb + 1) / ncb);
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
   // early so the load overlaps the scan)
   const int cchunk = (a.ntx + kRowThreads - 1) / kRowThreads;
   const int c0 = min(a.ntx, tid * cchunk), c1 = min(a.ntx, c0 + cchunk);
-  int32_t* cost_row = a.classes ? a.classes + kTileClasses * (1 + a.n_tiles) + r * a.ntx : nullptr;
+  int32_t* cost_row = a.classes ? a.classes + tile_cost_offset(a.n_tiles) + r * a.ntx : nullptr;
   const int cost0 = (cost_row && c0 < c1 && c0 >= cbeg && c0 < cend) ? cost_row[c0] : 0;
 
   // (a) stable compaction of the primitives covering row ty, z order kept
@@ -476,6 +477,7 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
         const int cl = tile_class(w > 0 ? w : v);
         const int rank = atomicAdd(&s_ccnt[cl], 1);
         ccls[c] = cl | (rank << 8);
+        ccnt[c] = v;
       }
     }
     run += v;
@@ -487,7 +489,9 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
     for (int c = max(c0, cbeg); c < min(c1, cend); ++c) {
       const int cl = ccls[c] & 0xff, rank = ccls[c] >> 8;
       const int p = s_cbase[cl] + rank;
-      if (p < a.n_tiles) a.classes[kTileClasses + cl * a.n_tiles + p] = r * a.ntx + c;
+      if (p < a.n_tiles)
+        reinterpret_cast<int4*>(a.classes + kTileClasses)[cl * a.n_tiles + p] =
+            make_int4(r * a.ntx + c, col[c], ccnt[c], c | ((a.ty_begin + r) << 16));
     }
   }
 
@@ -756,7 +760,7 @@ extern "C" int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, i
   ra.classes = tile_classes;
   ra.n_tiles = n_rows * ntx;
   ra.tl = pf_timeline_ptr();
-  const size_t smem = sizeof(int2) * kRowSmemList + 2 * sizeof(int) * (size_t)ntx;
+  const size_t smem = sizeof(int2) * kRowSmemList + 3 * sizeof(int) * (size_t)ntx;
   const bool cache = (n + kRowThreads - 1) / kRowThreads <= kRowCache;
   void (*kern)(RowArgs) = cache ? k_bin_rows<true> : k_bin_rows<false>;
   static size_t attr_smem[2] = {0, 0};

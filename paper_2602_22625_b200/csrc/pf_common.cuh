@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <utility>
 #include <cuda_runtime.h>
 
@@ -88,11 +89,15 @@ static_assert(sizeof(RecS) == 208, "RecS must be 208 bytes");
 
 // Tile cost classes for pf_fit_step's longest-first schedule.  pf_bin's
 // optional tile_classes buffer: int32 [kTileClasses] counts, then
-// [kTileClasses][n_tiles] tile lists, then [n_tiles] tile costs measured by the
-// previous pf_fit_step (its rects' candidate + backward-step counts, max over
-// the tile; 0 = unknown).  Class = cost / 4, or list length / 4 when the cost is
+// [kTileClasses][n_tiles] int4 tile entries (tile, list offset, list length,
+// tx | ty << 16), then [n_tiles] tile costs measured by the previous
+// pf_fit_step (its rects' candidate + backward-step counts, max over the tile;
+// 0 = unknown).  Class = cost / 4, or list length / 4 when the cost is
 // unknown, capped at kTileClasses - 1.
 constexpr int kTileClasses = 16;
+__host__ __device__ inline size_t tile_cost_offset(int n_tiles) {
+  return kTileClasses + 4 * (size_t)kTileClasses * n_tiles;
+}
 __host__ __device__ inline int tile_class(int L) { return L / 4 < kTileClasses - 1 ? L / 4 : kTileClasses - 1; }
 
 // Warp sub-tile shape (8 warps cover a 16x16 tile) -- used by the cull record.
@@ -294,8 +299,9 @@ inline cudaError_t launch_pdl2(void (*kern)(KArgs...), dim3 grid, int block, siz
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  static const bool no_pdl = getenv("PF_NO_PDL") != nullptr;  // A/B switch
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = no_pdl ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 template <typename... KArgs, typename... Args>

@@ -79,6 +79,7 @@ struct StepArgs {
   double* grads;
   unsigned* ctr;         // [2]: tile ticket, finished producers (self-resetting)
   int sched_lazy;        // 1: fetch the next ticket only once a ring slot is free
+  unsigned csleep, psleep;  // back-off (ns) of consumer / producer barrier waits
   const int32_t* classes;  // pf_bin's tile classes (counts + lists) or NULL: tile = ticket
   int32_t* classes_rw;
   int32_t* tile_cost;      // [n_tiles] measured work of each tile (next step's classes)
@@ -475,17 +476,27 @@ __global__ void __launch_bounds__(G * (kCW + 1) * 32, 1) k_step(StepArgs a) {
   Atl atl;
   if constexpr (ATL == 0) atl.p = reinterpret_cast<const uint32_t*>(a.apad);
   else atl.base = su32(satl);
-  if (ATL != 0) {
-    // staggered start: the CTAs do not all hit the same L2 lines at once
-    const int nq = ATL == 2 ? a.pad_texels >> 1 : a.pad_texels >> 2;
-    const float4* src = reinterpret_cast<const float4*>(ATL == 2 ? (const void*)a.apad64
-                                                                 : (const void*)a.apad);
-    float4* dst = reinterpret_cast<float4*>(satl);
-    const int rot = (int)((blockIdx.x * 37u) % (unsigned)max(nq, 1));
-    for (int k = t; k < nq; k += blockDim.x) {
-      int q = k + rot;
-      if (q >= nq) q -= nq;
-      dst[q] = __ldg(src + q);
+  // the atlas arrives asynchronously (TMA bulk copy, atl_bar); consumers wait for
+  // it before their first tile, so the copy overlaps the first tickets
+  __shared__ __align__(8) uint64_t atl_bar;
+  if (t == 0) {
+    mbar_init(&atl_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (ATL != 0) {
+      const uint32_t bytes = (uint32_t)a.pad_texels * (ATL == 2 ? 8u : 4u);
+      const char* src = reinterpret_cast<const char*>(ATL == 2 ? (const void*)a.apad64
+                                                               : (const void*)a.apad);
+      mbar_arrive_tx(&atl_bar, bytes);
+      // chunks of <= 32 KB, issued from a staggered start across CTAs
+      constexpr uint32_t kChunk = 32768;
+      const uint32_t nch = (bytes + kChunk - 1) / kChunk;
+      for (uint32_t k = 0; k < nch; ++k) {
+        const uint32_t q = (k + blockIdx.x) % nch;
+        const uint32_t off = q * kChunk, len = min(kChunk, bytes - off);
+        bulk_g2s(satl + off, src + off, len, &atl_bar);
+      }
+    } else {
+      mbar_arrive(&atl_bar);
     }
   }
   if (t < G * kNBuf) {
@@ -538,42 +549,54 @@ __global__ void __launch_bounds__(G * (kCW + 1) * 32, 1) k_step(StepArgs a) {
         if (lane >= o) cls_pre += y;
       }
     }
+    // tickets: the first one of each producer is static (blockIdx, group), later
+    // ones come from the global counter (offset by the static range)
+    int ticket_k = 0;
+    int tile = a.n_tiles, b0 = 0, L = 0, txy = 0, i0 = 0;
     auto next_tile = [&]() {
-      int t = 0;
-      if (lane == 0) t = (int)atomicAdd(a.ctr, 1u);
-      t = __shfl_sync(kFull, t, 0);
-      if (a.classes && t < a.n_tiles) {
+      int t = blockIdx.x * G + g;
+      if (ticket_k++ > 0) {
+        if (lane == 0) t = (int)atomicAdd(a.ctr, 1u) + (int)gridDim.x * G;
+        t = __shfl_sync(kFull, t, 0);
+      }
+      tile = a.n_tiles;
+      if (t >= a.n_tiles) return;
+      if (a.classes) {
         const unsigned below = __ballot_sync(kFull, lane < kTileClasses && cls_pre <= t);
         const int ci = __popc(below);  // rank of the class holding ticket t
         const int before = __shfl_sync(kFull, cls_pre, max(ci - 1, 0));
         const int idx = t - (ci > 0 ? before : 0);
         // (ci == kTileClasses: counts do not cover t -- never with pf_bin's lists)
-        t = ci < kTileClasses
-                ? __ldg(a.classes + kTileClasses + (kTileClasses - 1 - ci) * a.n_tiles + idx)
-                : a.n_tiles;
-      }
-      return t;
-    };
-    int tile = next_tile();
-    int b0 = 0, L = 0, i0 = 0;
-    auto load_list = [&]() {
-      if (tile < a.n_tiles) {
+        if (ci < kTileClasses) {
+          const int4 e = __ldg(reinterpret_cast<const int4*>(a.classes + kTileClasses) +
+                               (size_t)(kTileClasses - 1 - ci) * a.n_tiles + idx);
+          tile = e.x;
+          b0 = e.y;
+          L = e.z;
+          txy = e.w;
+        }
+      } else {
+        tile = t;
         b0 = __ldg(a.bin_off + tile);
         L = __ldg(a.bin_off + tile + 1) - b0;
-        i0 = lane < L ? __ldg(a.bin_idx + b0 + lane) : 0;
+        txy = (tile % a.ntx) | ((a.ty_begin + tile / a.ntx) << 16);
       }
     };
+    auto load_list = [&]() {
+      if (tile < a.n_tiles) i0 = lane < L ? __ldg(a.bin_idx + b0 + lane) : 0;
+    };
+    next_tile();
     load_list();
     int buf = 0;
     uint32_t eph = 0;  // parity of the empty barrier we wait on next, per slot (bit b)
     for (int k = 0;; ++k) {
       if (k >= kNBuf) {
         const unsigned long long c0 = a.prof ? clock64() : 0;
-        mbar_wait_sleep(&empty[g][buf], (eph >> buf) & 1u, 500);
+        mbar_wait_sleep(&empty[g][buf], (eph >> buf) & 1u, a.psleep);
         if (a.prof) p_wait += clock64() - c0;
         eph ^= 1u << buf;
         if (a.sched_lazy && k > 0) {
-          tile = next_tile();
+          next_tile();
           load_list();
         }
       }
@@ -596,12 +619,12 @@ __global__ void __launch_bounds__(G * (kCW + 1) * 32, 1) k_step(StepArgs a) {
         break;
       }
       const int nst = min(L, kStage);
-      const int tx = tile % a.ntx, ty = a.ty_begin + tile / a.ntx;
+      const int tx = txy & 0xffff, ty = txy >> 16;
       const int vw = min(kTile, a.W - tx * kTile);
       const int vh = min(kTile, a.H - ty * kTile);
       const uint32_t row_bytes = (uint32_t)vw * sizeof(float4);
       if (lane == 0) {
-        hdr[g][buf] = make_int4(tile, b0, L, tx | (ty << 16));
+        hdr[g][buf] = make_int4(tile, b0, L, txy);
         mbar_arrive_tx(&full[g][buf], (uint32_t)nst * kEntBytes +
                                           (uint32_t)vh * row_bytes * (has_bg ? 2u : 1u));
       }
@@ -617,7 +640,7 @@ __global__ void __launch_bounds__(G * (kCW + 1) * 32, 1) k_step(StepArgs a) {
       }
       buf = buf + 1 == kNBuf ? 0 : buf + 1;
       if (!a.sched_lazy || k + 1 < kNBuf) {
-        tile = next_tile();
+        next_tile();
         load_list();
       }
     }
@@ -625,9 +648,10 @@ __global__ void __launch_bounds__(G * (kCW + 1) * 32, 1) k_step(StepArgs a) {
     // ---------------- consumer warps
     int buf = 0;
     uint32_t fph = 0;
+    mbar_wait_sleep(&atl_bar, 0, 100);  // the shared-memory atlas has landed
     for (;;) {
       const unsigned long long c0 = a.prof ? clock64() : 0;
-      mbar_wait_sleep(&full[g][buf], (fph >> buf) & 1u, 200);
+      mbar_wait_sleep(&full[g][buf], (fph >> buf) & 1u, a.csleep);
       const unsigned long long c1 = a.prof ? clock64() : 0;
       if (a.prof) {
         p_wait += c1 - c0;
@@ -786,9 +810,11 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   a.grads = grads;
   a.ctr = counters;
   a.sched_lazy = getenv("PF_STEP_LAZY") ? 1 : 0;
+  a.csleep = getenv("PF_CSLEEP") ? (unsigned)atoi(getenv("PF_CSLEEP")) : 200u;
+  a.psleep = getenv("PF_PSLEEP") ? (unsigned)atoi(getenv("PF_PSLEEP")) : 500u;
   a.classes = getenv("PF_STEP_NOLPT") ? nullptr : tile_classes;
   a.classes_rw = const_cast<int32_t*>(a.classes);
-  a.tile_cost = tile_classes ? const_cast<int32_t*>(tile_classes) + kTileClasses * (1 + n_tiles)
+  a.tile_cost = tile_classes ? const_cast<int32_t*>(tile_classes) + tile_cost_offset(n_tiles)
                              : nullptr;
   a.prof = nullptr;
   a.tl = pf_timeline_ptr();
