@@ -52,6 +52,7 @@ extern "C" {
 #define PF_LOSS_NONE 0
 #define PF_LOSS_MSE 1        /* loss_mse, fit.py:112-116 */
 #define PF_LOSS_SPATIAL 2    /* loss_spatial, fit.py:128-151 */
+#define PF_LOSS_COMBINED 3   /* mse_w * loss_mse + gray_l1_w * loss_grayscale_l1, fit.py:119-125, 162-168 */
 
 /* ABI version; bumped on any signature change. */
 int pf_abi_version(void);
@@ -188,8 +189,10 @@ int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity
  *   img4       out float32 [H*W][4] = (r, g, b, alpha) (band rows written)
  *   tgt4       float32 [H*W][4] = (target r, g, b, target alpha); alpha read by SPATIAL
  *   d4         out float32 [H*W][4] = (dL/dI r, g, b, dL/dA)
+ *   w_mse, w_gray  LossSpec.mse_w / gray_l1_w (PF_LOSS_COMBINED only)
  *   part       out float64 [n_band_tiles * 8 * 3]: per-warp loss partials
- *              (sum (I-t)^2, sum ((I-t)*mask)^2, sum (I_a - t_a)^2), reduced in
+ *              (sum (I-t)^2; sum ((I-t)*mask)^2 or, for COMBINED, sum |(I-t).gray|;
+ *              sum (I_a - t_a)^2), reduced in
  *              fixed order by pf_backward (deterministic loss value)
  *   inv_3P, inv_P  1/(3*H*W), 1/(H*W) of the FULL canvas (band-independent)
  */
@@ -199,8 +202,8 @@ int pf_forward(const void* rec, int n, const double* tex, const float* quad, int
                double eps_skip, double mu_blend,
                double bg_r, double bg_g, double bg_b, const float* bg4,
                void* saved, long long saved_entries, int32_t* ent_n, float* img4,
-               int loss_kind, const float* tgt4, double alpha_w, double inv_3P, double inv_P,
-               float* d4, double* part, void* stream);
+               int loss_kind, const float* tgt4, double alpha_w, double w_mse, double w_gray,
+               double inv_3P, double inv_P, float* d4, double* part, void* stream);
 
 /*
  * K4 — backward: back-to-front over each pixel's saved contributions,
@@ -256,8 +259,9 @@ int pf_fit_step(const void* rec, int n, const double* tex, const float* apad,
                 const double* apad64, int pad_texels, int texels, const int32_t* bin_off, const int32_t* bin_idx, const int32_t* status,
                 int W, int H, int ty_begin, int ty_end, double eps_skip,
                 double bg_r, double bg_g, double bg_b, const float* bg4,
-                int loss_kind, const float* tgt4, double alpha_w, double inv_3P, double inv_P,
-                void* spill, float* img4, double* part, double* grads, uint32_t* counters,
+                int loss_kind, const float* tgt4, double alpha_w, double w_mse, double w_gray,
+                double inv_3P, double inv_P, void* spill, float* img4, double* part,
+                double* grads, uint32_t* counters,
                 const int32_t* tile_classes, void* stream);
 
 /* Fixed-order fold of n_part partial triples into sums[3] (deterministic). */

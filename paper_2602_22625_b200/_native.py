@@ -24,6 +24,7 @@ PF_ERR_TILE = 1003
 PF_LOSS_NONE = 0
 PF_LOSS_MSE = 1
 PF_LOSS_SPATIAL = 2
+PF_LOSS_COMBINED = 3
 
 _P = C.c_void_p
 _I = C.c_int
@@ -52,13 +53,13 @@ SIGNATURES: dict[str, tuple] = {
     "pf_forward": (
         _I,
         [_P, _I, _P, _P, _I, _P, _P, _P, _I, _I, _I, _I, _D, _D, _D, _D, _D, _P,
-         _P, C.c_longlong, _P, _P, _I, _P, _D, _D, _D, _P, _P, _P],
+         _P, C.c_longlong, _P, _P, _I, _P, _D, _D, _D, _D, _D, _P, _P, _P],
     ),
     "pf_step_spill_bytes": (_Z, [_I]),
     "pf_fit_step": (
         _I,
         [_P, _I, _P, _P, _P, _I, _I, _P, _P, _P, _I, _I, _I, _I, _D, _D, _D, _D, _P, _I, _P, _D,
-         _D, _D, _P, _P, _P, _P, _P, _P, _P],
+         _D, _D, _D, _D, _P, _P, _P, _P, _P, _P, _P],
     ),
     "pf_fold_loss": (_I, [_P, _I, _P, _P]),
     "pf_backward": (

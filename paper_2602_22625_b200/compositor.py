@@ -257,6 +257,7 @@ class Compositor:
     def forward(self, *, save: bool, eps_skip: float, bg_rgb=(1.0, 1.0, 1.0),
                 bg4: torch.Tensor | None = None, loss_kind: int = nat.PF_LOSS_NONE,
                 tgt4: torch.Tensor | None = None, alpha_w: float = 0.0,
+                w_mse: float = 1.0, w_gray: float = 0.0,
                 P_total: int | None = None, stream=None) -> None:
         lossy = loss_kind != nat.PF_LOSS_NONE
         self.alloc_render(save, lossy)
@@ -271,7 +272,8 @@ class Compositor:
                 float(eps_skip), self.mu_blend, float(bg_rgb[0]), float(bg_rgb[1]),
                 float(bg_rgb[2]), p(bg4), p(self.saved) if save else None,
                 self.saved_entries if save else 0, p(self.ent_n) if save else None,
-                self.img4.data_ptr(), int(loss_kind), p(tgt4), float(alpha_w),
+                self.img4.data_ptr(), int(loss_kind), p(tgt4), float(alpha_w), float(w_mse),
+                float(w_gray),
                 1.0 / (3.0 * P), 1.0 / P, p(self.d4) if lossy else None,
                 p(self.part) if lossy else None, _stream_handle(stream)),
             "pf_forward")
@@ -281,6 +283,7 @@ class Compositor:
     def fit_step(self, grads: torch.Tensor, sums: torch.Tensor | None, *, eps_skip: float,
                  bg_rgb=(1.0, 1.0, 1.0), bg4: torch.Tensor | None = None,
                  loss_kind: int = nat.PF_LOSS_MSE, tgt4: torch.Tensor, alpha_w: float = 0.0,
+                 w_mse: float = 1.0, w_gray: float = 0.0,
                  P_total: int | None = None, image: bool = False, stream=None) -> None:
         if self.mu_blend > 0.0:
             raise ValueError("pf_fit_step needs mu_blend == 0; use forward + backward")
@@ -306,7 +309,8 @@ class Compositor:
                 self.bin_off.data_ptr(), self.bin_idx.data_ptr(), self.status.data_ptr(),
                 self.W, self.H, self.band.ty_begin, self.band.ty_end, float(eps_skip),
                 float(bg_rgb[0]), float(bg_rgb[1]), float(bg_rgb[2]), p(bg4), int(loss_kind),
-                tgt4.data_ptr(), float(alpha_w), 1.0 / (3.0 * Pt), 1.0 / Pt,
+                tgt4.data_ptr(), float(alpha_w), float(w_mse), float(w_gray), 1.0 / (3.0 * Pt),
+                1.0 / Pt,
                 self.spill.data_ptr(), p(self.img4) if image else None, self.part.data_ptr(),
                 grads.data_ptr(), self.step_ctr.data_ptr(), nat.ptr(self.tile_classes),
                 _stream_handle(stream)),

@@ -96,7 +96,7 @@ struct FwdArgs {
   int32_t* ent_n;
   float4* img4;          // out: (r, g, b, alpha)
   const float4* tgt4;    // target (r, g, b, target alpha)
-  double alpha_w, inv_3P, inv_P;
+  double alpha_w, w_mse, w_gray, inv_3P, inv_P;
   float4* d4;            // out: (dL/dI r, g, b, dL/dA)
   double* part;
 };
@@ -190,6 +190,14 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_forward(FwdArgs a) {
       if (LOSS == PF_LOSS_MSE) {
         l1 = l0;
         a.d4[pix] = make_float4((float)(k * r0), (float)(k * r1), (float)(k * r2), 0.0f);
+      } else if (LOSS == PF_LOSS_COMBINED) {
+        // mse_w * loss_mse + gray_l1_w * loss_grayscale_l1 (fit.py:112-125, 162-168)
+        const double d = r0 * 0.299 + r1 * 0.587 + r2 * 0.114;
+        l1 = (float)fabs(d);
+        const double kg = a.w_gray * (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) * a.inv_P;
+        const double km = a.w_mse * k;
+        a.d4[pix] = make_float4((float)(km * r0 + kg * 0.299), (float)(km * r1 + kg * 0.587),
+                                (float)(km * r2 + kg * 0.114), 0.0f);
       } else {
         const double ta = (double)tg.w;
         const double mk = ta > 0.0 ? 1.0 : 0.0;
@@ -455,8 +463,8 @@ extern "C" int pf_forward(const void* rec, int n, const double* tex, const float
                           int ty_begin, int ty_end, double eps_skip, double mu_blend, double bg_r,
                           double bg_g, double bg_b, const float* bg4, void* saved,
                           long long saved_entries, int32_t* ent_n, float* img4, int loss_kind,
-                          const float* tgt4, double alpha_w, double inv_3P, double inv_P,
-                          float* d4, double* part, void* stream) {
+                          const float* tgt4, double alpha_w, double w_mse, double w_gray,
+                          double inv_3P, double inv_P, float* d4, double* part, void* stream) {
   if (W < 1 || H < 1 || n < 0 || !bin_off || !img4 || !tex || !quad) return PF_ERR_ARG;
   const int ntx = div_up(W, kTile), nty = div_up(H, kTile);
   if (ty_begin < 0 || ty_end > nty || ty_begin > ty_end) return PF_ERR_ARG;
@@ -464,7 +472,9 @@ extern "C" int pf_forward(const void* rec, int n, const double* tex, const float
   if (save && (!ent_n || saved_entries < 0)) return PF_ERR_ARG;
   if (loss_kind != PF_LOSS_NONE) {
     if (!tgt4 || !d4 || !part) return PF_ERR_ARG;
-    if (loss_kind != PF_LOSS_MSE && loss_kind != PF_LOSS_SPATIAL) return PF_ERR_ARG;
+    if (loss_kind != PF_LOSS_MSE && loss_kind != PF_LOSS_SPATIAL &&
+        loss_kind != PF_LOSS_COMBINED)
+      return PF_ERR_ARG;
   }
   const int n_tiles = (ty_end - ty_begin) * ntx;
   if (n_tiles == 0) return PF_OK;
@@ -492,6 +502,8 @@ extern "C" int pf_forward(const void* rec, int n, const double* tex, const float
   a.img4 = (float4*)img4;
   a.tgt4 = (const float4*)tgt4;
   a.alpha_w = alpha_w;
+  a.w_mse = w_mse;
+  a.w_gray = w_gray;
   a.inv_3P = inv_3P;
   a.inv_P = inv_P;
   a.d4 = (float4*)d4;
@@ -505,10 +517,12 @@ extern "C" int pf_forward(const void* rec, int n, const double* tex, const float
   if (save) {
     if (loss_kind == PF_LOSS_MSE) { PF_FWD_MU(true, PF_LOSS_MSE); }
     else if (loss_kind == PF_LOSS_SPATIAL) { PF_FWD_MU(true, PF_LOSS_SPATIAL); }
+    else if (loss_kind == PF_LOSS_COMBINED) { PF_FWD_MU(true, PF_LOSS_COMBINED); }
     else { PF_FWD_MU(true, PF_LOSS_NONE); }
   } else {
     if (loss_kind == PF_LOSS_MSE) { PF_FWD_MU(false, PF_LOSS_MSE); }
     else if (loss_kind == PF_LOSS_SPATIAL) { PF_FWD_MU(false, PF_LOSS_SPATIAL); }
+    else if (loss_kind == PF_LOSS_COMBINED) { PF_FWD_MU(false, PF_LOSS_COMBINED); }
     else { PF_FWD_MU(false, PF_LOSS_NONE); }
   }
 #undef PF_FWD_MU

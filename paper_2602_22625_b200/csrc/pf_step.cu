@@ -73,7 +73,7 @@ struct StepArgs {
   const float4* bg4;
   float4* img4;          // optional (r, g, b, alpha)
   const float4* tgt4;
-  double alpha_w, inv_3P, inv_P;
+  double alpha_w, w_mse, w_gray, inv_3P, inv_P;
   double* part;          // [n_tiles * 8][3] per-warp loss partials
   float4* spill;         // [slot][2] for stack depth >= kKS
   double* grads;
@@ -345,6 +345,15 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
       dI0 = (float)(k * r0);
       dI1 = (float)(k * r1);
       dI2 = (float)(k * r2);
+    } else if (LOSS == PF_LOSS_COMBINED) {
+      // mse_w * loss_mse + gray_l1_w * loss_grayscale_l1 (fit.py:112-125, 162-168)
+      const double d = r0 * 0.299 + r1 * 0.587 + r2 * 0.114;
+      l1 = (float)fabs(d);
+      const double kg = a.w_gray * (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) * a.inv_P;
+      const double km = a.w_mse * k;
+      dI0 = (float)(km * r0 + kg * 0.299);
+      dI1 = (float)(km * r1 + kg * 0.587);
+      dI2 = (float)(km * r2 + kg * 0.114);
     } else {
       const double ta = (double)tg.w;
       const double mk = ta > 0.0 ? 1.0 : 0.0;
@@ -765,13 +774,15 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
                            const int32_t* bin_idx, const int32_t* status, int W, int H,
                            int ty_begin, int ty_end, double eps_skip, double bg_r, double bg_g,
                            double bg_b, const float* bg4, int loss_kind, const float* tgt4,
-                           double alpha_w, double inv_3P, double inv_P, void* spill, float* img4,
+                           double alpha_w, double w_mse, double w_gray, double inv_3P,
+                           double inv_P, void* spill, float* img4,
                            double* part, double* grads, uint32_t* counters,
                            const int32_t* tile_classes, void* stream) {
   if (W < 1 || H < 1 || n < 0 || !bin_off || !bin_idx || !status || !tex || !apad || !tgt4 ||
       !spill || !part || !grads || !counters || pad_texels < 0 || (pad_texels & 3))
     return PF_ERR_ARG;
-  if (loss_kind != PF_LOSS_MSE && loss_kind != PF_LOSS_SPATIAL) return PF_ERR_ARG;
+  if (loss_kind != PF_LOSS_MSE && loss_kind != PF_LOSS_SPATIAL && loss_kind != PF_LOSS_COMBINED)
+    return PF_ERR_ARG;
   const int ntx = div_up(W, kTile), nty = div_up(H, kTile);
   if (ty_begin < 0 || ty_end > nty || ty_begin > ty_end) return PF_ERR_ARG;
   const int n_tiles = (ty_end - ty_begin) * ntx;
@@ -803,6 +814,8 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   a.img4 = (float4*)img4;
   a.tgt4 = (const float4*)tgt4;
   a.alpha_w = alpha_w;
+  a.w_mse = w_mse;
+  a.w_gray = w_gray;
   a.inv_3P = inv_3P;
   a.inv_P = inv_P;
   a.part = part;
@@ -861,6 +874,8 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   }
   if (loss_kind == PF_LOSS_MSE) {
     PF_PICK(PF_LOSS_MSE)
+  } else if (loss_kind == PF_LOSS_COMBINED) {
+    PF_PICK(PF_LOSS_COMBINED)
   } else {
     PF_PICK(PF_LOSS_SPATIAL)
   }

@@ -132,6 +132,16 @@ def loss_mse(I: FloatArray, target: FloatArray):
     return float(np.mean(diff**2)), 2.0 * diff / diff.size
 
 
+def loss_grayscale_l1(I: FloatArray, target: FloatArray):
+    """mean |luma(I - t)| and its subgradient (reference fit.py:119-125); the device
+    fit step fuses the same formula (PF_LOSS_COMBINED)."""
+    _check_image_pair(I, target)
+    d = (I - target) @ GRAY_WEIGHTS
+    n = d.size
+    grad = (np.sign(d)[:, :, None] * GRAY_WEIGHTS[None, None, :]) / n
+    return float(np.mean(np.abs(d))), grad
+
+
 def loss_spatial(I: FloatArray, I_alpha: FloatArray, spec: LossSpec):
     """Masked colour MSE + alpha_w * coverage MSE (reference fit.py:128-151)."""
     if spec.target_alpha is None:
@@ -156,7 +166,10 @@ def evaluate_loss(spec: LossSpec, I: FloatArray, I_alpha: FloatArray):
     if spec.kind == "spatial_constrained":
         return loss_spatial(I, I_alpha, spec)
     if spec.kind == "combined":
-        raise NotImplementedError("combined (gray-L1) loss is outside the ported hot path")
+        value_m, dI_m = loss_mse(I, spec.target)
+        value_g, dI_g = loss_grayscale_l1(I, spec.target)
+        return (spec.mse_w * value_m + spec.gray_l1_w * value_g,
+                spec.mse_w * dI_m + spec.gray_l1_w * dI_g, None)
     raise ValueError(f"unknown loss kind {spec.kind!r}")
 
 
@@ -255,8 +268,8 @@ class StepEngine:
                  use_graph: bool = True, device=None):
         if getattr(cfg, "do_reinit", False):
             raise NotImplementedError("low-opacity reinit is outside the ported hot path")
-        if loss_spec.kind not in ("mse", "spatial_constrained"):
-            raise NotImplementedError(f"loss {loss_spec.kind!r} is outside the ported hot path")
+        if loss_spec.kind not in ("mse", "spatial_constrained", "combined"):
+            raise ValueError(f"unknown loss kind {loss_spec.kind!r}")
         validate_scene(scene)
         self.dev = device or _device()
         self.scene = scene
@@ -267,8 +280,11 @@ class StepEngine:
         target = np.asarray(loss_spec.target, dtype=np.float64)
         if target.shape != (H, W, 3):
             raise ShapeMismatch(f"target shape {target.shape} != {(H, W, 3)}")
-        self.loss_kind = nat.PF_LOSS_MSE if loss_spec.kind == "mse" else nat.PF_LOSS_SPATIAL
+        self.loss_kind = {"mse": nat.PF_LOSS_MSE, "spatial_constrained": nat.PF_LOSS_SPATIAL,
+                          "combined": nat.PF_LOSS_COMBINED}[loss_spec.kind]
         self.alpha_w = float(loss_spec.alpha_w)
+        self.w_mse = float(getattr(loss_spec, "mse_w", 1.0))
+        self.w_gray = float(getattr(loss_spec, "gray_l1_w", 0.0))
         vec, layout = pack_params(scene)
         self.layout = layout
         self.n = n = layout.n_primitives
@@ -342,12 +358,13 @@ class StepEngine:
             # allreduce they are folded first so the sums travel with the grads
             c.fit_step(self.gbuf, None if fold_in_adam else self.sums, eps_skip=self.eps_skip,
                        bg_rgb=self.bg_rgb, bg4=self.bg4, loss_kind=self.loss_kind,
-                       tgt4=self.tgt4, alpha_w=self.alpha_w, P_total=self.P)
+                       tgt4=self.tgt4, alpha_w=self.alpha_w, w_mse=self.w_mse,
+                       w_gray=self.w_gray, P_total=self.P)
             mark("step")
         else:
             c.forward(save=True, eps_skip=self.eps_skip, bg_rgb=self.bg_rgb, bg4=self.bg4,
                       loss_kind=self.loss_kind, tgt4=self.tgt4, alpha_w=self.alpha_w,
-                      P_total=self.P)
+                      w_mse=self.w_mse, w_gray=self.w_gray, P_total=self.P)
             mark("forward")
             c.backward(c.d4, self.gbuf, bg_rgb=self.bg_rgb, bg4=self.bg4, sums=self.sums)
             mark("backward")
@@ -445,6 +462,8 @@ class StepEngine:
         mse = sums[:, 0] * inv_3P
         if self.loss_kind == nat.PF_LOSS_SPATIAL:
             loss = sums[:, 1] * inv_3P + self.alpha_w * (sums[:, 2] * inv_P)
+        elif self.loss_kind == nat.PF_LOSS_COMBINED:
+            loss = self.w_mse * mse + self.w_gray * (sums[:, 1] * inv_P)
         else:
             loss = mse
         with np.errstate(divide="ignore"):

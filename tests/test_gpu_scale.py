@@ -140,11 +140,46 @@ def _fused_grads(eng, image=True):
     c.bin()
     eng.gbuf.zero_()
     c.fit_step(eng.gbuf, eng.sums, eps_skip=eng.eps_skip, bg_rgb=eng.bg_rgb, bg4=eng.bg4,
-               loss_kind=eng.loss_kind, tgt4=eng.tgt4, alpha_w=eng.alpha_w, P_total=eng.P,
+               loss_kind=eng.loss_kind, tgt4=eng.tgt4, alpha_w=eng.alpha_w, w_mse=eng.w_mse,
+               w_gray=eng.w_gray, P_total=eng.P,
                image=image)
     c.check_overflow()
     return (eng.grads.view(-1, 8).cpu().numpy(), eng.sums.cpu().numpy(),
             c.color().double().cpu().numpy(), c.alpha().double().cpu().numpy())
+
+
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_fused_combined_loss_matches_oracle(torch_cuda, oracle, name):
+    """K34 with the combined loss (mse_w * MSE + gray_l1_w * grayscale L1,
+    reference fit.py:119-125, 162-168): loss sums and gradients against the
+    oracle's forward + backward driven by the reference formula's dL/dI."""
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.fit import LossSpec, StepEngine, effective_padding, evaluate_loss
+
+    w = synth.make_workload(name)
+    sc = w.scene
+    rng = np.random.default_rng(11)
+    for p in sc.primitives:
+        p.x += float(rng.uniform(-0.5, 0.5))
+        p.opacity_logit = float(rng.uniform(-2.0, 3.0))
+    spec = LossSpec(kind="combined", target=w.target, mse_w=0.7, gray_l1_w=0.4)
+    eng = StepEngine(sc, w.cfg, spec, 1, use_graph=False)
+    assert eng.fused
+    g, sums, color, alpha = _fused_grads(eng)
+    pk = oracle.Packed(sc)
+    off, idx = oracle.bin_tiles(pk, 32, effective_padding(w.cfg))
+    img, a_ref, sv = oracle.render_forward(pk, off, idx, 32, oracle.background(sc), True,
+                                           w.cfg.eps_skip)
+    ok, err = fwd_close(color, img)
+    assert ok, f"{name} combined colour rel err {err}"
+    value, dI, dA = evaluate_loss(spec, img, a_ref)
+    assert dA is None
+    P = img.shape[0] * img.shape[1]
+    loss_dev = 0.7 * sums[0] / (3 * P) + 0.4 * sums[1] / P
+    np.testing.assert_allclose(loss_dev, value, rtol=1e-5)
+    g_ref = oracle.backward(pk, sv, dI, None)
+    ok, err = grad_close(g, g_ref)
+    assert ok, f"{name} combined grad rel err {err}"
 
 
 @pytest.mark.parametrize("name", ["c1", "c3", "c4"])
