@@ -403,7 +403,15 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
       tally(rc);
     }
   } else {
-    for (int j = j0; j < j1; ++j) tally(a.s.rect[j]);
+    // long chunks: batches of kRowCache independent loads, then the tallies
+    for (int jb = j0; jb < j1; jb += kRowCache) {
+      int4 rb[kRowCache];
+#pragma unroll
+      for (int k = 0; k < kRowCache; ++k)
+        rb[k] = jb + k < j1 ? a.s.rect[jb + k] : make_int4(1, 1, 0, 0);
+#pragma unroll
+      for (int k = 0; k < kRowCache; ++k) tally(rb[k]);
+    }
   }
   int4 tot4;
   const int4 ex = block_excl_scan4(make_int4(cnt, below, below_rows, all), ws4, &tot4);
@@ -443,10 +451,20 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
       if (rc.x <= rc.z && rc.y <= ty && ty <= rc.w) put(zcache[k], rc);
     }
   } else {
-    for (int j = j0; j < j1; ++j) {
-      const int4 rc = a.s.rect[j];
-      if (rc.x > rc.z || rc.y > ty || ty > rc.w) continue;
-      put(__ldg(a.s.zprim + j), rc);
+    for (int jb = j0; jb < j1; jb += kRowCache) {
+      int4 rb[kRowCache];
+      int zb[kRowCache];
+#pragma unroll
+      for (int k = 0; k < kRowCache; ++k)
+        rb[k] = jb + k < j1 ? a.s.rect[jb + k] : make_int4(1, 1, 0, 0);
+#pragma unroll
+      for (int k = 0; k < kRowCache; ++k) {
+        const int4 rc = rb[k];
+        zb[k] = (rc.x <= rc.z && rc.y <= ty && ty <= rc.w) ? __ldg(a.s.zprim + jb + k) : -1;
+      }
+#pragma unroll
+      for (int k = 0; k < kRowCache; ++k)
+        if (zb[k] >= 0) put(zb[k], rb[k]);
     }
   }
   __syncthreads();
