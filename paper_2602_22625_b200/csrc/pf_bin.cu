@@ -277,13 +277,14 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
       double hi_x = fmin(floor(__dadd_rn(x, r)), (double)(a.W - 1));
       double lo_y = fmax(ceil(__dsub_rn(y, r)), 0.0);
       double hi_y = fmin(floor(__dadd_rn(y, r)), (double)(a.H - 1));
-      int4 rc = make_int4(1, 1, 0, 0);  // empty
+      // rect at the z rank: (tx0 | tx1 << 16, ty0, primitive, ty1); empty: ty0 > ty1
+      int4 rc = make_int4(0, 1, i, 0);
       // NaN-safe: every comparison with NaN is false -> treated as empty
       if (lo_x <= hi_x && lo_y <= hi_y) {
         const int tx0 = (int)lo_x / a.tile, tx1 = (int)hi_x / a.tile;
         const int ty0 = max((int)lo_y / a.tile, a.ty_begin);
         const int ty1 = min((int)hi_y / a.tile, a.ty_end - 1);
-        if (ty0 <= ty1) rc = make_int4(tx0, ty0, tx1, ty1);
+        if (ty0 <= ty1) rc = make_int4(tx0 | (tx1 << 16), ty0, i, ty1);
       }
       a.s.rect[pi.zrank] = rc;
     }
@@ -377,12 +378,13 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
   // (a) stable compaction of the primitives covering row ty, z order kept
   const int chunk = (a.n + kRowThreads - 1) / kRowThreads;
   const int j0 = min(a.n, tid * chunk), j1 = min(a.n, j0 + chunk);
+  // rects: (tx0 | tx1 << 16, ty0, primitive, ty1), empty when ty0 > ty1 (k_prim)
   int4 rcache[CACHE ? kRowCache : 1];
-  int zcache[CACHE ? kRowCache : 1];
   int cnt = 0, below = 0, below_rows = 0, all = 0;
+  constexpr int4 kEmpty = {0, 1, 0, 0};
   auto tally = [&](const int4& rc) {
-    if (rc.x > rc.z) return;  // empty
-    const int span = rc.z - rc.x + 1;
+    if (rc.y > rc.w) return;  // empty
+    const int span = (rc.x >> 16) - (rc.x & 0xffff) + 1;
     all += (rc.w - rc.y + 1) * span;
     if (rc.y <= ty && ty <= rc.w) ++cnt;
     if (rc.y < ty) {
@@ -394,21 +396,15 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
   if (CACHE) {
     // all loads first (independent), then the tallies
 #pragma unroll
-    for (int k = 0; k < kRowCache; ++k)
-      rcache[k] = j0 + k < j1 ? a.s.rect[j0 + k] : make_int4(1, 1, 0, 0);
+    for (int k = 0; k < kRowCache; ++k) rcache[k] = j0 + k < j1 ? a.s.rect[j0 + k] : kEmpty;
 #pragma unroll
-    for (int k = 0; k < kRowCache; ++k) {
-      const int4 rc = rcache[k];
-      zcache[k] = (rc.x <= rc.z && rc.y <= ty && ty <= rc.w) ? __ldg(a.s.zprim + j0 + k) : 0;
-      tally(rc);
-    }
+    for (int k = 0; k < kRowCache; ++k) tally(rcache[k]);
   } else {
     // long chunks: batches of kRowCache independent loads, then the tallies
     for (int jb = j0; jb < j1; jb += kRowCache) {
       int4 rb[kRowCache];
 #pragma unroll
-      for (int k = 0; k < kRowCache; ++k)
-        rb[k] = jb + k < j1 ? a.s.rect[jb + k] : make_int4(1, 1, 0, 0);
+      for (int k = 0; k < kRowCache; ++k) rb[k] = jb + k < j1 ? a.s.rect[jb + k] : kEmpty;
 #pragma unroll
       for (int k = 0; k < kRowCache; ++k) tally(rb[k]);
     }
@@ -437,9 +433,9 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
   if (tid < kTileClasses) s_ccnt[tid] = 0;
   // long rows spill the list to HBM (every column block writes the same values)
   const bool spill_list = tot > a.smem_list;
-  auto put = [&](int i, const int4& rc) {
+  auto put = [&](const int4& rc) {
     // (primitive index, column span): the list order is the z order
-    const int2 e = make_int2(i, rc.x | (rc.z << 16));
+    const int2 e = make_int2(rc.z, rc.x);
     if (pos < a.smem_list) rsm[pos] = e;
     if (spill_list) a.s.rowlist[rbase + pos] = e;  // rbase + pos < rows entries <= K <= cap
     ++pos;
@@ -448,23 +444,16 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
 #pragma unroll
     for (int k = 0; k < kRowCache; ++k) {
       const int4 rc = rcache[k];
-      if (rc.x <= rc.z && rc.y <= ty && ty <= rc.w) put(zcache[k], rc);
+      if (rc.y <= ty && ty <= rc.w) put(rc);
     }
   } else {
     for (int jb = j0; jb < j1; jb += kRowCache) {
       int4 rb[kRowCache];
-      int zb[kRowCache];
+#pragma unroll
+      for (int k = 0; k < kRowCache; ++k) rb[k] = jb + k < j1 ? a.s.rect[jb + k] : kEmpty;
 #pragma unroll
       for (int k = 0; k < kRowCache; ++k)
-        rb[k] = jb + k < j1 ? a.s.rect[jb + k] : make_int4(1, 1, 0, 0);
-#pragma unroll
-      for (int k = 0; k < kRowCache; ++k) {
-        const int4 rc = rb[k];
-        zb[k] = (rc.x <= rc.z && rc.y <= ty && ty <= rc.w) ? __ldg(a.s.zprim + jb + k) : -1;
-      }
-#pragma unroll
-      for (int k = 0; k < kRowCache; ++k)
-        if (zb[k] >= 0) put(zb[k], rb[k]);
+        if (rb[k].y <= ty && ty <= rb[k].w) put(rb[k]);
     }
   }
   __syncthreads();
@@ -501,17 +490,10 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
     run += v;
   }
   __syncthreads();
-  if (a.classes) {
-    if (tid < kTileClasses) s_cbase[tid] = s_ccnt[tid] ? atomicAdd(a.classes + tid, s_ccnt[tid]) : 0;
-    __syncthreads();
-    for (int c = max(c0, cbeg); c < min(c1, cend); ++c) {
-      const int cl = ccls[c] & 0xff, rank = ccls[c] >> 8;
-      const int p = s_cbase[cl] + rank;
-      if (p < a.n_tiles)
-        reinterpret_cast<int4*>(a.classes + kTileClasses)[cl * a.n_tiles + p] =
-            make_int4(r * a.ntx + c, col[c], ccnt[c], c | ((a.ty_begin + r) << 16));
-    }
-  }
+  // class bases: the global atomics' latency overlaps the ballot walks of (c)
+  int cbase_mine = 0;
+  if (a.classes && tid < kTileClasses)
+    cbase_mine = s_ccnt[tid] ? atomicAdd(a.classes + tid, s_ccnt[tid]) : 0;
 
   tl_mark(a.tl, 10, 1);
   // (c) one warp per column of this block: ordered ballot walk of the row list
@@ -530,6 +512,17 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
       const unsigned ball = __ballot_sync(kFull, hit);
       if (hit) a.bin_idx[out + __popc(ball & ((1u << lane) - 1u))] = j;
       out += __popc(ball);
+    }
+  }
+  if (a.classes) {
+    if (tid < kTileClasses) s_cbase[tid] = cbase_mine;
+    __syncthreads();
+    for (int c = max(c0, cbeg); c < min(c1, cend); ++c) {
+      const int cl = ccls[c] & 0xff, rank = ccls[c] >> 8;
+      const int p = s_cbase[cl] + rank;
+      if (p < a.n_tiles)
+        reinterpret_cast<int4*>(a.classes + kTileClasses)[cl * a.n_tiles + p] =
+            make_int4(r * a.ntx + c, col[c], ccnt[c], c | ((a.ty_begin + r) << 16));
     }
   }
   tl_mark(a.tl, 0, 3);

@@ -15,7 +15,7 @@ struct __align__(16) PrimInfo {
 static_assert(sizeof(PrimInfo) == 48, "PrimInfo must be 48 bytes");
 
 struct BinScratch {
-  int4* rect;        // [n] band-clipped tile rect per z position (tx0, ty0, tx1, ty1)
+  int4* rect;        // [n] per z rank: (tx0 | tx1 << 16, ty0, primitive, ty1); empty: ty0 > ty1
   int32_t* zprim;    // [n] primitive index per z position (static, set by pf_scratch_init)
   PrimInfo* pinfo;   // [n] static per-primitive structure (pf_scratch_init)
   int2* rowlist;     // [capacity] per-row z-ordered lists: (z position, tx0 | tx1 << 16)
