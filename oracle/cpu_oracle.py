@@ -234,3 +234,116 @@ class Loop:
         q = psnr(img, self.target)
         self.history.append((it, value, q, lr))
         return value, q
+
+
+# ---------------------------------------------------------------------------
+# f4 layered export and f3 video heuristics, numpy restatements.
+# Paths under /root/reference/pkg/src/primfit.
+
+def _expit(x):
+    x = np.asarray(x, dtype=np.float64)
+    return np.where(x >= 0, 1.0 / (1.0 + np.exp(-np.abs(x))), np.exp(-np.abs(x)) / (1.0 + np.exp(-np.abs(x))))
+
+
+LAYER_BBOX_PAD = 1.0  # exportio.py:78
+
+
+def export_layers_arrays(pk: Packed, rho: int):
+    """scale_scene (exportio.py:272-288) + layer_bbox (291-307) + render_layer (310-346)
+    for every primitive: (bbox int64 [n][4] (-1 rows: DegenerateBBox), offsets
+    int64 [n+1], premultiplied rgba float64 [sum of areas][4])."""
+    shift = (rho - 1) / 2.0
+    W, H = rho * pk.W, rho * pk.H
+    boxes, chunks, offs = [], [], [0]
+    for i in range(pk.n):
+        x = rho * pk.x[i] + shift
+        y = rho * pk.y[i] + shift
+        s = rho * pk.s[i]
+        q = float(pk.q[i])
+        r = s * math.hypot(1.0, max(1.0, q)) + LAYER_BBOX_PAD
+        x0, x1 = max(math.floor(x - r), 0), min(math.ceil(x + r), W - 1)
+        y0, y1 = max(math.floor(y - r), 0), min(math.ceil(y + r), H - 1)
+        if x0 > x1 or y0 > y1:
+            boxes.append((-1, -1, -1, -1))
+            offs.append(offs[-1])
+            continue
+        xx, yy = np.meshgrid(np.arange(x0, x1 + 1, dtype=np.float64),
+                             np.arange(y0, y1 + 1, dtype=np.float64))
+        ct, st = math.cos(pk.r[i]), math.sin(pk.r[i])   # raster.py:159-172
+        dx, dy = xx - x, yy - y
+        u = (ct * dx + st * dy) / s
+        v = (-st * dx + ct * dy) / (s * q)
+        t = int(pk.tid[i])
+        wt, ht = int(pk.tw[t]), int(pk.th[t])
+        U = (u + 1.0) * 0.5 * (wt - 1)                  # raster.py:175-179
+        V = (v + 1.0) * 0.5 * (ht - 1)
+        rgba_t = pk.tex[pk.toff[t]: pk.toff[t] + wt * ht].reshape(ht, wt, 4)
+
+        def plane(ch):                                  # raster.py:182-200
+            pl = rgba_t[:, :, ch]
+            inside = (U >= 0.0) & (U <= wt - 1.0) & (V >= 0.0) & (V <= ht - 1.0)
+            u0 = np.clip(np.floor(U).astype(np.int64), 0, wt - 1)
+            v0 = np.clip(np.floor(V).astype(np.int64), 0, ht - 1)
+            u1, v1 = np.minimum(u0 + 1, wt - 1), np.minimum(v0 + 1, ht - 1)
+            wu, wv = np.clip(U - u0, 0.0, 1.0), np.clip(V - v0, 0.0, 1.0)
+            val = ((1.0 - wu) * (1.0 - wv) * pl[v0, u0] + wu * (1.0 - wv) * pl[v0, u1]
+                   + (1.0 - wu) * wv * pl[v1, u0] + wu * wv * pl[v1, u1])
+            return np.where(inside, val, 0.0)
+
+        a = pk.alpha_max * _expit(pk.nu[i]) * plane(3)
+        cvar = _expit(pk.cv[i])
+        if pk.mu > 0.0:                                  # raster.py:214-219
+            c = np.stack([pk.mu * plane(ch) + (1.0 - pk.mu) * cvar[ch] for ch in range(3)], axis=-1)
+        else:
+            c = np.broadcast_to(cvar, a.shape + (3,))
+        rgba = np.empty(a.shape + (4,))
+        rgba[:, :, :3] = a[:, :, None] * c
+        rgba[:, :, 3] = a
+        boxes.append((x0, y0, x1, y1))
+        chunks.append(rgba.reshape(-1, 4))
+        offs.append(offs[-1] + rgba.shape[0] * rgba.shape[1])
+    rgba_all = np.concatenate(chunks, axis=0) if chunks else np.zeros((0, 4))
+    return np.asarray(boxes, dtype=np.int64), np.asarray(offs, dtype=np.int64), rgba_all
+
+
+def diff_mask(prev, cur, tau):
+    """dyn.py:86-97."""
+    return np.abs(np.asarray(prev, np.float64) - np.asarray(cur, np.float64)).max(axis=2) > tau
+
+
+def freeze_flags(pk: Packed, mask, padding):
+    """dyn.py:100-130 (the binning bbox, inclusive rounding, any change inside)."""
+    out = np.empty(pk.n, dtype=bool)
+    for i in range(pk.n):
+        r = pk.s[i] * pk.hyp[i] + padding
+        x0, x1 = max(math.ceil(pk.x[i] - r), 0), min(math.floor(pk.x[i] + r), pk.W - 1)
+        y0, y1 = max(math.ceil(pk.y[i] - r), 0), min(math.floor(pk.y[i] + r), pk.H - 1)
+        out[i] = not (x0 <= x1 and y0 <= y1 and mask[y0:y1 + 1, x0:x1 + 1].any())
+    return out
+
+
+def remove_stuck(pk: Packed, z, frozen, grid, k, tau_scale, tau_alpha, zeta, eta):
+    """dyn.py:133-177 -> (new opacity logits, sorted decayed indices)."""
+    rows, cols = grid
+    frozen = np.zeros(pk.n, dtype=bool) if frozen is None else np.asarray(frozen, dtype=bool)
+    regions = {}
+    for i in range(pk.n):
+        ry = min(max(int(pk.y[i] * rows / pk.H), 0), rows - 1)
+        rx = min(max(int(pk.x[i] * cols / pk.W), 0), cols - 1)
+        regions.setdefault((ry, rx), []).append(i)
+    decayed = []
+    for members in regions.values():
+        zs = np.asarray([z[i] for i in members])
+        scored = []
+        for i in members:
+            rank = int((zs > z[i]).sum())
+            alpha = pk.alpha_max * float(_expit(pk.nu[i]))
+            if (not frozen[i] and pk.s[i] >= tau_scale * pk.W and alpha >= tau_alpha
+                    and rank >= zeta * len(members)):
+                scored.append((pk.s[i] * alpha, i))
+        scored.sort(key=lambda t: (-t[0], t[1]))
+        decayed.extend(i for _, i in scored[:k])
+    nu = pk.nu.copy()
+    for i in decayed:
+        nu[i] = eta * nu[i]
+    return nu, sorted(decayed)

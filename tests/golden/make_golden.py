@@ -228,5 +228,61 @@ def main():
     print("synth c1 ok")
 
 
+def aux_cases():
+    """f3 / f4 rows of SURVEY §8: layered export (exportio.scale_scene / layer_bbox /
+    render_layer, exportio.py:272-346) and the video heuristics (dyn.diff_mask /
+    freeze_flags / remove_stuck, dyn.py:86-177), straight from the reference."""
+    from primfit import dyn as rdyn
+    from primfit import exportio as rex
+    from primfit.errors import DegenerateBBox
+
+    # export: mixed scenes (aspect + mu_blend > 0, plain), every layer at rho 1, 2, 4
+    for name, sc in (("export_aspect_mu", aspect_scene(1)), ("export_random", random_scene(3, n=10, w=40, h=36))):
+        d = scene_arrays(sc)
+        for rho in (1, 2, 4):
+            scaled = rex.scale_scene(sc, rho)
+            boxes, chunks, offs = [], [], [0]
+            for i in range(sc.n):
+                try:
+                    bbox, rgba = rex.render_layer(scaled, i)
+                except DegenerateBBox:
+                    bbox, rgba = (-1, -1, -1, -1), np.zeros((0, 0, 4))
+                boxes.append(bbox)
+                chunks.append(rgba.reshape(-1, 4))
+                offs.append(offs[-1] + rgba.shape[0] * rgba.shape[1])
+            d[f"rho{rho}_bbox"] = np.asarray(boxes, dtype=np.int64)
+            d[f"rho{rho}_off"] = np.asarray(offs, dtype=np.int64)
+            d[f"rho{rho}_rgba"] = np.concatenate(chunks, axis=0)
+        np.savez_compressed(OUT / f"{name}.npz", **d)
+
+    # video heuristics on a medium scene with a partly changed frame pair
+    sc = random_scene(4, n=60, w=96, h=80)
+    rng = np.random.default_rng(21)
+    prev = rng.random((80, 96, 3))
+    cur = prev.copy()
+    cur[10:40, 20:70] += rng.uniform(-0.05, 0.05, (30, 50, 3))
+    d = scene_arrays(sc)
+    d["prev"], d["cur"] = prev, cur
+    for tau in (0.0, 2.0 / 255.0, 0.02):
+        m = rdyn.diff_mask(prev, cur, tau).mask
+        d[f"mask_{tau!r}"] = m
+    m = rdyn.diff_mask(prev, cur, 2.0 / 255.0)
+    for pad in (2.0, 5.0):
+        d[f"frozen_p{int(pad)}"] = rdyn.freeze_flags(sc, m, pad)
+    frozen = d["frozen_p2"]
+    # a policy loose enough that several primitives qualify
+    pol = rdyn.StuckPolicy(grid=(3, 4), k=2, tau_scale=0.02, tau_alpha=0.3, zeta=0.3, eta=0.5)
+    new, decayed = rdyn.remove_stuck(sc, frozen, pol)
+    d["stuck_decayed"] = np.asarray(decayed, dtype=np.int64)
+    d["stuck_params"] = pack_params(new)[0].reshape(-1, 8)
+    d["stuck_policy"] = np.asarray([3, 4, 2, 0.02, 0.3, 0.3, 0.5])
+    new0, dec0 = rdyn.remove_stuck(sc, None, pol)
+    d["stuck_decayed_nofrozen"] = np.asarray(dec0, dtype=np.int64)
+    np.savez_compressed(OUT / "video_heuristics.npz", **d)
+
+
 if __name__ == "__main__":
+    if "--aux" in sys.argv:
+        aux_cases()
+        raise SystemExit(0)
     main()

@@ -106,3 +106,32 @@ def test_oracle_run_loop_rollout(oracle):
     np.testing.assert_allclose(hl, d["hist_loss"], rtol=1e-12)
     np.testing.assert_allclose(hp, d["hist_psnr"], rtol=1e-12)
     np.testing.assert_allclose(loop.vec.reshape(-1, 8), d["final_params"], rtol=1e-11, atol=1e-12)
+
+
+@pytest.mark.parametrize("case", ["export_aspect_mu", "export_random"])
+def test_oracle_export_layers_match_reference(oracle, case):
+    """f4: scale_scene + layer_bbox + render_layer (exportio.py:272-346) at rho 1, 2, 4."""
+    d = load_case(case)
+    pk = oracle.Packed(scene_from(d))
+    for rho in (1, 2, 4):
+        box, off, rgba = oracle.export_layers_arrays(pk, rho)
+        np.testing.assert_array_equal(box, d[f"rho{rho}_bbox"])
+        np.testing.assert_array_equal(off, d[f"rho{rho}_off"])
+        np.testing.assert_allclose(rgba, d[f"rho{rho}_rgba"], rtol=0, atol=1e-14)
+
+
+def test_oracle_video_heuristics_match_reference(oracle):
+    """f3: diff_mask, freeze_flags, remove_stuck (dyn.py:86-177)."""
+    d = load_case("video_heuristics")
+    pk = oracle.Packed(scene_from(d))
+    for tau in (0.0, 2.0 / 255.0, 0.02):
+        np.testing.assert_array_equal(oracle.diff_mask(d["prev"], d["cur"], tau),
+                                      d[f"mask_{tau!r}"])
+    m = d["mask_" + repr(2.0 / 255.0)]
+    for pad in (2.0, 5.0):
+        np.testing.assert_array_equal(oracle.freeze_flags(pk, m, pad), d[f"frozen_p{int(pad)}"])
+    nu, dec = oracle.remove_stuck(pk, d["z"], d["frozen_p2"], (3, 4), 2, 0.02, 0.3, 0.3, 0.5)
+    assert dec == list(d["stuck_decayed"])
+    np.testing.assert_allclose(nu, d["stuck_params"][:, 4], rtol=0, atol=1e-15)
+    _, dec0 = oracle.remove_stuck(pk, d["z"], None, (3, 4), 2, 0.02, 0.3, 0.3, 0.5)
+    assert dec0 == list(d["stuck_decayed_nofrozen"])
