@@ -23,7 +23,8 @@ from paper_2602_22625_b200.scene import PrimitiveParams, PrimitiveTemplate, Scen
 
 RENDER_CASES = sorted(
     Path(p).stem for p in glob.glob(str(GOLDEN / "*.npz"))
-    if Path(p).stem not in ("adam_rollout", "run_loop_small", "synth_c1_init")
+    if Path(p).stem not in ("adam_rollout", "run_loop_small", "synth_c1_init", "video_heuristics")
+    and not Path(p).stem.startswith("export_")
 )
 
 
