@@ -292,6 +292,48 @@ int pf_adam(double* params, double* grads, double* m, double* v, const uint8_t* 
             const double* sums, int loss_kind, double alpha_w, double inv_3P, double inv_P,
             double* hist_loss, double* hist_psnr, uint32_t* counter, void* stream);
 
+/*
+ * f4 layered export (exportio.py:272-346): every primitive alone over its own
+ * pixel box of the rho-times denser canvas (scale_scene: x' = rho x + (rho-1)/2,
+ * s' = rho s), premultiplied RGBA.
+ *   pf_layer_bboxes: bbox out int32 [n][4] (x0, y0, x1, y1; -1 rows = fully off
+ *   canvas, the reference's DegenerateBBox), area out int64 [n], offsets out
+ *   int64 [n + 1] (exclusive scan; offsets[n] = total pixels).
+ *   pf_render_layers: rgba out float32 [offsets[n]][4], layer i at offsets[i],
+ *   row-major over its box.  tpl_q = aspect per template (as pf_scratch_init).
+ */
+int pf_layer_bboxes(const double* params, const int32_t* template_id, const double* tpl_hyp,
+                    int n, int W, int H, int rho, int32_t* bbox, long long* area,
+                    long long* offsets, void* stream);
+int pf_render_layers(const double* params, const int32_t* template_id, const double* tex,
+                     int texels, const int32_t* tpl_base, const int32_t* tpl_w,
+                     const int32_t* tpl_h, const double* tpl_q, int n, double alpha_max,
+                     double mu_blend, int rho, const int32_t* bbox, const long long* offsets,
+                     float* rgba, void* stream);
+
+/*
+ * f3 video heuristics (dyn.py:86-177).
+ *   pf_diff_mask: prev, cur float64 [H][W][3]; mask out uint8 [H][W] =
+ *     max_c |prev - cur| > tau                                    (diff_mask)
+ *   pf_freeze_flags: frozen out uint8 [n] = 1 iff the binning box (padding)
+ *     holds no changed pixel                                      (freeze_flags)
+ *   pf_remove_stuck: per (grid_rows x grid_cols) region, at most k primitives
+ *     (not frozen, scale >= tau_scale * W, alpha >= tau_alpha, depth rank >=
+ *     zeta * members; ordered by scale * alpha desc, index asc) get their
+ *     opacity logit scaled by eta IN params; decayed out uint8 [n]  (remove_stuck)
+ *     z int32 [n]; frozen uint8 [n] or NULL; scratch pf_stuck_scratch_bytes.
+ */
+int pf_diff_mask(const double* prev, const double* cur, int W, int H, double tau, uint8_t* mask,
+                 void* stream);
+int pf_freeze_flags(const double* params, const int32_t* template_id, const double* tpl_hyp,
+                    int n, int W, int H, double padding, const uint8_t* mask, uint8_t* frozen,
+                    void* stream);
+size_t pf_stuck_scratch_bytes(int n, int regions);
+int pf_remove_stuck(double* params, const int32_t* z, const uint8_t* frozen, int n, int W, int H,
+                    int grid_rows, int grid_cols, int k, double tau_scale, double tau_alpha,
+                    double zeta, double eta, double alpha_max, uint8_t* decayed, void* scratch,
+                    size_t scratch_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,6 +67,14 @@ SIGNATURES: dict[str, tuple] = {
         [_P, _I, _P, _P, _I, _P, _P, _P, _P, C.c_longlong, _P, _P, _D, _D, _D, _P, _D,
          _I, _I, _I, _I, _P, _P, _P, _P],
     ),
+    "pf_layer_bboxes": (_I, [_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P]),
+    "pf_render_layers": (
+        _I, [_P, _P, _P, _I, _P, _P, _P, _P, _I, _D, _D, _I, _P, _P, _P, _P]),
+    "pf_diff_mask": (_I, [_P, _P, _I, _I, _D, _P, _P]),
+    "pf_freeze_flags": (_I, [_P, _P, _P, _I, _I, _I, _D, _P, _P, _P]),
+    "pf_stuck_scratch_bytes": (_Z, [_I, _I]),
+    "pf_remove_stuck": (
+        _I, [_P, _P, _P, _I, _I, _I, _I, _I, _I, _D, _D, _D, _D, _D, _P, _P, _Z, _P]),
     "pf_adam": (
         _I,
         [_P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _D, _D, _D, _I, _D, _D, _I,

@@ -1,0 +1,137 @@
+"""Video-fit heuristics on the GPU.
+
+Mirrors the reference's dyn (pkg/src/primfit/dyn.py:86-177): ``diff_mask``
+(changed pixels between two frames), ``freeze_flags`` (primitives whose binning
+box misses every change; their parameters and moments stay put in the device
+Adam) and ``remove_stuck`` (per grid region, decay the opacity logit of the
+top-k large, opaque, front-most primitives).  Kernels: ``pf_diff_mask``,
+``pf_freeze_flags``, ``pf_remove_stuck``.  There is no CPU path.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .compositor import _stream_handle
+from .errors import ShapeMismatch
+from .raster import _device
+from .scene import param_matrix, structure_arrays
+
+DEFAULT_DIFF_THRESHOLD = 2.0 / 255.0  # dyn.py:34
+
+
+@dataclass
+class DiffMask:
+    """Boolean canvas: true where two frames disagree (dyn.py:37-41)."""
+
+    mask: np.ndarray  # (H, W) bool
+
+
+@dataclass
+class StuckPolicy:
+    """Knobs of remove_stuck (dyn.py:44-72), same validation."""
+
+    grid: tuple[int, int] = (4, 4)
+    k: int = 4
+    tau_scale: float = 0.1
+    tau_alpha: float = 0.7
+    zeta: float = 0.7
+    eta: float = 0.3
+    triggers: tuple[int, ...] = (20, 45, 70)
+
+    def __post_init__(self) -> None:
+        if self.grid[0] < 1 or self.grid[1] < 1:
+            raise ValueError(f"grid {self.grid} must be at least 1x1")
+        if self.k < 0:
+            raise ValueError(f"k {self.k} must be nonnegative")
+        if not 0.0 < self.eta < 1.0:
+            raise ValueError(f"eta {self.eta} outside (0, 1)")
+        if not 0.0 < self.zeta < 1.0:
+            raise ValueError(f"zeta {self.zeta} outside (0, 1)")
+
+
+def _hyp_table(scene) -> np.ndarray:
+    """hypot(1, max(1, aspect)) per template, as bbox_half_side (raster.py:222-224)."""
+    out = []
+    for t in scene.templates:
+        h, w = np.asarray(t.rgba).shape[:2]
+        q = h / w if scene.preserve_aspect else 1.0
+        out.append(math.hypot(1.0, max(1.0, float(q))))
+    return np.asarray(out, dtype=np.float64)
+
+
+def diff_mask(prev, cur, tau_d: float = DEFAULT_DIFF_THRESHOLD) -> DiffMask:
+    """True wherever any channel moved by more than tau_d (dyn.py:86-97)."""
+    prev = np.asarray(prev, dtype=np.float64)
+    cur = np.asarray(cur, dtype=np.float64)
+    if prev.shape != cur.shape:
+        raise ShapeMismatch(f"frame shapes {prev.shape} vs {cur.shape}")
+    H, W = prev.shape[:2]
+    dev = _device()
+    a = torch.from_numpy(np.ascontiguousarray(prev)).to(dev)
+    b = torch.from_numpy(np.ascontiguousarray(cur)).to(dev)
+    m = torch.empty(H * W, dtype=torch.uint8, device=dev)
+    nat.check(nat.load().pf_diff_mask(a.data_ptr(), b.data_ptr(), W, H, float(tau_d),
+                                      m.data_ptr(), _stream_handle()), "pf_diff_mask")
+    return DiffMask(m.cpu().numpy().reshape(H, W).astype(bool))
+
+
+def freeze_flags(scene, mask: DiffMask, padding: float = 2.0) -> np.ndarray:
+    """Per-primitive: frozen iff the binning box misses every change (dyn.py:100-130)."""
+    m = np.asarray(mask.mask)
+    if m.shape != (scene.canvas_h, scene.canvas_w):
+        raise ShapeMismatch(f"mask {m.shape} vs canvas ({scene.canvas_h}, {scene.canvas_w})")
+    n = len(scene.primitives)
+    if n == 0:
+        return np.zeros(0, dtype=bool)
+    dev = _device()
+    pm = torch.from_numpy(np.ascontiguousarray(param_matrix(scene), dtype=np.float64)).to(dev)
+    tid, _ = structure_arrays(scene)
+    d_tid = torch.from_numpy(np.ascontiguousarray(tid, dtype=np.int32)).to(dev)
+    hyp = torch.from_numpy(_hyp_table(scene)).to(dev)
+    d_m = torch.from_numpy(np.ascontiguousarray(m, dtype=np.uint8).reshape(-1)).to(dev)
+    out = torch.empty(n, dtype=torch.uint8, device=dev)
+    nat.check(nat.load().pf_freeze_flags(pm.data_ptr(), d_tid.data_ptr(), hyp.data_ptr(), n,
+                                         scene.canvas_w, scene.canvas_h, float(padding),
+                                         d_m.data_ptr(), out.data_ptr(), _stream_handle()),
+              "pf_freeze_flags")
+    return out.cpu().numpy().astype(bool)
+
+
+def remove_stuck(scene, frozen: np.ndarray | None, policy: StuckPolicy):
+    """Decay the opacity logit of dominant primitives per grid region (dyn.py:133-177).
+    Returns (scene with decayed logits, sorted decayed indices)."""
+    n = len(scene.primitives)
+    if n == 0:
+        return scene, []
+    dev = _device()
+    lib = nat.load()
+    pm = torch.from_numpy(np.ascontiguousarray(param_matrix(scene), dtype=np.float64)).to(dev)
+    z = torch.from_numpy(np.asarray([p.z for p in scene.primitives], dtype=np.int32)).to(dev)
+    fr = None
+    if frozen is not None:
+        fr = torch.from_numpy(np.asarray(frozen, dtype=bool).astype(np.uint8)).to(dev)
+    rows, cols = policy.grid
+    nbytes = int(lib.pf_stuck_scratch_bytes(n, rows * cols))
+    scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    dec = torch.empty(n, dtype=torch.uint8, device=dev)
+    nat.check(lib.pf_remove_stuck(pm.data_ptr(), z.data_ptr(), nat.ptr(fr), n, scene.canvas_w,
+                                  scene.canvas_h, int(rows), int(cols), int(policy.k),
+                                  float(policy.tau_scale), float(policy.tau_alpha),
+                                  float(policy.zeta), float(policy.eta), float(scene.alpha_max),
+                                  dec.data_ptr(), scratch.data_ptr(), nbytes, _stream_handle()),
+              "pf_remove_stuck")
+    decayed = sorted(int(i) for i in np.flatnonzero(dec.cpu().numpy()))
+    if not decayed:
+        return scene, []
+    nu = pm[:, 4].cpu().numpy()
+    prims = list(scene.primitives)
+    for i in decayed:
+        prims[i] = dataclasses.replace(prims[i], opacity_logit=float(nu[i]))
+    return dataclasses.replace(scene, primitives=prims), decayed
