@@ -289,11 +289,11 @@ def run_ours(args) -> None:
     # bin, fit step, Adam, D2H of the updated vector + the step's loss sums, then
     # a host synchronisation (the host holds the step's result before the next).
     n = eng.n
+    nb = eng.adam_blocks
     h_params = torch.empty(n * 8, dtype=torch.float64, pin_memory=True)
     h_params.copy_(eng.params.view(-1).cpu())
-    nb = eng.adam_blocks
-    h_loss = torch.empty(nb * 3, dtype=torch.float64, pin_memory=True)
-    eng.capture_host_step(h_params, h_loss)
+    h_out = torch.empty(n * 8 + nb * 3, dtype=torch.float64, pin_memory=True)
+    eng.capture_host_step(h_params, h_out)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -302,7 +302,9 @@ def run_ours(args) -> None:
     for _ in range(e2e_steps):
         eng.host_step()
         torch.cuda.current_stream().synchronize()
-        loss_host = float(h_loss.numpy()[0::3].sum())  # the step's loss sum, on the host
+        out = h_out.numpy()
+        h_params.numpy()[:] = out[: n * 8]              # the host holds the new parameters
+        loss_host = float(out[n * 8 :: 3].sum())        # and the step's loss sum
     e_end.record()
     torch.cuda.synchronize()
     assert np.isfinite(loss_host)

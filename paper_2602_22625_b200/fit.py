@@ -291,7 +291,13 @@ class StepEngine:
         self.state = state if state is not None else OptimState.fresh(layout)
         self.step0 = int(self.state.step)
         dev = self.dev
-        self.params = torch.from_numpy(vec.reshape(n, 8).copy()).to(dev)
+        # parameters and the latest step's loss sums share one buffer, so a
+        # host-driven step reads both back with a single copy
+        self.adam_blocks = int(nat.load().pf_adam_blocks(n))
+        self.io = torch.zeros(n * 8 + self.adam_blocks * 3, dtype=torch.float64, device=dev)
+        self.params = self.io[: n * 8].view(n, 8)
+        self.params.copy_(torch.from_numpy(vec.reshape(n, 8).copy()))
+        self.last_part = self.io[n * 8 :]
         self.m = torch.from_numpy(np.asarray(self.state.m, dtype=np.float64).copy()).to(dev)
         self.v = torch.from_numpy(np.asarray(self.state.v, dtype=np.float64).copy()).to(dev)
         self.frozen = torch.from_numpy(np.asarray(self.state.frozen, dtype=bool).astype(np.uint8)).to(dev)
@@ -332,10 +338,9 @@ class StepEngine:
         else:
             self.comp.alloc_render(save=True, loss=True)
         # per-iteration loss sums per Adam block (history; folded in order on the host)
-        self.adam_blocks = self.comp.adam_blocks
+        assert self.adam_blocks == self.comp.adam_blocks
         self.hist_part = torch.zeros(max(self.total, 1) * self.adam_blocks * 3, dtype=torch.float64,
                                      device=dev)
-        self.last_part = torch.zeros(self.adam_blocks * 3, dtype=torch.float64, device=dev)
         self.allreduce = allreduce
         self.use_graph = use_graph
         self.graph: torch.cuda.CUDAGraph | None = None
@@ -391,20 +396,19 @@ class StepEngine:
         self.kernels_per_step = self.comp.launches - before  # this package's kernels only
         self.graph = g
 
-    def capture_host_step(self, h_params: torch.Tensor, h_loss: torch.Tensor) -> None:
+    def capture_host_step(self, h_in: torch.Tensor, h_out: torch.Tensor) -> None:
         """One CUDA graph for a step driven through HOST buffers: H2D of the packed
-        parameter vector (pinned ``h_params``), preprocess, bin, fit step, Adam,
-        D2H of the updated vector and of the step's loss sums (``h_loss``, pinned,
-        adam_blocks * 3 doubles).  Replay with host_step()."""
+        parameter vector (pinned ``h_in``, 8n doubles), preprocess, bin, fit step,
+        Adam, and ONE D2H of the updated vector followed by the step's loss sums
+        (pinned ``h_out``, 8n + 3 * adam_blocks doubles).  Replay with host_step()."""
         if self.graph is None and self.done == 0:
             raise RuntimeError("run one step() first (eager warm-up + capture)")
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self.params.view(-1).copy_(h_params, non_blocking=True)
+            self.params.view(-1).copy_(h_in, non_blocking=True)
             self.refresh()
             self.launch_step()
-            h_params.copy_(self.params.view(-1), non_blocking=True)
-            h_loss.copy_(self.last_part, non_blocking=True)
+            h_out.copy_(self.io, non_blocking=True)
         self.host_graph = g
 
     def host_step(self) -> None:
