@@ -290,9 +290,10 @@ def run_ours(args) -> None:
     # a host synchronisation (the host holds the step's result before the next).
     n = eng.n
     nb = eng.adam_blocks
-    h_params = torch.empty(n * 8, dtype=torch.float64, pin_memory=True)
-    h_params.copy_(eng.params.view(-1).cpu())
+    # one pinned host buffer: [parameters (the next step's input) | loss sums]
     h_out = torch.empty(n * 8 + nb * 3, dtype=torch.float64, pin_memory=True)
+    h_params = h_out[: n * 8]
+    h_params.copy_(eng.params.view(-1).cpu())
     eng.capture_host_step(h_params, h_out)
     torch.cuda.synchronize()
     if world > 1:
@@ -302,9 +303,9 @@ def run_ours(args) -> None:
     for _ in range(e2e_steps):
         eng.host_step()
         torch.cuda.current_stream().synchronize()
-        out = h_out.numpy()
-        h_params.numpy()[:] = out[: n * 8]              # the host holds the new parameters
-        loss_host = float(out[n * 8 :: 3].sum())        # and the step's loss sum
+        # the host now holds the updated parameters (h_params, the next step's input)
+        # and the step's loss sum
+        loss_host = float(h_out.numpy()[n * 8 :: 3].sum())
     e_end.record()
     torch.cuda.synchronize()
     assert np.isfinite(loss_host)

@@ -369,9 +369,12 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     l0 += __shfl_xor_sync(kFull, l0, o);
-    l1 += __shfl_xor_sync(kFull, l1, o);
-    l2 += __shfl_xor_sync(kFull, l2, o);
+    if (LOSS != PF_LOSS_MSE) {  // MSE: l1 == l0, l2 == 0
+      l1 += __shfl_xor_sync(kFull, l1, o);
+      l2 += __shfl_xor_sync(kFull, l2, o);
+    }
   }
+  if (LOSS == PF_LOSS_MSE) l1 = l0;
   if (lane == 0) {
     double* pp = a.part + ((size_t)tile * kCW + w) * 3;
     pp[0] = l0;
@@ -421,8 +424,9 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
                        dI2 * (r.c2f - S2 - g2 * B) + dA * B;
       const float dalpha = Tc * gg;
       g[4] = dalpha * r.sd * m;
-      if (r.omm > 0.0f) {
-        const float wc = Tc * aa * r.omm;
+      {
+        // colour logits (the fused path runs with mu_blend == 0: 1 - mu = 1)
+        const float wc = Tc * aa;
         g[5] = dI0 * wc * r.cd0;
         g[6] = dI1 * wc * r.cd1;
         g[7] = dI2 * wc * r.cd2;
