@@ -236,38 +236,34 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
       double2* ps = reinterpret_cast<double2*>(a.recs + i);
       float4* ps4 = reinterpret_cast<float4*>(a.recs + i);
       const double sa_d = __dmul_rn(a.alpha_max, sig);
+      // guard band of the affine U, V: >= 1e4 x their error bound
+      const double du = 1e-11 * (fabs(au) * a.W + fabs(bu) * a.H + fabs(cu) + (wt - 1) + 1.0);
+      const double dv = 1e-11 * (fabs(av) * a.W + fabs(bv) * a.H + fabs(cv) + (ht - 1) + 1.0);
+      const double dl = fmax(du, dv);
       switch (c) {
         case 0: ps[0] = make_double2(au, bu); break;
-        case 1: ps[1] = make_double2(cu, av); break;
-        case 2: ps[2] = make_double2(bv, cv); break;
+        case 1: ps[1] = make_double2(cu - hw, av); break;
+        case 2: ps[2] = make_double2(bv, cv - hh); break;
         case 3: ps[3] = make_double2(sa_d, __dmul_rn(omm, sc0)); break;
         case 4: ps[4] = make_double2(__dmul_rn(omm, sc1), __dmul_rn(omm, sc2)); break;
-        case 5: ps[5] = make_double2((double)(wt - 1), (double)(ht - 1)); break;
-        case 6: {
-          // guard band of the affine U, V: >= 1e4 x their error bound
-          const double du = 1e-11 * (fabs(au) * a.W + fabs(bu) * a.H + fabs(cu) + (wt - 1) + 1.0);
-          const double dv = 1e-11 * (fabs(av) * a.W + fabs(bv) * a.H + fabs(cv) + (ht - 1) + 1.0);
-          ps[6] = make_double2(fmax(du, dv), 0.0);
-          break;
-        }
-        default:
-          reinterpret_cast<int4*>(ps4)[7] =
-              make_int4(pi.pbase, wt + 1, i, 0);
-          break;
+        case 5: ps[5] = make_double2(hw, hh); break;
+        case 6: ps[6] = make_double2(hw - dl, hw + dl); break;
+        default: ps[7] = make_double2(hh - dl, hh + dl); break;
       }
       switch (c) {
-        case 0:
-          ps4[8] = make_float4((float)(a.alpha_max * sig * (1.0 - sig)), (float)(sc0 * (1.0 - sc0)),
+        case 0: reinterpret_cast<int4*>(ps4)[8] = make_int4(pi.pbase, wt + 1, i, 0); break;
+        case 1:
+          ps4[9] = make_float4((float)(a.alpha_max * sig * (1.0 - sig)), (float)(sc0 * (1.0 - sc0)),
                                (float)(sc1 * (1.0 - sc1)), (float)(sc2 * (1.0 - sc2)));
           break;
-        case 1:
-          ps4[9] = make_float4((float)(-ct * inv_s), (float)(st * inv_sq), (float)(-st * inv_s),
-                               (float)(-ct * inv_sq));
+        case 2:
+          ps4[10] = make_float4((float)(-ct * inv_s), (float)(st * inv_sq), (float)(-st * inv_s),
+                                (float)(-ct * inv_sq));
           break;
-        case 2: ps4[10] = make_float4((float)inv_s, (float)q, (float)(s * inv_sq), (float)hw); break;
-        case 3: ps4[11] = make_float4((float)hh, (float)omm, (float)sa_d, 0.0f); break;
-        case 4:
-          ps4[12] = make_float4((float)(omm * sc0), (float)(omm * sc1), (float)(omm * sc2), 0.0f);
+        case 3: ps4[11] = make_float4((float)inv_s, (float)q, (float)(s * inv_sq), (float)hw); break;
+        case 4: ps4[12] = make_float4((float)hh, (float)omm, (float)sa_d, 0.0f); break;
+        case 5:
+          ps4[13] = make_float4((float)(omm * sc0), (float)(omm * sc1), (float)(omm * sc2), 0.0f);
           break;
         default: break;
       }

@@ -59,24 +59,26 @@ struct __align__(16) RecC {
 };
 static_assert(sizeof(RecC) == 32, "RecC must be 32 bytes");
 
-// Step record (208 bytes): everything pf_fit_step reads per list entry, staged
+// Step record (224 bytes): everything pf_fit_step reads per list entry, staged
 // in shared memory once per tile by TMA bulk copies.
-//   forward  texel coordinates as one affine map per axis,
-//              U = au*x + bu*y + cu,  V = av*x + bv*y + cv   (float64, 2 DFMA each)
+//   forward  texel coordinates as one affine map per axis, centred on the box:
+//              U - hw = au*x + bu*y + cu,  V - hh = av*x + bv*y + cv   (float64)
 //            -- the reference's per-pair chain (_kernels.py:106-114) folded into
 //            per-primitive coefficients.  They differ from the reference's U, V
 //            by < 1e-10 texel; `delta` (>= 1e4 x that bound) is the guard band:
-//            a pair whose U or V lies within delta of a box edge re-takes the
-//            inside test with the reference's exact op order (texel_coords on
-//            RecF), so every inside/outside decision matches the reference.
-//            Opacity / colours in float64 for the compositing (no conversions on
-//            the hot path); pbase/wp address the zero-padded alpha plane.
+//            |U - hw| < hw - delta (both axes) is inside for the reference too,
+//            > hw + delta is outside; anything between re-takes the inside test
+//            with the reference's exact op order (texel_coords on RecF), so
+//            every inside/outside decision matches the reference.
+//            Opacity / colours in float64 for the compositing; pbase/wp address
+//            the zero-padded alpha plane.
 //   backward fp32 gradient coefficients (as RecG) and gidx = the row of grads.
 struct __align__(16) RecS {
   double au, bu, cu, av, bv, cv;
   double sa, c0, c1, c2;        // alpha_max*sig, (1-mu)*sigmoid(c)
-  double wm1, hm1;              // wt - 1, ht - 1
-  double delta, pad_d;          // guard band of the affine U, V (texels)
+  double hwd, hhd;              // (wt - 1) / 2, (ht - 1) / 2
+  double in_u, out_u;           // hw - delta, hw + delta
+  double in_v, out_v;           // hh - delta, hh + delta
   int32_t pbase, wp;            // padded-atlas base, padded row stride (wt + 1)
   int32_t gidx, pad_i;          // primitive index (row of params / grads)
   float sd, cd0, cd1, cd2;      // alpha_max*sig*(1-sig), sc*(1-sc)
@@ -85,7 +87,7 @@ struct __align__(16) RecS {
   float hh, omm, saf, pad_f;    // 0.5 (ht - 1), 1 - mu_blend, (float)sa
   float c0f, c1f, c2f, pad_g;   // (float)c
 };
-static_assert(sizeof(RecS) == 208, "RecS must be 208 bytes");
+static_assert(sizeof(RecS) == 224, "RecS must be 224 bytes");
 
 // Tile cost classes for pf_fit_step's longest-first schedule.  pf_bin's
 // optional tile_classes buffer: int32 [kTileClasses] counts, then

@@ -70,6 +70,7 @@ struct StepArgs {
   double eps_skip;
   double eps_band;       // eps re-check band (see warp_tile)
   double bg0, bg1, bg2;
+  float bgf0, bgf1, bgf2;  // the same as float (backward)
   const float4* bg4;
   float4* img4;          // optional (r, g, b, alpha)
   const float4* tgt4;
@@ -265,15 +266,15 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
       mask &= mask - 1;
       const int j = sub + bit;
       const RecS& r = R.rec(j);
-      double U = fma(r.au, xx, fma(r.bu, yy, r.cu));
-      double V = fma(r.av, xx, fma(r.bv, yy, r.cv));
-      const double dl = r.delta, wm1 = r.wm1, hm1 = r.hm1;
-      const bool exact = fabs(U) < dl || fabs(U - wm1) < dl || fabs(V) < dl || fabs(V - hm1) < dl;
-      if (exact) {
-        if (!texel_coords(a.recf[r.gidx], xx, yy, U, V)) continue;
-      } else if (!(U >= 0.0 && U <= wm1 && V >= 0.0 && V <= hm1)) {
-        continue;
-      }
+      // centred texel coordinates: |U - hw| against hw -/+ delta decides
+      // inside / outside / guard band (exact reference chain) per axis
+      const double Uc = fma(r.au, xx, fma(r.bu, yy, r.cu));
+      const double Vc = fma(r.av, xx, fma(r.bv, yy, r.cv));
+      const double aU = fabs(Uc), aV = fabs(Vc);
+      if (aU > r.out_u || aV > r.out_v) continue;
+      const bool exact = !(aU < r.in_u && aV < r.in_v);
+      double U = Uc + r.hwd, V = Vc + r.hhd;
+      if (exact && !texel_coords(a.recf[r.gidx], xx, yy, U, V)) continue;
       int u0, v0;
       double wu, wv;
       cell_of(U, u0, wu);
@@ -325,9 +326,9 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
   // ---- loss (fit.py:112-151), pixel-local
   const float4 tg = tgs[tp_];
   const float4 bgp = bgs ? bgs[tp_] : make_float4(0.f, 0.f, 0.f, 0.f);
-  const float g0 = a.bg4 ? bgp.x : (float)a.bg0;
-  const float g1 = a.bg4 ? bgp.y : (float)a.bg1;
-  const float g2 = a.bg4 ? bgp.z : (float)a.bg2;
+  const float g0 = a.bg4 ? bgp.x : a.bgf0;
+  const float g1 = a.bg4 ? bgp.y : a.bgf1;
+  const float g2 = a.bg4 ? bgp.z : a.bgf2;
   float dI0 = 0.f, dI1 = 0.f, dI2 = 0.f, dA = 0.f;
   float l0 = 0.f, l1 = 0.f, l2 = 0.f;
   if (valid) {
@@ -814,6 +815,9 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   a.bg0 = bg_r;
   a.bg1 = bg_g;
   a.bg2 = bg_b;
+  a.bgf0 = (float)bg_r;
+  a.bgf1 = (float)bg_g;
+  a.bgf2 = (float)bg_b;
   a.bg4 = (const float4*)bg4;
   a.img4 = (float4*)img4;
   a.tgt4 = (const float4*)tgt4;
