@@ -44,6 +44,20 @@ constexpr int kStage = 32;                              // list entries staged p
 constexpr int kNBuf = 2;                                // stage buffers per group (ring)
 constexpr int kKS = 5;                                  // contribution-stack depth in smem
 constexpr uint32_t kEntBytes = sizeof(RecS) + sizeof(RecC);
+// CTA shape for G groups: warps [0, 8G) consume (group = warp / 8), warps
+// [8G, 9G) produce, padded to whole warpgroups so the producers' warpgroup can
+// hand registers to the consumers' (setmaxnreg)
+__host__ __device__ constexpr int step_warps(int G) { return (9 * G + 3) / 4 * 4; }
+__host__ __device__ constexpr int step_threads(int G) { return 32 * step_warps(G); }
+// registers per thread: launch budget, producer warpgroup after dec, consumers after inc
+__host__ __device__ constexpr int step_regs(int G) { return (65536 / step_threads(G)) / 8 * 8; }
+// (the pool setmaxnreg.inc draws from is what the launch allocated)
+constexpr int kProdRegs = 24;
+__host__ __device__ constexpr int step_cons_regs(int G) {
+  return ((step_regs(G) * step_threads(G) - 32 * (step_warps(G) - 8 * G) * kProdRegs) /
+          (256 * G)) / 8 * 8;
+}
+static_assert(step_cons_regs(3) == 80 && step_cons_regs(2) == 112, "register split");
 // one stage buffer: kStage RecS + kStage RecC + the tile's target (+ background) pixels
 constexpr size_t kBufRec = (size_t)kStage * kEntBytes;
 constexpr size_t kBufPix = (size_t)kTilePix * sizeof(float4);
@@ -474,7 +488,7 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
 // (ATL == 2) when it fits, else float32 (ATL == 1); ATL == 0 reads the global
 // fp32 plane.
 template <int LOSS, int ATL, int G, bool BG>
-__global__ void __launch_bounds__(G * (kCW + 1) * 32, 1) k_step(StepArgs a) {
+__global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t full[G][kNBuf], empty[G][kNBuf];
   __shared__ int4 hdr[G][kNBuf];
@@ -531,7 +545,9 @@ __global__ void __launch_bounds__(G * (kCW + 1) * 32, 1) k_step(StepArgs a) {
     return;
   }
 
-  const int g = warp / (kCW + 1), wg = warp % (kCW + 1);
+  const bool consumer = warp < G * kCW;
+  const int g = consumer ? warp / kCW : warp - G * kCW;
+  const int wg = consumer ? warp % kCW : kCW;
   unsigned char* gs = sm + g * gbytes;
   float4* stA = reinterpret_cast<float4*>(gs + kNBuf * bbytes);
   float* stB = reinterpret_cast<float*>(stA + kKS * kTilePix);
@@ -545,7 +561,25 @@ __global__ void __launch_bounds__(G * (kCW + 1) * 32, 1) k_step(StepArgs a) {
   };
 
   unsigned long long p_wait = 0, p_work = 0, p_n = 0, p_first = 0, p_t0 = a.prof ? gtimer() : 0;
-  if (wg == kCW) {
+  auto finish = [&]() {
+    tl_mark(a.tl, 1, 3);
+    if (a.prof && lane == 0) {
+      unsigned long long* o = a.prof + ((size_t)blockIdx.x * blockDim.x / 32 + warp) * 6;
+      o[0] = p_wait;
+      o[1] = p_work;
+      o[2] = p_n;
+      o[3] = p_t0;
+      o[4] = gtimer();
+      o[5] = (unsigned long long)(wg == kCW) | (p_first << 1);
+    }
+  };
+  // Register hand-over (warpgroup-uniform: warps [8G, ...) are whole
+  // warpgroups): the producer / padding warpgroup shrinks, the consumer
+  // warpgroups grow.  The two roles never re-join, so each is allocated
+  // against its own limit.
+  if (!consumer) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProdRegs));
+    if (g >= G) return;  // padding warp
     // ---------------- producer warp
     // Dynamic schedule: a global ticket t is mapped to a tile through the
     // per-class tile lists pf_bin wrote (classes by list length, heaviest
@@ -658,7 +692,9 @@ __global__ void __launch_bounds__(G * (kCW + 1) * 32, 1) k_step(StepArgs a) {
         load_list();
       }
     }
+    finish();
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(step_cons_regs(G)));
     // ---------------- consumer warps
     int buf = 0;
     uint32_t fph = 0;
@@ -695,16 +731,7 @@ __global__ void __launch_bounds__(G * (kCW + 1) * 32, 1) k_step(StepArgs a) {
       }
       buf = buf + 1 == kNBuf ? 0 : buf + 1;
     }
-  }
-  tl_mark(a.tl, 1, 3);
-  if (a.prof && lane == 0) {
-    unsigned long long* o = a.prof + ((size_t)blockIdx.x * blockDim.x / 32 + warp) * 6;
-    o[0] = p_wait;
-    o[1] = p_work;
-    o[2] = p_n;
-    o[3] = p_t0;
-    o[4] = gtimer();
-    o[5] = (unsigned long long)(wg == kCW) | (p_first << 1);
+    finish();
   }
 }
 
@@ -897,6 +924,6 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
     last_smem = smem;
   }
   const int grid = min(sms, max(1, (n_tiles + G - 1) / G));
-  g_prof_slots = grid * G * (kCW + 1);
-  return (int)launch_pdl(kern, grid, G * (kCW + 1) * 32, smem, st, a);
+  g_prof_slots = grid * (G == 3 ? step_warps(3) : step_warps(2));
+  return (int)launch_pdl(kern, grid, G == 3 ? step_threads(3) : step_threads(2), smem, st, a);
 }

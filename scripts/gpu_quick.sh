@@ -2,7 +2,7 @@
 # Quick GPU iteration: build, GPU parity tests, bench variants (no CPU baseline), launch list.
 set -u
 mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
+timeout 180 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log; grep -q "smoke ok\|OK" gpurun_out/smoke.log || { echo SMOKE FAILED; exit 1; }
 timeout 600 python -m pytest tests -m gpu -q -x --timeout 300 > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
 for v in ${VARIANTS:-"-"}; do
   if [ "$v" = "-" ]; then env_v=""; else env_v="$v"; fi
