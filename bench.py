@@ -284,28 +284,33 @@ def run_ours(args) -> None:
         for (_, e0), (name, e1) in zip(marks, marks[1:]):
             stage_ms[name] = stage_ms.get(name, 0.0) + e0.elapsed_time(e1) / prof_steps
 
-    # end-to-end through the public step API with HOST buffers each step: one
-    # graph per step = H2D of the packed parameter vector (pinned), preprocess,
-    # bin, fit step, Adam, D2H of the updated vector + the step's loss sums, then
-    # a host synchronisation (the host holds the step's result before the next).
-    n = eng.n
-    nb = eng.adam_blocks
-    # one pinned host buffer: [parameters (the next step's input) | loss sums]
-    h_out = torch.empty(n * 8 + nb * 3, dtype=torch.float64, pin_memory=True)
-    h_params = h_out[: n * 8]
-    h_params.copy_(eng.params.view(-1).cpu())
-    eng.capture_host_step(h_params, h_out)
+    # end-to-end through the public step API with HOST buffers each step: the
+    # parameter vector and the loss partials live in pinned host memory
+    # (StepEngine(host_io=True)); one graph per step reads the parameters over
+    # the host link (preprocess), bins, renders, runs the backward and Adam, and
+    # writes the updated vector + the step's loss partials back to host memory
+    # (zero-copy), then a host synchronisation: the host holds the step's result
+    # (the next step's input) before the next.
+    eh = StepEngine(sc, w.cfg, w.loss, total, band=band,
+                    allreduce=make_allreduce() if world > 1 else None, use_graph=True,
+                    host_io=True)
+    eh.run(args.warmup)
+    torch.cuda.synchronize()
+    eh.capture_host_io_step()
+    n = eh.n
+    nb = eh.adam_blocks
+    h_out = eh.io.numpy()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_start.record()
     for _ in range(e2e_steps):
-        eng.host_step()
+        eh.host_step()
         torch.cuda.current_stream().synchronize()
-        # the host now holds the updated parameters (h_params, the next step's input)
-        # and the step's loss sum
-        loss_host = float(h_out.numpy()[n * 8 :: 3].sum())
+        # the host now holds the updated parameters (h_out[:8n], the next step's
+        # input) and the step's loss partials
+        loss_host = float(h_out[n * 8 :: 3].sum())
     e_end.record()
     torch.cuda.synchronize()
     assert np.isfinite(loss_host)
@@ -315,6 +320,7 @@ def run_ours(args) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
     eng.check()
+    eh.check()
 
     nodes = eng.kernels_per_step
     if rank != 0:

@@ -265,7 +265,7 @@ class StepEngine:
 
     def __init__(self, scene, cfg, loss_spec: LossSpec, total: int, state: OptimState | None = None,
                  *, band: Band | None = None, allreduce: Callable | None = None,
-                 use_graph: bool = True, device=None):
+                 use_graph: bool = True, device=None, host_io: bool = False):
         if getattr(cfg, "do_reinit", False):
             raise NotImplementedError("low-opacity reinit is outside the ported hot path")
         if loss_spec.kind not in ("mse", "spatial_constrained", "combined"):
@@ -294,7 +294,15 @@ class StepEngine:
         # parameters and the latest step's loss sums share one buffer, so a
         # host-driven step reads both back with a single copy
         self.adam_blocks = int(nat.load().pf_adam_blocks(n))
-        self.io = torch.zeros(n * 8 + self.adam_blocks * 3, dtype=torch.float64, device=dev)
+        # host_io: the buffer lives in pinned host memory and the kernels read the
+        # parameters / write the updated ones and the loss partials through it
+        # directly (zero-copy over the host link): a host-driven step needs no
+        # copy nodes (see capture_host_io_step)
+        self.host_io = bool(host_io)
+        if self.host_io:
+            self.io = torch.zeros(n * 8 + self.adam_blocks * 3, dtype=torch.float64).pin_memory()
+        else:
+            self.io = torch.zeros(n * 8 + self.adam_blocks * 3, dtype=torch.float64, device=dev)
         self.params = self.io[: n * 8].view(n, 8)
         self.params.copy_(torch.from_numpy(vec.reshape(n, 8).copy()))
         self.last_part = self.io[n * 8 :]
@@ -409,6 +417,21 @@ class StepEngine:
             self.refresh()
             self.launch_step()
             h_out.copy_(self.io, non_blocking=True)
+        self.host_graph = g
+
+    def capture_host_io_step(self) -> None:
+        """host_io engines: one CUDA graph = preprocess from the host parameter
+        vector, bin, fit step, Adam writing the updated vector and the loss
+        partials back to host memory.  The caller edits / reads ``io`` (pinned
+        host) between host_step() replays."""
+        if not self.host_io:
+            raise RuntimeError("capture_host_io_step needs StepEngine(host_io=True)")
+        if self.graph is None and self.done == 0:
+            raise RuntimeError("run one step() first (eager warm-up + capture)")
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.refresh()
+            self.launch_step()
         self.host_graph = g
 
     def host_step(self) -> None:

@@ -69,3 +69,33 @@ timeit("H2D 320 KB + sync", h2d_only)
 timeit("D2H 320 KB + sync", d2h_only)
 timeit("refresh kernel + sync", refresh_only)
 timeit("empty sync", lambda: torch.cuda.current_stream().synchronize())
+
+# zero-copy host buffer engine
+eh = StepEngine(w.scene, w.cfg, w.loss, 2000, use_graph=True, host_io=True)
+eh.run(5)
+torch.cuda.synchronize()
+eh.capture_host_io_step()
+hv = eh.io.numpy()
+
+
+def host_io_step():
+    eh.host_step()
+    torch.cuda.current_stream().synchronize()
+    float(hv[eh.n * 8 :: 3].sum())
+
+
+def host_io_dev_graph():
+    eh.graph.replay(); eh.done += 1
+    torch.cuda.current_stream().synchronize()
+
+
+timeit("host_io step (zero-copy) + sync", host_io_step, 300)
+timeit("host_io device graph + sync", host_io_dev_graph, 300)
+timeit("host step graph + sync (again)", host_step_sync, 300)
+# parity: the two engines ran the same number of steps from the same init
+eng2 = StepEngine(w.scene, w.cfg, w.loss, 2000, use_graph=True)
+eh2 = StepEngine(w.scene, w.cfg, w.loss, 2000, use_graph=True, host_io=True)
+eng2.run(20); eh2.run(20)
+torch.cuda.synchronize()
+print("host_io vs device params max abs diff:",
+      float((eng2.params.cpu() - eh2.params.cpu()).abs().max()))

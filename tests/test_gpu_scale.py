@@ -108,6 +108,36 @@ def test_graph_replay_equals_eager(torch_cuda):
     np.testing.assert_allclose(a.params_host(), b.params_host(), rtol=1e-9, atol=1e-12)
 
 
+def test_host_io_zero_copy_matches_device(torch_cuda):
+    """host_io engine (parameters + loss partials in pinned host memory, read and
+    written by the kernels directly) == device-resident engine, including a host
+    edit of the parameters between two host-driven steps."""
+    torch = torch_cuda
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.fit import StepEngine
+
+    w = synth.make_workload("c1")
+    w.cfg.num_iterations = 8
+    a = StepEngine(w.scene, w.cfg, w.loss, 8, use_graph=True)
+    b = StepEngine(w.scene, w.cfg, w.loss, 8, use_graph=True, host_io=True)
+    a.run(2)
+    b.run(2)
+    b.capture_host_io_step()
+    n = b.n
+    for k in range(4):
+        if k == 2:  # host edit: move every primitive by +0.75 px in x
+            edited = b.io.numpy()[: n * 8].reshape(n, 8)
+            edited[:, 0] += 0.75
+            a.params[:, 0] += 0.75
+        a.refresh()
+        a.step()
+        b.host_step()
+        torch.cuda.synchronize()
+    np.testing.assert_array_equal(a.params_host(), b.io.numpy()[: n * 8])
+    np.testing.assert_array_equal(a.last_part.cpu().numpy(), b.io.numpy()[n * 8 :])
+    assert [h.loss for h in a.history()] == [h.loss for h in b.history()]
+
+
 def test_autograd_function_matches_api(torch_cuda):
     torch = torch_cuda
     from paper_2602_22625_b200 import grad, raster
