@@ -193,9 +193,12 @@ def _config(name: str, w) -> dict:
             "l2": "flushed (256 MiB write) before every timed step"}
 
 
-def ncu_traffic(kernel_prefix: str) -> float | None:
-    """dram bytes (read + write) per launch of the named kernel from the committed
-    ncu --set full summary under profiles/ (newest file), or None."""
+KNAME = {"step": "k_step", "forward": "k_forward", "backward": "k_backward"}
+
+
+def ncu_summary(kernel_prefix: str) -> dict | None:
+    """The named kernel's entry of the newest committed ncu --set full summary
+    under profiles/ (scripts/ncu_extract.py), or None."""
     files = sorted((ROOT / "profiles").glob("*ncu_kernels*.json"))
     for f in reversed(files):
         try:
@@ -204,8 +207,14 @@ def ncu_traffic(kernel_prefix: str) -> float | None:
             continue
         for name, v in d.items():
             if kernel_prefix in name and "dram_traffic_bytes" in v:
-                return float(v["dram_traffic_bytes"])
+                return v
     return None
+
+
+def ncu_traffic(kernel_prefix: str) -> float | None:
+    """dram bytes (read + write) per launch of the named kernel (ncu summary), or None."""
+    v = ncu_summary(kernel_prefix)
+    return float(v["dram_traffic_bytes"]) if v else None
 
 
 def run_ours(args) -> None:
@@ -342,11 +351,17 @@ def run_ours(args) -> None:
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved,
                      "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"],
-                     "traffic": ncu_traffic({"step": "k_step", "forward": "k_forward",
-                                             "backward": "k_backward"}[dom]),
+                     "traffic": ncu_traffic(KNAME[dom]),
                      "peak_src": peaks["src"], "algorithmic_bytes": ab[dom],
                      "kernel_ms": stage_ms[dom],
                      "step_frac": ab["total"] * value / 1e9 / peaks["hbm_gbs"]},
+        # SURVEY 8(d) secondary unit: binned (pixel, list entry) evaluations per
+        # second (256 pixels per tile-list entry at tile 16), plus the ncu L1/tex
+        # hit rate and warp execution efficiency of the dominant kernel
+        "secondary": {"pair_evals_per_s": 256.0 * K16 * value, "unit": "pairs/s",
+                      "ncu": {k: (ncu_summary(KNAME[dom]) or {}).get(k)
+                              for k in ("l1tex_hit_pct", "warp_exec_efficiency_threads",
+                                        "fp64_pipe_pct", "warps_active_pct")}},
         "stage_ms": stage_ms,
         "e2e": {"value": 1e3 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": n * 8 * 8,
                 "d2h_bytes_per_step": n * 8 * 8 + nb * 3 * 8},

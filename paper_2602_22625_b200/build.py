@@ -45,6 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         obj = LIB.parent / (Path(s).stem + ".o")
         cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-I", str(ROOT / "include"), "-c", str(CSRC / s), "-o", str(obj)]
+        # diagnostics only: extra -D switches for A/B builds (e.g. -DPF_NBUF=3)
+        cmd += os.environ.get("PF_NVCC_DEFS", "").split()
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)

@@ -25,7 +25,9 @@ lib = nat.load()
 lib.pf_step_prof_dump.restype = C.c_int
 buf = np.zeros((148 * 32, 6), dtype=np.uint64)
 n = lib.pf_step_prof_dump(buf.ctypes.data_as(C.c_void_p), 148 * 32)
-d = buf[:n].astype(np.float64)
+buf = buf[:n][buf[:n, 3] > 0]  # padding warps leave their slot empty
+n = len(buf)
+d = buf.astype(np.float64)
 kind = buf[:n, 5] & 1
 first = (buf[:n, 5] >> 1).astype(np.float64)
 prod = kind == 1
@@ -37,6 +39,13 @@ for name, m in (("consumer", cons), ("producer", prod)):
     print(f"{name}: wait {x[:, 0].mean() / 1965:.1f} us  work {x[:, 1].mean() / 1965:.1f} us  tiles {x[:, 2].mean():.2f}  "
           f"end spread {(x[:, 4].min() - t0) / 1e3:.1f}..{(x[:, 4].max() - t0) / 1e3:.1f} us  first wait {first[m].mean() / 1965:.1f} us")
 
+xe = (d[cons][:, 4] - t0) / 1e3
+xs = (d[cons][:, 3] - t0) / 1e3
+print("consumer end percentiles (us) p0/p10/p50/p90/p100:",
+      [round(float(np.percentile(xe, q)), 1) for q in (0, 10, 50, 90, 100)])
+print("consumer start percentiles (us):", [round(float(np.percentile(xs, q)), 1) for q in (0, 50, 100)])
+busy = d[cons][:, 1].sum() / 1965 / 1e0
+print(f"total consumer work {busy / 1e3:.1f} ms-warp; ideal span at {cons.sum()} warps {busy / cons.sum():.1f} us")
 nt = eng.comp.n_tiles
 tb = np.zeros((nt, 8), dtype=np.uint64)
 lib.pf_step_prof_tiles(tb.ctypes.data_as(C.c_void_p), nt)
