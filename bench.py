@@ -238,7 +238,9 @@ def run_ours(args) -> None:
     band = row_bands(nty, world)[rank]
     prof_steps = 20
     e2e_steps = max(10, args.steps // 2)
-    total = max(w.steps, args.warmup + args.steps + prof_steps + e2e_steps + 2)
+    loop_chunks = 10
+    total = max(w.steps, args.warmup + args.steps + prof_steps + e2e_steps + 2 +
+                loop_chunks * StepEngine.CHUNK + StepEngine.CHUNK)
     w.cfg.num_iterations = total
     eng = StepEngine(sc, w.cfg, w.loss, total, band=band,
                      allreduce=make_allreduce() if world > 1 else None, use_graph=True)
@@ -331,6 +333,22 @@ def run_ours(args) -> None:
     eng.check()
     eh.check()
 
+    # run_loop's own issue pattern (informative, not the headline): CHUNK-step
+    # graphs back to back, no L2 flush between steps
+    loop = None
+    if world == 1:
+        eng.run(StepEngine.CHUNK)  # captures the chunk graph
+        torch.cuda.synchronize()
+        l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0.record()
+        eng.run(loop_chunks * StepEngine.CHUNK)
+        l1.record()
+        torch.cuda.synchronize()
+        loop_ms = l0.elapsed_time(l1) / (loop_chunks * StepEngine.CHUNK)
+        loop = {"value": 1e3 / loop_ms, "unit": UNIT, "steps_per_graph": StepEngine.CHUNK,
+                "l2": "not flushed (back-to-back steps, as run_loop issues them)"}
+        eng.check()
+
     nodes = eng.kernels_per_step
     if rank != 0:
         if world > 1:
@@ -362,6 +380,7 @@ def run_ours(args) -> None:
                       "ncu": {k: (ncu_summary(KNAME[dom]) or {}).get(k)
                               for k in ("l1tex_hit_pct", "warp_exec_efficiency_threads",
                                         "fp64_pipe_pct", "warps_active_pct")}},
+        "run_loop": loop,
         "stage_ms": stage_ms,
         "e2e": {"value": 1e3 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": n * 8 * 8,
                 "d2h_bytes_per_step": n * 8 * 8 + nb * 3 * 8},

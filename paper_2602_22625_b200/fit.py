@@ -458,9 +458,34 @@ class StepEngine:
                 self.capture()  # step 0 ran eagerly (warm-up); later steps replay
         self.done += 1
 
+    # steps per multi-step graph (run()): consecutive steps chained by
+    # programmatic (PDL) edges instead of one graph launch per step
+    CHUNK = 8
+
+    def capture_chunk(self) -> None:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(self.CHUNK):
+                self.launch_step()
+        self.chunk_graph = g
+
     def run(self, k: int, rng=None) -> None:
-        for _ in range(k):
-            self.step(rng)
+        """k steps.  Without a per-step host input (noise background) the steps go
+        out as CHUNK-step graph replays once the single-step graph exists; the
+        device iteration counter indexes the lr / bias-correction tables, so the
+        result is identical to k single steps (test_chunked_run_equals_steps)."""
+        chunked = self.use_graph and not self.noise_bg and self.allreduce is None
+        while k > 0:
+            if chunked and self.graph is not None and k >= self.CHUNK and \
+                    self.done + self.CHUNK <= self.total:
+                if getattr(self, "chunk_graph", None) is None:
+                    self.capture_chunk()
+                self.chunk_graph.replay()
+                self.done += self.CHUNK
+                k -= self.CHUNK
+            else:
+                self.step(rng)
+                k -= 1
 
     # host views (synchronising)
     def check(self) -> None:

@@ -108,6 +108,23 @@ def test_graph_replay_equals_eager(torch_cuda):
     np.testing.assert_allclose(a.params_host(), b.params_host(), rtol=1e-9, atol=1e-12)
 
 
+def test_chunked_run_equals_steps(torch_cuda):
+    """run() with multi-step graphs (CHUNK steps per replay) == single-step replays."""
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.fit import StepEngine
+
+    w = synth.make_workload("c1")
+    w.cfg.num_iterations = 21
+    a = StepEngine(w.scene, w.cfg, w.loss, 21, use_graph=True)
+    b = StepEngine(w.scene, w.cfg, w.loss, 21, use_graph=True)
+    a.run(21)  # 1 eager + 2 chunks of 8 + 4 single replays
+    for _ in range(21):
+        b.step()
+    np.testing.assert_array_equal(a.params_host(), b.params_host())
+    assert [h.loss for h in a.history()] == [h.loss for h in b.history()]
+    assert [h.lr for h in a.history()] == [h.lr for h in b.history()]
+
+
 def test_host_io_zero_copy_matches_device(torch_cuda):
     """host_io engine (parameters + loss partials in pinned host memory, read and
     written by the kernels directly) == device-resident engine, including a host
