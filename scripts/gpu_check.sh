@@ -2,7 +2,7 @@
 # One GPU round: build, smoke, gpu tests, bench, ncu launch list + full capture of the top kernels.
 set -u
 mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 900 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/pytest_gpu.log 2>&1
 tail -3 gpurun_out/pytest_gpu.log
 timeout 300 python bench.py --steps 100 --warmup 5 > gpurun_out/bench.log 2>&1
