@@ -137,6 +137,9 @@ int pf_preprocess(const double* params, int n, double alpha_max, double mu_blend
  *              HistoryEntry loss of the iteration (fit.py:502-505), or NULL
  *   last_part  [pf_adam_blocks(n)][3]: the same sums of the latest step only (a
  *              fixed address a per-step host read can use), or NULL
+ *   rec        the records of the next step, or NULL for Adam only (no records,
+ *              no rects: the caller runs pf_preprocess before the next pf_bin --
+ *              a host-driven step that re-reads the parameters every step)
  */
 int pf_adam_blocks(int n);
 int pf_adam_preprocess(double* params, double* grads, double* m, double* v, const uint8_t* frozen,

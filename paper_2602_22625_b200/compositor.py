@@ -213,8 +213,9 @@ class Compositor:
 
     def adam_preprocess(self, params, grads, m, v, *, frozen, gains, lr_table, bc1_table,
                         bc2_table, s_min, s_max, sums=None, part=None, hist_part=None,
-                        last_part=None, stream=None) -> None:
-        """K5+K1 fused: Adam on every parameter, then the next step's records + rects.
+                        last_part=None, records: bool = True, stream=None) -> None:
+        """K5+K1 fused: Adam on every parameter, then the next step's records + rects
+        (``records=False``: Adam only -- the caller re-runs preprocess() first).
         ``part``: pf_fit_step's loss partials (folded per block into ``hist_part``);
         ``sums``: already reduced loss sums (multi-rank path)."""
         g8 = (C.c_double * 8)(*[float(g) for g in gains])
@@ -226,7 +227,8 @@ class Compositor:
                 self.n_part if part is not None else 0, nat.ptr(hist_part), nat.ptr(last_part),
                 self.n,
                 self.alpha_max, self.mu_blend, self.padding, self.W, self.H, self.tile,
-                self.band.ty_begin, self.band.ty_end, self.capacity, self.rec.data_ptr(),
+                self.band.ty_begin, self.band.ty_end, self.capacity,
+                self.rec.data_ptr() if records else None,
                 self.scratch.data_ptr(), self.scratch_bytes, _stream_handle(stream)),
             "pf_adam_preprocess")
         self.launches += 1

@@ -58,6 +58,7 @@ struct PreArgs {
   RecG* recg;
   RecC* recc;
   RecS* recs;
+  bool records;  // write records + rects (false: Adam only)
   BinScratch s;
   AdamPart ad;
   unsigned long long* tl;  // diagnostics timeline or NULL
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
   const bool live = i < a.n;
   // static structure: one 48-byte record, independent of the parameter loads
   PrimInfo pi{2, 2, 0, 0, 1.0, 1.0, 0, 0, 0, 0};
-  if (live) {
+  if (live && a.records) {
     const int4* src = reinterpret_cast<const int4*>(a.s.pinfo + i);
     const int4 w0 = __ldg(src), w1 = __ldg(src + 1), w2 = __ldg(src + 2);
     pi.wt = w0.x; pi.ht = w0.y; pi.base = w0.z; pi.pbase = w0.w;
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
     pdl_trigger();
   }
   if (ADAM) tl_mark(a.tl, 5, 1);
+  if (a.records) {
   // gather the primitive's 8 parameters from its lane group
   const double x = __shfl_sync(kFull, pc, gb + 0), y = __shfl_sync(kFull, pc, gb + 1);
   const double s = __shfl_sync(kFull, pc, gb + 2), rot = __shfl_sync(kFull, pc, gb + 3);
@@ -285,6 +287,7 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
       a.s.rect[pi.zrank] = rc;
     }
   }
+  }  // a.records
 
   if (ADAM) {
     // this block's loss sums of the step (fixed-order fold of its chunk of
@@ -616,6 +619,7 @@ static int fill_pre_args(PreArgs& a, double* params, int n, double alpha_max, do
   a.recg = (RecG*)((char*)rec + sizeof(RecF) * (size_t)n);
   a.recc = (RecC*)((char*)rec + (sizeof(RecF) + sizeof(RecG)) * (size_t)n);
   a.recs = (RecS*)((char*)rec + (sizeof(RecF) + sizeof(RecG) + sizeof(RecC)) * (size_t)n);
+  a.records = true;
   a.s = carve(scratch, n, capacity);
   a.ad = AdamPart{};
   a.tl = pf_timeline_ptr();
@@ -712,9 +716,13 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
                                   int ty_end, int capacity, void* rec, void* scratch,
                                   size_t scratch_bytes, void* stream) {
   PreArgs a;
+  // rec == NULL: Adam only (no records / rects; the caller runs pf_preprocess
+  // before the next pf_bin, e.g. a host-driven step that re-reads the parameters)
+  static char dummy_rec[16];
   const int rc = fill_pre_args(a, params, n, alpha_max, mu_blend, padding, W, H, tile, ty_begin,
-                               ty_end, capacity, rec, scratch, scratch_bytes);
+                               ty_end, capacity, rec ? rec : dummy_rec, scratch, scratch_bytes);
   if (rc != PF_OK) return rc;
+  a.records = rec != nullptr;
   if (!lr_table || !bc1_table || !bc2_table || (n > 0 && (!grads || !m || !v)))
     return PF_ERR_ARG;
   if (part && n_part < 0) return PF_ERR_ARG;

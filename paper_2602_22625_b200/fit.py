@@ -360,7 +360,8 @@ class StepEngine:
     #   [K2 bin] -> [K3 forward + loss] -> [K4 backward]
     #   -> (allreduce) -> [K5+K1 Adam + next step's records/offsets]
     # (the very first step is preceded by a stand-alone K1, see step()).
-    def launch_step(self, mark: Callable[[str], None] | None = None) -> None:
+    def launch_step(self, mark: Callable[[str], None] | None = None,
+                    records: bool = True) -> None:
         c = self.comp
         mark = mark or (lambda name: None)
         c.bin()
@@ -389,7 +390,7 @@ class StepEngine:
                           bc2_table=self.bc2_table, s_min=self.cfg.scale_min,
                           s_max=self.cfg.scale_max, sums=None if fold_in_adam else self.sums,
                           part=c.part if fold_in_adam else None, hist_part=self.hist_part,
-                          last_part=self.last_part)
+                          last_part=self.last_part, records=records)
         mark("adam_preprocess")
 
     def refresh(self) -> None:
@@ -431,7 +432,8 @@ class StepEngine:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             self.refresh()
-            self.launch_step()
+            # the next replay re-reads the parameters (refresh): Adam only here
+            self.launch_step(records=False)
         self.host_graph = g
 
     def host_step(self) -> None:
