@@ -279,9 +279,12 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
       int4 rc = make_int4(0, 1, i, 0);
       // NaN-safe: every comparison with NaN is false -> treated as empty
       if (lo_x <= hi_x && lo_y <= hi_y) {
-        const int tx0 = (int)lo_x / a.tile, tx1 = (int)hi_x / a.tile;
-        const int ty0 = max((int)lo_y / a.tile, a.ty_begin);
-        const int ty1 = min((int)hi_y / a.tile, a.ty_end - 1);
+        // (tile 16, the fit step's, as a shift: the operands are >= 0)
+        const bool t16 = a.tile == 16;
+        const int tx0 = t16 ? (int)lo_x >> 4 : (int)lo_x / a.tile;
+        const int tx1 = t16 ? (int)hi_x >> 4 : (int)hi_x / a.tile;
+        const int ty0 = max(t16 ? (int)lo_y >> 4 : (int)lo_y / a.tile, a.ty_begin);
+        const int ty1 = min(t16 ? (int)hi_y >> 4 : (int)hi_y / a.tile, a.ty_end - 1);
         if (ty0 <= ty1) rc = make_int4(tx0 | (tx1 << 16), ty0, i, ty1);
       }
       a.s.rect[pi.zrank] = rc;

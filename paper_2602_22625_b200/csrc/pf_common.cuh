@@ -149,11 +149,13 @@ __device__ __forceinline__ SavedView unpack_saved(const SavedEnt& s) {
 }
 static_assert(sizeof(SavedEnt) == 16, "SavedEnt must be 16 bytes");
 
-// Stable two-branch logistic, _kernels.py:27-32.
+// Stable two-branch logistic, _kernels.py:27-32, without the branch: both arms
+// evaluate exp(-|x|) (exp(-x) for x >= 0, exp(x) below) and divide by 1 + e, so
+// one exp and one division give the reference's value for every x (NaN, +-0,
+// +-inf included) and divergent lanes do not run both arms.
 __device__ __forceinline__ double sigmoid(double x) {
-  if (x >= 0.0) return 1.0 / (1.0 + exp(-x));
-  double e = exp(x);
-  return e / (1.0 + e);
+  const double e = exp(-fabs(x));
+  return (x >= 0.0 ? 1.0 : e) / (1.0 + e);
 }
 
 // a / b given inv = RN(1/b): Markstein correction step.  The result is exact

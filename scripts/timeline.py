@@ -15,7 +15,11 @@ from paper_2602_22625_b200.fit import StepEngine
 
 w = synth.make_workload(sys.argv[1] if len(sys.argv) > 1 else "c3")
 w.cfg.num_iterations = 60
-eng = StepEngine(w.scene, w.cfg, w.loss, 60, use_graph=True)
+hostio = "hostio" in sys.argv[2:]
+eng = StepEngine(w.scene, w.cfg, w.loss, 60, use_graph=True, host_io=hostio)
+if hostio:  # the e2e graph: refresh from host parameters, bin, step, Adam only
+    eng.run(2)
+    eng.capture_host_io_step()
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 lib = nat.load()
 names = {0: "k_bin_rows", 1: "k_step", 2: "k_prim<adam>", 3: "k_prim<pre>", 4: " .adam done",
@@ -27,7 +31,7 @@ for rep in range(12):
     lib.pf_timeline_reset()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    eng.step()
+    eng.host_step() if hostio else eng.step()
     e1.record()
     torch.cuda.synchronize()
     buf = np.zeros(64, dtype=np.uint64)
