@@ -298,14 +298,18 @@ class StepEngine:
         # parameters / write the updated ones and the loss partials through it
         # directly (zero-copy over the host link): a host-driven step needs no
         # copy nodes (see capture_host_io_step)
+        # (host_io: two loss-partial slots, alternating between host steps, so a
+        # step's loss can be read while the next step runs)
         self.host_io = bool(host_io)
+        nb3 = self.adam_blocks * 3
         if self.host_io:
-            self.io = torch.zeros(n * 8 + self.adam_blocks * 3, dtype=torch.float64).pin_memory()
+            self.io = torch.zeros(n * 8 + 2 * nb3, dtype=torch.float64).pin_memory()
         else:
-            self.io = torch.zeros(n * 8 + self.adam_blocks * 3, dtype=torch.float64, device=dev)
+            self.io = torch.zeros(n * 8 + nb3, dtype=torch.float64, device=dev)
         self.params = self.io[: n * 8].view(n, 8)
         self.params.copy_(torch.from_numpy(vec.reshape(n, 8).copy()))
-        self.last_part = self.io[n * 8 :]
+        self.last_part = self.io[n * 8 : n * 8 + nb3]
+        self.loss_slots = [self.last_part] + ([self.io[n * 8 + nb3 :]] if self.host_io else [])
         self.m = torch.from_numpy(np.asarray(self.state.m, dtype=np.float64).copy()).to(dev)
         self.v = torch.from_numpy(np.asarray(self.state.v, dtype=np.float64).copy()).to(dev)
         self.frozen = torch.from_numpy(np.asarray(self.state.frozen, dtype=bool).astype(np.uint8)).to(dev)
@@ -429,18 +433,45 @@ class StepEngine:
             raise RuntimeError("capture_host_io_step needs StepEngine(host_io=True)")
         if self.graph is None and self.done == 0:
             raise RuntimeError("run one step() first (eager warm-up + capture)")
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self.refresh()
-            # the next replay re-reads the parameters (refresh): Adam only here
-            self.launch_step(records=False)
-        self.host_graph = g
+        graphs = []
+        keep = self.last_part
+        for slot in self.loss_slots:  # one graph per loss slot
+            self.last_part = slot
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.refresh()
+                # the next replay re-reads the parameters (refresh): Adam only here
+                self.launch_step(records=False)
+            graphs.append(g)
+        self.last_part = keep
+        self.host_graphs = graphs
+        self.host_graph = graphs[0]
+        self.host_events = [torch.cuda.Event() for _ in graphs]
+        self.host_issued = []  # (iteration, slot) of the host steps in flight / done
 
     def host_step(self) -> None:
+        """Enqueue one host-driven step (asynchronous).  host_io engines alternate
+        two graphs / loss slots; read a step's loss with host_loss_part(), at most
+        one step behind the newest."""
         if self.done >= self.total:
             raise ValueError(f"iteration {self.done} outside [0, {self.total})")
-        self.host_graph.replay()
+        if self.host_io and getattr(self, "host_graphs", None):
+            slot = len(self.host_issued) % len(self.host_graphs)
+            self.host_graphs[slot].replay()
+            self.host_events[slot].record()
+            self.host_issued.append((self.done, slot))
+        else:
+            self.host_graph.replay()
         self.done += 1
+
+    def host_loss_part(self, k: int = -1) -> np.ndarray:
+        """Loss partials [adam_blocks][3] of host step k (default: the newest),
+        after waiting for that step; valid for the two newest host steps."""
+        it, slot = self.host_issued[k]
+        if len(self.host_issued) - (k % len(self.host_issued)) > len(self.host_graphs):
+            raise ValueError(f"host step {k} has been overwritten")
+        self.host_events[slot].synchronize()
+        return self.loss_slots[slot].numpy().reshape(-1, 3)
 
     def step(self, rng: np.random.Generator | None = None) -> None:
         if self.done >= self.total:

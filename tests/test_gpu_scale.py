@@ -151,7 +151,9 @@ def test_host_io_zero_copy_matches_device(torch_cuda):
         b.host_step()
         torch.cuda.synchronize()
     np.testing.assert_array_equal(a.params_host(), b.io.numpy()[: n * 8])
-    np.testing.assert_array_equal(a.last_part.cpu().numpy(), b.io.numpy()[n * 8 :])
+    np.testing.assert_array_equal(a.last_part.cpu().numpy().reshape(-1, 3), b.host_loss_part())
+    np.testing.assert_array_equal(a.hist_part.cpu().numpy().reshape(8, -1, 3)[4],
+                                  b.host_loss_part(-2))
     assert [h.loss for h in a.history()] == [h.loss for h in b.history()]
 
 
