@@ -321,3 +321,57 @@ def test_fused_step_deep_stack_spill(torch_cuda, oracle):
     g_ref = oracle.backward(pk, sv, dI, None)
     ok, err = grad_close(g, g_ref)
     assert ok, f"spill grad rel err {err}"
+
+
+def _edge_scene(kind: str):
+    """Edge scenes for the fused step: primitives off the canvas and one covering
+    all of it; a canvas smaller than one tile; a single primitive."""
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.fit import LossSpec
+    from paper_2602_22625_b200.scene import PrimitiveParams, Scene
+
+    w = synth.make_workload("c1")
+    rng = np.random.default_rng(19)
+    if kind == "offcanvas":
+        sc = w.scene
+        for i, p in enumerate(sc.primitives):
+            if i % 3 == 0:
+                p.x = -400.0 - 10.0 * i  # far outside (empty rect)
+            elif i % 3 == 1:
+                p.y = 256.0 + p.scale * 0.5  # straddling the bottom edge
+        sc.primitives[5].scale = 200.0  # covers the whole canvas
+        sc.primitives[5].opacity_logit = -1.0
+        return sc, w.cfg, w.loss
+    W, H, n = (13, 9, 6) if kind == "tiny" else (40, 36, 1)
+    prims = [PrimitiveParams(x=float(rng.uniform(0, W)), y=float(rng.uniform(0, H)),
+                             scale=float(rng.uniform(3, 9)), rotation=float(rng.uniform(-3, 3)),
+                             opacity_logit=float(rng.uniform(-1, 2)),
+                             color_logits=tuple(float(v) for v in rng.uniform(-2, 2, 3)), z=i)
+             for i in range(n)]
+    sc = Scene(prims, w.scene.templates, W, H, background=(0.3, 0.6, 0.9))
+    target = rng.random((H, W, 3))
+    return sc, w.cfg, LossSpec(kind="mse", target=target)
+
+
+@pytest.mark.parametrize("kind", ["offcanvas", "tiny", "single"])
+def test_fused_step_edge_scenes(torch_cuda, oracle, kind):
+    from paper_2602_22625_b200.fit import StepEngine, effective_padding
+
+    sc, cfg, loss = _edge_scene(kind)
+    eng = StepEngine(sc, cfg, loss, 1, use_graph=False)
+    g, sums, color, alpha = _fused_grads(eng)
+    pk = oracle.Packed(sc)
+    off, idx = oracle.bin_tiles(pk, 32, effective_padding(cfg))
+    img, a_ref, sv = oracle.render_forward(pk, off, idx, 32, oracle.background(sc), True,
+                                           cfg.eps_skip)
+    ok, err = fwd_close(color, img)
+    assert ok, f"{kind} colour rel err {err}"
+    ok, err = fwd_close(alpha, a_ref)
+    assert ok, f"{kind} alpha rel err {err}"
+    diff = img - loss.target
+    np.testing.assert_allclose(sums[0], np.sum(diff**2), rtol=1e-5)
+    g_ref = oracle.backward(pk, sv, 2.0 * diff / diff.size, None)
+    ok, err = grad_close(g, g_ref)
+    assert ok, f"{kind} grad rel err {err}"
+    if kind == "offcanvas":
+        assert not g[::3].any()  # empty rects: exactly zero gradient
