@@ -169,6 +169,12 @@ int pf_adam_preprocess(double* params, double* grads, double* m, double* v, cons
  *            list length stands in until a first fit step).
  *            Order inside a class is not deterministic; it only steers scheduling.
  */
+/* Kernels one pf_bin call launches for this shape (1, or 4 on the two-level
+ * path for many primitives x many rows: per-chunk row counts, their prefix over
+ * chunks, a stable scatter into per-row lists, then the column pass); -1 on bad
+ * arguments. */
+int pf_bin_launches(int n, int W, int H, int tile, int ty_begin, int ty_end);
+
 int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity,
            void* scratch, size_t scratch_bytes,
            int32_t* bin_off, int32_t* bin_idx, int32_t* status,

@@ -37,6 +37,7 @@ SIGNATURES: dict[str, tuple] = {
     "pf_record_bytes": (_Z, []),
     "pf_render_tile": (_I, []),
     "pf_bin_scratch_bytes": (_Z, [_I, _I, _I]),
+    "pf_bin_launches": (_I, [_I, _I, _I, _I, _I, _I]),
     "pf_saved_capacity": (C.c_longlong, [_I]),
     "pf_saved_bytes": (_Z, [_I]),
     "pf_preprocess": (_I, [_P, _I, _D, _D, _D, _I, _I, _I, _I, _I, _I, _P, _P, _Z, _P]),

@@ -246,7 +246,8 @@ class Compositor:
                             self.bin_idx.data_ptr(), self.status.data_ptr(),
                             nat.ptr(self.tile_classes), _stream_handle(stream)),
             "pf_bin")
-        self.launches += 1
+        self.launches += int(self.lib.pf_bin_launches(self.n, self.W, self.H, self.tile,
+                                                      self.band.ty_begin, self.band.ty_end))
 
     def check_overflow(self) -> int:
         """Synchronising read of K; raises BinOverflow when capacity was exceeded."""

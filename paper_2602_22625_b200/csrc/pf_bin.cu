@@ -336,10 +336,164 @@ struct RowArgs {
   int32_t* status;
   int32_t* classes;  // optional tile cost classes (see kTileClasses), or NULL
   int n_tiles;
+  int prebuilt;      // row lists come from k_row_scatter (two-level path)
   unsigned long long* tl;
 };
 
 constexpr int kRowThreads = 1024;
+
+// Two-level path, for many primitives x many rows (one-level K2 re-reads every
+// rect once per (row, column block)).  Pass 1 (k_row_counts): per chunk of
+// kRowChunk z positions, the (row pairs, tile entries) counts of every row.
+// Pass 2 (k_row_offsets, one block): per row, the exclusive prefix over chunks
+// (in place) and the row's list start / length / entries before it (rowinfo).
+// Pass 3 (k_row_scatter): every chunk writes its (primitive, column span) pairs
+// into the per-row lists, z order kept (chunk, then warp, then lane order).
+// k_bin_rows then starts from the prebuilt row lists instead of scanning all
+// rects.
+__global__ void __launch_bounds__(kRowChunk) k_row_counts(RowArgs a) {
+  extern __shared__ int2 sc[];  // [n_rows]
+  const int tid = threadIdx.x;
+  tl_mark(a.tl, 11, 0);
+  for (int r = tid; r < a.n_rows; r += kRowChunk) sc[r] = make_int2(0, 0);
+  pdl_wait();  // rects come from K1
+  tl_mark(a.tl, 11, 1);
+  pdl_trigger();
+  __syncthreads();
+  const int zp = blockIdx.x * kRowChunk + tid;
+  if (zp < a.n) {
+    const int4 rc = a.s.rect[zp];
+    if (rc.y <= rc.w) {
+      const int span = (rc.x >> 16) - (rc.x & 0xffff) + 1;
+      for (int ty = rc.y; ty <= rc.w; ++ty) {
+        atomicAdd(&sc[ty - a.ty_begin].x, 1);
+        atomicAdd(&sc[ty - a.ty_begin].y, span);
+      }
+    }
+  }
+  __syncthreads();
+  for (int r = tid; r < a.n_rows; r += kRowChunk)
+    a.s.rowcnt[(size_t)blockIdx.x * a.n_rows + r] = sc[r];
+  tl_mark(a.tl, 11, 3);
+}
+
+// One warp per row (4 per block): the exclusive prefix over chunks of the
+// row's pair counts, in place, and the row's totals (pairs, tile entries) in
+// rowinfo[r].  Row offsets (a scan over rows) are left to the consumers.
+__global__ void __launch_bounds__(128) k_row_offsets(RowArgs a, int nch) {
+  const int lane = threadIdx.x & 31, r = blockIdx.x * 4 + (threadIdx.x >> 5);
+  tl_mark(a.tl, 13, 0);
+  pdl_wait();  // the count matrix
+  tl_mark(a.tl, 13, 1);
+  pdl_trigger();
+  if (r >= a.n_rows) return;
+  int carry = 0, ent = 0;
+  constexpr int kB = 8;  // chunks per lane per batch: all loads first
+  for (int c0 = 0; c0 < nch; c0 += 32 * kB) {
+    int2 v[kB];
+#pragma unroll
+    for (int i = 0; i < kB; ++i) {
+      const int c = c0 + i * 32 + lane;
+      v[i] = c < nch ? a.s.rowcnt[(size_t)c * a.n_rows + r] : make_int2(0, 0);
+    }
+#pragma unroll
+    for (int i = 0; i < kB; ++i) {
+      const int c = c0 + i * 32 + lane;
+      int x = v[i].x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+      }
+      if (c < nch) a.s.rowcnt[(size_t)c * a.n_rows + r].x = carry + x - v[i].x;
+      carry += __shfl_sync(kFull, x, 31);
+      ent += v[i].y;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ent += __shfl_xor_sync(kFull, ent, o);
+  if (lane == 0) a.s.rowinfo[r] = make_int4(carry, ent, 0, 0);
+  tl_mark(a.tl, 13, 3);
+}
+
+__global__ void __launch_bounds__(kRowChunk) k_row_scatter(RowArgs a) {
+  constexpr int kW = kRowChunk / 32;
+  extern __shared__ int2 smem_rs[];
+  int2* spans = smem_rs;                                    // [kRowChunk] (ty0, ty1)
+  int* wcnt = reinterpret_cast<int*>(spans + kRowChunk);    // [kW warps][n_rows]: counts, offsets
+  int* roff = wcnt + kW * a.n_rows;                         // [n_rows] row start + earlier chunks
+  __shared__ int ws[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int chunk = blockIdx.x;
+  for (int k = tid; k < kW * a.n_rows; k += kRowChunk) wcnt[k] = 0;
+  const int zp = chunk * kRowChunk + tid;
+  tl_mark(a.tl, 12, 0);
+  pdl_wait();  // offsets of k_row_offsets (and, through it, the rects of K1)
+  tl_mark(a.tl, 12, 1);
+  pdl_trigger();
+  // every load up front (independent): rect, the rows' totals and chunk prefixes
+  const int4 rc = zp < a.n ? a.s.rect[zp] : make_int4(0, 1, 0, 0);
+  constexpr int kRP = 1024 / kRowChunk;  // rows per thread (n_rows <= 1024), contiguous
+  int tot[kRP], pre[kRP];
+#pragma unroll
+  for (int q = 0; q < kRP; ++q) {
+    const int r = tid * kRP + q;
+    tot[q] = r < a.n_rows ? a.s.rowinfo[r].x : 0;
+    pre[q] = r < a.n_rows ? a.s.rowcnt[(size_t)chunk * a.n_rows + r].x : 0;
+  }
+  const int y0 = rc.y - a.ty_begin, y1 = rc.w - a.ty_begin;  // empty: y0 > y1
+  spans[tid] = make_int2(y0, y1);
+  int local = 0;
+#pragma unroll
+  for (int q = 0; q < kRP; ++q) local += tot[q];
+  int rows_total;
+  int acc = block_excl_scan(local, ws, &rows_total);
+#pragma unroll
+  for (int q = 0; q < kRP; ++q) {
+    const int r = tid * kRP + q;
+    if (r < a.n_rows) roff[r] = acc + pre[q];
+    acc += tot[q];
+  }
+  const bool fits = rows_total <= a.cap;  // else K > cap: k_bin_rows flags it
+  __syncthreads();
+  // this warp's pairs per row: lane L's rank in row r = covering lanes l < L
+  const int wb = warp * 32;
+  for (int ty = y0; ty <= y1; ++ty) {
+    int before = 0, after = 0;
+    for (int l = 0; l < 32; ++l) {
+      const int2 sp = spans[wb + l];
+      const int cov = sp.x <= ty && ty <= sp.y;
+      before += (l < lane) & cov;
+      after += (l > lane) & cov;
+    }
+    if (after == 0) wcnt[warp * a.n_rows + ty] = before + 1;  // the row's last lane
+  }
+  __syncthreads();
+  // per row: offsets of the warps' pairs (row start + earlier chunks + earlier warps)
+  for (int r = tid; r < a.n_rows; r += kRowChunk) {
+    int o = roff[r];
+#pragma unroll
+    for (int w = 0; w < kW; ++w) {
+      const int t = wcnt[w * a.n_rows + r];
+      wcnt[w * a.n_rows + r] = o;
+      o += t;
+    }
+  }
+  __syncthreads();
+  // scatter: (primitive, column span) at row start + offsets + lane rank
+  if (fits) {
+    for (int ty = y0; ty <= y1; ++ty) {
+      int before = 0;
+      for (int l = 0; l < lane; ++l) {
+        const int2 sp = spans[wb + l];
+        before += sp.x <= ty && ty <= sp.y;
+      }
+      a.s.rowlist[wcnt[warp * a.n_rows + ty] + before] = make_int2(rc.z, rc.x);
+    }
+  }
+  tl_mark(a.tl, 12, 3);
+}
+
 constexpr int kRowCache = 8;  // rects per thread kept in registers between the passes
 
 // K2: blocks (r, cb): tile row r, column block cb of gridDim.y.  See the file
@@ -353,6 +507,7 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
   __shared__ int4 ws4[32];
   __shared__ int s_rl, s_base, s_rbase;
   __shared__ int s_ccnt[kTileClasses], s_cbase[kTileClasses];
+  __shared__ int2 wfifo[32 * 64];  // (c) per-warp FIFO of wide column blocks
   int* col = reinterpret_cast<int*>(rsm + a.smem_list);
   int* ccls = col + a.ntx;  // per-column tile class | rank within the block << 8
   int* ccnt = ccls + a.ntx;  // per-column tile list length
@@ -395,26 +550,48 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
       below_rows += rows;
     }
   };
-  if (CACHE) {
-    // all loads first (independent), then the tallies
-#pragma unroll
-    for (int k = 0; k < kRowCache; ++k) rcache[k] = j0 + k < j1 ? a.s.rect[j0 + k] : kEmpty;
-#pragma unroll
-    for (int k = 0; k < kRowCache; ++k) tally(rcache[k]);
-  } else {
-    // long chunks: batches of kRowCache independent loads, then the tallies
-    for (int jb = j0; jb < j1; jb += kRowCache) {
-      int4 rb[kRowCache];
-#pragma unroll
-      for (int k = 0; k < kRowCache; ++k) rb[k] = jb + k < j1 ? a.s.rect[jb + k] : kEmpty;
-#pragma unroll
-      for (int k = 0; k < kRowCache; ++k) tally(rb[k]);
+  int tot, base, rbase, K, pos = 0;
+  if (a.prebuilt) {
+    // two-level path: the row lists come from k_row_scatter; this row's list
+    // start / entries before it / K from a scan of the rows' totals
+    const int4 ri = tid < a.n_rows ? a.s.rowinfo[tid] : make_int4(0, 0, 0, 0);
+    int4 tot4;
+    const int4 ex = block_excl_scan4(make_int4(ri.x, ri.y, 0, 0), ws4, &tot4);
+    if (tid == r) {
+      s_rl = ri.x;
+      s_rbase = ex.x;
+      s_base = ex.y;
     }
+    __syncthreads();
+    tot = s_rl;
+    rbase = s_rbase;
+    base = s_base;
+    K = tot4.y;
+  } else {
+    if (CACHE) {
+      // all loads first (independent), then the tallies
+#pragma unroll
+      for (int k = 0; k < kRowCache; ++k) rcache[k] = j0 + k < j1 ? a.s.rect[j0 + k] : kEmpty;
+#pragma unroll
+      for (int k = 0; k < kRowCache; ++k) tally(rcache[k]);
+    } else {
+      // long chunks: batches of kRowCache independent loads, then the tallies
+      for (int jb = j0; jb < j1; jb += kRowCache) {
+        int4 rb[kRowCache];
+#pragma unroll
+        for (int k = 0; k < kRowCache; ++k) rb[k] = jb + k < j1 ? a.s.rect[jb + k] : kEmpty;
+#pragma unroll
+        for (int k = 0; k < kRowCache; ++k) tally(rb[k]);
+      }
+    }
+    int4 tot4;
+    const int4 ex = block_excl_scan4(make_int4(cnt, below, below_rows, all), ws4, &tot4);
+    tot = tot4.x;
+    base = tot4.y;
+    rbase = tot4.z;
+    K = tot4.w;
+    pos = ex.x;
   }
-  int4 tot4;
-  const int4 ex = block_excl_scan4(make_int4(cnt, below, below_rows, all), ws4, &tot4);
-  const int tot = tot4.x, base = tot4.y, rbase = tot4.z, K = tot4.w;
-  int pos = ex.x;
   if (r == 0 && cb == 0 && tid == 0) {
     // every block knows K; block (0, 0) publishes it (TileBins.offsets[-1], overflow flag)
     a.bin_off[a.n_rows * a.ntx] = K;
@@ -442,7 +619,10 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
     if (spill_list) a.s.rowlist[rbase + pos] = e;  // rbase + pos < rows entries <= K <= cap
     ++pos;
   };
-  if (CACHE) {
+  if (a.prebuilt) {
+    if (tot <= a.smem_list)
+      for (int k = tid; k < tot; k += kRowThreads) rsm[k] = a.s.rowlist[rbase + k];
+  } else if (CACHE) {
 #pragma unroll
     for (int k = 0; k < kRowCache; ++k) {
       const int4 rc = rcache[k];
@@ -498,22 +678,83 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
     cbase_mine = s_ccnt[tid] ? atomicAdd(a.classes + tid, s_ccnt[tid]) : 0;
 
   tl_mark(a.tl, 10, 1);
-  // (c) one warp per column of this block: ordered ballot walk of the row list
+  // (c) ordered ballot walks of the row list.  Narrow column blocks: one warp
+  // per column.  Wide ones (more columns than warps): one warp per segment of
+  // w consecutive columns, which first compacts the entries meeting its
+  // segment (z order kept, 64-entry warp FIFO in shared memory), then writes
+  // them column by column -- the list is read once per segment, not per column.
   const int lane = tid & 31, warp = tid >> 5;
-  for (int c = cbeg + warp; c < cend; c += kRowThreads / 32) {
-    int out = col[c];
-    for (int b = 0; b < RL; b += 32) {
-      const int k = b + lane;
-      bool hit = false;
-      int j = 0;
-      if (k < RL) {
-        const int2 e = list[k];
-        j = e.x;
-        hit = (e.y & 0xffff) <= c && c <= (e.y >> 16);
+  const unsigned lt = (1u << lane) - 1u;
+  const int wseg = (cend - cbeg + 31) / 32;
+  if (wseg <= 1) {
+    for (int c = cbeg + warp; c < cend; c += kRowThreads / 32) {
+      int out = col[c];
+      for (int b = 0; b < RL; b += 32) {
+        const int k = b + lane;
+        bool hit = false;
+        int j = 0;
+        if (k < RL) {
+          const int2 e = list[k];
+          j = e.x;
+          hit = (e.y & 0xffff) <= c && c <= (e.y >> 16);
+        }
+        const unsigned ball = __ballot_sync(kFull, hit);
+        if (hit) a.bin_idx[out + __popc(ball & lt)] = j;
+        out += __popc(ball);
       }
-      const unsigned ball = __ballot_sync(kFull, hit);
-      if (hit) a.bin_idx[out + __popc(ball & ((1u << lane) - 1u))] = j;
-      out += __popc(ball);
+    }
+  } else {
+    int2* fifo = wfifo + warp * 64;
+    const int s0 = cbeg + warp * wseg, s1 = min(s0 + wseg, cend) - 1;
+    for (int q0 = s0; q0 <= s1; q0 += 32) {  // sub-segments of <= 32 columns (lane counters)
+      const int q1 = min(q0 + 31, s1);
+      int out = q0 + lane <= q1 ? col[q0 + lane] : 0;  // write position of column q0 + lane
+      auto drain = [&](int ne) {  // the first ne FIFO entries, column by column
+        int lo = 1, hi = 0, j = 0;
+        if (lane < ne) {
+          const int2 e = fifo[lane];
+          j = e.x;
+          lo = max(e.y & 0xffff, q0);
+          hi = min(e.y >> 16, q1);
+        }
+        const bool any = lo <= hi;
+        const unsigned cmin = __reduce_min_sync(kFull, any ? (unsigned)lo : 0xffffffffu);
+        const unsigned cmax = __reduce_max_sync(kFull, any ? (unsigned)hi : 0u);
+        for (int c = (int)cmin; c <= (int)cmax; ++c) {
+          const bool cov = lo <= c && c <= hi;
+          const unsigned m = __ballot_sync(kFull, cov);
+          if (m == 0u) continue;
+          const int at = __shfl_sync(kFull, out, c - q0);
+          if (cov) a.bin_idx[at + __popc(m & lt)] = j;
+          if (lane == c - q0) out += __popc(m);
+        }
+      };
+      int nb = 0;
+      for (int b = 0; b < RL; b += 32) {
+        const int k = b + lane;
+        int2 e = make_int2(0, 0);
+        bool meet = false;
+        if (k < RL) {
+          e = list[k];
+          meet = (e.y & 0xffff) <= q1 && (e.y >> 16) >= q0;
+        }
+        const unsigned m = __ballot_sync(kFull, meet);
+        if (meet) fifo[nb + __popc(m & lt)] = e;
+        nb += __popc(m);
+        __syncwarp();
+        if (nb >= 32) {
+          drain(32);
+          const int rem = nb - 32;
+          int2 t = make_int2(0, 0);
+          if (lane < rem) t = fifo[32 + lane];
+          __syncwarp();
+          if (lane < rem) fifo[lane] = t;
+          __syncwarp();
+          nb = rem;
+        }
+      }
+      if (nb > 0) drain(nb);
+      __syncwarp();
     }
   }
   if (a.classes) {
@@ -586,7 +827,7 @@ using namespace pf;
 
 extern "C" size_t pf_bin_scratch_bytes(int n, int n_tiles, int capacity) {
   if (n < 0 || n_tiles < 0 || capacity < 0) return 0;
-  return carve(nullptr, n, capacity).total;
+  return carve(nullptr, n, capacity, n_tiles).total;
 }
 
 static bool band_ok(int W, int H, int tile, int ty_begin, int ty_end, int* ntx, int* n_rows) {
@@ -749,6 +990,45 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
   return launch_prim(true, a, (cudaStream_t)stream);
 }
 
+static int sms_count() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+static int row_blocks(int n, int n_rows, int ntx, bool cache) {
+  // column blocks per row: as many as fit in one wave (1024-thread blocks, one
+  // per SM with the register cache), >= 16 columns each
+  const int ncb = (cache ? 1 : 2) * sms_count() / n_rows;
+  return max(1, min(ncb, ntx / 16));
+}
+
+// Two-level path when re-reading every rect per (row, column block) is the
+// cost: n x rows x column blocks above ~2M (c5 4K / 20k), or forced by
+// PF_BIN_TWO_LEVEL=0/1 (A/B and tests).
+static bool bin_two_level(int n, int n_rows, int ncb, size_t scat_smem) {
+  bool two = (size_t)n * (size_t)n_rows * (size_t)ncb > 2000000u;
+  if (const char* e = getenv("PF_BIN_TWO_LEVEL")) two = atoi(e) != 0;
+  return two && n > 0 && n_rows <= 1024 && scat_smem <= 200 * 1024;
+}
+
+static size_t scatter_smem(int n_rows) {
+  return sizeof(int) * (kRowChunk / 32 + 1) * (size_t)n_rows + sizeof(int2) * kRowChunk;
+}
+
+extern "C" int pf_bin_launches(int n, int W, int H, int tile, int ty_begin, int ty_end) {
+  int ntx, n_rows;
+  if (n < 0 || !band_ok(W, H, tile, ty_begin, ty_end, &ntx, &n_rows)) return -1;
+  if (n_rows == 0) return 0;
+  const bool cache = (n + kRowThreads - 1) / kRowThreads <= kRowCache;
+  const int ncb = row_blocks(n, n_rows, ntx, cache);
+  return bin_two_level(n, n_rows, ncb, scatter_smem(n_rows)) ? 4 : 1;
+}
+
 extern "C" int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity,
                       void* scratch, size_t scratch_bytes, int32_t* bin_off, int32_t* bin_idx,
                       int32_t* status, int32_t* tile_classes, void* stream) {
@@ -771,12 +1051,13 @@ extern "C" int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, i
   ra.n_rows = n_rows;
   ra.cap = capacity;
   ra.smem_list = kRowSmemList;
-  ra.s = carve(scratch, n, capacity);
+  ra.s = carve(scratch, n, capacity, n_rows * ntx);
   ra.bin_off = bin_off;
   ra.bin_idx = bin_idx;
   ra.status = status;
   ra.classes = tile_classes;
   ra.n_tiles = n_rows * ntx;
+  ra.prebuilt = 0;
   ra.tl = pf_timeline_ptr();
   const size_t smem = sizeof(int2) * kRowSmemList + 3 * sizeof(int) * (size_t)ntx;
   const bool cache = (n + kRowThreads - 1) / kRowThreads <= kRowCache;
@@ -787,16 +1068,24 @@ extern "C" int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, i
                          (int)(smem > 48 * 1024 ? smem : 48 * 1024));
     attr_smem[cache] = smem;
   }
-  // column blocks per row: as many as fit in one wave (1024-thread blocks, one
-  // per SM with the register cache), >= 16 columns each
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int ncb = row_blocks(n, n_rows, ntx, cache);
+  const size_t scat_smem = scatter_smem(n_rows);
+  if (bin_two_level(n, n_rows, ncb, scat_smem)) {
+    static size_t attr_scat = 0;
+    if (scat_smem > attr_scat) {
+      cudaFuncSetAttribute(k_row_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(scat_smem > 48 * 1024 ? scat_smem : 48 * 1024));
+      attr_scat = scat_smem;
+    }
+    const int chunks = div_up(n, kRowChunk);
+    int e = (int)launch_pdl2(k_row_counts, dim3(chunks), kRowChunk, sizeof(int2) * n_rows, st, ra);
+    if (e == 0) e = (int)launch_pdl2(k_row_offsets, dim3(div_up(n_rows, 4)), 128, 0, st, ra, chunks);
+    if (e == 0) e = (int)launch_pdl2(k_row_scatter, dim3(chunks), kRowChunk, scat_smem, st, ra);
+    if (e != 0) return e;
+    ra.prebuilt = 1;
+    // no rect re-reads left to spread: one wave of column blocks
+    ncb = max(1, min(sms_count() / n_rows, ntx / 16));
   }
-  int ncb = (cache ? 1 : 2) * sms / n_rows;
-  ncb = max(1, min(ncb, ntx / 16));
   return (int)launch_pdl2(kern, dim3(n_rows, ncb), kRowThreads, smem, st, ra);
 }
 

@@ -21,12 +21,17 @@ struct BinScratch {
   int2* rowlist;     // [capacity] per-row z-ordered lists: (z position, tx0 | tx1 << 16)
   uint32_t* done;    // [4] last-block ticket
   double* fold;      // [prim blocks][3] per-block loss-partial folds (pf_adam_preprocess)
+  // two-level binning (large n x rows; sized from n_tiles >= rows, 0 = absent)
+  int2* rowcnt;      // [row chunks][n_rows] per chunk of kRowChunk z positions: (pairs, entries)
+  int4* rowinfo;     // [n_rows] per row (row-list pairs, tile entries, 0, 0)
   size_t total;
 };
 
+constexpr int kRowChunk = 128;  // z positions per block of the two-level row pass
+
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-static inline BinScratch carve(void* base, int n, int cap) {
+static inline BinScratch carve(void* base, int n, int cap, int n_tiles = 0) {
   BinScratch s;
   char* p = (char*)base;
   size_t off = 0;
@@ -41,6 +46,10 @@ static inline BinScratch carve(void* base, int n, int cap) {
   s.rowlist = (int2*)take(sizeof(int2) * (size_t)cap);
   s.done = (uint32_t*)take(sizeof(uint32_t) * 4);
   s.fold = (double*)take(sizeof(double) * 3 * (size_t)((8 * (size_t)n + 255) / 256 + 1));
+  // (appended: the offsets above do not depend on n_tiles)
+  const size_t chunks = ((size_t)n + kRowChunk - 1) / kRowChunk;
+  s.rowcnt = (int2*)take(sizeof(int2) * chunks * (size_t)n_tiles);
+  s.rowinfo = (int4*)take(sizeof(int4) * ((size_t)n_tiles + 1));
   s.total = off;
   return s;
 }

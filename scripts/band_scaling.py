@@ -1,0 +1,72 @@
+"""Projected row-band scaling on ONE GPU: the step time of every band of an
+N-way row split, measured one band at a time (graph replay, L2 flushed), so the
+N-GPU step is max over bands + the gradient allreduce (not measurable here).
+
+    python scripts/band_scaling.py c5 1 2 4 8
+"""
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import numpy as np
+import torch
+
+from paper_2602_22625_b200 import synth
+from paper_2602_22625_b200.dist import row_bands, row_cost_from_bins
+from paper_2602_22625_b200.fit import StepEngine
+
+name = sys.argv[1]
+worlds = [int(v) for v in sys.argv[2:]] or [1, 2, 4, 8]
+w = synth.make_workload(name)
+H, W = w.scene.canvas_h, w.scene.canvas_w
+nty, ntx = -(-H // 16), -(-W // 16)
+flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+K, WARM = 20, 4
+w.cfg.num_iterations = K + WARM + 2
+
+
+def band_ms(band) -> float:
+    eng = StepEngine(w.scene, w.cfg, w.loss, K + WARM + 2, band=band, use_graph=True)
+    eng.run(WARM)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(K):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        eng.step()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    eng.check()
+    out = float(np.median(ts))
+    del eng
+    torch.cuda.empty_cache()
+    return out
+
+
+# full-canvas bins of the initial state for cost-balanced bands
+full = StepEngine(w.scene, w.cfg, w.loss, 2, use_graph=False)
+full.refresh()
+full.comp.bin()
+cost = row_cost_from_bins(full.comp.bin_off.cpu().numpy()[: nty * ntx + 1], ntx, nty)
+del full
+res = {"config": name, "n": w.scene.n, "canvas": [W, H], "grad_allreduce_bytes": 8 * (8 * w.scene.n + 4)}
+base = None
+for N in worlds:
+    for kind, rc in (("uniform", None), ("balanced", cost)):
+        if N == 1 and kind == "balanced":
+            continue
+        bands = row_bands(nty, N, rc)
+        ms = [band_ms(b) for b in bands]
+        if N == 1:
+            base = ms[0]
+        eff = base / (N * max(ms)) if base else None
+        res[f"N{N}_{kind}"] = {"band_ms": [round(m, 4) for m in ms], "max_ms": max(ms),
+                              "projected_eff_no_allreduce": eff}
+        print(f"N={N} {kind:8s} max {max(ms) * 1e3:8.1f} us  mean {np.mean(ms) * 1e3:8.1f} us  "
+              f"eff(no allreduce) {eff:.3f}", flush=True)
+Path("gpurun_out").mkdir(exist_ok=True)
+Path(f"gpurun_out/band_scaling_{name}.json").write_text(json.dumps(res, indent=1))

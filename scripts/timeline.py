@@ -16,7 +16,13 @@ from paper_2602_22625_b200.fit import StepEngine
 w = synth.make_workload(sys.argv[1] if len(sys.argv) > 1 else "c3")
 w.cfg.num_iterations = 60
 hostio = "hostio" in sys.argv[2:]
-eng = StepEngine(w.scene, w.cfg, w.loss, 60, use_graph=True, host_io=hostio)
+band = None
+for a in sys.argv[2:]:
+    if a.startswith("band="):  # band=N:r -- rank r of an N-way uniform row split
+        from paper_2602_22625_b200.dist import row_bands
+        N, r = (int(v) for v in a[5:].split(":"))
+        band = row_bands(-(-w.scene.canvas_h // 16), N)[r]
+eng = StepEngine(w.scene, w.cfg, w.loss, 60, use_graph=True, host_io=hostio, band=band)
 if hostio:  # the e2e graph: refresh from host parameters, bin, step, Adam only
     eng.run(2)
     eng.capture_host_io_step()
@@ -24,7 +30,7 @@ flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 lib = nat.load()
 names = {0: "k_bin_rows", 1: "k_step", 2: "k_prim<adam>", 3: "k_prim<pre>", 4: " .adam done",
          5: " .fold done", 6: " .records done", 7: " .ticket done", 8: " bin.scan done",
-         9: " bin.list done", 10: " bin.counts done"}
+         9: " bin.list done", 10: " bin.counts done", 11: "k_row_counts", 12: "k_row_scatter", 13: "k_row_offsets"}
 for rep in range(12):
     flush.zero_()
     torch.cuda.synchronize()
@@ -38,7 +44,7 @@ for rep in range(12):
     lib.pf_timeline_dump(buf.ctypes.data_as(C.c_void_p))
 if True:
     b = buf.reshape(16, 4).astype(np.float64)
-    valid = [k for k in range(11) if b[k, 3] > 0 or b[k, 2] > 0]
+    valid = [k for k in range(14) if b[k, 3] > 0 or b[k, 2] > 0]
     t0 = min(b[k, 0] for k in valid if b[k, 3] > 0)
     print(f"step (events) {e0.elapsed_time(e1) * 1e3:.1f} us; kernels (start / wait-done min..max / end, us from first start):")
     for k in valid:

@@ -92,6 +92,46 @@ def test_step_engine_matches_oracle_loop(torch_cuda, oracle):
     assert np.all(np.abs(p_gpu - p_ref) <= bound[None, :])
 
 
+@pytest.mark.parametrize("name,two", [("c3", "1"), ("c5", "auto"), ("c5", "0")])
+def test_bins_two_level_bit_exact(torch_cuda, oracle, monkeypatch, name, two):
+    """Both binning paths (one-level row scan; two-level row counts + stable
+    scatter, the default for c5) against the oracle's bin_tiles, full canvas and
+    every band of an 8-way row split (the multi-GPU bands)."""
+    from paper_2602_22625_b200 import raster, synth
+    from paper_2602_22625_b200.dist import row_bands
+    from paper_2602_22625_b200.fit import effective_padding
+
+    if two != "auto":
+        monkeypatch.setenv("PF_BIN_TWO_LEVEL", two)
+    w = synth.make_workload(name)
+    sc = w.scene
+    pad = effective_padding(w.cfg)
+    pk = oracle.Packed(sc)
+    off, idx = oracle.bin_tiles(pk, 16, pad)
+    b = raster.bin_tiles(sc, 16, pad)
+    np.testing.assert_array_equal(b.offsets, off)
+    np.testing.assert_array_equal(b.indices, idx)
+    if name == "c5":
+        from paper_2602_22625_b200 import _native as nat
+
+        lib = nat.load()
+        H, W = sc.canvas_h, sc.canvas_w
+        nty, ntx = -(-H // 16), -(-W // 16)
+        launches = lib.pf_bin_launches(sc.n, W, H, 16, 0, nty)
+        assert launches == (1 if two == "0" else 4)
+        from paper_2602_22625_b200.fit import StepEngine
+
+        for band in row_bands(nty, 8):
+            eng = StepEngine(sc, w.cfg, w.loss, 1, band=band, use_graph=False)
+            eng.refresh()
+            eng.comp.bin()
+            k = eng.comp.check_overflow()
+            t0, t1 = band.ty_begin * ntx, band.ty_end * ntx
+            np.testing.assert_array_equal(eng.comp.bin_off.cpu().numpy()[: t1 - t0 + 1],
+                                          off[t0 : t1 + 1] - off[t0])
+            np.testing.assert_array_equal(eng.comp.bin_idx[:k].cpu().numpy(), idx[off[t0] : off[t1]])
+
+
 def test_graph_replay_equals_eager(torch_cuda):
     from paper_2602_22625_b200 import synth
     from paper_2602_22625_b200.fit import StepEngine
