@@ -151,7 +151,33 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
   const int t = pi.tid, wt = pi.wt, ht = pi.ht;
   const double q = pi.q, hyp = pi.hyp;
   const double sq = __dmul_rn(s, q);
-
+  // bbox, float64 with Python's rounding: r = s*hyp + pad, ceil(x-r), floor(x+r)
+  const double r = __dadd_rn(__dmul_rn(s, hyp), a.padding);
+  // rect at the z rank: (tx0 | tx1 << 16, ty0, primitive, ty1); empty: ty0 > ty1
+  // (every lane of the group computes it; lane 0 stores it)
+  int4 rc = make_int4(0, 1, i, 0);
+  {
+    const double lo_x = fmax(ceil(__dsub_rn(x, r)), 0.0);
+    const double hi_x = fmin(floor(__dadd_rn(x, r)), (double)(a.W - 1));
+    const double lo_y = fmax(ceil(__dsub_rn(y, r)), 0.0);
+    const double hi_y = fmin(floor(__dadd_rn(y, r)), (double)(a.H - 1));
+    // NaN-safe: every comparison with NaN is false -> treated as empty
+    if (lo_x <= hi_x && lo_y <= hi_y) {
+      // (tile 16, the fit step's, as a shift: the operands are >= 0)
+      const bool t16 = a.tile == 16;
+      const int tx0 = t16 ? (int)lo_x >> 4 : (int)lo_x / a.tile;
+      const int tx1 = t16 ? (int)hi_x >> 4 : (int)hi_x / a.tile;
+      const int ty0 = max(t16 ? (int)lo_y >> 4 : (int)lo_y / a.tile, a.ty_begin);
+      const int ty1 = min(t16 ? (int)hi_y >> 4 : (int)hi_y / a.tile, a.ty_end - 1);
+      if (ty0 <= ty1) rc = make_int4(tx0 | (tx1 << 16), ty0, i, ty1);
+    }
+  }
+  if (live && c == 0) a.s.rect[pi.zrank] = rc;
+  // records only for primitives in some tile of this band: nothing reads the
+  // others' (every consumer walks the tile lists) -- on a row band of a
+  // multi-GPU split most primitives skip the work below
+  const bool need = live && rc.y <= rc.w;
+  if (__any_sync(kFull, need)) {
   // transcendental / division work split across the lane group
   double r0 = 0.0, r1 = 0.0;
   if (c == 0) {
@@ -168,10 +194,8 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
   const double sc2 = __shfl_sync(kFull, r0, gb + 4);
   const double inv_s = __shfl_sync(kFull, r0, gb + 5), inv_sq = __shfl_sync(kFull, r1, gb + 5);
   const double omm = __dsub_rn(1.0, a.mu_blend);
-  // bbox, float64 with Python's rounding: r = s*hyp + pad, ceil(x-r), floor(x+r)
-  const double r = __dadd_rn(__dmul_rn(s, hyp), a.padding);
 
-  if (live) {
+  if (need) {
     // each lane stores one 16-byte slice of RecF (8 slices) and of RecG (5) / RecC (2)
     double2* pf = reinterpret_cast<double2*>(a.recf + i);
     switch (c) {
@@ -270,26 +294,8 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
         default: break;
       }
     }
-    if (c == 0) {
-      double lo_x = fmax(ceil(__dsub_rn(x, r)), 0.0);
-      double hi_x = fmin(floor(__dadd_rn(x, r)), (double)(a.W - 1));
-      double lo_y = fmax(ceil(__dsub_rn(y, r)), 0.0);
-      double hi_y = fmin(floor(__dadd_rn(y, r)), (double)(a.H - 1));
-      // rect at the z rank: (tx0 | tx1 << 16, ty0, primitive, ty1); empty: ty0 > ty1
-      int4 rc = make_int4(0, 1, i, 0);
-      // NaN-safe: every comparison with NaN is false -> treated as empty
-      if (lo_x <= hi_x && lo_y <= hi_y) {
-        // (tile 16, the fit step's, as a shift: the operands are >= 0)
-        const bool t16 = a.tile == 16;
-        const int tx0 = t16 ? (int)lo_x >> 4 : (int)lo_x / a.tile;
-        const int tx1 = t16 ? (int)hi_x >> 4 : (int)hi_x / a.tile;
-        const int ty0 = max(t16 ? (int)lo_y >> 4 : (int)lo_y / a.tile, a.ty_begin);
-        const int ty1 = min(t16 ? (int)hi_y >> 4 : (int)hi_y / a.tile, a.ty_end - 1);
-        if (ty0 <= ty1) rc = make_int4(tx0 | (tx1 << 16), ty0, i, ty1);
-      }
-      a.s.rect[pi.zrank] = rc;
-    }
   }
+  }  // any record in this warp
   }  // a.records
 
   if (ADAM) {
