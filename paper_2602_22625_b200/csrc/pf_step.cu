@@ -476,8 +476,11 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
 
 }  // namespace
 
-// Persistent, warp-specialised.  One CTA per SM; G groups of 9 warps: one
-// producer warp and 8 consumer warps (one 8x4 pixel sub-tile each).
+// Persistent, warp-specialised.  One CTA per SM; G groups of one producer warp
+// and 8 consumer warps (one 8x4 pixel sub-tile each).  Warps [0, 8G) consume
+// (group = warp / 8), warps [8G, 9G) produce, padded to whole warpgroups: the
+// producer / padding warpgroup drops to 24 registers (setmaxnreg) so that the
+// consumer warpgroups run at 80 (G = 3).
 //   producer  takes a tile ticket, reads the tile's list, then (once the ring
 //             slot is free) TMA bulk-copies the list's step + cull records and
 //             the tile's target (+ background) rows into an nbuf-deep ring of
