@@ -123,6 +123,19 @@ int pf_preprocess(const double* params, int n, double alpha_max, double mu_blend
                   void* rec, void* scratch, size_t scratch_bytes, void* stream);
 
 /*
+ * K1, incremental: the parameters are taken from `src` (e.g. the caller's
+ * pinned host vector, read in place over the host link); only primitives whose
+ * 8 values differ bitwise from `params` (the device copy) are copied into
+ * `params` and get new records / rects -- the others' are current from the
+ * pf_adam_preprocess launch that wrote `params` (and mirrored them to `src`).
+ * The per-step H2D of a host-driven fit loop.
+ */
+int pf_preprocess_sync(double* params, const double* src, int n, double alpha_max,
+                       double mu_blend, double padding, int W, int H, int tile, int ty_begin,
+                       int ty_end, int capacity, void* rec, void* scratch, size_t scratch_bytes,
+                       void* stream);
+
+/*
  * K5+K1 fused: one Adam step (fit.py:195-238) on every parameter, then the
  * records / tile rects of the NEXT step from the updated parameters (as
  * pf_preprocess) -- one launch between two renders.  Gradients are zeroed.
@@ -138,8 +151,9 @@ int pf_preprocess(const double* params, int n, double alpha_max, double mu_blend
  *   last_part  [pf_adam_blocks(n)][3]: the same sums of the latest step only (a
  *              fixed address a per-step host read can use), or NULL
  *   rec        the records of the next step, or NULL for Adam only (no records,
- *              no rects: the caller runs pf_preprocess before the next pf_bin --
- *              a host-driven step that re-reads the parameters every step)
+ *              no rects: the caller runs pf_preprocess before the next pf_bin)
+ *   mirror     the updated parameters are also written here (e.g. the caller's
+ *              pinned host vector: the per-step D2H of a host-driven loop), or NULL
  */
 int pf_adam_blocks(int n);
 int pf_adam_preprocess(double* params, double* grads, double* m, double* v, const uint8_t* frozen,
@@ -148,7 +162,7 @@ int pf_adam_preprocess(double* params, double* grads, double* m, double* v, cons
                        const double* sums, const double* part, int n_part, double* hist_part,
                        double* last_part, int n, double alpha_max, double mu_blend, double padding, int W, int H,
                        int tile, int ty_begin, int ty_end, int capacity, void* rec, void* scratch,
-                       size_t scratch_bytes, void* stream);
+                       size_t scratch_bytes, double* mirror, void* stream);
 
 /*
  * K2 — tile binning from the rects of pf_preprocess: one block per tile row,

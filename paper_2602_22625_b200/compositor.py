@@ -211,9 +211,22 @@ class Compositor:
             "pf_preprocess")
         self.launches += 1
 
+    def preprocess_sync(self, params: torch.Tensor, src: torch.Tensor, stream=None) -> None:
+        """K1 from ``src`` (e.g. a pinned host vector), recomputing only the
+        primitives whose parameters differ from the device copy ``params``."""
+        nat.check(
+            self.lib.pf_preprocess_sync(
+                params.data_ptr(), src.data_ptr(), self.n, self.alpha_max, self.mu_blend,
+                self.padding, self.W, self.H, self.tile, self.band.ty_begin, self.band.ty_end,
+                self.capacity, self.rec.data_ptr(), self.scratch.data_ptr(), self.scratch_bytes,
+                _stream_handle(stream)),
+            "pf_preprocess_sync")
+        self.launches += 1
+
     def adam_preprocess(self, params, grads, m, v, *, frozen, gains, lr_table, bc1_table,
                         bc2_table, s_min, s_max, sums=None, part=None, hist_part=None,
-                        last_part=None, records: bool = True, stream=None) -> None:
+                        last_part=None, records: bool = True, mirror=None,
+                        stream=None) -> None:
         """K5+K1 fused: Adam on every parameter, then the next step's records + rects
         (``records=False``: Adam only -- the caller re-runs preprocess() first).
         ``part``: pf_fit_step's loss partials (folded per block into ``hist_part``);
@@ -229,7 +242,8 @@ class Compositor:
                 self.alpha_max, self.mu_blend, self.padding, self.W, self.H, self.tile,
                 self.band.ty_begin, self.band.ty_end, self.capacity,
                 self.rec.data_ptr() if records else None,
-                self.scratch.data_ptr(), self.scratch_bytes, _stream_handle(stream)),
+                self.scratch.data_ptr(), self.scratch_bytes, nat.ptr(mirror),
+                _stream_handle(stream)),
             "pf_adam_preprocess")
         self.launches += 1
 

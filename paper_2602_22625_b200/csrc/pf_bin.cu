@@ -59,6 +59,8 @@ struct PreArgs {
   RecC* recc;
   RecS* recs;
   bool records;  // write records + rects (false: Adam only)
+  double* mirror;     // Adam: updated parameters also written here (e.g. pinned host), or NULL
+  const double* src;  // preprocess: parameters to take from here (e.g. pinned host), or NULL
   BinScratch s;
   AdamPart ad;
   unsigned long long* tl;  // diagnostics timeline or NULL
@@ -106,6 +108,17 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
   }
   const size_t pidx = (size_t)i * 8 + c;
   double pc = live ? a.params[pidx] : 1.0;
+  // incremental preprocess (src != NULL): the parameters come from src; only
+  // primitives whose 8 values differ from the device copy are copied and get
+  // new records / rects (the Adam launch before wrote the others' already)
+  bool grp_changed = true;
+  if (!ADAM && a.src) {
+    const double hv = live ? a.src[pidx] : 1.0;
+    const bool ch = __double_as_longlong(hv) != __double_as_longlong(pc);
+    grp_changed = ((__ballot_sync(kFull, ch) >> gb) & 0xffu) != 0u;
+    if (ch && live) a.params[pidx] = hv;
+    pc = hv;
+  }
   int it = 0;
   double fv0 = 0.0, fv1 = 0.0, fv2 = 0.0;  // loss-fold partial sums of this thread
   if (ADAM) {
@@ -133,6 +146,7 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
       a.ad.grads[pidx] = 0.0;  // ready for the next backward
       pc = adam_scalar(a.ad, pidx, c, live_p, pc, gr, m0, v0, lr, bc1, bc2);
       a.params[pidx] = pc;
+      if (a.mirror) a.mirror[pidx] = pc;
     }
     tl_mark(a.tl, 4, 1);
   }
@@ -172,11 +186,11 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
       if (ty0 <= ty1) rc = make_int4(tx0 | (tx1 << 16), ty0, i, ty1);
     }
   }
-  if (live && c == 0) a.s.rect[pi.zrank] = rc;
+  if (live && c == 0 && grp_changed) a.s.rect[pi.zrank] = rc;
   // records only for primitives in some tile of this band: nothing reads the
   // others' (every consumer walks the tile lists) -- on a row band of a
   // multi-GPU split most primitives skip the work below
-  const bool need = live && rc.y <= rc.w;
+  const bool need = live && rc.y <= rc.w && grp_changed;
   if (__any_sync(kFull, need)) {
   // transcendental / division work split across the lane group
   double r0 = 0.0, r1 = 0.0;
@@ -870,6 +884,8 @@ static int fill_pre_args(PreArgs& a, double* params, int n, double alpha_max, do
   a.recc = (RecC*)((char*)rec + (sizeof(RecF) + sizeof(RecG)) * (size_t)n);
   a.recs = (RecS*)((char*)rec + (sizeof(RecF) + sizeof(RecG) + sizeof(RecC)) * (size_t)n);
   a.records = true;
+  a.mirror = nullptr;
+  a.src = nullptr;
   a.s = carve(scratch, n, capacity);
   a.ad = AdamPart{};
   a.tl = pf_timeline_ptr();
@@ -953,6 +969,19 @@ extern "C" int pf_preprocess(const double* params, int n, double alpha_max, doub
   return launch_prim(false, a, (cudaStream_t)stream);
 }
 
+extern "C" int pf_preprocess_sync(double* params, const double* src, int n, double alpha_max,
+                                  double mu_blend, double padding, int W, int H, int tile,
+                                  int ty_begin, int ty_end, int capacity, void* rec, void* scratch,
+                                  size_t scratch_bytes, void* stream) {
+  if (n > 0 && !src) return PF_ERR_ARG;
+  PreArgs a;
+  const int rc = fill_pre_args(a, params, n, alpha_max, mu_blend, padding, W, H, tile, ty_begin,
+                               ty_end, capacity, rec, scratch, scratch_bytes);
+  if (rc != PF_OK) return rc;
+  a.src = src;
+  return launch_prim(false, a, (cudaStream_t)stream);
+}
+
 extern "C" int pf_adam_blocks(int n) { return div_up(n > 0 ? n * 8 : 1, kPrimThreads); }
 
 extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, double* v,
@@ -964,7 +993,7 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
                                   double mu_blend,
                                   double padding, int W, int H, int tile, int ty_begin,
                                   int ty_end, int capacity, void* rec, void* scratch,
-                                  size_t scratch_bytes, void* stream) {
+                                  size_t scratch_bytes, double* mirror, void* stream) {
   PreArgs a;
   // rec == NULL: Adam only (no records / rects; the caller runs pf_preprocess
   // before the next pf_bin, e.g. a host-driven step that re-reads the parameters)
@@ -973,6 +1002,7 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
                                ty_end, capacity, rec ? rec : dummy_rec, scratch, scratch_bytes);
   if (rc != PF_OK) return rc;
   a.records = rec != nullptr;
+  a.mirror = mirror;
   if (!lr_table || !bc1_table || !bc2_table || (n > 0 && (!grads || !m || !v)))
     return PF_ERR_ARG;
   if (part && n_part < 0) return PF_ERR_ARG;

@@ -299,15 +299,21 @@ class StepEngine:
         # directly (zero-copy over the host link): a host-driven step needs no
         # copy nodes (see capture_host_io_step)
         # (host_io: two loss-partial slots, alternating between host steps, so a
-        # step's loss can be read while the next step runs)
+        # step's loss can be read while the next step runs; the parameters stay
+        # on the device and io[:8n] is their host mirror, written by every Adam
+        # launch and read back -- changed primitives only -- by the next step)
         self.host_io = bool(host_io)
         nb3 = self.adam_blocks * 3
         if self.host_io:
             self.io = torch.zeros(n * 8 + 2 * nb3, dtype=torch.float64).pin_memory()
+            self.io[: n * 8].copy_(torch.from_numpy(vec))
+            self.params = torch.from_numpy(vec.reshape(n, 8).copy()).to(dev)
+            self.host_params = self.io[: n * 8]
         else:
             self.io = torch.zeros(n * 8 + nb3, dtype=torch.float64, device=dev)
-        self.params = self.io[: n * 8].view(n, 8)
-        self.params.copy_(torch.from_numpy(vec.reshape(n, 8).copy()))
+            self.params = self.io[: n * 8].view(n, 8)
+            self.params.copy_(torch.from_numpy(vec.reshape(n, 8).copy()))
+            self.host_params = None
         self.last_part = self.io[n * 8 : n * 8 + nb3]
         self.loss_slots = [self.last_part] + ([self.io[n * 8 + nb3 :]] if self.host_io else [])
         self.m = torch.from_numpy(np.asarray(self.state.m, dtype=np.float64).copy()).to(dev)
@@ -394,7 +400,8 @@ class StepEngine:
                           bc2_table=self.bc2_table, s_min=self.cfg.scale_min,
                           s_max=self.cfg.scale_max, sums=None if fold_in_adam else self.sums,
                           part=c.part if fold_in_adam else None, hist_part=self.hist_part,
-                          last_part=self.last_part, records=records)
+                          last_part=self.last_part, records=records,
+                          mirror=self.host_params)
         mark("adam_preprocess")
 
     def refresh(self) -> None:
@@ -426,9 +433,10 @@ class StepEngine:
 
     def capture_host_io_step(self) -> None:
         """host_io engines: one CUDA graph = preprocess from the host parameter
-        vector, bin, fit step, Adam writing the updated vector and the loss
-        partials back to host memory.  The caller edits / reads ``io`` (pinned
-        host) between host_step() replays."""
+        vector (incremental: changed primitives only), bin, fit step, Adam (+ the
+        next records) writing the updated vector and the loss partials back to
+        host memory.  The caller edits / reads ``io`` (pinned host) between
+        host_step() replays."""
         if not self.host_io:
             raise RuntimeError("capture_host_io_step needs StepEngine(host_io=True)")
         if self.graph is None and self.done == 0:
@@ -439,9 +447,10 @@ class StepEngine:
             self.last_part = slot
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                self.refresh()
-                # the next replay re-reads the parameters (refresh): Adam only here
-                self.launch_step(records=False)
+                # H2D: the host vector, read in place; primitives the host edited
+                # since the last Adam launch get new records (pf_preprocess_sync)
+                self.comp.preprocess_sync(self.params, self.host_params)
+                self.launch_step()
             graphs.append(g)
         self.last_part = keep
         self.host_graphs = graphs
@@ -536,6 +545,8 @@ class StepEngine:
     def push_host(self, vec: np.ndarray, state: OptimState) -> None:
         """Re-upload params/moments/frozen in place (graph pointers stay valid)."""
         self.params.copy_(torch.from_numpy(np.asarray(vec, dtype=np.float64).reshape(self.n, 8)))
+        if self.host_params is not None:
+            self.host_params.copy_(self.params.view(-1).cpu())
         self.m.copy_(torch.from_numpy(np.asarray(state.m, dtype=np.float64)))
         self.v.copy_(torch.from_numpy(np.asarray(state.v, dtype=np.float64)))
         self.frozen.copy_(torch.from_numpy(np.asarray(state.frozen, dtype=bool).astype(np.uint8)))
