@@ -174,25 +174,30 @@ def test_host_io_zero_copy_matches_device(torch_cuda):
     from paper_2602_22625_b200.fit import StepEngine
 
     w = synth.make_workload("c1")
-    w.cfg.num_iterations = 8
-    a = StepEngine(w.scene, w.cfg, w.loss, 8, use_graph=True)
-    b = StepEngine(w.scene, w.cfg, w.loss, 8, use_graph=True, host_io=True)
+    w.cfg.num_iterations = 9
+    a = StepEngine(w.scene, w.cfg, w.loss, 9, use_graph=True)
+    b = StepEngine(w.scene, w.cfg, w.loss, 9, use_graph=True, host_io=True)
     a.run(2)
     b.run(2)
     b.capture_host_io_step()
     n = b.n
-    for k in range(4):
+    for k in range(5):
         if k == 2:  # host edit: move every primitive by +0.75 px in x
             edited = b.io.numpy()[: n * 8].reshape(n, 8)
             edited[:, 0] += 0.75
             a.params[:, 0] += 0.75
+        if k == 3:  # sparse edit: three primitives jump by 40 px (other tiles)
+            edited = b.io.numpy()[: n * 8].reshape(n, 8)
+            for i in (0, 17, n - 1):
+                edited[i, 1] += 40.0
+                a.params[i, 1] += 40.0
         a.refresh()
         a.step()
         b.host_step()
         torch.cuda.synchronize()
     np.testing.assert_array_equal(a.params_host(), b.io.numpy()[: n * 8])
     np.testing.assert_array_equal(a.last_part.cpu().numpy().reshape(-1, 3), b.host_loss_part())
-    np.testing.assert_array_equal(a.hist_part.cpu().numpy().reshape(8, -1, 3)[4],
+    np.testing.assert_array_equal(a.hist_part.cpu().numpy().reshape(9, -1, 3)[5],
                                   b.host_loss_part(-2))
     assert [h.loss for h in a.history()] == [h.loss for h in b.history()]
 
