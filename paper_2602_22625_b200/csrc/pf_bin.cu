@@ -1049,7 +1049,7 @@ static int row_blocks(int n, int n_rows, int ntx, bool cache) {
 static bool bin_two_level(int n, int n_rows, int ncb, size_t scat_smem) {
   bool two = (size_t)n * (size_t)n_rows * (size_t)ncb > 2000000u;
   if (const char* e = getenv("PF_BIN_TWO_LEVEL")) two = atoi(e) != 0;
-  return two && n > 0 && n_rows <= 1024 && scat_smem <= 200 * 1024;
+  return two && n > 0 && n_rows <= kMaxRows2 && scat_smem <= 200 * 1024;
 }
 
 static size_t scatter_smem(int n_rows) {

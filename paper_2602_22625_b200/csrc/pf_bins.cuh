@@ -28,6 +28,7 @@ struct BinScratch {
 };
 
 constexpr int kRowChunk = 128;  // z positions per block of the two-level row pass
+constexpr int kMaxRows2 = 1024;  // band rows the two-level path handles
 
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -47,9 +48,11 @@ static inline BinScratch carve(void* base, int n, int cap, int n_tiles = 0) {
   s.done = (uint32_t*)take(sizeof(uint32_t) * 4);
   s.fold = (double*)take(sizeof(double) * 3 * (size_t)((8 * (size_t)n + 255) / 256 + 1));
   // (appended: the offsets above do not depend on n_tiles)
+  // (rows <= n_tiles, and the two-level path runs only for <= kMaxRows2 rows)
   const size_t chunks = ((size_t)n + kRowChunk - 1) / kRowChunk;
-  s.rowcnt = (int2*)take(sizeof(int2) * chunks * (size_t)n_tiles);
-  s.rowinfo = (int4*)take(sizeof(int4) * ((size_t)n_tiles + 1));
+  const size_t rows = n_tiles < kMaxRows2 ? (size_t)n_tiles : (size_t)kMaxRows2;
+  s.rowcnt = (int2*)take(sizeof(int2) * chunks * rows);
+  s.rowinfo = (int4*)take(sizeof(int4) * (rows + 1));
   s.total = off;
   return s;
 }
