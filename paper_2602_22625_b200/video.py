@@ -135,3 +135,75 @@ def remove_stuck(scene, frozen: np.ndarray | None, policy: StuckPolicy):
     for i in decayed:
         prims[i] = dataclasses.replace(prims[i], opacity_logit=float(nu[i]))
     return dataclasses.replace(scene, primitives=prims), decayed
+
+
+def policy_from_config(cfg) -> StuckPolicy:
+    """StuckPolicy from a FitConfig's video fields (dyn.py:74-83); this package's
+    FitConfig has no video fields, so the reference defaults stand in."""
+    g = lambda k, d: getattr(cfg, k, d)  # noqa: E731
+    return StuckPolicy(grid=(int(g("stuck_grid_y", 4)), int(g("stuck_grid_x", 4))),
+                       k=int(g("stuck_top_k", 4)), tau_scale=float(g("stuck_tau_scale", 0.1)),
+                       tau_alpha=float(g("stuck_tau_alpha", 0.7)), zeta=float(g("stuck_zeta", 0.7)),
+                       eta=float(g("stuck_eta", 0.3)),
+                       triggers=tuple(g("stuck_triggers", (20, 45, 70))))
+
+
+def optimize_video(frames, init, cfg):
+    """Fit one scene per frame, warm-starting each from the previous
+    (dyn.py:180-238): frame 0 runs ``cfg.num_iterations`` steps; every later
+    frame runs ``cfg.sequential_iterations`` from fresh Adam moments, with the
+    primitives whose binning box misses every changed pixel frozen
+    (``freeze_static``; diff_mask + freeze_flags on the GPU) and the stuck-
+    primitive decay applied at the policy's trigger iterations (``remove_stuck``).
+    Every step runs in the GPU fit loop (fit.run_loop).
+
+    ``init`` is the frame-0 scene (the reference builds it with prep.init_scene,
+    which is outside the ported path) or a template list, in which case the
+    scene is this package's restated structure-aware init (synth.py).
+    Returns (scenes, histories), one per frame.
+    """
+    from .fit import LossSpec, OptimState, effective_padding, run_loop
+    from .scene import Scene, pack_params
+
+    if not frames:
+        raise ValueError("need at least one frame")
+    frames = [np.asarray(f, dtype=np.float64) for f in frames]
+    for f in frames:
+        if f.shape != frames[0].shape:
+            raise ShapeMismatch("all frames must share one shape")
+    if cfg.loss in ("spatial", "spatial_constrained"):
+        raise ValueError("spatial loss is single-image only")
+    rng = np.random.default_rng(cfg.seed)
+    if isinstance(init, Scene):
+        scene = init
+    else:
+        from .synth import structure_aware_scene
+
+        scene = structure_aware_scene(frames[0], list(init), int(cfg.num_primitives),
+                                      float(cfg.scale_min), float(cfg.scale_max), rng)
+    padding = effective_padding(cfg)
+    policy = policy_from_config(cfg)
+
+    def spec(frame):
+        return LossSpec(kind=cfg.loss, target=frame, mse_w=cfg.mse_weight,
+                        gray_l1_w=cfg.gray_l1_weight)
+
+    scene, hist, _ = run_loop(scene, cfg, spec(frames[0]), rng, iterations=cfg.num_iterations)
+    scenes, histories = [scene], [hist]
+    for f in range(1, len(frames)):
+        _, layout = pack_params(scene)
+        state = OptimState.fresh(layout)
+        if getattr(cfg, "freeze_static", True):
+            mask = diff_mask(frames[f - 1], frames[f],
+                             float(getattr(cfg, "diff_threshold", DEFAULT_DIFF_THRESHOLD)))
+            state.frozen = freeze_flags(scene, mask, padding)
+        hooks = None
+        if getattr(cfg, "remove_stuck", False):
+            hooks = {t: (lambda s, st: remove_stuck(s, st.frozen, policy)[0])
+                     for t in policy.triggers}
+        scene, hist, state = run_loop(scene, cfg, spec(frames[f]), rng,
+                                      iterations=int(getattr(cfg, "sequential_iterations", 100)),
+                                      state=state, hooks=hooks)
+        scenes.append(scene)
+        histories.append(hist)
+    return scenes, histories

@@ -72,3 +72,33 @@ def test_video_heuristics_match_reference(torch_cuda):
     np.testing.assert_allclose(nu, d["stuck_params"][:, 4], rtol=0, atol=1e-15)
     _, dec0 = video.remove_stuck(sc, None, pol)
     assert dec0 == list(d["stuck_decayed_nofrozen"])
+
+
+def test_optimize_video_chain(torch_cuda):
+    """optimize_video (dyn.py:180-238) on the GPU fit loop: frame 0 == run_loop
+    alone; on frame 1 every primitive frozen by the diff mask keeps its
+    parameters bit for bit, the others move; the stuck-decay hooks run."""
+    import copy
+
+    from paper_2602_22625_b200 import synth, video
+    from paper_2602_22625_b200.fit import LossSpec, effective_padding, run_loop
+    from paper_2602_22625_b200.scene import pack_params
+
+    w = synth.make_workload("c1")
+    cfg = copy.deepcopy(w.cfg)
+    cfg.num_iterations, cfg.sequential_iterations = 10, 8
+    cfg.freeze_static, cfg.remove_stuck, cfg.stuck_triggers = True, True, (3, 6)
+    f0 = w.target
+    f1 = f0.copy()
+    f1[100:160, 60:120] = 1.0 - f1[100:160, 60:120]  # one changed region
+    scenes, hists = video.optimize_video([f0, f1], copy.deepcopy(w.scene), cfg)
+    assert [len(h) for h in hists] == [10, 8]
+    # frame 0 is run_loop alone (same rng stream)
+    s0, _, _ = run_loop(copy.deepcopy(w.scene), cfg, LossSpec(kind="mse", target=f0),
+                        np.random.default_rng(cfg.seed), iterations=10)
+    p0, p1 = pack_params(scenes[0])[0].reshape(-1, 8), pack_params(scenes[1])[0].reshape(-1, 8)
+    np.testing.assert_array_equal(p0, pack_params(s0)[0].reshape(-1, 8))
+    frozen = video.freeze_flags(scenes[0], video.diff_mask(f0, f1), effective_padding(cfg))
+    assert 0 < frozen.sum() < len(frozen)
+    np.testing.assert_array_equal(p1[frozen], p0[frozen])
+    assert (p1[~frozen] != p0[~frozen]).any(axis=1).all()
