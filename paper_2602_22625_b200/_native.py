@@ -16,6 +16,9 @@ from pathlib import Path
 
 LIB_DIR = Path(__file__).resolve().parent / "_lib"
 LIB_PATH = LIB_DIR / "libprimfit_b200.so"
+# diagnostics: PF_LIB=<path> loads another build (A/B runs on one box)
+if os.environ.get("PF_LIB"):
+    LIB_PATH = Path(os.environ["PF_LIB"])
 
 PF_OK = 0
 PF_ERR_ARG = 1001
