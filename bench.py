@@ -211,6 +211,16 @@ def ncu_summary(kernel_prefix: str) -> dict | None:
     return None
 
 
+def issue_frac(kernel_prefix: str, sms: int = 148, mhz: float = 1965.0) -> float | None:
+    """Issued warp instructions per SM per cycle / 4 (one issue per SMSP per cycle)
+    for the named kernel, from the committed ncu summary (duration at SM clock)."""
+    v = ncu_summary(kernel_prefix)
+    if not v or not v.get("warp_instructions") or not v.get("duration_ns"):
+        return None
+    cycles = float(v["duration_ns"]) * 1e-9 * mhz * 1e6
+    return float(v["warp_instructions"]) / (sms * cycles) / 4.0
+
+
 def ncu_traffic(kernel_prefix: str) -> float | None:
     """dram bytes (read + write) per launch of the named kernel (ncu summary), or None."""
     v = ncu_summary(kernel_prefix)
@@ -383,7 +393,10 @@ def run_ours(args) -> None:
                      "traffic": ncu_traffic(KNAME[dom]),
                      "peak_src": peaks["src"], "algorithmic_bytes": ab[dom],
                      "kernel_ms": stage_ms[dom],
-                     "step_frac": ab["total"] * value / 1e9 / peaks["hbm_gbs"]},
+                     "step_frac": ab["total"] * value / 1e9 / peaks["hbm_gbs"],
+                     # what does bound it: instruction issue (ncu summary of the
+                     # same kernel: warp instructions per SM cycle against 4)
+                     "issue_frac": issue_frac(KNAME[dom])},
         # SURVEY 8(d) secondary unit: binned (pixel, list entry) evaluations per
         # second (256 pixels per tile-list entry at tile 16), plus the ncu L1/tex
         # hit rate and warp execution efficiency of the dominant kernel
