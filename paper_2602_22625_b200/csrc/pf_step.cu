@@ -83,6 +83,7 @@ struct StepArgs {
   int W, H, ntx, ty_begin, n_tiles;
   double eps_skip;
   double eps_band;       // eps re-check band (see warp_tile)
+  float k2_3P;           // (float)(2 / (3 P)): fp32 MSE gradient scale
   double bg0, bg1, bg2;
   float bgf0, bgf1, bgf2;  // the same as float (backward)
   const float4* bg4;
@@ -345,7 +346,22 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
   const float g2 = a.bg4 ? bgp.z : a.bgf2;
   float dI0 = 0.f, dI1 = 0.f, dI2 = 0.f, dA = 0.f;
   float l0 = 0.f, l1 = 0.f, l2 = 0.f;
-  if (valid) {
+#ifndef PF_LOSS32
+#define PF_LOSS32 1
+#endif
+  if (valid && PF_LOSS32 && LOSS == PF_LOSS_MSE) {
+    // MSE in fp32 end to end: the image is stored as fp32 and the per-warp
+    // partials are fp32 sums already; (I - t) to ~1 ulp of I (< 1e-7)
+    const float I0 = fmaf(T, g0, C0), I1 = fmaf(T, g1, C1), I2 = fmaf(T, g2, C2);
+    if (a.img4) a.img4[pix] = make_float4(I0, I1, I2, Aacc);
+    const float r0 = I0 - tg.x, r1 = I1 - tg.y, r2 = I2 - tg.z;
+    l0 = fmaf(r0, r0, fmaf(r1, r1, r2 * r2));
+    l1 = l0;
+    const float k = a.k2_3P;
+    dI0 = k * r0;
+    dI1 = k * r1;
+    dI2 = k * r2;
+  } else if (valid) {
     const double I0 = (double)C0 + (double)T * (a.bg4 ? (double)bgp.x : a.bg0);
     const double I1 = (double)C1 + (double)T * (a.bg4 ? (double)bgp.y : a.bg1);
     const double I2 = (double)C2 + (double)T * (a.bg4 ? (double)bgp.z : a.bg2);
@@ -842,6 +858,7 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   a.eps_skip = eps_skip;
   // eps re-check band: fp32 taps (<= 6e-8 relative) + affine U, V (<= 1e-10 texel)
   a.eps_band = 1e-6 * eps_skip + 1e-9;
+  a.k2_3P = (float)(2.0 * inv_3P);
   a.bg0 = bg_r;
   a.bg1 = bg_g;
   a.bg2 = bg_b;
