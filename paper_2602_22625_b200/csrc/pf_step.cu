@@ -475,7 +475,10 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
       B *= om;
     }
     double* gp = a.grads + (size_t)r.gidx * 8;
-    if (__popc(ball) <= 2) {
+#ifndef PF_DIRECT_MAX
+#define PF_DIRECT_MAX 2  // entries with at most this many lanes skip the warp reduction
+#endif
+    if (__popc(ball) <= PF_DIRECT_MAX) {
       if (act) {
 #pragma unroll
         for (int c = 0; c < 8; ++c)
