@@ -301,9 +301,12 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
                                 (float)(-ct * inv_sq));
           break;
         case 3: ps4[11] = make_float4((float)inv_s, (float)q, (float)(s * inv_sq), (float)hw); break;
-        case 4: ps4[12] = make_float4((float)hh, (float)omm, (float)sa_d, 0.0f); break;
+        case 4:
+          ps4[12] = make_float4((float)hh, (float)omm, (float)sa_d, 1.0f / (float)hw);
+          break;
         case 5:
-          ps4[13] = make_float4((float)(omm * sc0), (float)(omm * sc1), (float)(omm * sc2), 0.0f);
+          ps4[13] = make_float4((float)(omm * sc0), (float)(omm * sc1), (float)(omm * sc2),
+                                1.0f / (float)hh);
           break;
         default: break;
       }

@@ -84,8 +84,8 @@ struct __align__(16) RecS {
   float sd, cd0, cd1, cd2;      // alpha_max*sig*(1-sig), sc*(1-sc)
   float gxu, gxv, gyu, gyv;     // -ct/s, st/(s q), -st/s, -ct/(s q)
   float inv_s, q, inv_q, hw;    // 1/s, aspect, 1/aspect, 0.5 (wt - 1)
-  float hh, omm, saf, pad_f;    // 0.5 (ht - 1), 1 - mu_blend, (float)sa
-  float c0f, c1f, c2f, pad_g;   // (float)c
+  float hh, omm, saf, inv_hw;   // 0.5 (ht - 1), 1 - mu_blend, (float)sa, 1 / hw
+  float c0f, c1f, c2f, inv_hh;  // (float)c, 1 / hh
 };
 static_assert(sizeof(RecS) == 224, "RecS must be 224 bytes");
 
