@@ -26,7 +26,7 @@ def torch_cuda():
     return torch
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
 def test_workload_bins_forward_backward_vs_oracle(torch_cuda, oracle, name):
     from paper_2602_22625_b200 import grad, raster, synth
     from paper_2602_22625_b200.fit import effective_padding
