@@ -450,3 +450,45 @@ def test_bins_large_scene_4k(torch_cuda, oracle):
     eng.check()
     h = eng.history()
     assert len(h) == 2 and all(np.isfinite(x.loss) for x in h)
+
+
+@pytest.mark.parametrize("kind", ["noise_bg", "aspect_alpha_max"])
+def test_fused_step_bg_and_aspect(torch_cuda, oracle, kind):
+    """K34 with a per-pixel (noise) background (the BG kernel variant, staged
+    background rows) and with preserve_aspect + alpha_max < 1 templates."""
+    import dataclasses
+
+    from conftest import load_case, scene_from
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.compositor import pixels4
+    from paper_2602_22625_b200.fit import LossSpec, StepEngine, effective_padding
+
+    torch = torch_cuda
+    rng = np.random.default_rng(31)
+    w = synth.make_workload("c1")
+    if kind == "noise_bg":
+        sc = dataclasses.replace(w.scene, background="noise")
+        bg = rng.random((sc.canvas_h, sc.canvas_w, 3)).astype(np.float32).astype(np.float64)
+        target = w.target
+    else:
+        sc = dataclasses.replace(scene_from(load_case("aspect_mu_s0")), mu_blend=0.0)
+        bg = None
+        target = rng.random((sc.canvas_h, sc.canvas_w, 3))
+    eng = StepEngine(sc, w.cfg, LossSpec(kind="mse", target=target), 1, use_graph=False)
+    assert eng.fused
+    if bg is not None:
+        eng.bg4.copy_(torch.from_numpy(pixels4(bg)))
+    g, sums, color, alpha = _fused_grads(eng)
+    pk = oracle.Packed(sc)
+    off, idx = oracle.bin_tiles(pk, 32, effective_padding(w.cfg))
+    img, a_ref, sv = oracle.render_forward(pk, off, idx, 32, oracle.background(sc, bg), True,
+                                           w.cfg.eps_skip)
+    ok, err = fwd_close(color, img)
+    assert ok, f"{kind} colour rel err {err}"
+    ok, err = fwd_close(alpha, a_ref)
+    assert ok, f"{kind} alpha rel err {err}"
+    diff = img - target
+    np.testing.assert_allclose(sums[0], np.sum(diff**2), rtol=1e-5)
+    g_ref = oracle.backward(pk, sv, 2.0 * diff / diff.size, None)  # (bg saved in sv)
+    ok, err = grad_close(g, g_ref)
+    assert ok, f"{kind} grad rel err {err}"
