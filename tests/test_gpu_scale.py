@@ -492,3 +492,27 @@ def test_fused_step_bg_and_aspect(torch_cuda, oracle, kind):
     g_ref = oracle.backward(pk, sv, 2.0 * diff / diff.size, None)  # (bg saved in sv)
     ok, err = grad_close(g, g_ref)
     assert ok, f"{kind} grad rel err {err}"
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_row_band_gradients_sum_to_full_canvas(torch_cuda, world):
+    """The multi-GPU decomposition on one GPU: the K34 gradients and loss sums of
+    the row bands of an N-way split (each band binned and rendered alone, as a
+    rank does) add up to the full-canvas step's (fp64 atomics: round-off only)."""
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.dist import row_bands
+    from paper_2602_22625_b200.fit import StepEngine
+
+    w = synth.make_workload("c3")
+    full = StepEngine(w.scene, w.cfg, w.loss, 1, use_graph=False)
+    g_full, s_full, _, _ = _fused_grads(full)
+    nty = -(-w.scene.canvas_h // 16)
+    g_sum, s_sum = np.zeros_like(g_full), np.zeros_like(s_full)
+    for band in row_bands(nty, world):
+        eng = StepEngine(w.scene, w.cfg, w.loss, 1, band=band, use_graph=False)
+        g, s, _, _ = _fused_grads(eng)
+        g_sum += g
+        s_sum += s
+    np.testing.assert_allclose(s_sum[:3], s_full[:3], rtol=1e-12)
+    ok, err = grad_close(g_sum, g_full, rel=1e-9)
+    assert ok, f"band-sum grad rel err {err}"
