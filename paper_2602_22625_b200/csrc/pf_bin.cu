@@ -1042,7 +1042,8 @@ static int sms_count() {
 static int row_blocks(int n, int n_rows, int ntx, bool cache) {
   // column blocks per row: as many as fit in one wave (1024-thread blocks, one
   // per SM with the register cache), >= 16 columns each
-  const int ncb = (cache ? 1 : 2) * sms_count() / n_rows;
+  int ncb = (cache ? 1 : 2) * sms_count() / n_rows;
+  if (const char* e = getenv("PF_BIN_NCB")) ncb = atoi(e);  // diagnostics (A/B)
   return max(1, min(ncb, ntx / 16));
 }
 
