@@ -11,7 +11,6 @@ with ``eps_skip = 0``.  There is no CPU path.
 
 from __future__ import annotations
 
-import ctypes as C
 import dataclasses
 from dataclasses import dataclass
 from pathlib import Path

@@ -20,7 +20,7 @@ import os
 import csv
 import math
 from collections.abc import Callable
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from pathlib import Path
 
 import numpy as np
@@ -30,7 +30,8 @@ from . import _native as nat
 from .compositor import Band, Compositor, DeviceAtlas, adam_launch, bin_capacity, pixels4
 from .errors import LayoutMismatch, MissingAlphaTarget, ShapeMismatch
 from .raster import DEFAULT_EPS_SKIP, _device, noisy_background
-from .scene import NOISE_BACKGROUND, FloatArray, ParamLayout, pack_params, param_matrix, structure_arrays, unpack_params, validate_scene
+from .scene import (NOISE_BACKGROUND, FloatArray, ParamLayout, pack_params, structure_arrays,
+                    unpack_params, validate_scene)
 
 ADAM_BETA1 = 0.9
 ADAM_BETA2 = 0.999
