@@ -516,3 +516,27 @@ def test_row_band_gradients_sum_to_full_canvas(torch_cuda, world):
     np.testing.assert_allclose(s_sum[:3], s_full[:3], rtol=1e-12)
     ok, err = grad_close(g_sum, g_full, rel=1e-9)
     assert ok, f"band-sum grad rel err {err}"
+
+
+def test_adam_only_then_preprocess_equals_fused_records(torch_cuda):
+    """pf_adam_preprocess with rec = NULL (Adam only) followed by pf_preprocess
+    gives the same next step as the fused Adam + records launch."""
+    torch = torch_cuda
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.fit import StepEngine
+
+    w = synth.make_workload("c1")
+    w.cfg.num_iterations = 6
+    a = StepEngine(w.scene, w.cfg, w.loss, 6, use_graph=False)
+    b = StepEngine(w.scene, w.cfg, w.loss, 6, use_graph=False)
+    a.refresh()
+    b.refresh()
+    for _ in range(3):
+        a.launch_step()
+        a.done += 1
+        b.launch_step(records=False)
+        b.refresh()
+        b.done += 1
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(a.params_host(), b.params_host())
+    assert [h.loss for h in a.history()] == [h.loss for h in b.history()]
