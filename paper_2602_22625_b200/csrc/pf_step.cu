@@ -913,10 +913,14 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   const bool bg = bg4 != nullptr;
   const size_t gb = group_bytes(bg);
   const size_t a32 = (size_t)pad_texels * sizeof(float), a64 = 2 * a32;
+  // atlas placement at the chosen group count: fp64 in shared memory when it
+  // fits, else fp32, else the global fp32 plane through L1 -- never fewer groups
+  // (measured at c5, 4 templates: 3 groups + global atlas 422 us/step against
+  // 2 groups + shared fp32 atlas 485 us)
   int atl = 0;
-  for (int gg = G; gg >= 2 && atl == 0; --gg) {
-    if (apad64 && !no64 && gg * gb + a64 <= budget) { G = gg; atl = 2; }
-    else if (gg * gb + a32 <= budget) { G = gg; atl = 1; }
+  if (getenv("PF_STEP_ATL0") == nullptr) {  // (diagnostics: force the global plane)
+    if (apad64 && !no64 && G * gb + a64 <= budget) atl = 2;
+    else if (G * gb + a32 <= budget) atl = 1;
   }
   const size_t smem = G * gb + (atl == 2 ? a64 : atl == 1 ? a32 : 0);
   void (*kern)(StepArgs);
