@@ -64,12 +64,12 @@ def test_workload_bins_forward_backward_vs_oracle(torch_cuda, oracle, name):
     assert ok, f"{name} grad rel err {err}"
 
 
-def test_step_engine_matches_oracle_loop(torch_cuda, oracle):
+@pytest.mark.parametrize("name,total", [("c1", 8), ("c3", 5)])
+def test_step_engine_matches_oracle_loop(torch_cuda, oracle, name, total):
     from paper_2602_22625_b200 import synth
     from paper_2602_22625_b200.fit import StepEngine, effective_padding
 
-    w = synth.make_workload("c1")
-    total = 8
+    w = synth.make_workload(name)
     w.cfg.num_iterations = total
     eng = StepEngine(w.scene, w.cfg, w.loss, total)
     loop = oracle.Loop(w.scene, w.target, w.cfg, effective_padding(w.cfg), tile=32)
@@ -540,3 +540,22 @@ def test_adam_only_then_preprocess_equals_fused_records(torch_cuda):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(a.params_host(), b.params_host())
     assert [h.loss for h in a.history()] == [h.loss for h in b.history()]
+
+
+def test_long_run_c3(torch_cuda):
+    """300 graph-replayed steps of the metric config through run_loop: finite
+    history, the loss falls, no bin overflow, parameters finite."""
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.fit import run_loop
+
+    w = synth.make_workload("c3")
+    w.cfg.num_iterations = 300
+    sc, hist, state = run_loop(w.scene, w.cfg, w.loss, np.random.default_rng(0))
+    losses = np.array([h.loss for h in hist])
+    assert len(losses) == 300 and np.isfinite(losses).all()
+    assert losses[-1] < 0.5 * losses[0]
+    assert np.all(np.diff(losses[:50]) < 0.05 * losses[0])  # no blow-up early on
+    assert state.step == 300
+    from paper_2602_22625_b200.scene import pack_params
+
+    assert np.isfinite(pack_params(sc)[0]).all()
