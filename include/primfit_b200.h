@@ -276,6 +276,8 @@ int pf_atlas_pad(const double* tex, int texels, const int32_t* tpl_base, const i
  *   counters uint32[2] zeroed once at allocation (tile ticket; self-resetting)
  *   tile_classes  pf_bin's tile classes of this band (longest-first schedule; the
  *           counts are re-zeroed for the next pf_bin), or NULL (tile order)
+ *   stage   list entries staged in shared memory per tile: 32, or 64 for scenes
+ *           with long tile lists (a hint: entries beyond it are read from L2)
  */
 size_t pf_step_spill_bytes(int capacity);
 int pf_fit_step(const void* rec, int n, const double* tex, const float* apad,
@@ -285,7 +287,7 @@ int pf_fit_step(const void* rec, int n, const double* tex, const float* apad,
                 int loss_kind, const float* tgt4, double alpha_w, double w_mse, double w_gray,
                 double inv_3P, double inv_P, void* spill, float* img4, double* part,
                 double* grads, uint32_t* counters,
-                const int32_t* tile_classes, void* stream);
+                const int32_t* tile_classes, int stage, void* stream);
 
 /* Fixed-order fold of n_part partial triples into sums[3] (deterministic). */
 int pf_fold_loss(const double* part, int n_part, double* sums, void* stream);

@@ -64,7 +64,7 @@ SIGNATURES: dict[str, tuple] = {
     "pf_fit_step": (
         _I,
         [_P, _I, _P, _P, _P, _I, _I, _P, _P, _P, _I, _I, _I, _I, _D, _D, _D, _D, _P, _I, _P, _D,
-         _D, _D, _D, _D, _P, _P, _P, _P, _P, _P, _P],
+         _D, _D, _D, _D, _P, _P, _P, _P, _P, _P, _I, _P],
     ),
     "pf_fold_loss": (_I, [_P, _I, _P, _P]),
     "pf_backward": (

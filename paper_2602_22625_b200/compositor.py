@@ -139,6 +139,9 @@ class Compositor:
         self.band = band or Band(0, self.nty)
         self.n_tiles = (self.band.ty_end - self.band.ty_begin) * self.ntx
         self.capacity = int(capacity)
+        # K34 stage depth: 64 staged list entries per tile when the capacity bound
+        # says lists run long (c2 / c4: ~70 entries per tile bound), else 32
+        self.stage_hint = 64 if self.capacity > 48 * max(self.n_tiles, 1) else 32
         dev = self.device
         if d_tid is None:
             d_tid = torch.from_numpy(np.ascontiguousarray(template_id, dtype=np.int32)).to(dev)
@@ -330,7 +333,7 @@ class Compositor:
                 1.0 / Pt,
                 self.spill.data_ptr(), p(self.img4) if image else None, self.part.data_ptr(),
                 grads.data_ptr(), self.step_ctr.data_ptr(), nat.ptr(self.tile_classes),
-                _stream_handle(stream)),
+                self.stage_hint, _stream_handle(stream)),
             "pf_fit_step")
         self.launches += 1
         if sums is not None:

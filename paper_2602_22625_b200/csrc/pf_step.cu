@@ -40,7 +40,8 @@ namespace pf {
 namespace {
 
 constexpr int kCW = kTilePix / 32;                      // consumer warps per group (one tile)
-constexpr int kStage = 32;                              // list entries staged per tile
+// list entries staged per tile: ST = 32, or 64 for long-list scenes (template
+// parameter of k_step; pf_fit_step's `stage` hint picks it)
 constexpr int kNBuf = 2;                                // stage buffers per group (ring)
 constexpr int kKS = 5;                                  // contribution-stack depth in smem
 constexpr uint32_t kEntBytes = sizeof(RecS) + sizeof(RecC);
@@ -58,14 +59,16 @@ __host__ __device__ constexpr int step_cons_regs(int G) {
           (256 * G)) / 8 * 8;
 }
 static_assert(step_cons_regs(3) == 80 && step_cons_regs(2) == 112, "register split");
-// one stage buffer: kStage RecS + kStage RecC + the tile's target (+ background) pixels
-constexpr size_t kBufRec = (size_t)kStage * kEntBytes;
+// one stage buffer: ST RecS + ST RecC + the tile's target (+ background) pixels
+__host__ __device__ constexpr size_t buf_rec_bytes(int st) { return (size_t)st * kEntBytes; }
 constexpr size_t kBufPix = (size_t)kTilePix * sizeof(float4);
 constexpr size_t kStackLevel = (size_t)kTilePix * (sizeof(float4) + sizeof(float));
-__host__ __device__ constexpr size_t buf_bytes(bool bg) { return kBufRec + kBufPix * (bg ? 2 : 1); }
+__host__ __device__ constexpr size_t buf_bytes(bool bg, int st) {
+  return buf_rec_bytes(st) + kBufPix * (bg ? 2 : 1);
+}
 // per group: kNBuf stage buffers + a kKS-deep contribution stack per consumer thread
-__host__ __device__ constexpr size_t group_bytes(bool bg) {
-  return kNBuf * buf_bytes(bg) + kKS * kStackLevel;
+__host__ __device__ constexpr size_t group_bytes(bool bg, int st) {
+  return kNBuf * buf_bytes(bg, st) + kKS * kStackLevel;
 }
 
 struct StepArgs {
@@ -221,13 +224,14 @@ __device__ __forceinline__ void cell_of(double U, int& u0, double& wu) {
 }
 
 // Record access for one tile: staged (shared) entries, plus -- for lists longer
-// than kStage, a rare case -- the remaining entries straight from HBM/L2.
+// than ST -- the remaining entries straight from HBM/L2.
 struct StagedRecs {
   const RecS* s;
   const RecC* c;
   __device__ __forceinline__ const RecS& rec(int j) const { return s[j]; }
   __device__ __forceinline__ const RecC& cull(int j) const { return c[j]; }
 };
+template <int ST>
 struct MixedRecs {
   const RecS* s;
   const RecC* c;
@@ -235,10 +239,10 @@ struct MixedRecs {
   const RecC* gc;
   const int32_t* idx;  // bin_idx + b0
   __device__ __forceinline__ const RecS& rec(int j) const {
-    return j < kStage ? s[j] : gs[__ldg(idx + j)];
+    return j < ST ? s[j] : gs[__ldg(idx + j)];
   }
   __device__ __forceinline__ const RecC& cull(int j) const {
-    return j < kStage ? c[j] : gc[__ldg(idx + j)];
+    return j < ST ? c[j] : gc[__ldg(idx + j)];
   }
 };
 
@@ -510,7 +514,7 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
 // The padded alpha atlas is loaded into shared memory once per CTA: float64
 // (ATL == 2) when it fits, else float32 (ATL == 1); ATL == 0 reads the global
 // fp32 plane.
-template <int LOSS, int ATL, int G, bool BG>
+template <int LOSS, int ATL, int G, bool BG, int ST>
 __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t full[G][kNBuf], empty[G][kNBuf];
@@ -520,7 +524,7 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
   constexpr bool has_bg = BG;
-  constexpr size_t gbytes = group_bytes(BG), bbytes = buf_bytes(BG);
+  constexpr size_t gbytes = group_bytes(BG, ST), bbytes = buf_bytes(BG, ST);
   unsigned char* satl = sm + G * gbytes;
   using Atl = typename std::conditional<
       ATL == 2, AtlasS64, typename std::conditional<ATL == 1, AtlasS32, AtlasG32>::type>::type;
@@ -576,11 +580,13 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
   float* stB = reinterpret_cast<float*>(stA + kKS * kTilePix);
   auto buf_rec = [&](int b) { return reinterpret_cast<RecS*>(gs + b * bbytes); };
   auto buf_cull = [&](int b) {
-    return reinterpret_cast<RecC*>(gs + b * bbytes + kStage * sizeof(RecS));
+    return reinterpret_cast<RecC*>(gs + b * bbytes + ST * sizeof(RecS));
   };
-  auto buf_tgt = [&](int b) { return reinterpret_cast<float4*>(gs + b * bbytes + kBufRec); };
+  auto buf_tgt = [&](int b) {
+    return reinterpret_cast<float4*>(gs + b * bbytes + buf_rec_bytes(ST));
+  };
   auto buf_bg = [&](int b) {
-    return reinterpret_cast<float4*>(gs + b * bbytes + kBufRec + kBufPix);
+    return reinterpret_cast<float4*>(gs + b * bbytes + buf_rec_bytes(ST) + kBufPix);
   };
 
   unsigned long long p_wait = 0, p_work = 0, p_n = 0, p_first = 0, p_t0 = a.prof ? gtimer() : 0;
@@ -623,7 +629,7 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
     // tickets: the first one of each producer is static (blockIdx, group), later
     // ones come from the global counter (offset by the static range)
     int ticket_k = 0;
-    int tile = a.n_tiles, b0 = 0, L = 0, txy = 0, i0 = 0;
+    int tile = a.n_tiles, b0 = 0, L = 0, txy = 0, i0 = 0, i1 = 0;
     auto next_tile = [&]() {
       int t = blockIdx.x * G + g;
       if (ticket_k++ > 0) {
@@ -655,6 +661,7 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
     };
     auto load_list = [&]() {
       if (tile < a.n_tiles) i0 = lane < L ? __ldg(a.bin_idx + b0 + lane) : 0;
+      if (ST > 32 && tile < a.n_tiles) i1 = lane + 32 < L ? __ldg(a.bin_idx + b0 + lane + 32) : 0;
     };
     next_tile();
     load_list();
@@ -689,7 +696,7 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
         }
         break;
       }
-      const int nst = min(L, kStage);
+      const int nst = min(L, ST);
       const int tx = txy & 0xffff, ty = txy >> 16;
       const int vw = min(kTile, a.W - tx * kTile);
       const int vh = min(kTile, a.H - ty * kTile);
@@ -703,6 +710,10 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
       if (lane < nst) {
         bulk_g2s(buf_rec(buf) + lane, a.recs + i0, sizeof(RecS), &full[g][buf]);
         bulk_g2s(buf_cull(buf) + lane, a.recc + i0, sizeof(RecC), &full[g][buf]);
+      }
+      if (ST > 32 && lane + 32 < nst) {  // (ST = 64: two entries per lane)
+        bulk_g2s(buf_rec(buf) + lane + 32, a.recs + i1, sizeof(RecS), &full[g][buf]);
+        bulk_g2s(buf_cull(buf) + lane + 32, a.recc + i1, sizeof(RecC), &full[g][buf]);
       }
       if (lane < vh) {
         const size_t row = (size_t)(ty * kTile + lane) * a.W + (size_t)tx * kTile;
@@ -737,10 +748,10 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
       const RecC* rc = buf_cull(buf);
       const float4* tgs = buf_tgt(buf);
       const float4* bgs = has_bg ? buf_bg(buf) : nullptr;
-      if (h.z <= kStage) {
+      if (h.z <= ST) {
         warp_tile<LOSS>(a, StagedRecs{rs, rc}, atl, tgs, bgs, stA, stB, h.x, h.y, h.z, h.w, wg);
       } else {
-        warp_tile<LOSS>(a, MixedRecs{rs, rc, a.recs, a.recc, a.bin_idx + h.y}, atl, tgs, bgs,
+        warp_tile<LOSS>(a, MixedRecs<ST>{rs, rc, a.recs, a.recc, a.bin_idx + h.y}, atl, tgs, bgs,
                         stA, stB, h.x, h.y, h.z, h.w, wg);
       }
       __syncwarp();
@@ -832,7 +843,7 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
                            double alpha_w, double w_mse, double w_gray, double inv_3P,
                            double inv_P, void* spill, float* img4,
                            double* part, double* grads, uint32_t* counters,
-                           const int32_t* tile_classes, void* stream) {
+                           const int32_t* tile_classes, int stage, void* stream) {
   if (W < 1 || H < 1 || n < 0 || !bin_off || !bin_idx || !status || !tex || !apad || !tgt4 ||
       !spill || !part || !grads || !counters || pad_texels < 0 || (pad_texels & 3))
     return PF_ERR_ARG;
@@ -905,13 +916,14 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   }
   const size_t budget = (size_t)optin - 1024;  // static smem (barriers, headers)
-  // groups per CTA (PF_STEP_GROUPS overrides for A/B runs); the atlas goes to
-  // shared memory as float64 when it fits, else float32, else stays global
-  int G = 3;
-  if (const char* e = getenv("PF_STEP_GROUPS")) G = atoi(e) == 2 ? 2 : 3;
+  // three groups per CTA; the atlas goes to shared memory as float64 when it
+  // fits, else float32, else stays global; stage depth 64 on the caller's hint
+  // (long tile lists), else 32
+  constexpr int G = 3;
+  const int ST = stage >= 64 ? 64 : 32;
   const bool no64 = getenv("PF_STEP_ATL32") != nullptr;
   const bool bg = bg4 != nullptr;
-  const size_t gb = group_bytes(bg);
+  const size_t gb = group_bytes(bg, ST);
   const size_t a32 = (size_t)pad_texels * sizeof(float), a64 = 2 * a32;
   // atlas placement at the chosen group count: fp64 in shared memory when it
   // fits, else fp32, else the global fp32 plane through L1 -- never fewer groups
@@ -924,16 +936,16 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   }
   const size_t smem = G * gb + (atl == 2 ? a64 : atl == 1 ? a32 : 0);
   void (*kern)(StepArgs);
-#define PF_PICK3(LS, GG)                                                                 \
-  kern = bg ? (atl == 2 ? k_step<LS, 2, GG, true> : atl == 1 ? k_step<LS, 1, GG, true>      \
-                                                           : k_step<LS, 0, GG, true>)       \
-            : (atl == 2 ? k_step<LS, 2, GG, false> : atl == 1 ? k_step<LS, 1, GG, false>    \
-                                                            : k_step<LS, 0, GG, false>);
+#define PF_PICK3(LS, SS)                                                                     \
+  kern = bg ? (atl == 2 ? k_step<LS, 2, 3, true, SS> : atl == 1 ? k_step<LS, 1, 3, true, SS>     \
+                                                            : k_step<LS, 0, 3, true, SS>)        \
+            : (atl == 2 ? k_step<LS, 2, 3, false, SS> : atl == 1 ? k_step<LS, 1, 3, false, SS>   \
+                                                             : k_step<LS, 0, 3, false, SS>);
 #define PF_PICK(LS)      \
-  if (G == 3) {          \
-    PF_PICK3(LS, 3)      \
+  if (ST == 64) {        \
+    PF_PICK3(LS, 64)     \
   } else {               \
-    PF_PICK3(LS, 2)      \
+    PF_PICK3(LS, 32)     \
   }
   if (loss_kind == PF_LOSS_MSE) {
     PF_PICK(PF_LOSS_MSE)
@@ -952,6 +964,6 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
     last_smem = smem;
   }
   const int grid = min(sms, max(1, (n_tiles + G - 1) / G));
-  g_prof_slots = grid * (G == 3 ? step_warps(3) : step_warps(2));
-  return (int)launch_pdl(kern, grid, G == 3 ? step_threads(3) : step_threads(2), smem, st, a);
+  g_prof_slots = grid * step_warps(G);
+  return (int)launch_pdl(kern, grid, step_threads(G), smem, st, a);
 }

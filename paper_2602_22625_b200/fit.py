@@ -349,6 +349,12 @@ class StepEngine:
         self.comp = Compositor(tid, z, self.atlas, W, H, alpha_max=scene.alpha_max,
                                mu_blend=scene.mu_blend, padding=self.padding, capacity=cap,
                                band=band, device=dev)
+        # K34 stage depth from the FULL canvas's capacity bound, so every row band
+        # of a multi-GPU split runs the same kernel configuration (same numerics)
+        nty_full = -(-H // 16)
+        full_cap = cap if (band.ty_begin, band.ty_end) == (0, nty_full) else bin_capacity(
+            scales, tid, self.atlas.hyp, self.padding, 16, -(-W // 16), nty_full)
+        self.comp.stage_hint = 64 if full_cap > 48 * (-(-W // 16)) * nty_full else 32
         # K34 (one kernel for render -> loss -> backward) whenever colour does not
         # come from the texture; PF_TWO_KERNEL=1 forces K3 + K4 (A/B checks)
         self.fused = scene.mu_blend == 0.0 and os.environ.get("PF_TWO_KERNEL", "0") != "1"
