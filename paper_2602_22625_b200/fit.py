@@ -465,12 +465,18 @@ class StepEngine:
         self.host_events = [torch.cuda.Event() for _ in graphs]
         self.host_issued = []  # (iteration, slot) of the host steps in flight / done
 
-    def host_step(self) -> None:
+    def host_step(self, rng: np.random.Generator | None = None) -> None:
         """Enqueue one host-driven step (asynchronous).  host_io engines alternate
         two graphs / loss slots; read a step's loss with host_loss_part(), at most
-        one step behind the newest."""
+        one step behind the newest.  A noise-background scene draws this step's
+        background from ``rng`` (stream-ordered upload, as step())."""
         if self.done >= self.total:
             raise ValueError(f"iteration {self.done} outside [0, {self.total})")
+        if self.noise_bg:
+            if rng is None:
+                raise ValueError("noise background needs the caller's rng")
+            bg = pixels4(noisy_background(self.W, self.H, rng))
+            self.bg4.copy_(torch.from_numpy(bg), non_blocking=False)
         if self.host_io and getattr(self, "host_graphs", None):
             slot = len(self.host_issued) % len(self.host_graphs)
             self.host_graphs[slot].replay()

@@ -559,3 +559,30 @@ def test_long_run_c3(torch_cuda):
     from paper_2602_22625_b200.scene import pack_params
 
     assert np.isfinite(pack_params(sc)[0]).all()
+
+
+def test_host_io_noise_background_matches_step(torch_cuda):
+    """Host-driven steps of a noise-background scene draw the background from the
+    caller's rng every step, like step(): same parameters as the device engine."""
+    import dataclasses
+
+    torch = torch_cuda
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.fit import StepEngine
+
+    w = synth.make_workload("c1")
+    sc = dataclasses.replace(w.scene, background="noise")
+    w.cfg.num_iterations = 7
+    a = StepEngine(sc, w.cfg, w.loss, 7, use_graph=True)
+    b = StepEngine(sc, w.cfg, w.loss, 7, use_graph=True, host_io=True)
+    ra, rb = np.random.default_rng(9), np.random.default_rng(9)
+    a.run(2, ra)
+    b.run(2, rb)
+    b.capture_host_io_step()
+    for _ in range(4):
+        a.step(ra)
+        b.host_step(rb)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(a.params_host(), b.io.numpy()[: b.n * 8])
+    with pytest.raises(ValueError, match="rng"):
+        b.host_step()
