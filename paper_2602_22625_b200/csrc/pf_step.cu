@@ -9,25 +9,30 @@
 // composites a pixel already holds everything its backward needs, and the
 // saved contribution lists never leave the SM.
 //
-// Layout per block (persistent, one CTA per SM slot, tiles from an atomic ticket):
-//   shared  zero-padded fp32 alpha plane of the whole atlas (loaded once per
-//           block; 36 KB at c3), the tile's step records (RecS, 160 B) and cull
-//           records (RecC, 32 B) staged by cp.async in chunks of kS2Stage list
-//           entries, and a per-thread contribution stack kS2KS deep (deeper
-//           entries spill to HBM at a slot unique to (tile, depth, pixel)).
-//   forward  per warp (8x4 pixels): lane-parallel footprint cull of 32 list
-//           entries, then per surviving entry the affine float64 texel map
-//           (2 DFMA per axis; the reference's exact op order re-runs only inside
-//           a guard band around the box edges / the eps threshold), 4 shared
-//           taps, float64 bilinear, eps test, float64 compositing (T, C) --
-//           identical decisions to _kernels.py:183-255 -- and a 32-byte stack
-//           push (list position, incoming T, m, dm/dU, dm/dV, u, v).
-//   loss     pixel-local loss, dL/dI, dL/dA in registers; per-tile partial sums
-//           written at a fixed slot (the fold in pf_adam_preprocess is fixed-order,
-//           so the loss value is deterministic).
-//   backward the same back-to-front warp walk as k_backward (list position picked
-//           with __reduce_max_sync) over the stack, records from shared memory;
-//           warp transpose-butterfly reduction and float64 RED atomics into grads.
+// Layout per CTA (persistent, one per SM; 3 warp groups of 1 producer + 8
+// consumer warps; tiles from a longest-first ticket stream, see pf_bin's classes):
+//   shared  the zero-padded alpha atlas (float64 when it fits next to the groups,
+//           else float32, else read from the global fp32 plane through L1),
+//           per group a 2-slot ring of stage buffers -- ST (32 or 64) step +
+//           cull records (RecS 224 B + RecC 32 B per list entry) and the tile's
+//           target (+ background) rows, all by TMA bulk copies under mbarriers --
+//           and a 5-deep per-pixel contribution stack (deeper entries spill to
+//           HBM at a slot unique to (tile entry, pixel)).
+//   forward  per consumer warp (8x4 pixels): lane-parallel fp32 footprint cull of
+//           32 list entries, then per surviving entry the centred affine float64
+//           texel map (2 DFMA per axis; the reference's exact op order re-runs
+//           only inside a guard band around the box edges / the eps threshold),
+//           4 shared taps, float64 bilinear and eps test -- identical decisions
+//           to _kernels.py:183-255 -- fp32 compositing (T, colour, alpha as
+//           sum T a) and a 20-byte stack push (list position, incoming T, m,
+//           dm/dU, dm/dV).
+//   loss     pixel-local loss, dL/dI, dL/dA in registers (MSE in fp32); per-warp
+//           partial sums written at a fixed slot (folded in fixed order by the
+//           Adam launch, so the loss value is deterministic).
+//   backward back-to-front walk over the stack (list position picked with
+//           __reduce_max_sync), records from shared memory, template coordinates
+//           u, v from the float64 affine map; warp transpose-butterfly reduction
+//           and float64 RED atomics into grads.
 // mu_blend > 0 (colour from the texture) keeps the two-kernel path.
 #include <cstdlib>
 #include <type_traits>
