@@ -23,7 +23,15 @@
 //                    (b) per-column counts (shared-memory atomics) -> block scan
 //                        -> TileBins.offsets for the row's tiles;
 //                    (c) one warp per column walks the row list with ballots and
-//                        writes that tile's z-ascending primitive list.
+//                        writes that tile's z-ascending primitive list (wide
+//                        column blocks: one warp per column segment through a
+//                        warp FIFO of the entries meeting it).
+//   Many primitives x rows (c5, row bands): a two-level path builds the row lists
+//   first -- per-chunk row counts, per-row chunk prefixes, a stable scatter --
+//   and (a) reads them instead of re-reading every rect per (row, column block).
+//   K1 stores records only for primitives that touch a tile of the band, and the
+//   incremental variant (pf_preprocess_sync) only for primitives whose
+//   parameters changed since the device copy.
 // The CSR bins are bit-identical to the reference's offsets/indices.
 #include "../../include/primfit_b200.h"
 #include "pf_bins.cuh"
