@@ -163,3 +163,31 @@ def test_synth_reproduces_reference_structure_aware_init():
 def test_golden_files_present():
     assert len(RENDER_CASES) >= 15
     assert (GOLDEN / "make_golden.py").exists()
+
+
+def test_video_host_logic_matches_reference_semantics():
+    """Host side of the f3 row (no GPU): StuckPolicy validation (dyn.py:44-72),
+    policy_from_config over a config without video fields (reference defaults),
+    and optimize_video's argument checks (dyn.py:190-199)."""
+    import types
+
+    from paper_2602_22625_b200 import video
+    from paper_2602_22625_b200.errors import ShapeMismatch
+
+    for bad in ({"grid": (0, 4)}, {"k": -1}, {"eta": 1.0}, {"zeta": 0.0}):
+        with pytest.raises(ValueError):
+            video.StuckPolicy(**bad)
+    cfg = types.SimpleNamespace(loss="mse", seed=0)
+    pol = video.policy_from_config(cfg)
+    assert (pol.grid, pol.k, pol.triggers) == ((4, 4), 4, (20, 45, 70))
+    cfg2 = types.SimpleNamespace(stuck_grid_x=3, stuck_grid_y=2, stuck_top_k=1,
+                                 stuck_triggers=(5,))
+    pol2 = video.policy_from_config(cfg2)
+    assert (pol2.grid, pol2.k, pol2.triggers) == ((2, 3), 1, (5,))
+    with pytest.raises(ValueError):
+        video.optimize_video([], None, cfg)
+    with pytest.raises(ShapeMismatch):
+        video.optimize_video([np.zeros((4, 4, 3)), np.zeros((5, 4, 3))], None, cfg)
+    with pytest.raises(ValueError):
+        video.optimize_video([np.zeros((4, 4, 3))], None,
+                             types.SimpleNamespace(loss="spatial", seed=0))
