@@ -242,7 +242,7 @@ def _fused_grads(eng, image=True):
             c.color().double().cpu().numpy(), c.alpha().double().cpu().numpy())
 
 
-@pytest.mark.parametrize("name", ["c1", "c3"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
 def test_fused_combined_loss_matches_oracle(torch_cuda, oracle, name):
     """K34 with the combined loss (mse_w * MSE + gray_l1_w * grayscale L1,
     reference fit.py:119-125, 162-168): loss sums and gradients against the
@@ -452,7 +452,7 @@ def test_bins_large_scene_4k(torch_cuda, oracle):
     assert len(h) == 2 and all(np.isfinite(x.loss) for x in h)
 
 
-@pytest.mark.parametrize("kind", ["noise_bg", "aspect_alpha_max"])
+@pytest.mark.parametrize("kind", ["noise_bg", "noise_bg_c2", "aspect_alpha_max"])
 def test_fused_step_bg_and_aspect(torch_cuda, oracle, kind):
     """K34 with a per-pixel (noise) background (the BG kernel variant, staged
     background rows) and with preserve_aspect + alpha_max < 1 templates."""
@@ -465,8 +465,8 @@ def test_fused_step_bg_and_aspect(torch_cuda, oracle, kind):
 
     torch = torch_cuda
     rng = np.random.default_rng(31)
-    w = synth.make_workload("c1")
-    if kind == "noise_bg":
+    w = synth.make_workload("c2" if kind.endswith("c2") else "c1")  # c2: 64-entry stage
+    if kind.startswith("noise_bg"):
         sc = dataclasses.replace(w.scene, background="noise")
         bg = rng.random((sc.canvas_h, sc.canvas_w, 3)).astype(np.float32).astype(np.float64)
         target = w.target
