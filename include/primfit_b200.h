@@ -293,6 +293,19 @@ int pf_fit_step(const void* rec, int n, const double* tex, const float* apad,
 int pf_fold_loss(const double* part, int n_part, double* sums, void* stream);
 
 /*
+ * Cross-band gradient exchange (row-band split; replaces the
+ * sequential tile-order sum of reduce_partials, grad.py:190-206, across bands):
+ * for i in [begin, end): s = srcs[0][i] + srcs[1][i] + ... (fixed order), then
+ * dsts[k][i] = s for every k.  srcs / dsts are HOST arrays of device pointers
+ * (<= PF_MAX_BANDS each; in place is allowed): the band buffers of one device,
+ * or NVLink-mapped peer buffers with [begin, end) = this rank's slice (one-shot
+ * reduce-scatter + all-gather).  Every destination gets bit-identical values.
+ */
+#define PF_MAX_BANDS 16
+int pf_sum_bands(const double* const* srcs, int nsrc, double* const* dsts, int ndst,
+                 long long begin, long long end, void* stream);
+
+/*
  * K5 — fused Adam step (+ loss/psnr history, + gradient zeroing for the next step).
  * Replaces: adam_step (fit.py:195-238), lr_schedule lookup (fit.py:174-186),
  * psnr (fit.py:241-247) and the HistoryEntry bookkeeping (fit.py:505).

@@ -67,6 +67,7 @@ SIGNATURES: dict[str, tuple] = {
          _D, _D, _D, _D, _P, _P, _P, _P, _P, _P, _I, _P],
     ),
     "pf_fold_loss": (_I, [_P, _I, _P, _P]),
+    "pf_sum_bands": (_I, [_P, _I, _P, _I, C.c_longlong, C.c_longlong, _P]),
     "pf_backward": (
         _I,
         [_P, _I, _P, _P, _I, _P, _P, _P, _P, C.c_longlong, _P, _P, _D, _D, _D, _P, _D,

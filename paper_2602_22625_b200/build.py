@@ -14,7 +14,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-SOURCES = ["pf_bin.cu", "pf_render.cu", "pf_step.cu", "pf_adam.cu", "pf_aux.cu"]
+SOURCES = ["pf_bin.cu", "pf_render.cu", "pf_step.cu", "pf_adam.cu", "pf_aux.cu", "pf_comm.cu"]
 HEADERS = ["pf_common.cuh", "pf_bins.cuh"]
 LIB = PKG / "_lib" / "libprimfit_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
