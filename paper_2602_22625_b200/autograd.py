@@ -9,9 +9,9 @@ compositor composes with any torch loss:
     img, alpha = r(params)            # params: (N, 8) float64 CUDA, requires_grad
     ((img - target) ** 2).mean().backward()   # params.grad = dL/dparams
 
-The saved contribution lists live in the per-call Compositor held by ctx
-(the reference keeps them in SavedForward + a fingerprint; autograd's graph
-ownership replaces the fingerprint check).
+The saved contribution lists live in a pooled Compositor held by ctx until
+the backward (the reference keeps them in SavedForward + a fingerprint;
+autograd's graph ownership replaces the fingerprint check).
 """
 
 from __future__ import annotations
@@ -19,39 +19,61 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from .compositor import Compositor, DeviceAtlas, bin_capacity
+from .compositor import Compositor, bin_capacity, cached_atlas
+from .errors import BinOverflow
 from .raster import DEFAULT_EPS_SKIP
 
 
 class _Composite(torch.autograd.Function):
     @staticmethod
     def forward(ctx, params, renderer: "Renderer", bg4):
-        comp = renderer._new_compositor(params)
+        comp = renderer._lease(params)
         comp.preprocess(params)
         comp.bin()
         comp.forward(save=True, eps_skip=renderer.eps_skip, bg_rgb=renderer.bg_rgb, bg4=bg4)
-        ctx.comp = comp
+        renderer._watch(comp)
+        img, alpha = comp.color().clone(), comp.alpha().clone()
+        if torch.is_grad_enabled() and params.requires_grad:
+            ctx.comp = comp  # the saved contribution lists: held until backward
+        else:
+            renderer._give_back(comp)
         ctx.renderer = renderer
         ctx.bg4 = bg4
-        return comp.color().clone(), comp.alpha().clone()
+        return img, alpha
 
     @staticmethod
     def backward(ctx, d_img, d_alpha):
         comp: Compositor = ctx.comp
         r = ctx.renderer
+        r._raise_pending()
         n = comp.n
-        grads = torch.zeros(n * 8 + 4, dtype=torch.float64, device=comp.device)
-        d4 = torch.zeros(r.H, r.W, 4, dtype=torch.float32, device=comp.device)
+        grads = r._grads(n)
+        d4 = r._d4()
+        d4.zero_()
         if d_img is not None:
             d4[:, :, :3] = d_img
         if d_alpha is not None:
             d4[:, :, 3] = d_alpha
         comp.backward(d4.view(-1), grads, bg_rgb=r.bg_rgb, bg4=ctx.bg4)
-        return grads[: n * 8].view(n, 8), None, None
+        out = grads[: n * 8].view(n, 8).clone()
+        ctx.comp = None
+        r._give_back(comp)
+        return out, None, None
 
 
 class Renderer:
-    """Scene structure bound to a device; call with (N, 8) float64 params."""
+    """Scene structure bound to a device; call with (N, 8) float64 params.
+
+    Per call there is no allocation and -- with ``s_max`` -- no host sync: the
+    compositors (HBM buffers sized by the bin capacity) come from a small pool
+    owned by the renderer, a forward's compositor being held by its autograd ctx
+    until the backward ran.  ``s_max`` must bound every scale the renderer sees
+    (an Adam loop with the reference's clamp guarantees it); the kernels flag a
+    capacity overflow on the device and the flag is checked asynchronously:
+    ``BinOverflow`` is raised at the next backward / call once the flagged
+    forward has completed, or at ``check()``.  Without ``s_max`` every call sizes
+    the capacity from the current scales (one device-to-host read).
+    """
 
     def __init__(self, templates, template_id, z, canvas_w: int, canvas_h: int, *,
                  background=(1.0, 1.0, 1.0), alpha_max: float = 1.0, mu_blend: float = 0.0,
@@ -63,23 +85,77 @@ class Renderer:
         self.eps_skip, self.padding, self.s_max = float(eps_skip), float(padding), s_max
         self.tid = np.ascontiguousarray(template_id, dtype=np.int32)
         self.z = np.asarray(z, dtype=np.int64)
-        self.atlas = DeviceAtlas(templates, preserve_aspect, self.dev)
+        self.atlas = cached_atlas(templates, preserve_aspect, self.dev)
         self.d_tid = torch.from_numpy(self.tid).to(self.dev)
         order = np.argsort(self.z, kind="stable").astype(np.int32)
         self.d_zorder = torch.from_numpy(order).to(self.dev)
         self.bg_rgb = tuple(float(c) for c in background)
+        self._free: list[Compositor] = []
+        self._pending: list[tuple] = []  # (event, pinned status copy, capacity)
+        self._gbuf = None
+        self._d4buf = None
 
-    def _new_compositor(self, params: torch.Tensor) -> Compositor:
+    # -- pooled per-call state
+    def _capacity(self, params: torch.Tensor) -> int:
         n = len(self.tid)
         if self.s_max is not None:
             scales = np.full(n, float(self.s_max))
         else:
             scales = params[:, 2].detach().double().cpu().numpy() if n else np.zeros(0)
-        cap = bin_capacity(scales, self.tid, self.atlas.hyp, self.padding, 16,
-                           -(-self.W // 16), -(-self.H // 16))
+        return bin_capacity(scales, self.tid, self.atlas.hyp, self.padding, 16,
+                            -(-self.W // 16), -(-self.H // 16))
+
+    def _lease(self, params: torch.Tensor) -> Compositor:
+        self._raise_pending()
+        cap = self._capacity(params)
+        for i, c in enumerate(self._free):
+            if c.capacity >= cap:
+                return self._free.pop(i)
         return Compositor(self.tid, self.z, self.atlas, self.W, self.H, alpha_max=self.alpha_max,
                           mu_blend=self.mu_blend, padding=self.padding, capacity=cap,
                           device=self.dev, d_tid=self.d_tid, d_zorder=self.d_zorder)
+
+    def _give_back(self, comp: Compositor) -> None:
+        if len(self._free) < 2:
+            self._free.append(comp)
+
+    def _grads(self, n: int) -> torch.Tensor:
+        if self._gbuf is None:
+            self._gbuf = torch.zeros(n * 8 + 4, dtype=torch.float64, device=self.dev)
+        else:
+            self._gbuf.zero_()
+        return self._gbuf
+
+    def _d4(self) -> torch.Tensor:
+        if self._d4buf is None:
+            self._d4buf = torch.zeros(self.H, self.W, 4, dtype=torch.float32, device=self.dev)
+        return self._d4buf
+
+    # -- asynchronous overflow check
+    def _watch(self, comp: Compositor) -> None:
+        st = torch.empty(2, dtype=torch.int32, pin_memory=True)
+        st.copy_(comp.status[:2], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._pending.append((ev, st, comp.capacity))
+
+    def _raise_pending(self, wait: bool = False) -> None:
+        keep = []
+        for ev, st, cap in self._pending:
+            if wait:
+                ev.synchronize()
+            elif not ev.query():
+                keep.append((ev, st, cap))
+                continue
+            if int(st[1]):
+                self._pending = []
+                raise BinOverflow(f"{int(st[0])} bin entries exceed capacity {cap}: a scale "
+                                  f"exceeded s_max={self.s_max}")
+        self._pending = keep
+
+    def check(self) -> None:
+        """Wait for every issued forward and raise BinOverflow if one overflowed."""
+        self._raise_pending(wait=True)
 
     def __call__(self, params: torch.Tensor, bg_img: torch.Tensor | None = None):
         """Render; ``bg_img`` (H, W, 3) is an optional per-pixel background."""

@@ -401,3 +401,60 @@ def adam_launch(params, grads, m, v, *, frozen=None, gains=None, n: int,
             float(alpha_w), 1.0 / (3.0 * P), 1.0 / P, p(hist_loss), p(hist_psnr), p(counter),
             _stream_handle(stream)),
         "pf_adam")
+
+
+# -- per-structure caches for the per-call API (raster.render_forward, grad.backward,
+#    bin_tiles, autograd.Renderer): the atlas upload and the compositor's HBM
+#    buffers are built once per scene structure, not once per call.
+_ATLASES: dict[tuple, DeviceAtlas] = {}
+
+
+def cached_atlas(templates, preserve_aspect: bool, device) -> DeviceAtlas:
+    """DeviceAtlas keyed by template content (sha256 of shape + texels)."""
+    key = (tuple(t.content_hash() if hasattr(t, "content_hash") else
+                 _rgba_hash(np.asarray(t.rgba)) for t in templates),
+           bool(preserve_aspect), str(torch.device(device)))
+    atlas = _ATLASES.get(key)
+    if atlas is None:
+        if len(_ATLASES) >= 16:
+            _ATLASES.pop(next(iter(_ATLASES)))
+        atlas = _ATLASES[key] = DeviceAtlas(templates, preserve_aspect, device)
+    return atlas
+
+
+def _rgba_hash(a: np.ndarray) -> str:
+    import hashlib
+
+    h = hashlib.sha256()
+    h.update(np.asarray(a.shape, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(a, dtype=np.float64).tobytes())
+    return h.hexdigest()
+
+
+class CompositorPool:
+    """Free compositors per structure key.  ``acquire`` returns one whose capacity
+    covers the request (or builds one); ``release`` hands it back once its
+    buffers are no longer referenced (the caller's saved forward state is gone).
+    A leased compositor is never handed out twice, so saved contribution lists
+    stay valid while their SavedForward / autograd ctx lives."""
+
+    def __init__(self, max_keys: int = 8, per_key: int = 2):
+        self.free: dict[tuple, list[Compositor]] = {}
+        self.max_keys, self.per_key = max_keys, per_key
+
+    def acquire(self, key: tuple, capacity: int, factory) -> Compositor:
+        lst = self.free.get(key, [])
+        for i, c in enumerate(lst):
+            if c.capacity >= capacity:
+                return lst.pop(i)
+        return factory(capacity)
+
+    def release(self, key: tuple, comp: Compositor) -> None:
+        lst = self.free.setdefault(key, [])
+        if len(lst) < self.per_key:
+            lst.append(comp)
+        while len(self.free) > self.max_keys:
+            self.free.pop(next(iter(self.free)))
+
+
+POOL = CompositorPool()

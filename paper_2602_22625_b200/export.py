@@ -104,39 +104,192 @@ def render_layer(scene, i: int):
     return render_layers(scene, 1).layer(i)
 
 
-def export_layers(scene, rho: int, outdir: str | Path):
-    """Per-primitive 16-bit PNG layers in paint order, a composite and a text
-    manifest (exportio.py:349-410); the rendering runs on the GPU."""
+@dataclass
+class LayerRecord:
+    """One manifest entry; bbox and file are None for skipped layers
+    (exportio.py:250-258)."""
+
+    z: int
+    prim: int
+    params: tuple[float, ...]
+    bbox: tuple[int, int, int, int] | None
+    file: str | None
+
+
+@dataclass
+class LayerManifest:
+    """Everything needed to re-composite an exported scene (exportio.py:261-269)."""
+
+    scale: int
+    canvas_w: int
+    canvas_h: int
+    background: tuple[float, float, float]
+    composite: str
+    layers: list[LayerRecord]
+
+
+MANIFEST_FORMAT = "primfit-layers"  # exportio.py:75
+MANIFEST_VERSION = 1                # exportio.py:76
+
+
+def save_image(path: str | Path, rgb, alpha=None, bits: int = 8) -> None:
+    """Float RGB(A) in [0, 1] -> 8- or 16-bit PNG, round-half-even quantisation
+    (save_image, exportio.py:108-126)."""
     import cv2  # image encoding only
 
-    if rho not in EXPORT_SCALES:
-        raise ValueError(f"export scale {rho} not in {EXPORT_SCALES}")
+    if bits not in (8, 16):
+        raise ValueError(f"bits must be 8 or 16, got {bits}")
+    peak, dtype = (255, np.uint8) if bits == 8 else (65535, np.uint16)
+    img = np.asarray(rgb, dtype=np.float64)[:, :, ::-1]  # RGB -> BGR (cv2 order)
+    if alpha is not None:
+        img = np.concatenate([img, np.asarray(alpha, dtype=np.float64)[:, :, None]], axis=2)
+    if not cv2.imwrite(str(path), np.rint(np.clip(img, 0.0, 1.0) * peak).astype(dtype)):
+        raise OSError(f"could not write image {path}")
+
+
+def load_image(path: str | Path):
+    """PNG -> float RGB in [0, 1] + optional alpha (load_image, exportio.py:83-106)."""
+    import cv2
+
+    raw = cv2.imread(str(path), cv2.IMREAD_UNCHANGED)
+    if raw is None:
+        raise OSError(f"could not decode {path}")
+    img = raw.astype(np.float64) / (65535.0 if raw.dtype == np.uint16 else 255.0)
+    if img.ndim == 2:
+        return np.repeat(img[:, :, None], 3, axis=2), None
+    if img.shape[2] == 3:
+        return img[:, :, ::-1].copy(), None
+    return img[:, :, 2::-1].copy(), np.ascontiguousarray(img[:, :, 3])
+
+
+def write_manifest(path: str | Path, manifest: LayerManifest) -> None:
+    """The reference's fixed-field manifest grammar (write_manifest,
+    exportio.py:413-431; module docstring 18-33)."""
+    lines = [
+        f"format {MANIFEST_FORMAT}",
+        f"version {MANIFEST_VERSION}",
+        f"scale {manifest.scale}",
+        f"canvas {manifest.canvas_w} {manifest.canvas_h}",
+        "background " + " ".join(repr(float(v)) for v in manifest.background),
+        f"composite {manifest.composite}",
+        f"layers {len(manifest.layers)}",
+    ]
+    for rec in manifest.layers:
+        if rec.bbox is None:
+            mid = "skipped off-canvas"
+        else:
+            x0, y0, x1, y1 = rec.bbox
+            mid = f"bbox {x0} {y0} {x1} {y1} file {rec.file}"
+        params = " ".join(repr(float(v)) for v in rec.params)
+        lines.append(f"layer {rec.z} prim {rec.prim} {mid} params {params}")
+    Path(path).write_text("\n".join(lines) + "\n")
+
+
+def parse_manifest(text: str) -> LayerManifest:
+    """Inverse of write_manifest; ValueError on malformed text (exportio.py:435-478)."""
+    lines = [ln for ln in text.splitlines() if ln.strip()]
+
+    def field(k: int, key: str) -> list[str]:
+        parts = lines[k].split()
+        if parts[0] != key:
+            raise ValueError(f"manifest line {k + 1}: expected {key!r}")
+        return parts[1:]
+
+    if field(0, "format") != [MANIFEST_FORMAT]:
+        raise ValueError("not a layer manifest")
+    if int(field(1, "version")[0]) != MANIFEST_VERSION:
+        raise ValueError("unsupported manifest version")
+    scale = int(field(2, "scale")[0])
+    cw, ch = (int(v) for v in field(3, "canvas"))
+    bg = tuple(float(v) for v in field(4, "background"))
+    composite = field(5, "composite")[0]
+    layers = []
+    for k in range(int(field(6, "layers")[0])):
+        parts = lines[7 + k].split()
+        if parts[0] != "layer" or parts[2] != "prim":
+            raise ValueError(f"manifest layer line {k} malformed")
+        if parts[4] == "bbox" and parts[9] == "file":
+            bbox, file, rest = tuple(int(v) for v in parts[5:9]), parts[10], parts[11:]
+        elif parts[4] == "skipped":
+            bbox, file, rest = None, None, parts[6:]
+        else:
+            raise ValueError(f"manifest layer line {k} malformed")
+        if rest[0] != "params" or len(rest) != 9:
+            raise ValueError(f"manifest layer line {k}: bad params")
+        layers.append(LayerRecord(int(parts[1]), int(parts[3]),
+                                  tuple(float(v) for v in rest[1:]), bbox, file))
+    return LayerManifest(scale, cw, ch, bg, composite, layers)
+
+
+def read_manifest(path: str | Path) -> LayerManifest:
+    return parse_manifest(Path(path).read_text())
+
+
+def compose_layers(manifest: LayerManifest, layer_dir: str | Path):
+    """Back-to-front "over" of the stored premultiplied layers (compose_layers,
+    exportio.py:482-512): the export's consistency check, host-side."""
+    from .raster import RenderOutput
+
+    layer_dir = Path(layer_dir)
+    h, w = manifest.canvas_h, manifest.canvas_w
+    rgb = np.broadcast_to(np.asarray(manifest.background, dtype=np.float64), (h, w, 3)).copy()
+    cov = np.zeros((h, w))
+    for rec in sorted(manifest.layers, key=lambda r: r.z):
+        if rec.file is None:
+            continue
+        lrgb, la = load_image(layer_dir / rec.file)
+        if la is None:
+            raise OSError(f"layer {rec.file} lost its alpha channel")
+        x0, y0, x1, y1 = rec.bbox
+        view = rgb[y0 : y1 + 1, x0 : x1 + 1]
+        view *= 1.0 - la[:, :, None]
+        view += lrgb
+        cov[y0 : y1 + 1, x0 : x1 + 1] = la + (1.0 - la) * cov[y0 : y1 + 1, x0 : x1 + 1]
+    return RenderOutput(color=rgb, alpha=cov)
+
+
+def write_export(scene, rho: int, outdir: str | Path, layer, composite) -> LayerManifest:
+    """The export's file side (exportio.py:370-410): ``layer(i)`` gives primitive
+    i's (bbox, premultiplied float RGBA) on the scaled canvas or raises
+    DegenerateBBox; ``composite`` is the scaled render (H, W, 3).  Layers are
+    written back to front (descending z), 16-bit premultiplied RGB + alpha."""
     outdir = Path(outdir)
     outdir.mkdir(parents=True, exist_ok=True)
+    scaled_w, scaled_h = rho * scene.canvas_w, rho * scene.canvas_h
+    noise = isinstance(scene.background, str)
+    bg = (1.0, 1.0, 1.0) if noise else tuple(float(v) for v in scene.background)
+    z = np.asarray([p.z for p in scene.primitives], dtype=np.int64)
+    paint = np.argsort(z, kind="stable")[::-1]  # ascending z is front to back
+    records = []
+    for k, i in enumerate(int(v) for v in paint):
+        p = scene.primitives[i]
+        params = (p.x, p.y, p.scale, p.rotation, p.opacity_logit, *p.color_logits)
+        params = tuple(float(v) for v in params)
+        try:
+            bbox, rgba = layer(i)
+        except DegenerateBBox:
+            records.append(LayerRecord(k, i, params, None, None))
+            continue
+        name = f"layer_{k:04d}.png"
+        save_image(outdir / name, rgba[:, :, :3], rgba[:, :, 3], bits=16)
+        records.append(LayerRecord(k, i, params, tuple(int(v) for v in bbox), name))
+    save_image(outdir / "composite.png", composite)
+    manifest = LayerManifest(rho, scaled_w, scaled_h, bg, "composite.png", records)
+    write_manifest(outdir / "manifest.txt", manifest)
+    return manifest
+
+
+def export_layers(scene, rho: int, outdir: str | Path) -> LayerManifest:
+    """Per-primitive layers, a composite and the manifest (exportio.py:349-410),
+    rendered on the GPU: all layers in one primitive-parallel launch, the
+    composite through render_forward with eps_skip = 0 and a noise background
+    resolved to white.  Returns the LayerManifest, as the reference."""
+    if rho not in EXPORT_SCALES:
+        raise ValueError(f"export scale {rho} not in {EXPORT_SCALES}")
     layers = render_layers(scene, rho)
     scaled = scale_scene(scene, rho)
     noise = isinstance(scene.background, str)
     bg = (1.0, 1.0, 1.0) if noise else tuple(float(v) for v in scene.background)
-    z = np.asarray([p.z for p in scene.primitives], dtype=np.int64)
-    paint = np.argsort(z, kind="stable")[::-1]  # ascending z composites front-to-back
-    lines = [f"scale {rho}", f"canvas {scaled.canvas_w} {scaled.canvas_h}",
-             "background " + " ".join(repr(v) for v in bg), "composite composite.png"]
-    for k, i in enumerate(paint):
-        try:
-            bbox, rgba = layers.layer(int(i))
-        except DegenerateBBox:
-            lines.append(f"layer {k} {int(i)} none")
-            continue
-        name = f"layer_{k:04d}.png"
-        a = np.clip(rgba[:, :, 3], 0.0, 1.0)
-        c = np.where(a[..., None] > 0, rgba[:, :, :3] / np.maximum(a[..., None], 1e-300), 0.0)
-        img = np.concatenate([c[:, :, ::-1], a[..., None]], axis=2)
-        cv2.imwrite(str(outdir / name), np.round(np.clip(img, 0, 1) * 65535).astype(np.uint16))
-        lines.append(f"layer {k} {int(i)} {' '.join(str(v) for v in bbox)} {name}")
-    out, _ = render_forward(scaled, background=np.broadcast_to(np.asarray(bg),
-                                                               (scaled.canvas_h, scaled.canvas_w, 3)),
-                            eps_skip=0.0)
-    cv2.imwrite(str(outdir / "composite.png"),
-                np.round(np.clip(out.color[:, :, ::-1], 0, 1) * 255).astype(np.uint8))
-    (outdir / "manifest.txt").write_text("\n".join(lines) + "\n")
-    return layers
+    out, _ = render_forward(scaled, background=np.broadcast_to(
+        np.asarray(bg), (scaled.canvas_h, scaled.canvas_w, 3)), eps_skip=0.0)
+    return write_export(scene, rho, outdir, layers.layer, out.color)

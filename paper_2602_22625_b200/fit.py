@@ -42,13 +42,14 @@ _GAIN_GROUPS = ("x", "y", "scale", "rotation", "opacity", "color", "color", "col
 
 @dataclass
 class FitConfig:
-    """Hot-path subset of the reference FitConfig (config.py:20-99), same defaults.
+    """The reference FitConfig (config.py:20-99): same fields, same defaults.
 
-    run_loop accepts any object with these attributes, including the
-    reference's own FitConfig.
+    run_loop / optimize_video accept any object with these attributes,
+    including the reference's own FitConfig.
     """
 
     num_iterations: int = 100
+    sequential_iterations: int = 100
     num_primitives: int = 500
     learning_rate: float = 0.1
     lr_gain_x: float = 10.0
@@ -65,18 +66,41 @@ class FitConfig:
     alpha_loss_weight: float = 0.3
     do_gaussian_blur: bool = True
     blur_sigma: float = 1.0
+    radial_falloff: bool = False
+    initializer: str = "structure_aware"
+    variance_window_size: int = 7
+    variance_base_prob: float = 0.1
+    max_prims_per_pixel: int = 100
+    opacity_logit_init: float = -4.0
+    color_init_noise: float = 0.02
     scale_min: float = 2.0
     scale_max: float = 16.0
     alpha_max: float = 1.0
     mu_blend: float = 0.0
+    bg_color: str = "white"
     preserve_aspect: bool = False
     do_reinit: bool = False
+    reinit_threshold: float = 0.3
+    reinit_period: int = 50
+    reinit_warmup: int = 199
     tile_size: int = 32
     tile_padding: float = 2.0
     eps_skip: float = DEFAULT_EPS_SKIP
+    freeze_static: bool = True
+    diff_threshold: float = 2.0 / 255.0
+    remove_stuck: bool = False
+    stuck_grid_x: int = 4
+    stuck_grid_y: int = 4
+    stuck_top_k: int = 4
+    stuck_tau_scale: float = 0.1
+    stuck_tau_alpha: float = 0.7
+    stuck_zeta: float = 0.7
+    stuck_eta: float = 0.3
+    stuck_triggers: tuple[int, ...] = (20, 45, 70)
     seed: int = 0
     compute_psnr: bool = True
     dump_every: int = 0
+    threads: int = 0
 
 
 @dataclass
@@ -267,8 +291,6 @@ class StepEngine:
     def __init__(self, scene, cfg, loss_spec: LossSpec, total: int, state: OptimState | None = None,
                  *, band: Band | None = None, allreduce: Callable | None = None,
                  use_graph: bool = True, device=None, host_io: bool = False):
-        if getattr(cfg, "do_reinit", False):
-            raise NotImplementedError("low-opacity reinit is outside the ported hot path")
         if loss_spec.kind not in ("mse", "spatial_constrained", "combined"):
             raise ValueError(f"unknown loss kind {loss_spec.kind!r}")
         validate_scene(scene)
@@ -379,11 +401,29 @@ class StepEngine:
     # (the very first step is preceded by a stand-alone K1, see step()).
     def launch_step(self, mark: Callable[[str], None] | None = None,
                     records: bool = True) -> None:
+        mark = mark or (lambda name: None)
+        self.launch_render(mark)
+        if self.allreduce is not None:
+            self.allreduce(self.gbuf)
+            mark("allreduce")
+        self.launch_update(mark, records)
+
+    # The step's two halves around the cross-rank exchange: launch_render fills
+    # gbuf (this band's gradients + loss sums), launch_update applies Adam and
+    # builds the next records.  A caller that drives several band engines with
+    # its own reduction between the halves (tests/test_gpu_multirank.py) calls
+    # them directly; ``reduced`` says the gradients will be summed across bands
+    # before launch_update (the loss partials are then folded into gbuf's sums).
+    def launch_render(self, mark: Callable[[str], None] | None = None,
+                      reduced: bool | None = None) -> None:
         c = self.comp
         mark = mark or (lambda name: None)
+        if reduced is None:
+            reduced = self.allreduce is not None
+        self._reduced = bool(reduced)
         c.bin()
         mark("bin")
-        fold_in_adam = self.fused and self.allreduce is None
+        fold_in_adam = self.fused and not reduced
         if self.fused:
             # one rank: the loss partials are folded inside the Adam launch; with an
             # allreduce they are folded first so the sums travel with the grads
@@ -399,9 +439,12 @@ class StepEngine:
             mark("forward")
             c.backward(c.d4, self.gbuf, bg_rgb=self.bg_rgb, bg4=self.bg4, sums=self.sums)
             mark("backward")
-        if self.allreduce is not None:
-            self.allreduce(self.gbuf)
-            mark("allreduce")
+
+    def launch_update(self, mark: Callable[[str], None] | None = None,
+                      records: bool = True) -> None:
+        c = self.comp
+        mark = mark or (lambda name: None)
+        fold_in_adam = self.fused and not getattr(self, "_reduced", self.allreduce is not None)
         c.adam_preprocess(self.params, self.grads, self.m, self.v, frozen=self.frozen,
                           gains=self.gains, lr_table=self.lr_table, bc1_table=self.bc1_table,
                           bc2_table=self.bc2_table, s_min=self.cfg.scale_min,
@@ -442,8 +485,9 @@ class StepEngine:
         """host_io engines: one CUDA graph = preprocess from the host parameter
         vector (incremental: changed primitives only), bin, fit step, Adam (+ the
         next records) writing the updated vector and the loss partials back to
-        host memory.  The caller edits / reads ``io`` (pinned host) between
-        host_step() replays."""
+        host memory.  The caller reads / edits the parameters between host_step()
+        replays through host_vector() (which first waits for the step in flight:
+        the kernels write and read that memory)."""
         if not self.host_io:
             raise RuntimeError("capture_host_io_step needs StepEngine(host_io=True)")
         if self.graph is None and self.done == 0:
@@ -486,6 +530,18 @@ class StepEngine:
             self.host_graph.replay()
         self.done += 1
 
+    def host_vector(self) -> np.ndarray:
+        """The pinned host parameter vector (8n doubles, primitive-major) for
+        reading or editing between host steps.  Every Adam launch writes it (the
+        mirror) and the next step reads it in place, so it may only be touched
+        while no host step is in flight: this waits for the newest one first.
+        Edits are picked up by the next host_step (changed primitives only)."""
+        if not self.host_io:
+            raise RuntimeError("host_vector needs StepEngine(host_io=True)")
+        if getattr(self, "host_issued", None):
+            self.host_events[self.host_issued[-1][1]].synchronize()
+        return self.io.numpy()[: self.n * 8]
+
     def host_loss_part(self, k: int = -1) -> np.ndarray:
         """Loss partials [adam_blocks][3] of host step k (default: the newest),
         after waiting for that step; valid for the two newest host steps."""
@@ -495,14 +551,18 @@ class StepEngine:
         self.host_events[slot].synchronize()
         return self.loss_slots[slot].numpy().reshape(-1, 3)
 
-    def step(self, rng: np.random.Generator | None = None) -> None:
+    def step(self, rng: np.random.Generator | None = None,
+             background: np.ndarray | None = None) -> None:
+        """One step; a noise-background scene draws this step's background from
+        ``rng`` (or takes the already drawn ``background``, (H, W, 3))."""
         if self.done >= self.total:
             raise ValueError(f"iteration {self.done} outside [0, {self.total})")
         if self.noise_bg:
-            if rng is None:
-                raise ValueError("noise background needs the caller's rng")
-            bg = pixels4(noisy_background(self.W, self.H, rng))
-            self.bg4.copy_(torch.from_numpy(bg), non_blocking=False)
+            if background is None:
+                if rng is None:
+                    raise ValueError("noise background needs the caller's rng")
+                background = noisy_background(self.W, self.H, rng)
+            self.bg4.copy_(torch.from_numpy(pixels4(background)), non_blocking=False)
         if self.graph is not None:
             self.graph.replay()
         else:
@@ -595,43 +655,140 @@ class StepEngine:
                              self.lr_host[i], 0) for i in range(k)]
 
 
+def should_reinit(iteration: int, total: int, period: int, warmup: int) -> bool:
+    """Period boundary, past warmup, a full period still to run (fit.py:250-258)."""
+    return iteration % period == 0 and iteration > warmup and iteration + period <= total
+
+
+def reinit_low_opacity(scene, target, threshold: float = 0.3,
+                       rng: np.random.Generator | None = None, state: OptimState | None = None,
+                       *, s_min: float = 2.0, s_max: float = 16.0, v_init_bias: float = -4.0,
+                       sigma_c: float = 0.02, density_cap: int = 100, base_prob: float = 0.1,
+                       window: int = 7, nlv=None, frozen: np.ndarray | None = None):
+    """Re-seed every non-frozen primitive whose opacity fell below ``threshold``
+    with the structure-aware law, keeping depth and template; zero their Adam
+    moments (fit.py:261-335).  Host-side: a few draws from the caller's rng at a
+    period boundary of the fit loop, in the reference's draw order."""
+    import dataclasses
+
+    from scipy.special import expit
+
+    from .prep import color_logits_near, local_variance_map, sample_cells
+
+    if not 0.0 < threshold < 1.0:
+        raise ValueError(f"threshold {threshold} outside (0, 1)")
+    rng = rng or np.random.default_rng()
+    idx = [i for i, p in enumerate(scene.primitives)
+           if expit(p.opacity_logit) < threshold and (frozen is None or not frozen[i])]
+    if not idx:
+        return scene, 0
+    target = np.asarray(target, dtype=np.float64)
+    h, w = target.shape[:2]
+    if nlv is None:
+        nlv = local_variance_map(target, window)
+    k = len(idx)
+    chosen = sample_cells(nlv.nlv, k, base_prob, density_cap, rng)
+    scales = s_max - (s_max - s_min) * nlv.nlv.reshape(-1)[chosen]
+    thetas = rng.uniform(0.0, 2.0 * np.pi, k)
+    cl = color_logits_near(target[chosen // w, chosen % w, :], sigma_c, rng)
+    prims = list(scene.primitives)
+    for j, i in enumerate(idx):
+        prims[i] = dataclasses.replace(
+            prims[i], x=float(chosen[j] % w), y=float(chosen[j] // w), scale=float(scales[j]),
+            rotation=float(thetas[j]), opacity_logit=v_init_bias,
+            color_logits=(float(cl[j, 0]), float(cl[j, 1]), float(cl[j, 2])))
+    if state is not None:
+        for i in idx:
+            state.m[8 * i : 8 * i + 8] = 0.0
+            state.v[8 * i : 8 * i + 8] = 0.0
+    return dataclasses.replace(scene, primitives=prims), k
+
+
 def run_loop(scene, cfg, loss_spec: LossSpec, rng: np.random.Generator,
              iterations: int | None = None, state: OptimState | None = None, nlv=None,
              log_path: str | Path | None = None, dump_dir: str | Path | None = None,
              hooks: dict[int, Callable] | None = None):
     """GPU fit loop with the reference's contract (fit.py:403-521).
 
-    Returns (scene after the last update, history, state).  History entries
-    describe the render before each update, as in the reference.
+    The steps between host events run as CUDA-graph replays with no host sync.
+    Host events are the iterations where the reference touches the scene on the
+    host: a hook (before that iteration's render), a low-opacity reinit
+    (``cfg.do_reinit`` at should_reinit boundaries, drawing from ``rng`` before
+    the iteration's noise background, as the reference), and an image dump
+    (``dump_dir`` with ``cfg.dump_every``: the iteration's pre-update render).
+    Returns (scene after the last update, history, state); history entries
+    describe the render before each update and carry the reinit counts.
     """
-    if dump_dir is not None and getattr(cfg, "dump_every", 0) > 0:
-        raise NotImplementedError("per-iteration image dumps are outside the ported hot path")
     total = cfg.num_iterations if iterations is None else iterations
     vec, layout = pack_params(scene)
     if state is None:
         state = OptimState.fresh(layout)
     eng = StepEngine(scene, cfg, loss_spec, total, state)
+    g = lambda k, d: getattr(cfg, k, d)  # noqa: E731  (duck-typed FitConfig)
+    reinit = bool(g("do_reinit", False))
+    period, warmup = int(g("reinit_period", 50)), int(g("reinit_warmup", 199))
+    dump_every = int(g("dump_every", 0)) if dump_dir is not None else 0
+    if dump_every > 0:
+        Path(dump_dir).mkdir(parents=True, exist_ok=True)
+    events = set(hooks or ())
+    if reinit:
+        events |= {it for it in range(total) if should_reinit(it, total, period, warmup)}
+    if dump_every > 0:
+        events |= set(range(0, total, dump_every))
+    reinit_counts = [0] * total
     it = 0
     while it < total:
-        if hooks and it in hooks:
-            cur = unpack_params(eng.params_host(), layout, scene)
-            st = eng.sync_state()
-            cur = hooks[it](cur, st)
-            vec2, layout2 = pack_params(cur)
-            if layout2 != layout:
-                raise LayoutMismatch("hooks must keep the primitive count")
-            scene = cur
-            eng.push_host(vec2, st)
-        nxt = total
-        if hooks:
-            later = [k for k in hooks if k > it]
-            if later:
-                nxt = min(nxt, min(later))
+        if it in events:
+            if hooks and it in hooks:
+                cur = unpack_params(eng.params_host(), layout, scene)
+                st = eng.sync_state()
+                cur = hooks[it](cur, st)
+                vec2, layout2 = pack_params(cur)
+                if layout2 != layout:
+                    raise LayoutMismatch("hooks must keep the primitive count")
+                scene = cur
+                eng.push_host(vec2, st)
+            if reinit and should_reinit(it, total, period, warmup):
+                if nlv is None:
+                    from .prep import local_variance_map
+
+                    nlv = local_variance_map(loss_spec.target, int(g("variance_window_size", 7)))
+                cur = unpack_params(eng.params_host(), layout, scene)
+                st = eng.sync_state()
+                cur, count = reinit_low_opacity(
+                    cur, loss_spec.target, float(g("reinit_threshold", 0.3)), rng, st,
+                    s_min=cfg.scale_min, s_max=cfg.scale_max,
+                    v_init_bias=float(g("opacity_logit_init", -4.0)),
+                    sigma_c=float(g("color_init_noise", 0.02)),
+                    density_cap=int(g("max_prims_per_pixel", 100)),
+                    base_prob=float(g("variance_base_prob", 0.1)),
+                    window=int(g("variance_window_size", 7)), nlv=nlv, frozen=st.frozen)
+                reinit_counts[it] = count
+                if count:
+                    scene = cur
+                    eng.push_host(pack_params(cur)[0], st)
+            bg = None
+            if dump_every > 0 and it % dump_every == 0:
+                from .export import save_image
+                from .raster import render_forward
+
+                cur = unpack_params(eng.params_host(), layout, scene)
+                if eng.noise_bg:
+                    bg = noisy_background(eng.W, eng.H, rng)
+                out, _ = render_forward(cur, background=bg, eps_skip=eng.eps_skip)
+                save_image(Path(dump_dir) / f"iter_{it:05d}.png", out.color)
+            eng.step(rng, background=bg)
+            it += 1
+            continue
+        later = [k for k in events if k > it]
+        nxt = min(later) if later else total
         eng.run(nxt - it, rng)
         it = nxt
     eng.check()
     state = eng.sync_state()
     history = eng.history(getattr(cfg, "compute_psnr", True))
+    for h in history:
+        h.reinit_count = reinit_counts[h.iteration]
     if log_path is not None:
         with open(log_path, "w", newline="") as fh:
             w = csv.writer(fh)

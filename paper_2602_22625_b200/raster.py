@@ -19,12 +19,14 @@ host CSR arrays.
 from __future__ import annotations
 
 import math
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
 import torch
 
-from .compositor import RENDER_TILE, Compositor, DeviceAtlas, bin_capacity, pixels4
+from .compositor import (POOL, RENDER_TILE, Compositor, DeviceAtlas, bin_capacity, cached_atlas,
+                         pixels4)
 from .errors import ShapeMismatch
 from .scene import NOISE_BACKGROUND, FloatArray, param_matrix, scene_fingerprint, structure_arrays, validate_scene
 
@@ -129,32 +131,54 @@ def _device():
 
 def make_compositor(scene, *, padding: float, bin_tile: int = RENDER_TILE,
                     params: np.ndarray | None = None, device=None) -> tuple[Compositor, torch.Tensor]:
-    """Upload a scene and size a compositor whose capacity bounds this scene's bins."""
+    """Upload a scene and size a compositor whose capacity bounds this scene's bins
+    (a fresh one; the per-call API leases pooled ones through lease_compositor)."""
+    comp, d_params, _ = lease_compositor(scene, padding=padding, bin_tile=bin_tile,
+                                         params=params, device=device)
+    return comp, d_params
+
+
+def lease_compositor(scene, *, padding: float, bin_tile: int = RENDER_TILE,
+                     params: np.ndarray | None = None, device=None):
+    """(compositor, device params, release) for one call: the atlas is cached by
+    template content and the compositor comes from the per-structure pool;
+    ``release()`` returns it once its buffers are no longer needed."""
     dev = device or _device()
     pm = param_matrix(scene) if params is None else params
     tid, z = structure_arrays(scene)
-    atlas = DeviceAtlas(scene.templates, bool(scene.preserve_aspect), dev)
+    atlas = cached_atlas(scene.templates, bool(scene.preserve_aspect), dev)
     ntx = -(-scene.canvas_w // bin_tile)
     nty = -(-scene.canvas_h // bin_tile)
     cap = bin_capacity(pm[:, 2] if len(pm) else np.zeros(0), tid, atlas.hyp, padding,
                        bin_tile, ntx, nty)
-    comp = Compositor(tid, z, atlas, scene.canvas_w, scene.canvas_h,
-                      alpha_max=scene.alpha_max, mu_blend=scene.mu_blend, padding=padding,
-                      capacity=cap, bin_tile=bin_tile, device=dev)
+    tid32 = np.ascontiguousarray(tid, dtype=np.int32)
+    z64 = np.ascontiguousarray(z, dtype=np.int64)
+    key = (id(atlas), tid32.tobytes(), z64.tobytes(), scene.canvas_w, scene.canvas_h,
+           float(scene.alpha_max), float(scene.mu_blend), float(padding), int(bin_tile), str(dev))
+
+    def factory(capacity):
+        return Compositor(tid32, z64, atlas, scene.canvas_w, scene.canvas_h,
+                          alpha_max=scene.alpha_max, mu_blend=scene.mu_blend, padding=padding,
+                          capacity=capacity, bin_tile=bin_tile, device=dev)
+
+    comp = POOL.acquire(key, cap, factory)
     d_params = torch.from_numpy(np.ascontiguousarray(pm, dtype=np.float64)).to(dev)
-    return comp, d_params
+    return comp, d_params, (lambda: POOL.release(key, comp))
 
 
 def bin_tiles(scene, tile_size: int = DEFAULT_TILE_SIZE,
               padding: float = DEFAULT_TILE_PADDING) -> TileBins:
     """GPU tile binning (K1 + K2), bit-identical to the reference's bin_tiles."""
     validate_scene(scene)
-    comp, d_params = make_compositor(scene, padding=padding, bin_tile=tile_size)
-    comp.preprocess(d_params)
-    comp.bin()
-    k = comp.check_overflow()
-    offsets = comp.bin_off.cpu().numpy().astype(np.int64)
-    indices = comp.bin_idx[:k].cpu().numpy().astype(np.int32)
+    comp, d_params, release = lease_compositor(scene, padding=padding, bin_tile=tile_size)
+    try:
+        comp.preprocess(d_params)
+        comp.bin()
+        k = comp.check_overflow()
+        offsets = comp.bin_off.cpu().numpy().astype(np.int64)
+        indices = comp.bin_idx[:k].cpu().numpy().astype(np.int32)
+    finally:
+        release()
     return TileBins(tile_size, padding, scene.canvas_w, scene.canvas_h, comp.ntx, comp.nty,
                     offsets, indices)
 
@@ -170,25 +194,33 @@ def render_forward(scene, bins: TileBins | None = None, background=None, save: b
         padding = bins.padding
     bg = resolve_background(scene, background)
     rgb = _solid_rgb(scene, background)
-    comp, d_params = make_compositor(scene, padding=padding)
+    comp, d_params, release = lease_compositor(scene, padding=padding)
     dev = comp.device
     bg4 = None
     if rgb is None:
         bg4 = torch.from_numpy(pixels4(bg)).to(dev)
         rgb = (0.0, 0.0, 0.0)
-    comp.preprocess(d_params)
-    comp.bin()
-    comp.forward(save=save, eps_skip=eps_skip, bg_rgb=rgb, bg4=bg4)
-    comp.check_overflow()
-    H, W = scene.canvas_h, scene.canvas_w
-    color = comp.color().double().cpu().numpy()
-    alpha = comp.alpha().double().cpu().numpy()
+    try:
+        comp.preprocess(d_params)
+        comp.bin()
+        comp.forward(save=save, eps_skip=eps_skip, bg_rgb=rgb, bg4=bg4)
+        comp.check_overflow()
+        H, W = scene.canvas_h, scene.canvas_w
+        color = comp.color().double().cpu().numpy()
+        alpha = comp.alpha().double().cpu().numpy()
+    except BaseException:
+        release()
+        raise
     out = RenderOutput(color, alpha)
     if not save:
+        release()
         return out, None
     saved = SavedForward(
         canvas_w=W, canvas_h=H, compositor=comp, t_final=1.0 - alpha, background=bg,
         bg_rgb=None if bg4 is not None else rgb, bg4=bg4,
         fingerprint=scene_fingerprint(scene), eps_skip=eps_skip,
         n_entries=int(comp.ent_n.sum().item()))
+    # the saved contribution lists live in the leased compositor's buffers: it
+    # goes back to the pool only when this SavedForward is collected
+    weakref.finalize(saved, release)
     return out, saved

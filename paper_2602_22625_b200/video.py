@@ -138,8 +138,8 @@ def remove_stuck(scene, frozen: np.ndarray | None, policy: StuckPolicy):
 
 
 def policy_from_config(cfg) -> StuckPolicy:
-    """StuckPolicy from a FitConfig's video fields (dyn.py:74-83); this package's
-    FitConfig has no video fields, so the reference defaults stand in."""
+    """StuckPolicy from a FitConfig's video fields (dyn.py:74-83); missing fields
+    take the reference defaults."""
     g = lambda k, d: getattr(cfg, k, d)  # noqa: E731
     return StuckPolicy(grid=(int(g("stuck_grid_y", 4)), int(g("stuck_grid_x", 4))),
                        k=int(g("stuck_top_k", 4)), tau_scale=float(g("stuck_tau_scale", 0.1)),
@@ -148,21 +148,25 @@ def policy_from_config(cfg) -> StuckPolicy:
                        triggers=tuple(g("stuck_triggers", (20, 45, 70))))
 
 
-def optimize_video(frames, init, cfg):
+def optimize_video(frames, templates, cfg):
     """Fit one scene per frame, warm-starting each from the previous
-    (dyn.py:180-238): frame 0 runs ``cfg.num_iterations`` steps; every later
-    frame runs ``cfg.sequential_iterations`` from fresh Adam moments, with the
-    primitives whose binning box misses every changed pixel frozen
-    (``freeze_static``; diff_mask + freeze_flags on the GPU) and the stuck-
-    primitive decay applied at the policy's trigger iterations (``remove_stuck``).
-    Every step runs in the GPU fit loop (fit.run_loop).
+    (dyn.py:180-238), every step in the GPU fit loop (fit.run_loop).
 
-    ``init`` is the frame-0 scene (the reference builds it with prep.init_scene,
-    which is outside the ported path) or a template list, in which case the
-    scene is this package's restated structure-aware init (synth.py).
+    As the reference: ``templates`` (a template list, or None for the built-in
+    default) go through prepare_templates with the config's blur / falloff, and
+    frame 0's scene comes from init_scene (initializer, opacity / colour init,
+    density cap, variance window, background, alpha_max, mu_blend,
+    preserve_aspect) drawing from ``default_rng(cfg.seed)``; frame 0 runs
+    ``cfg.num_iterations`` steps; every later frame runs
+    ``cfg.sequential_iterations`` from fresh Adam moments, with the primitives
+    whose binning box misses every changed pixel frozen (``freeze_static``;
+    diff_mask + freeze_flags on the GPU) and the stuck-primitive decay at the
+    policy's trigger iterations (``remove_stuck``).  Extension: a prepared
+    ``Scene`` in place of ``templates`` is used as frame 0's scene directly.
     Returns (scenes, histories), one per frame.
     """
     from .fit import LossSpec, OptimState, effective_padding, run_loop
+    from .prep import default_templates, init_scene, prepare_templates
     from .scene import Scene, pack_params
 
     if not frames:
@@ -174,35 +178,37 @@ def optimize_video(frames, init, cfg):
     if cfg.loss in ("spatial", "spatial_constrained"):
         raise ValueError("spatial loss is single-image only")
     rng = np.random.default_rng(cfg.seed)
-    if isinstance(init, Scene):
-        scene = init
+    g = lambda k, d: getattr(cfg, k, d)  # noqa: E731  (duck-typed FitConfig)
+    if isinstance(templates, Scene):
+        scene = templates
     else:
-        from .synth import structure_aware_scene
-
-        scene = structure_aware_scene(frames[0], list(init), int(cfg.num_primitives),
-                                      float(cfg.scale_min), float(cfg.scale_max), rng)
+        tpls = prepare_templates(list(templates) if templates else default_templates(),
+                                 blur_sigma=g("blur_sigma", 1.0),
+                                 do_blur=g("do_gaussian_blur", True),
+                                 falloff=g("radial_falloff", False))
+        scene = init_scene(frames[0], tpls, cfg, rng)
     padding = effective_padding(cfg)
     policy = policy_from_config(cfg)
 
-    def spec(frame):
-        return LossSpec(kind=cfg.loss, target=frame, mse_w=cfg.mse_weight,
-                        gray_l1_w=cfg.gray_l1_weight)
+    def spec(frame):  # dyn.py:241-247
+        return LossSpec(kind=cfg.loss, target=frame, mse_w=g("mse_weight", 1.0),
+                        gray_l1_w=g("gray_l1_weight", 0.0))
 
     scene, hist, _ = run_loop(scene, cfg, spec(frames[0]), rng, iterations=cfg.num_iterations)
     scenes, histories = [scene], [hist]
     for f in range(1, len(frames)):
         _, layout = pack_params(scene)
         state = OptimState.fresh(layout)
-        if getattr(cfg, "freeze_static", True):
+        if g("freeze_static", True):
             mask = diff_mask(frames[f - 1], frames[f],
-                             float(getattr(cfg, "diff_threshold", DEFAULT_DIFF_THRESHOLD)))
+                             float(g("diff_threshold", DEFAULT_DIFF_THRESHOLD)))
             state.frozen = freeze_flags(scene, mask, padding)
         hooks = None
-        if getattr(cfg, "remove_stuck", False):
+        if g("remove_stuck", False):
             hooks = {t: (lambda s, st: remove_stuck(s, st.frozen, policy)[0])
                      for t in policy.triggers}
         scene, hist, state = run_loop(scene, cfg, spec(frames[f]), rng,
-                                      iterations=int(getattr(cfg, "sequential_iterations", 100)),
+                                      iterations=int(g("sequential_iterations", 100)),
                                       state=state, hooks=hooks)
         scenes.append(scene)
         histories.append(hist)

@@ -23,7 +23,9 @@ from paper_2602_22625_b200.scene import PrimitiveParams, PrimitiveTemplate, Scen
 
 RENDER_CASES = sorted(
     Path(p).stem for p in glob.glob(str(GOLDEN / "*.npz"))
-    if Path(p).stem not in ("adam_rollout", "run_loop_small", "synth_c1_init", "video_heuristics")
+    if Path(p).stem not in ("adam_rollout", "run_loop_small", "synth_c1_init", "video_heuristics",
+                            "reinit_unit", "run_loop_reinit", "run_loop_reinit_noise",
+                            "video_dropin")
     and not Path(p).stem.startswith("export_")
 )
 

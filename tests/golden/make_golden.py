@@ -281,7 +281,85 @@ def aux_cases():
     np.savez_compressed(OUT / "video_heuristics.npz", **d)
 
 
+def loop_cases():
+    """f1 / f3 callers of the fit loop, straight from the reference: low-opacity
+    reinit (fit.reinit_low_opacity, fit.py:261-335, unit + inside run_loop at
+    period boundaries, also with a noise background so the rng draw order is
+    pinned) and the video driver (dyn.optimize_video, dyn.py:180-238, default
+    templates)."""
+    from primfit import dyn as rdyn
+    from paper_2602_22625_b200 import synth
+
+    # unit: reinit on a scene with mixed opacities, some frozen, non-zero moments
+    sc = random_scene(5, n=30, w=48, h=40)
+    rng = np.random.default_rng(17)
+    prims = list(sc.primitives)
+    for i in range(len(prims)):
+        prims[i].opacity_logit = float(-3.0 if i % 3 else 1.5)
+    target = synth.smooth_target(48, 40, seed=5)
+    vec, layout = pack_params(sc)
+    st = rfit.OptimState.fresh(layout)
+    st.m[:] = rng.normal(size=st.m.shape)
+    st.v[:] = rng.random(st.v.shape)
+    frozen = np.zeros(sc.n, dtype=bool)
+    frozen[[1, 4, 7]] = True
+    d = scene_arrays(sc)
+    d.update(target=target, m0=st.m.copy(), v0=st.v.copy(), frozen=frozen)
+    new, count = rfit.reinit_low_opacity(sc, target, 0.3, np.random.default_rng(23), st,
+                                         s_min=2.0, s_max=9.0, v_init_bias=-4.0, sigma_c=0.02,
+                                         density_cap=100, base_prob=0.1, window=7, frozen=frozen)
+    d.update(new_params=pack_params(new)[0].reshape(-1, 8), count=np.int64(count), m1=st.m,
+             v1=st.v)
+    np.savez_compressed(OUT / "reinit_unit.npz", **d)
+    print("reinit unit", count)
+
+    # run_loop with reinit every 3 iterations past warmup 1 (boundaries 3 and 6)
+    tpls = [PrimitiveTemplate(t.rgba) for t in synth.prepare([synth.disc(32)])]
+    for name, bg in (("run_loop_reinit", "white"), ("run_loop_reinit_noise", "noise")):
+        target = synth.smooth_target(64, 48, seed=3)
+        cfg = rconfig.FitConfig(num_iterations=9, num_primitives=40, seed=3, scale_min=2.0,
+                                scale_max=9.0, do_reinit=True, reinit_period=3,
+                                reinit_warmup=1, bg_color=bg)
+        scene = rfit.init_scene(target, tpls, cfg, np.random.default_rng(3))
+        for i, p in enumerate(scene.primitives):
+            if i % 2 == 0:
+                p.opacity_logit = 1.0  # well above the threshold: never re-seeded
+        spec = rfit.LossSpec(kind="mse", target=target)
+        scene_end, hist, st = rfit.run_loop(scene, cfg, spec, np.random.default_rng(4))
+        d = scene_arrays(scene)
+        d.update(target=target, final_params=pack_params(scene_end)[0].reshape(-1, 8),
+                 hist_loss=np.asarray([h.loss for h in hist]),
+                 hist_psnr=np.asarray([h.psnr for h in hist]),
+                 hist_lr=np.asarray([h.lr for h in hist]),
+                 hist_reinit=np.asarray([h.reinit_count for h in hist]), m=st.m, v=st.v,
+                 iters=np.int64(9), scale_min=2.0, scale_max=9.0,
+                 padding=np.float64(rfit.effective_padding(cfg)))
+        np.savez_compressed(OUT / f"{name}.npz", **d)
+        print(name, [h.reinit_count for h in hist], hist[0].loss, hist[-1].loss)
+
+    # the video driver: default templates, init_scene from the config, 2 frames
+    f0 = synth.smooth_target(48, 40, seed=8)
+    f1 = f0.copy()
+    f1[10:25, 12:30] = 1.0 - f1[10:25, 12:30]
+    cfg = rconfig.FitConfig(num_iterations=5, sequential_iterations=4, num_primitives=30,
+                            seed=5, scale_min=2.0, scale_max=8.0, freeze_static=True,
+                            remove_stuck=True, stuck_triggers=(1, 3), stuck_tau_scale=0.5,
+                            stuck_tau_alpha=0.5)
+    scenes, hists = rdyn.optimize_video([f0, f1], None, cfg)
+    np.savez_compressed(
+        OUT / "video_dropin.npz", f0=f0, f1=f1,
+        params0=pack_params(scenes[0])[0].reshape(-1, 8),
+        params1=pack_params(scenes[1])[0].reshape(-1, 8),
+        loss0=np.asarray([h.loss for h in hists[0]]), loss1=np.asarray([h.loss for h in hists[1]]),
+        tid=np.asarray([p.template_id for p in scenes[0].primitives]),
+        z=np.asarray([p.z for p in scenes[0].primitives]), tpl0=scenes[0].templates[0].rgba)
+    print("video", hists[0][-1].loss, hists[1][-1].loss)
+
+
 if __name__ == "__main__":
+    if "--loops" in sys.argv:
+        loop_cases()
+        raise SystemExit(0)
     if "--aux" in sys.argv:
         aux_cases()
         raise SystemExit(0)

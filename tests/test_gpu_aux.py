@@ -102,3 +102,29 @@ def test_optimize_video_chain(torch_cuda):
     assert 0 < frozen.sum() < len(frozen)
     np.testing.assert_array_equal(p1[frozen], p0[frozen])
     assert (p1[~frozen] != p0[~frozen]).any(axis=1).all()
+
+
+@pytest.mark.parametrize("rho", [1, 2])
+def test_export_layers_files_recompose(torch_cuda, tmp_path, rho):
+    """export_layers end to end on the GPU: the reference's file format (premultiplied
+    16-bit layers, write_manifest grammar), re-composited back to front within PNG
+    quantisation of render_forward on the scaled canvas (exportio.py:482-512; the
+    reference's bar, test_export.py:250-254)."""
+    import dataclasses
+
+    from paper_2602_22625_b200 import export, raster
+
+    sc = scene_from(load_case("export_random"))
+    prims = list(sc.primitives)
+    prims[2] = dataclasses.replace(prims[2], x=-500.0, y=-500.0)
+    sc = dataclasses.replace(sc, primitives=prims)
+    man = export.export_layers(sc, rho, tmp_path)
+    assert isinstance(man, export.LayerManifest)
+    assert export.read_manifest(tmp_path / "manifest.txt") == man
+    assert [r.prim for r in man.layers if r.file is None] == [2]
+    scaled = export.scale_scene(sc, rho)
+    bg = np.broadcast_to(np.asarray(man.background), (scaled.canvas_h, scaled.canvas_w, 3))
+    ref, _ = raster.render_forward(scaled, background=bg, eps_skip=0.0)
+    composed = export.compose_layers(man, tmp_path)
+    assert np.abs(composed.color - ref.color).max() < 5e-4
+    assert np.abs(composed.alpha - ref.alpha).max() < 5e-4

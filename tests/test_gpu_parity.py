@@ -161,3 +161,49 @@ def test_gpu_run_loop_rollout(pf):
     got = pack_params(end)[0].reshape(-1, 8)
     np.testing.assert_allclose(got, d["final_params"], rtol=1e-4, atol=1e-5)
     assert st.step == int(d["iters"])
+
+
+@pytest.mark.parametrize("case", ["run_loop_reinit", "run_loop_reinit_noise"])
+def test_gpu_run_loop_reinit(pf, case):
+    """run_loop with low-opacity reinit at period boundaries (fit.py:454-475):
+    the reinit draws come from the caller's rng before the iteration's noise
+    background, exactly as the reference; reinit counts, loss history and final
+    parameters against the reference's own run."""
+    _, _, fit = pf
+    from paper_2602_22625_b200.scene import pack_params
+
+    d = load_case(case)
+    sc = scene_from(d)
+    cfg = fit.FitConfig(num_iterations=int(d["iters"]), num_primitives=sc.n, seed=3,
+                        scale_min=float(d["scale_min"]), scale_max=float(d["scale_max"]),
+                        do_reinit=True, reinit_period=3, reinit_warmup=1)
+    spec = fit.LossSpec(kind="mse", target=d["target"])
+    end, hist, st = fit.run_loop(sc, cfg, spec, np.random.default_rng(4))
+    assert [h.reinit_count for h in hist] == list(d["hist_reinit"])
+    np.testing.assert_allclose([h.loss for h in hist], d["hist_loss"], rtol=1e-5)
+    np.testing.assert_allclose([h.psnr for h in hist], d["hist_psnr"], rtol=1e-6)
+    got = pack_params(end)[0].reshape(-1, 8)
+    np.testing.assert_allclose(got, d["final_params"], rtol=1e-4, atol=1e-5)
+    assert st.step == int(d["iters"])
+
+
+def test_gpu_optimize_video_dropin(pf):
+    """video.optimize_video(frames, None, cfg) against dyn.optimize_video: default
+    templates through prepare_templates, init_scene from the config, frame 1
+    with freezing and stuck decay at the trigger iterations."""
+    _, _, fit = pf
+    from paper_2602_22625_b200 import video
+    from paper_2602_22625_b200.scene import pack_params
+
+    d = load_case("video_dropin")
+    cfg = fit.FitConfig(num_iterations=5, sequential_iterations=4, num_primitives=30, seed=5,
+                        scale_min=2.0, scale_max=8.0, freeze_static=True, remove_stuck=True,
+                        stuck_triggers=(1, 3), stuck_tau_scale=0.5, stuck_tau_alpha=0.5)
+    scenes, hists = video.optimize_video([d["f0"], d["f1"]], None, cfg)
+    np.testing.assert_array_equal(np.asarray(scenes[0].templates[0].rgba), d["tpl0"])
+    assert [p.template_id for p in scenes[0].primitives] == list(d["tid"])
+    np.testing.assert_allclose([h.loss for h in hists[0]], d["loss0"], rtol=1e-5)
+    np.testing.assert_allclose([h.loss for h in hists[1]], d["loss1"], rtol=1e-5)
+    for k in (0, 1):
+        got = pack_params(scenes[k])[0].reshape(-1, 8)
+        np.testing.assert_allclose(got, d[f"params{k}"], rtol=1e-4, atol=1e-5)

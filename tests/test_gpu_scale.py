@@ -183,11 +183,11 @@ def test_host_io_zero_copy_matches_device(torch_cuda):
     n = b.n
     for k in range(5):
         if k == 2:  # host edit: move every primitive by +0.75 px in x
-            edited = b.io.numpy()[: n * 8].reshape(n, 8)
+            edited = b.host_vector().reshape(n, 8)
             edited[:, 0] += 0.75
             a.params[:, 0] += 0.75
         if k == 3:  # sparse edit: three primitives jump by 40 px (other tiles)
-            edited = b.io.numpy()[: n * 8].reshape(n, 8)
+            edited = b.host_vector().reshape(n, 8)
             for i in (0, 17, n - 1):
                 edited[i, 1] += 40.0
                 a.params[i, 1] += 40.0
