@@ -39,19 +39,34 @@ def _peaks() -> dict:
 
 
 def algorithmic_bytes(P: int, K16: int, N: int, atlas_texels: int) -> dict:
-    """B_step = 68 P + 12 K16 + 288 N + 16 * texels (fp32 model)."""
+    """B_step = 68 P + 12 K16 + 288 N + A, A = 16 * texels (the
+    fp32 model of the reference's per-step tensors), split by the kernel that
+    does that work in this implementation:
+      bin   (K2)    the bin index written                       4 K16
+      step  (K34)   every per-pixel term (the render, loss and
+                    backward all run in it), the index read by
+                    forward and backward, the gradient write, A  68 P + 8 K16 + 32 N + A
+      adam  (K1+K5) parameter read in preprocess + the Adam
+                    touches (p r/w, m r/w, v r/w, g r)          256 N
+    The two-kernel path splits `step` into forward 48 P + 4 K16 + A and
+    backward 20 P + 4 K16 + 32 N."""
     A = 16 * atlas_texels
     return {
         "total": 68 * P + 12 * K16 + 288 * N + A,
-        # per-kernel split of the same model (DESIGN.md §5)
+        "bin": 4 * K16,
+        "step": 68 * P + 8 * K16 + 32 * N + A,
+        "adam": 256 * N,
         "forward": 48 * P + 4 * K16 + A,
         "backward": 20 * P + 4 * K16 + 32 * N,
-        # K34 fused render+loss+backward: target in, per-entry index + records,
-        # atlas taps (the contribution stack never leaves the SM)
-        "step": 16 * P + 4 * K16 + 256 * N + A,
-        "bin": 4 * K16 + 32 * N,
-        "adam": 224 * N,
     }
+
+
+def compulsory_bytes(P: int, K16: int, N: int, atlas_texels: int) -> int:
+    """This implementation's own compulsory HBM traffic of the fused K34 launch
+    (target in, per-entry index + staged records, atlas; the image, dL/dI and the
+    contribution lists never leave the SM): 16 P + 4 K16 + 256 N + A.  Reported
+    beside the §8(d) figure; ncu's dram bytes per launch sit close to it."""
+    return 16 * P + 4 * K16 + 256 * N + 16 * atlas_texels
 
 
 class ClockSampler:
@@ -139,6 +154,24 @@ def cpu_baseline(config: str, max_seconds: float = 15.0, max_steps: int = 20) ->
             "ms_per_step": med * 1e3, "cpu_model": _cpu_model()}
 
 
+def numba_reference_baseline(config: str, timeout_s: float = 300.0) -> dict | None:
+    """The UNMODIFIED numba reference (baseline/_ref) timed on its own run_loop
+    body (scripts/numba_ref_step.py, subprocess: numba's pool owns every core),
+    or None when it is not installed / not importable on this host."""
+    import subprocess
+
+    if not (ROOT / "baseline" / "_ref" / "primfit").is_dir():
+        return None
+    try:
+        r = subprocess.run([sys.executable, str(ROOT / "scripts" / "numba_ref_step.py"), config,
+                            "5", "15"], capture_output=True, text=True, timeout=timeout_s)
+        out = json.loads(r.stdout.strip().splitlines()[-1])
+        out["cpu_model"] = _cpu_model()
+        return out
+    except Exception as exc:  # noqa: BLE001 - a reported reading, never the product
+        return {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
+
+
 def _cpu_model() -> str:
     try:
         for line in open("/proc/cpuinfo"):
@@ -180,6 +213,7 @@ def run_reference(args) -> None:
                                    f"float64, bit-identical to it on golden vectors)",
                          "cpu_model": _cpu_model()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline_reference": numba_reference_baseline(args.config),
     }
     print(json.dumps(line), flush=True)
 
@@ -383,11 +417,14 @@ def run_ours(args) -> None:
     ab = algorithmic_bytes(eng.P, K16, n, eng.atlas.texels)
     dom = max(("forward", "backward", "step"), key=lambda k: stage_ms.get(k, 0.0))
     achieved = ab[dom] / (stage_ms[dom] * 1e-3) / 1e9
+    comp_b = compulsory_bytes(eng.P, K16, n, eng.atlas.texels)
     cpu = cpu_baseline(args.config) if (world == 1 and not args.no_cpu) else None
+    cpu_ref = numba_reference_baseline(args.config) if (world == 1 and not args.no_cpu) else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "mixed (f64 decisions/params/Adam, f32 compositing/gradients)",
         "data": "synthetic (seeded structure-aware init; procedural templates; smooth random target)",
         "config": {**_config(args.config, w), "parallelism": f"rowband{world}",
                    "K16": K16, "band": [band.ty_begin, band.ty_end]},
@@ -396,8 +433,15 @@ def run_ours(args) -> None:
                      "frac": achieved / peaks["hbm_gbs"],
                      "traffic": ncu_traffic(KNAME[dom]),
                      "peak_src": peaks["src"], "algorithmic_bytes": ab[dom],
+                     "bytes_model": "SURVEY 8(d) share of the dominant kernel: "
+                                    "68 P + 8 K16 + 32 N + 16 texels",
                      "kernel_ms": stage_ms[dom],
+                     # the whole step: 8(d) B_step over the device-timed step
                      "step_frac": ab["total"] * value / 1e9 / peaks["hbm_gbs"],
+                     "step_bytes": ab["total"],
+                     # this implementation's compulsory traffic of the same launch
+                     "compulsory_bytes": comp_b,
+                     "compulsory_frac": comp_b / (stage_ms[dom] * 1e-3) / 1e9 / peaks["hbm_gbs"],
                      # what does bound it: instruction issue (ncu summary of the
                      # same kernel: warp instructions per SM cycle against 4)
                      "issue_frac": issue_frac(KNAME[dom])},
@@ -418,6 +462,9 @@ def run_ours(args) -> None:
         "kernels_per_step": nodes,
         "clocks": clk,
         "cpu_baseline": cpu,
+        # second CPU reading: the unmodified numba reference itself (slower than
+        # the port above, which stays the baseline)
+        "cpu_baseline_reference": cpu_ref,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -57,6 +57,10 @@ extern "C" {
 /* ABI version; bumped on any signature change. */
 int pf_abi_version(void);
 
+/* Diagnostics: the PF_* environment switches (A/B variants, profiling) are read
+ * once at load; this re-reads them (tests that flip a switch at run time). */
+int pf_diag_reload(void);
+
 /* Bytes of the per-primitive device record written by pf_preprocess
  * (replaces PackedScene, raster.py:45-96, as the kernels' view of a scene). */
 size_t pf_record_bytes(void);

@@ -201,10 +201,28 @@ def lr_schedule(it: int, total: int, base: float, decay: bool = True, final: flo
     return base * final ** (it / (total - 1))
 
 
-class Loop:
-    """The body of fit.run_loop (mse loss, solid background) on the oracle."""
+GRAY = np.asarray([0.299, 0.587, 0.114])
 
-    def __init__(self, scene, target, cfg, padding: float, tile: int = 32):
+
+def loss_gray_l1(I, t):
+    """loss_grayscale_l1 (fit.py:119-125): mean |luma(I - t)| and its subgradient."""
+    d = (I - t) @ GRAY
+    return float(np.mean(np.abs(d))), (np.sign(d)[:, :, None] * GRAY[None, None, :]) / d.size
+
+
+def loss_combined(I, t, mse_w: float, gray_w: float):
+    """evaluate_loss kind "combined" (fit.py:162-168)."""
+    vm, gm = loss_mse(I, t)
+    vg, gg = loss_gray_l1(I, t)
+    return mse_w * vm + gray_w * vg, mse_w * gm + gray_w * gg
+
+
+class Loop:
+    """The body of fit.run_loop (solid background; mse, or the combined loss with
+    ``loss=("combined", mse_w, gray_w)``) on the oracle."""
+
+    def __init__(self, scene, target, cfg, padding: float, tile: int = 32, loss=None):
+        self.loss = loss
         self.pk = Packed(scene)
         self.target = np.asarray(target, dtype=np.float64)
         self.cfg = cfg
@@ -226,7 +244,10 @@ class Loop:
         self.pk.set_params(self.vec)
         off, idx = bin_tiles(self.pk, self.tile, self.padding)
         img, alpha, sv = render_forward(self.pk, off, idx, self.tile, self.bg, True, c.eps_skip)
-        value, dI = loss_mse(img, self.target)
+        if self.loss is None:
+            value, dI = loss_mse(img, self.target)
+        else:
+            value, dI = loss_combined(img, self.target, self.loss[1], self.loss[2])
         g = backward(self.pk, sv, dI, None).reshape(-1)
         self.t += 1
         adam(self.vec, g, self.m, self.v, self.t, lr, gains8=self.gains8, s_min=c.scale_min,

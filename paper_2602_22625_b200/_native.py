@@ -37,6 +37,7 @@ _Z = C.c_size_t
 # name -> (restype, argtypes); mirrors include/primfit_b200.h one to one
 SIGNATURES: dict[str, tuple] = {
     "pf_abi_version": (_I, []),
+    "pf_diag_reload": (_I, []),
     "pf_record_bytes": (_Z, []),
     "pf_render_tile": (_I, []),
     "pf_bin_scratch_bytes": (_Z, [_I, _I, _I]),

@@ -33,7 +33,7 @@ class _Composite(torch.autograd.Function):
         comp.forward(save=True, eps_skip=renderer.eps_skip, bg_rgb=renderer.bg_rgb, bg4=bg4)
         renderer._watch(comp)
         img, alpha = comp.color().clone(), comp.alpha().clone()
-        if torch.is_grad_enabled() and params.requires_grad:
+        if ctx.needs_input_grad[0]:
             ctx.comp = comp  # the saved contribution lists: held until backward
         else:
             renderer._give_back(comp)

@@ -1,3 +1,4 @@
+#include <mutex>
 // K5 fused Adam step + loss/psnr history + gradient zeroing.
 //
 // Reference: adam_step (pkg/src/primfit/fit.py:195-238):
@@ -150,6 +151,60 @@ extern "C" long long pf_saved_capacity(int capacity) {
   return (long long)capacity * (long long)kTilePix;
 }
 
+static pf::Diag read_diag() {
+    using pf::Diag;
+    auto flag = [](const char* k) { return getenv(k) != nullptr; };
+    auto num = [](const char* k, int dflt) { const char* e = getenv(k); return e ? atoi(e) : dflt; };
+    Diag v;
+    v.no_pdl = flag("PF_NO_PDL");
+    v.step_lazy = flag("PF_STEP_LAZY");
+    v.step_nolpt = flag("PF_STEP_NOLPT");
+    v.step_prof = flag("PF_STEP_PROF");
+    v.step_atl32 = flag("PF_STEP_ATL32");
+    v.step_atl0 = flag("PF_STEP_ATL0");
+    v.timeline = flag("PF_TIMELINE");
+    v.csleep = (unsigned)num("PF_CSLEEP", 200);
+    v.psleep = (unsigned)num("PF_PSLEEP", 500);
+    v.bin_ncb = num("PF_BIN_NCB", -1);
+    v.bin_two_level = num("PF_BIN_TWO_LEVEL", -1);
+    return v;
+}
+static pf::Diag g_diag = read_diag();
+const pf::Diag& pf::diag() { return g_diag; }
+// Diagnostics only: re-read the PF_* switches (tests that flip them at run time).
+extern "C" int pf_diag_reload(void) {
+  g_diag = read_diag();
+  return 0;
+}
+
+cudaError_t pf::ensure_dyn_smem(const void* kern, size_t smem) {
+  struct Entry {
+    int dev;
+    const void* kern;
+    size_t smem;
+  };
+  static Entry table[256];
+  static int used = 0;
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < used; ++i) {
+    Entry& e = table[i];
+    if (e.dev == dev && e.kern == kern) {
+      if (smem <= e.smem) return cudaSuccess;
+      const cudaError_t r =
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (r == cudaSuccess) e.smem = smem;
+      return r;
+    }
+  }
+  const cudaError_t r =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (r == cudaSuccess && used < 256) table[used++] = Entry{dev, kern, smem};
+  return r;
+}
+
 // Diagnostics timeline buffer (see tl_mark in pf_common.cuh): allocated on the
 // first call when PF_TIMELINE is set in the environment, else NULL.
 static unsigned long long* g_tl = nullptr;
@@ -158,7 +213,7 @@ unsigned long long* pf::pf_timeline_ptr() {
   static bool checked = false;
   if (!checked) {
     checked = true;
-    if (getenv("PF_TIMELINE")) {
+    if (diag().timeline) {
       cudaMalloc(&g_tl, sizeof(unsigned long long) * 64);
       pf_timeline_reset();
     }

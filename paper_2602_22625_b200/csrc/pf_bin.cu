@@ -1037,21 +1037,13 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
   return launch_prim(true, a, (cudaStream_t)stream);
 }
 
-static int sms_count() {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return sms;
-}
+static int sms_count() { return dev_attrs().sms; }
 
 static int row_blocks(int n, int n_rows, int ntx, bool cache) {
   // column blocks per row: as many as fit in one wave (1024-thread blocks, one
   // per SM with the register cache), >= 16 columns each
   int ncb = (cache ? 1 : 2) * sms_count() / n_rows;
-  if (const char* e = getenv("PF_BIN_NCB")) ncb = atoi(e);  // diagnostics (A/B)
+  if (diag().bin_ncb >= 0) ncb = diag().bin_ncb;  // diagnostics (A/B)
   return max(1, min(ncb, ntx / 16));
 }
 
@@ -1060,7 +1052,7 @@ static int row_blocks(int n, int n_rows, int ntx, bool cache) {
 // PF_BIN_TWO_LEVEL=0/1 (A/B and tests).
 static bool bin_two_level(int n, int n_rows, int ncb, size_t scat_smem) {
   bool two = (size_t)n * (size_t)n_rows * (size_t)ncb > 2000000u;
-  if (const char* e = getenv("PF_BIN_TWO_LEVEL")) two = atoi(e) != 0;
+  if (diag().bin_two_level >= 0) two = diag().bin_two_level != 0;
   return two && n > 0 && n_rows <= kMaxRows2 && scat_smem <= 200 * 1024;
 }
 
@@ -1110,21 +1102,16 @@ extern "C" int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, i
   const size_t smem = sizeof(int2) * kRowSmemList + 3 * sizeof(int) * (size_t)ntx;
   const bool cache = (n + kRowThreads - 1) / kRowThreads <= kRowCache;
   void (*kern)(RowArgs) = cache ? k_bin_rows<true> : k_bin_rows<false>;
-  static size_t attr_smem[2] = {0, 0};
-  if (smem > attr_smem[cache]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(smem > 48 * 1024 ? smem : 48 * 1024));
-    attr_smem[cache] = smem;
-  }
+  // (always: the kernel's static shared memory plus 48 KB dynamic exceeds the
+  // default per-block limit, so the opt-in attribute is needed at any size)
+  if (const cudaError_t e = ensure_dyn_smem((const void*)kern, smem > 48 * 1024 ? smem : 48 * 1024))
+    return (int)e;
   int ncb = row_blocks(n, n_rows, ntx, cache);
   const size_t scat_smem = scatter_smem(n_rows);
   if (bin_two_level(n, n_rows, ncb, scat_smem)) {
-    static size_t attr_scat = 0;
-    if (scat_smem > attr_scat) {
-      cudaFuncSetAttribute(k_row_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(scat_smem > 48 * 1024 ? scat_smem : 48 * 1024));
-      attr_scat = scat_smem;
-    }
+    if (const cudaError_t e = ensure_dyn_smem((const void*)k_row_scatter,
+                                              scat_smem > 48 * 1024 ? scat_smem : 48 * 1024))
+      return (int)e;
     const int chunks = div_up(n, kRowChunk);
     int e = (int)launch_pdl2(k_row_counts, dim3(chunks), kRowChunk, sizeof(int2) * n_rows, st, ra);
     if (e == 0) e = (int)launch_pdl2(k_row_offsets, dim3(div_up(n_rows, 4)), 128, 0, st, ra, chunks);

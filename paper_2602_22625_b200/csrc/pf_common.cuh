@@ -292,6 +292,35 @@ __device__ __forceinline__ void tl_mark(unsigned long long* tl, int slot, int wh
 }
 unsigned long long* pf_timeline_ptr();
 
+// ---- host-side launch helpers, per device (one process may drive several GPUs)
+constexpr int kMaxDevices = 64;
+struct DevAttrs {
+  int sms, optin;  // SM count, opt-in shared memory per block
+};
+inline DevAttrs dev_attrs() {
+  static DevAttrs cache[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevAttrs a = {0, 0};
+  if (dev >= 0 && dev < kMaxDevices && cache[dev].sms > 0) return cache[dev];
+  cudaDeviceGetAttribute(&a.sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&a.optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (dev >= 0 && dev < kMaxDevices) cache[dev] = a;  // (benign race: same values)
+  return a;
+}
+// cudaFuncAttributeMaxDynamicSharedMemorySize >= smem for `kern` on the current
+// device, set at most once per (device, kernel) and size increase.
+cudaError_t ensure_dyn_smem(const void* kern, size_t smem);
+
+// Diagnostics switches (A/B runs, profiling), read from the environment once per
+// process -- never on the launch path.
+struct Diag {
+  bool no_pdl, step_lazy, step_nolpt, step_prof, step_atl32, step_atl0, timeline;
+  unsigned csleep, psleep;
+  int bin_ncb, bin_two_level;  // -1: not set
+};
+const Diag& diag();
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl2(void (*kern)(KArgs...), dim3 grid, int block, size_t smem,
                                cudaStream_t st, Args&&... args) {
@@ -303,9 +332,8 @@ inline cudaError_t launch_pdl2(void (*kern)(KArgs...), dim3 grid, int block, siz
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  static const bool no_pdl = getenv("PF_NO_PDL") != nullptr;  // A/B switch
   cfg.attrs = attr;
-  cfg.numAttrs = no_pdl ? 0 : 1;
+  cfg.numAttrs = diag().no_pdl ? 0 : 1;  // (A/B switch PF_NO_PDL)
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 template <typename... KArgs, typename... Args>

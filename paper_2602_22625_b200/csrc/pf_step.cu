@@ -897,36 +897,32 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   a.spill = (float4*)spill;
   a.grads = grads;
   a.ctr = counters;
-  a.sched_lazy = getenv("PF_STEP_LAZY") ? 1 : 0;
-  a.csleep = getenv("PF_CSLEEP") ? (unsigned)atoi(getenv("PF_CSLEEP")) : 200u;
-  a.psleep = getenv("PF_PSLEEP") ? (unsigned)atoi(getenv("PF_PSLEEP")) : 500u;
-  a.classes = getenv("PF_STEP_NOLPT") ? nullptr : tile_classes;
+  const Diag& dg = diag();
+  a.sched_lazy = dg.step_lazy ? 1 : 0;
+  a.csleep = dg.csleep;
+  a.psleep = dg.psleep;
+  a.classes = dg.step_nolpt ? nullptr : tile_classes;
   a.classes_rw = const_cast<int32_t*>(a.classes);
   a.tile_cost = tile_classes ? const_cast<int32_t*>(tile_classes) + tile_cost_offset(n_tiles)
                              : nullptr;
   a.prof = nullptr;
   a.tl = pf_timeline_ptr();
   static unsigned long long* prof_buf = nullptr;
-  if (getenv("PF_STEP_PROF")) {
+  if (dg.step_prof) {
     if (!prof_buf) cudaMalloc(&prof_buf, sizeof(unsigned long long) * (6 * 148 * 32 + 65536 * 8));
     a.prof = prof_buf;
   }
   g_prof_buf = prof_buf;
   cudaStream_t st = (cudaStream_t)stream;
-  static int sms = 0, optin = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  }
+  const DevAttrs da = dev_attrs();
+  const int sms = da.sms, optin = da.optin;
   const size_t budget = (size_t)optin - 1024;  // static smem (barriers, headers)
   // three groups per CTA; the atlas goes to shared memory as float64 when it
   // fits, else float32, else stays global; stage depth 64 on the caller's hint
   // (long tile lists), else 32
   constexpr int G = 3;
   const int ST = stage >= 64 ? 64 : 32;
-  const bool no64 = getenv("PF_STEP_ATL32") != nullptr;
+  const bool no64 = dg.step_atl32;
   const bool bg = bg4 != nullptr;
   const size_t gb = group_bytes(bg, ST);
   const size_t a32 = (size_t)pad_texels * sizeof(float), a64 = 2 * a32;
@@ -935,7 +931,7 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   // (measured at c5, 4 templates: 3 groups + global atlas 422 us/step against
   // 2 groups + shared fp32 atlas 485 us)
   int atl = 0;
-  if (getenv("PF_STEP_ATL0") == nullptr) {  // (diagnostics: force the global plane)
+  if (!dg.step_atl0) {  // (diagnostics: force the global plane)
     if (apad64 && !no64 && G * gb + a64 <= budget) atl = 2;
     else if (G * gb + a32 <= budget) atl = 1;
   }
@@ -961,13 +957,7 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   }
 #undef PF_PICK3
 #undef PF_PICK
-  static void (*last_kern)(StepArgs) = nullptr;
-  static size_t last_smem = 0;
-  if (kern != last_kern || smem != last_smem) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    last_kern = kern;
-    last_smem = smem;
-  }
+  if (const cudaError_t e = ensure_dyn_smem((const void*)kern, smem)) return (int)e;
   const int grid = min(sms, max(1, (n_tiles + G - 1) / G));
   g_prof_slots = grid * step_warps(G);
   return (int)launch_pdl(kern, grid, step_threads(G), smem, st, a);

@@ -92,8 +92,18 @@ def test_step_engine_matches_oracle_loop(torch_cuda, oracle, name, total):
     assert np.all(np.abs(p_gpu - p_ref) <= bound[None, :])
 
 
+@pytest.fixture
+def diag_reload():
+    """Re-read the PF_* switches after the test's monkeypatch is undone (list this
+    fixture before monkeypatch so its teardown runs after the env is restored)."""
+    yield
+    from paper_2602_22625_b200 import _native
+
+    _native.load().pf_diag_reload()
+
+
 @pytest.mark.parametrize("name,two", [("c3", "1"), ("c5", "auto"), ("c5", "0")])
-def test_bins_two_level_bit_exact(torch_cuda, oracle, monkeypatch, name, two):
+def test_bins_two_level_bit_exact(diag_reload, torch_cuda, oracle, monkeypatch, name, two):
     """Both binning paths (one-level row scan; two-level row counts + stable
     scatter, the default for c5) against the oracle's bin_tiles, full canvas and
     every band of an 8-way row split (the multi-GPU bands)."""
@@ -101,8 +111,13 @@ def test_bins_two_level_bit_exact(torch_cuda, oracle, monkeypatch, name, two):
     from paper_2602_22625_b200.dist import row_bands
     from paper_2602_22625_b200.fit import effective_padding
 
+    from paper_2602_22625_b200 import _native
+
     if two != "auto":
         monkeypatch.setenv("PF_BIN_TWO_LEVEL", two)
+    else:
+        monkeypatch.delenv("PF_BIN_TWO_LEVEL", raising=False)
+    _native.load().pf_diag_reload()  # the switches are read once per process
     w = synth.make_workload(name)
     sc = w.scene
     pad = effective_padding(w.cfg)
@@ -586,3 +601,39 @@ def test_host_io_noise_background_matches_step(torch_cuda):
     np.testing.assert_array_equal(a.params_host(), b.io.numpy()[: b.n * 8])
     with pytest.raises(ValueError, match="rng"):
         b.host_step()
+
+
+@pytest.mark.parametrize("name,total,loss", [("c1", 8, "mse"), ("c1", 8, "combined"),
+                                             ("c3", 5, "mse")])
+def test_two_kernel_step_engine_matches_oracle_loop(torch_cuda, oracle, name, total, loss):
+    """The two-kernel StepEngine path (mu_blend > 0: K3 forward with the loss fused
+    and saved 16-byte entries, K4 backward, K5+K1) against the oracle's run_loop
+    body over a graph-replayed rollout, for MSE and the combined loss on K3."""
+    import dataclasses
+
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.fit import LossSpec, StepEngine, effective_padding
+
+    w = synth.make_workload(name)
+    sc = dataclasses.replace(w.scene, mu_blend=0.3)
+    w.cfg.num_iterations = total
+    spec = w.loss if loss == "mse" else LossSpec(kind="combined", target=w.target, mse_w=0.7,
+                                                 gray_l1_w=0.4)
+    eng = StepEngine(sc, w.cfg, spec, total)
+    assert not eng.fused
+    loop = oracle.Loop(sc, w.target, w.cfg, effective_padding(w.cfg), tile=32,
+                       loss=None if loss == "mse" else ("combined", 0.7, 0.4))
+    for it in range(total):
+        eng.step()
+        loop.step(it, total)
+    eng.check()
+    np.testing.assert_allclose([h.loss for h in eng.history()], [h[1] for h in loop.history],
+                               rtol=1e-5)
+    p_gpu = eng.params_host().reshape(-1, 8)
+    p_ref = loop.vec.reshape(-1, 8)
+    close = np.isclose(p_gpu, p_ref, rtol=1e-4, atol=1e-4)
+    # (the combined loss's L1 term has a sign() subgradient: pixels with d ~ 0
+    # flip with round-off, so a few more components carry Adam noise)
+    assert close.mean() > (0.99 if loss == "mse" else 0.98), close.mean()
+    gains = np.asarray([10, 10, 10, 1, 1.5, 1, 1, 1.0])
+    assert np.all(np.abs(p_gpu - p_ref) <= 2 * w.cfg.learning_rate * gains[None, :] * total)
