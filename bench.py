@@ -265,6 +265,68 @@ def ncu_traffic(kernel_prefix: str) -> float | None:
     return float(v["dram_traffic_bytes"]) if v else None
 
 
+def autograd_bench(w, steps: int, warmup: int, flush) -> dict:
+    """The north_star's autograd entry point in a plain training loop: the
+    Renderer's torch.autograd.Function (K1+K2+K3 forward, K4 backward) under a
+    torch MSE loss, then the device Adam (pf_adam table mode), no host sync per
+    step (s_max bounds the capacity).  CUDA-event timed, L2 flushed per step."""
+    import torch
+
+    from paper_2602_22625_b200.autograd import Renderer
+    from paper_2602_22625_b200.compositor import adam_launch
+    from paper_2602_22625_b200.fit import _cfg_gains, effective_padding, lr_schedule
+    from paper_2602_22625_b200.scene import param_matrix, structure_arrays
+
+    sc, cfg = w.scene, w.cfg
+    tid, z = structure_arrays(sc)
+    r = Renderer(sc.templates, tid, z, sc.canvas_w, sc.canvas_h,
+                 background=tuple(sc.background), alpha_max=sc.alpha_max,
+                 mu_blend=sc.mu_blend, preserve_aspect=sc.preserve_aspect,
+                 eps_skip=cfg.eps_skip, padding=effective_padding(cfg), s_max=cfg.scale_max)
+    dev = torch.device("cuda")
+    params = torch.tensor(param_matrix(sc), device=dev, requires_grad=True)
+    target = torch.tensor(w.target, device=dev, dtype=torch.float32)
+    n = params.shape[0]
+    m = torch.zeros(n * 8, dtype=torch.float64, device=dev)
+    v = torch.zeros_like(m)
+    total = warmup + steps
+    lr = torch.tensor([lr_schedule(i, total, cfg.learning_rate) for i in range(total)],
+                      dtype=torch.float64, device=dev)
+    bc1 = torch.tensor([1 - 0.9 ** (i + 1) for i in range(total)], dtype=torch.float64, device=dev)
+    bc2 = torch.tensor([1 - 0.999 ** (i + 1) for i in range(total)], dtype=torch.float64,
+                       device=dev)
+    it = torch.zeros(1, dtype=torch.int32, device=dev)
+    ctr = torch.zeros(1, dtype=torch.int32, device=dev)
+    gains = _cfg_gains(cfg)
+
+    def step():
+        img, _ = r(params)
+        loss = ((img - target) ** 2).mean()
+        loss.backward()
+        with torch.no_grad():
+            adam_launch(params.view(-1), params.grad.view(-1), m, v, gains=gains, n=n,
+                        lr_table=lr, bc1_table=bc1, bc2_table=bc2, iter_counter=it, counter=ctr,
+                        clamp=True, s_min=cfg.scale_min, s_max=cfg.scale_max, zero_grads=True)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for e0, e1 in evs:
+        flush.zero_()
+        e0.record()
+        step()
+        e1.record()
+    torch.cuda.synchronize()
+    r.check()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / steps
+    return {"value": 1e3 / ms, "unit": UNIT, "ms_per_step": ms,
+            "path": "autograd.Renderer forward (K1+K2+K3) + torch MSE + backward (K4) + pf_adam; "
+                    "no host sync per step",
+            "l2": "flushed (256 MiB write) before every timed step"}
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -408,6 +470,10 @@ def run_ours(args) -> None:
                 "l2": "not flushed (back-to-back steps, as run_loop issues them)"}
         eng.check()
 
+    autograd = None
+    if world == 1 and not args.no_autograd:
+        autograd = autograd_bench(w, max(10, args.steps // 2), 3, flush)
+
     nodes = eng.kernels_per_step
     if rank != 0:
         if world > 1:
@@ -453,6 +519,7 @@ def run_ours(args) -> None:
                               for k in ("l1tex_hit_pct", "warp_exec_efficiency_threads",
                                         "fp64_pipe_pct", "warps_active_pct")}},
         "run_loop": loop,
+        "autograd": autograd,
         "stage_ms": stage_ms,
         "e2e": {"value": 1e3 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": n * 8 * 8,
                 "d2h_bytes_per_step": n * 8 * 8 + nb * 3 * 8,
@@ -479,6 +546,7 @@ def main() -> None:
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-autograd", action="store_true", help="skip the autograd sub-line")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

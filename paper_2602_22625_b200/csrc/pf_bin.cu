@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
     tl_mark(a.tl, 0, 3);
     return;
   }
-  if (tid == 0) {
+  if (tid == 0 && !a.prebuilt) {  // (prebuilt: already published above)
     s_rl = tot;
     s_base = base;
     s_rbase = rbase;
