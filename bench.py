@@ -233,9 +233,11 @@ KNAME = {"step": "k_step", "forward": "k_forward", "backward": "k_backward"}
 def ncu_summary(kernel_prefix: str) -> dict | None:
     """The named kernel's entry of the newest committed ncu --set full summary
     under profiles/ (scripts/ncu_extract.py), or None."""
-    def version(f: Path) -> int:  # r01_ncu_kernels_v11.json -> 11 (natural order)
+    def version(f: Path) -> tuple:  # (round, version): r02_* after r01_*_v11
+        rnd = f.stem.split("_", 1)[0]
         tail = f.stem.rsplit("_v", 1)
-        return int(tail[1]) if len(tail) == 2 and tail[1].isdigit() else -1
+        return (int(rnd[1:]) if rnd[1:].isdigit() else -1,
+                int(tail[1]) if len(tail) == 2 and tail[1].isdigit() else -1)
 
     files = sorted((ROOT / "profiles").glob("*ncu_kernels*.json"), key=version)
     for f in reversed(files):
