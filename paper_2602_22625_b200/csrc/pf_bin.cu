@@ -195,14 +195,6 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
     }
   }
   if (live && c == 0 && grp_changed) a.s.rect[pi.zrank] = rc;
-  // this block's rects are published: K2 starts binning on the count of
-  // publishing blocks (done[4]) instead of this whole grid, so the record
-  // math below overlaps the binning (K2 waits for the grid only at its end)
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(a.s.done + 4, 1u);
-  }
   // records only for primitives in some tile of this band: nothing reads the
   // others' (every consumer walks the tile lists) -- on a row band of a
   // multi-GPU split most primitives skip the work below
@@ -369,7 +361,6 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
 
 struct RowArgs {
   int n, ntx, ty_begin, n_rows, cap, smem_list;
-  uint32_t rect_blocks;  // K1 blocks that publish rects before this binning (done[4])
   BinScratch s;
   int32_t* bin_off;
   int32_t* bin_idx;
@@ -391,51 +382,15 @@ constexpr int kRowThreads = 1024;
 // into the per-row lists, z order kept (chunk, then warp, then lane order).
 // k_bin_rows then starts from the prebuilt row lists instead of scanning all
 // rects.
-// Start of K2: wait until every K1 block has published its rects (done[4]),
-// not for the whole K1 grid (its records are still being written).  Bounded:
-// a binning not preceded by a K1 launch falls back to the grid dependency wait.
-__device__ __forceinline__ void wait_rects(const RowArgs& a) {
-  if (threadIdx.x == 0) {
-    if (a.rect_blocks == 0) {
-      pdl_wait();
-    } else {
-      const unsigned long long t0 = gtime_ns();
-      unsigned v;
-      for (;;) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.s.done + 4) : "memory");
-        if (v >= a.rect_blocks) break;
-        if (gtime_ns() - t0 > 200000ull) {  // (no K1 in flight: 200 us, then the grid wait)
-          pdl_wait();
-          break;
-        }
-        __nanosleep(32);
-      }
-    }
-  }
-  __syncthreads();
-}
-
-// End of K2 (every exit path): wait for the whole K1 grid, so that this grid's
-// completion -- what the fit step waits for -- implies K1's (records, Adam);
-// the last block past wait_rects re-arms the counters for the next step.
-__device__ __forceinline__ void finish_rects(const RowArgs& a, unsigned grid_blocks) {
-  pdl_wait();
-  if (threadIdx.x == 0 && a.rect_blocks) {
-    if (atomicAdd(a.s.done + 5, 1u) == grid_blocks - 1) {
-      atomicExch(a.s.done + 4, 0u);
-      atomicExch(a.s.done + 5, 0u);
-    }
-  }
-}
-
 __global__ void __launch_bounds__(kRowChunk) k_row_counts(RowArgs a) {
   extern __shared__ int2 sc[];  // [n_rows]
   const int tid = threadIdx.x;
   tl_mark(a.tl, 11, 0);
   for (int r = tid; r < a.n_rows; r += kRowChunk) sc[r] = make_int2(0, 0);
-  wait_rects(a);  // rects come from K1
+  pdl_wait();  // rects come from K1
   tl_mark(a.tl, 11, 1);
   pdl_trigger();
+  __syncthreads();
   const int zp = blockIdx.x * kRowChunk + tid;
   if (zp < a.n) {
     const int4 rc = a.s.rect[zp];
@@ -450,7 +405,6 @@ __global__ void __launch_bounds__(kRowChunk) k_row_counts(RowArgs a) {
   __syncthreads();
   for (int r = tid; r < a.n_rows; r += kRowChunk)
     a.s.rowcnt[(size_t)blockIdx.x * a.n_rows + r] = sc[r];
-  finish_rects(a, gridDim.x);
   tl_mark(a.tl, 11, 3);
 }
 
@@ -593,30 +547,14 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
   const int cbeg = (int)((long long)a.ntx * cb / ncb), cend = (int)((long long)a.ntx * (cb + 1) / ncb);
   const int tid = threadIdx.x;
   tl_mark(a.tl, 0, 0);
-  // rects: from K1 (published per block, wait_rects), or from the two-level
-  // passes (prebuilt row lists: the grid dependency on k_row_scatter)
-  if (a.prebuilt) {
-    pdl_wait();
-  } else {
-    wait_rects(a);
-  }
+  pdl_wait();     // rects come from K1
   tl_mark(a.tl, 0, 1);
-  // (early: the fit step waits for this grid, whose completion waits for K1's)
-  pdl_trigger();
-  const unsigned nblk = gridDim.x * gridDim.y;
-  auto finish = [&]() {
-    if (a.prebuilt) {
-      pdl_wait();
-    } else {
-      finish_rects(a, nblk);
-    }
-    if (r == 0 && cb == 0 && tid == 0 && a.s.done[2]) {
-      // the Adam step before this binning is complete (K1 grid done): advance
-      // the iteration counter
-      a.s.done[1] += 1u;
-      a.s.done[2] = 0u;
-    }
-  };
+  pdl_trigger();  // after the wait: a dependent that starts early sees K1 complete
+  if (r == 0 && cb == 0 && tid == 0 && a.s.done[2]) {
+    // the Adam step before this binning is complete: advance the iteration counter
+    a.s.done[1] += 1u;
+    a.s.done[2] = 0u;
+  }
 
   // measured cost of this thread's column tile (first column of its chunk; read
   // early so the load overlaps the scan)
@@ -693,7 +631,6 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
   }
   tl_mark(a.tl, 8, 1);
   if (K > a.cap) {  // overflow (grid-uniform): nothing is written
-    finish();
     tl_mark(a.tl, 0, 3);
     return;
   }
@@ -862,7 +799,6 @@ __global__ void __launch_bounds__(kRowThreads) k_bin_rows(RowArgs a) {
             make_int4(r * a.ntx + c, col[c], ccnt[c], c | ((a.ty_begin + r) << 16));
     }
   }
-  finish();
   tl_mark(a.tl, 0, 3);
 }
 
@@ -1041,12 +977,6 @@ extern "C" int pf_preprocess(const double* params, int n, double alpha_max, doub
                                W, H, tile, ty_begin, ty_end, capacity, rec, scratch,
                                scratch_bytes);
   if (rc != PF_OK) return rc;
-  // the rect-publication counter (done[4], see wait_rects) counts THIS launch's
-  // blocks only: clear what an earlier K1 (e.g. the Adam launch of the previous
-  // step) published, stream-ordered before this launch
-  if (const cudaError_t e = cudaMemsetAsync(a.s.done + 4, 0, 2 * sizeof(uint32_t),
-                                            (cudaStream_t)stream))
-    return (int)e;
   return launch_prim(false, a, (cudaStream_t)stream);
 }
 
@@ -1060,9 +990,6 @@ extern "C" int pf_preprocess_sync(double* params, const double* src, int n, doub
                                ty_end, capacity, rec, scratch, scratch_bytes);
   if (rc != PF_OK) return rc;
   a.src = src;
-  if (const cudaError_t e = cudaMemsetAsync(a.s.done + 4, 0, 2 * sizeof(uint32_t),
-                                            (cudaStream_t)stream))  // (see pf_preprocess)
-    return (int)e;
   return launch_prim(false, a, (cudaStream_t)stream);
 }
 
@@ -1171,7 +1098,6 @@ extern "C" int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, i
   ra.classes = tile_classes;
   ra.n_tiles = n_rows * ntx;
   ra.prebuilt = 0;
-  ra.rect_blocks = n > 0 ? (uint32_t)div_up(n * 8, kPrimThreads) : 0u;  // = launch_prim's grid
   ra.tl = pf_timeline_ptr();
   const size_t smem = sizeof(int2) * kRowSmemList + 3 * sizeof(int) * (size_t)ntx;
   const bool cache = (n + kRowThreads - 1) / kRowThreads <= kRowCache;

@@ -19,8 +19,7 @@ struct BinScratch {
   int32_t* zprim;    // [n] primitive index per z position (static, set by pf_scratch_init)
   PrimInfo* pinfo;   // [n] static per-primitive structure (pf_scratch_init)
   int2* rowlist;     // [capacity] per-row z-ordered lists: (z position, tx0 | tx1 << 16)
-  uint32_t* done;    // [8] [1] iteration, [2] Adam ran, [4] K1 blocks whose rects are
-                     // published (K2 starts on it), [5] K2 blocks past that wait
+  uint32_t* done;    // [4] last-block ticket
   double* fold;      // [prim blocks][3] per-block loss-partial folds (pf_adam_preprocess)
   // two-level binning (large n x rows; sized from n_tiles >= rows, 0 = absent)
   int2* rowcnt;      // [row chunks][n_rows] per chunk of kRowChunk z positions: (pairs, entries)
@@ -46,7 +45,7 @@ static inline BinScratch carve(void* base, int n, int cap, int n_tiles = 0) {
   s.zprim = (int32_t*)take(sizeof(int32_t) * (size_t)n);
   s.pinfo = (PrimInfo*)take(sizeof(PrimInfo) * (size_t)n);
   s.rowlist = (int2*)take(sizeof(int2) * (size_t)cap);
-  s.done = (uint32_t*)take(sizeof(uint32_t) * 8);
+  s.done = (uint32_t*)take(sizeof(uint32_t) * 4);
   s.fold = (double*)take(sizeof(double) * 3 * (size_t)((8 * (size_t)n + 255) / 256 + 1));
   // (appended: the offsets above do not depend on n_tiles)
   // (rows <= n_tiles, and the two-level path runs only for <= kMaxRows2 rows)
