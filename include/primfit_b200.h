@@ -55,7 +55,7 @@ extern "C" {
 #define PF_LOSS_COMBINED 3   /* mse_w * loss_mse + gray_l1_w * loss_grayscale_l1, fit.py:119-125, 162-168 */
 
 /* ABI version; bumped on any signature change. */
-int pf_abi_version(void);
+int pf_abi_version(void);  /* 6 */
 
 /* Diagnostics: the PF_* environment switches (A/B variants, profiling) are read
  * once at load; this re-reads them (tests that flip a switch at run time). */
@@ -124,7 +124,27 @@ int pf_scratch_init(void* scratch, size_t scratch_bytes, const int32_t* template
  */
 int pf_preprocess(const double* params, int n, double alpha_max, double mu_blend, double padding,
                   int W, int H, int tile, int ty_begin, int ty_end, int capacity,
-                  void* rec, void* scratch, size_t scratch_bytes, void* stream);
+                  void* rec, void* scratch, size_t scratch_bytes, void* slots, int slot_m,
+                  int32_t* tile_classes, void* stream);
+
+/*
+ * Slot binning (the fit step's tile lists without pf_bin).  With `slots` set
+ * (pf_slot_bytes(n_band_tiles, slot_m, capacity) bytes; NULL = CSR mode), every
+ * K1 launch (pf_preprocess, pf_preprocess_sync, pf_adam_preprocess with rec)
+ * also appends each of its primitives' (tile, z rank) pairs to the tile's slot
+ * list (arrival order; past slot_m slots to an overflow list sized from
+ * `capacity`), writes the K34-only records at the z rank, and (except
+ * pf_preprocess_sync) rebuilds the tile cost classes from the costs the last
+ * pf_fit_step measured.  pf_fit_step then sorts each tile's list by z rank
+ * (= bin_tiles' z-ascending list, raster.py:227-265) before staging it, and
+ * empties the slots for the next K1.  pf_slot_reset empties them (and the class
+ * counts) before a full pf_preprocess; pf_preprocess_sync re-scatters only
+ * edited primitives and flags the step, whose lists are then validated against
+ * the current rects and de-duplicated.  The render tile (16) is required.
+ */
+size_t pf_slot_bytes(int n_tiles, int slot_m, int capacity);
+int pf_slot_reset(void* slots, int n_tiles, int slot_m, int capacity, int32_t* tile_classes,
+                  void* stream);
 
 /*
  * K1, incremental: the parameters are taken from `src` (e.g. the caller's
@@ -137,7 +157,7 @@ int pf_preprocess(const double* params, int n, double alpha_max, double mu_blend
 int pf_preprocess_sync(double* params, const double* src, int n, double alpha_max,
                        double mu_blend, double padding, int W, int H, int tile, int ty_begin,
                        int ty_end, int capacity, void* rec, void* scratch, size_t scratch_bytes,
-                       void* stream);
+                       void* slots, int slot_m, int32_t* tile_classes, void* stream);
 
 /*
  * K5+K1 fused: one Adam step (fit.py:195-238) on every parameter, then the
@@ -166,7 +186,8 @@ int pf_adam_preprocess(double* params, double* grads, double* m, double* v, cons
                        const double* sums, const double* part, int n_part, double* hist_part,
                        double* last_part, int n, double alpha_max, double mu_blend, double padding, int W, int H,
                        int tile, int ty_begin, int ty_end, int capacity, void* rec, void* scratch,
-                       size_t scratch_bytes, double* mirror, void* stream);
+                       size_t scratch_bytes, double* mirror, void* slots, int slot_m,
+                       int32_t* tile_classes, void* stream);
 
 /*
  * K2 — tile binning from the rects of pf_preprocess: one block per tile row,
@@ -277,11 +298,18 @@ int pf_atlas_pad(const double* tex, int texels, const int32_t* tpl_base, const i
  *           sum ((I-t)*mask)^2, sum (I_a-t_a)^2); fold them with pf_fold_loss or
  *           pass them to pf_adam_preprocess
  *   grads   float64 [n][8] accumulated into (zeroed by pf_adam_preprocess)
- *   counters uint32[2] zeroed once at allocation (tile ticket; self-resetting)
+ *   counters uint32[4] zeroed once at allocation (tile ticket, finished producers,
+ *           slot-mode grid barrier; self-resetting)
  *   tile_classes  pf_bin's tile classes of this band (longest-first schedule; the
  *           counts are re-zeroed for the next pf_bin), or NULL (tile order)
  *   stage   list entries staged in shared memory per tile: 32, or 64 for scenes
  *           with long tile lists (a hint: entries beyond it are read from L2)
+ *   scratch, scratch_bytes, capacity, slots, slot_m
+ *           slot mode (slots != NULL, see pf_slot_bytes): the lists come from the
+ *           slots K1 filled (bin_off / bin_idx unused, may be NULL), sorted here
+ *           by z rank; `scratch` is the K1 scratch (rects, iteration counter);
+ *           K of the step is published to status[0] (status[1]: list overflow).
+ *           NULL: CSR mode, lists from pf_bin.
  */
 size_t pf_step_spill_bytes(int capacity);
 int pf_fit_step(const void* rec, int n, const double* tex, const float* apad,
@@ -291,7 +319,8 @@ int pf_fit_step(const void* rec, int n, const double* tex, const float* apad,
                 int loss_kind, const float* tgt4, double alpha_w, double w_mse, double w_gray,
                 double inv_3P, double inv_P, void* spill, float* img4, double* part,
                 double* grads, uint32_t* counters,
-                const int32_t* tile_classes, int stage, void* stream);
+                const int32_t* tile_classes, int stage, void* scratch, size_t scratch_bytes,
+                int capacity, void* slots, int slot_m, void* stream);
 
 /* Fixed-order fold of n_part partial triples into sums[3] (deterministic). */
 int pf_fold_loss(const double* part, int n_part, double* sums, void* stream);

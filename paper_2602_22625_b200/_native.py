@@ -44,14 +44,18 @@ SIGNATURES: dict[str, tuple] = {
     "pf_bin_launches": (_I, [_I, _I, _I, _I, _I, _I]),
     "pf_saved_capacity": (C.c_longlong, [_I]),
     "pf_saved_bytes": (_Z, [_I]),
-    "pf_preprocess": (_I, [_P, _I, _D, _D, _D, _I, _I, _I, _I, _I, _I, _P, _P, _Z, _P]),
-    "pf_preprocess_sync": (_I, [_P, _P, _I, _D, _D, _D, _I, _I, _I, _I, _I, _I, _P, _P, _Z, _P]),
+    "pf_preprocess": (_I, [_P, _I, _D, _D, _D, _I, _I, _I, _I, _I, _I, _P, _P, _Z, _P, _I, _P,
+                           _P]),
+    "pf_preprocess_sync": (_I, [_P, _P, _I, _D, _D, _D, _I, _I, _I, _I, _I, _I, _P, _P, _Z, _P,
+                                _I, _P, _P]),
+    "pf_slot_bytes": (_Z, [_I, _I, _I]),
+    "pf_slot_reset": (_I, [_P, _I, _I, _I, _P, _P]),
     "pf_scratch_init": (_I, [_P, _Z, _P, _P, _I, _P, _P, _P, _P, _P, _P, _I, _I, _P]),
     "pf_adam_blocks": (_I, [_I]),
     "pf_adam_preprocess": (
         _I,
         [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _D, _D, _P, _P, _I, _P, _P, _I, _D, _D, _D, _I,
-         _I, _I, _I, _I, _I, _P, _P, _Z, _P, _P],
+         _I, _I, _I, _I, _I, _P, _P, _Z, _P, _P, _I, _P, _P],
     ),
     "pf_atlas_quad": (_I, [_P, _I, _P, _P, _P, _I, _P, _P]),
     "pf_atlas_pad": (_I, [_P, _I, _P, _P, _P, _P, _I, _I, _P, _P]),
@@ -65,7 +69,7 @@ SIGNATURES: dict[str, tuple] = {
     "pf_fit_step": (
         _I,
         [_P, _I, _P, _P, _P, _I, _I, _P, _P, _P, _I, _I, _I, _I, _D, _D, _D, _D, _P, _I, _P, _D,
-         _D, _D, _D, _D, _P, _P, _P, _P, _P, _P, _I, _P],
+         _D, _D, _D, _D, _P, _P, _P, _P, _P, _P, _I, _P, _Z, _I, _P, _I, _P],
     ),
     "pf_fold_loss": (_I, [_P, _I, _P, _P]),
     "pf_sum_bands": (_I, [_P, _I, _P, _I, C.c_longlong, C.c_longlong, _P]),

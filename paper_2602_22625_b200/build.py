@@ -40,8 +40,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale(LIB, deps):
         return LIB
     LIB.parent.mkdir(parents=True, exist_ok=True)
-    objs = []
-    for s in SOURCES:
+    objs, procs = [], []
+    for s in SOURCES:  # one nvcc per translation unit, concurrently
         obj = LIB.parent / (Path(s).stem + ".o")
         cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-I", str(ROOT / "include"), "-c", str(CSRC / s), "-o", str(obj)]
@@ -50,8 +50,11 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
+        procs.append((subprocess.Popen(cmd), cmd))
         objs.append(str(obj))
+    failed = [cmd for p, cmd in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, failed[0])
     tmp = LIB.with_suffix(".so.tmp")
     subprocess.run([nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs], check=True)
     os.replace(tmp, LIB)

@@ -164,18 +164,61 @@ class Compositor:
         self.bin_idx = torch.zeros(max(self.capacity, 1), dtype=torch.int32, device=dev)
         # tile cost classes for pf_fit_step's longest-first schedule (fused path only)
         self.tile_classes = None
+        # slot binning (fit step; enable_step_schedule(slot_m)): None = CSR lists
+        self.slots = None
+        self.slot_m = 0
         self.status = torch.zeros(4, dtype=torch.int32, device=dev)
         self._saved_alloc = False
         self.launches = 0  # kernels launched through this object (one per stage call)
 
-    def enable_step_schedule(self) -> None:
-        """Have pf_bin emit tile cost classes for pf_fit_step's longest-first
-        schedule (call before the first bin() of a fused fit loop)."""
+    def enable_step_schedule(self, slot_m: int = 0) -> None:
+        """Tile cost classes for pf_fit_step's longest-first schedule (call before
+        the first preprocess / bin() of a fused fit loop).  ``slot_m > 0``: slot
+        binning -- K1 scatters the tile lists itself (``slot_m`` slots per tile,
+        overflow list beyond), pf_fit_step sorts them, bin() is a no-op."""
         if self.tile_classes is None:
             # counts, per-class tile lists, measured tile costs
             nt = max(self.n_tiles, 1)
             self.tile_classes = torch.zeros(16 + 16 * 4 * nt + nt, dtype=torch.int32,
                                             device=self.device)
+        if slot_m > 0 and self.slots is None:
+            if self.tile != RENDER_TILE:
+                raise ValueError(f"slot binning needs bin tile {RENDER_TILE}, got {self.tile}")
+            self.slot_m = int(slot_m)
+            nbytes = int(self.lib.pf_slot_bytes(self.n_tiles, self.slot_m, self.capacity))
+            self.slots = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
+
+    def _slot_args(self, classes: bool = True):
+        if self.slots is None:
+            return (None, 0, None)
+        return (self.slots.data_ptr(), self.slot_m, self.tile_classes.data_ptr())
+
+    def slot_lists(self) -> tuple[np.ndarray, np.ndarray]:
+        """Diagnostics / tests (synchronising): the current slot lists (after a K1,
+        before the fit step consumes them) as CSR (offsets, primitive indices),
+        each tile's list sorted by z rank -- what pf_fit_step stages."""
+        nt, m = self.n_tiles, self.slot_m
+        raw = self.slots.cpu().numpy()
+        ctl = raw[:256].view(np.uint32)
+        off = 256
+        cnt = raw[off : off + 4 * nt].view(np.int32).copy()
+        off = -(-(off + 4 * max(nt, 1)) // 256) * 256
+        slot = raw[off : off + 4 * nt * m].view(np.uint32).reshape(nt, m)
+        # (the slot array is followed by the general-path pool, capacity + 64 entries)
+        off = -(-(off + 4 * (nt * m + self.capacity + 64)) // 256) * 256
+        novf = int(ctl[0])
+        ovf = raw[off : off + 8 * novf].view(np.int32).reshape(-1, 2)
+        zorder = self.d_zorder.cpu().numpy()
+        lists = [list(slot[t, : min(int(cnt[t]), m)]) for t in range(nt)]
+        for t, z in ovf:
+            lists[int(t)].append(int(z))
+        offs = np.zeros(nt + 1, dtype=np.int64)
+        idx = []
+        for t in range(nt):
+            zs = sorted(int(z) for z in lists[t])
+            idx.extend(int(zorder[z]) for z in zs)
+            offs[t + 1] = offs[t] + len(zs)
+        return offs, np.asarray(idx, dtype=np.int32)
 
     # -- buffers for rendering (allocated lazily; binning-only users skip them)
     def alloc_render(self, save: bool, loss: bool = False):
@@ -205,12 +248,17 @@ class Compositor:
 
     # -- K1 + K2
     def preprocess(self, params: torch.Tensor, stream=None) -> None:
+        if self.slots is not None:
+            # a full K1 re-scatters every primitive: empty the lists (and classes) first
+            nat.check(self.lib.pf_slot_reset(self.slots.data_ptr(), self.n_tiles, self.slot_m,
+                                             self.capacity, self.tile_classes.data_ptr(),
+                                             _stream_handle(stream)), "pf_slot_reset")
         nat.check(
             self.lib.pf_preprocess(
                 params.data_ptr(), self.n, self.alpha_max, self.mu_blend, self.padding, self.W,
                 self.H, self.tile, self.band.ty_begin, self.band.ty_end, self.capacity,
                 self.rec.data_ptr(), self.scratch.data_ptr(), self.scratch_bytes,
-                _stream_handle(stream)),
+                *self._slot_args(), _stream_handle(stream)),
             "pf_preprocess")
         self.launches += 1
 
@@ -222,7 +270,7 @@ class Compositor:
                 params.data_ptr(), src.data_ptr(), self.n, self.alpha_max, self.mu_blend,
                 self.padding, self.W, self.H, self.tile, self.band.ty_begin, self.band.ty_end,
                 self.capacity, self.rec.data_ptr(), self.scratch.data_ptr(), self.scratch_bytes,
-                _stream_handle(stream)),
+                *self._slot_args(), _stream_handle(stream)),
             "pf_preprocess_sync")
         self.launches += 1
 
@@ -246,7 +294,7 @@ class Compositor:
                 self.band.ty_begin, self.band.ty_end, self.capacity,
                 self.rec.data_ptr() if records else None,
                 self.scratch.data_ptr(), self.scratch_bytes, nat.ptr(mirror),
-                _stream_handle(stream)),
+                *self._slot_args(), _stream_handle(stream)),
             "pf_adam_preprocess")
         self.launches += 1
 
@@ -255,7 +303,10 @@ class Compositor:
         return int(self.lib.pf_adam_blocks(self.n))
 
     def bin(self, stream=None) -> None:
-        """K2: CSR tile bins (z-ascending lists) from the rects of the last K1."""
+        """K2: CSR tile bins (z-ascending lists) from the rects of the last K1
+        (slot mode: nothing to do -- K1 scattered the lists)."""
+        if self.slots is not None:
+            return
         nat.check(
             self.lib.pf_bin(self.n, self.W, self.H, self.tile, self.band.ty_begin,
                             self.band.ty_end, self.capacity, self.scratch.data_ptr(),
@@ -313,7 +364,7 @@ class Compositor:
         if not hasattr(self, "spill"):
             nbytes = int(self.lib.pf_step_spill_bytes(max(self.capacity, 1)))
             self.spill = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-            self.step_ctr = torch.zeros(2, dtype=torch.int32, device=dev)
+            self.step_ctr = torch.zeros(4, dtype=torch.int32, device=dev)
             if not hasattr(self, "part"):
                 self.part = torch.zeros(max(self.n_tiles, 1) * 8 * 3, dtype=torch.float64,
                                         device=dev)
@@ -333,7 +384,8 @@ class Compositor:
                 1.0 / Pt,
                 self.spill.data_ptr(), p(self.img4) if image else None, self.part.data_ptr(),
                 grads.data_ptr(), self.step_ctr.data_ptr(), nat.ptr(self.tile_classes),
-                self.stage_hint, _stream_handle(stream)),
+                self.stage_hint, self.scratch.data_ptr(), self.scratch_bytes, self.capacity,
+                nat.ptr(self.slots), self.slot_m, _stream_handle(stream)),
             "pf_fit_step")
         self.launches += 1
         if sums is not None:

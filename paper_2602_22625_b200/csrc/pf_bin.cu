@@ -72,10 +72,19 @@ struct PreArgs {
   BinScratch s;
   AdamPart ad;
   unsigned long long* tl;  // diagnostics timeline or NULL
+  // slot binning (pf_fit_step lists, see SlotBins): slots.cnt == NULL -> CSR mode
+  // (records by primitive index, pf_bin builds the lists); else records RecS /
+  // RecC go to the primitive's z rank and K1 scatters the pairs itself
+  SlotBins slots;
+  int ntx, n_tiles;   // band tiles (slot mode)
 };
 
 constexpr double kB1 = 0.9, kB2 = 0.999, kAdamEps = 1e-8;
 constexpr int kPrimThreads = 256;
+// resident blocks per SM the two K1 variants are compiled for: 3 (80 registers)
+// while the grid fits one wave at that occupancy (c3: 157 blocks), else 5 (48
+// registers, some spills; c5: 625 blocks in one wave instead of two)
+constexpr int kPrimMinBlocksLo = 3, kPrimMinBlocksHi = 5;
 
 // adam_step for one scalar (fit.py:224-237), reference op order, no contraction.
 // m, v, frozen are loaded by the caller before the PDL wait (k_step does not
@@ -97,8 +106,8 @@ __device__ __forceinline__ double adam_scalar(const AdamPart& d, size_t idx, int
   return p;
 }
 
-template <bool ADAM>
-__global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
+template <bool ADAM, int MINB>
+__global__ void __launch_bounds__(kPrimThreads, MINB) k_prim(PreArgs a) {
   tl_mark(a.tl, ADAM ? 2 : 3, 0);
   const int g = blockIdx.x * kPrimThreads + threadIdx.x;
   const int i = g >> 3, c = g & 7;  // primitive, parameter column
@@ -131,7 +140,7 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
   double fv0 = 0.0, fv1 = 0.0, fv2 = 0.0;  // loss-fold partial sums of this thread
   if (ADAM) {
     // everything k_step (the predecessor) does not write, before the PDL wait
-    it = (int)a.s.done[1];  // advanced by K2 of the next step (see k_bin_rows)
+    it = (int)a.s.done[1];  // advanced by the next pf_bin / slot-mode pf_fit_step
     const double lr = a.ad.lr_table[it], bc1 = a.ad.bc1_table[it], bc2 = a.ad.bc2_table[it];
     const double m0 = live ? a.ad.m[pidx] : 0.0, v0 = live ? a.ad.v[pidx] : 0.0;
     const bool live_p = live && (a.ad.frozen == nullptr || a.ad.frozen[i] == 0);
@@ -199,6 +208,37 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
   // others' (every consumer walks the tile lists) -- on a row band of a
   // multi-GPU split most primitives skip the work below
   const bool need = live && rc.y <= rc.w && grp_changed;
+  const bool slots = a.slots.cnt != nullptr;
+  // K34-only records (RecS, RecC) sit at the z rank in slot mode: the sorted
+  // tile lists hold z ranks
+  const int ri = slots ? pi.zrank : i;
+  // the pair scatter (see SlotBins): the rect's tiles split over the lane group;
+  // the first two per lane go out before the record math (their atomics' round
+  // trip overlaps it), the rest after
+  const int sc_tx0 = rc.x & 0xffff, sc_nx = (rc.x >> 16) - sc_tx0 + 1;
+  const int sc_nt = (slots && need) ? sc_nx * (rc.w - rc.y + 1) : 0;
+  auto sc_tile = [&](int k) {
+    const int ry = k / sc_nx;
+    return (rc.y + ry - a.ty_begin) * a.ntx + sc_tx0 + (k - ry * sc_nx);
+  };
+  auto sc_put = [&](int t, int p) {
+    if (p < a.slots.m) {
+      a.slots.slot[(size_t)t * a.slots.m + p] = (uint32_t)pi.zrank;
+    } else {
+      const uint32_t o = atomicAdd(a.slots.ctl + kSlotOvf, 1u);
+      if (o < (uint32_t)a.slots.ovf_cap) a.slots.ovf[o] = make_int2(t, pi.zrank);
+      else a.slots.ctl[kSlotErr] = 1u;
+    }
+  };
+  int sc_t0 = -1, sc_t1 = -1, sc_p0 = 0, sc_p1 = 0;
+  if (c < sc_nt) {
+    sc_t0 = sc_tile(c);
+    sc_p0 = atomicAdd(a.slots.cnt + sc_t0, 1);
+  }
+  if (c + 8 < sc_nt) {
+    sc_t1 = sc_tile(c + 8);
+    sc_p1 = atomicAdd(a.slots.cnt + sc_t1, 1);
+  }
   if (__any_sync(kFull, need)) {
   // transcendental / division work split across the lane group
   double r0 = 0.0, r1 = 0.0;
@@ -264,7 +304,7 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
         const double e_px = fabs(x - (double)fx) + fabs(y - (double)fy);
         const double span = e_px + 1e-6 * (fabs(r) + 2.0 * kTile);
         const double act = fabs(ct), ast = fabs(st);
-        float4* pc4 = reinterpret_cast<float4*>(a.recc + i);
+        float4* pc4 = reinterpret_cast<float4*>(a.recc + ri);
         if (c == 6) {
           pc4[0] = make_float4(fx, fy, (float)(ct * inv_s), (float)(st * inv_s));
         } else {
@@ -281,8 +321,8 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
       const double cu = hw * (1.0 - (ct * x + st * y) * inv_s);
       const double av = -hh * st * inv_sq, bv = hh * ct * inv_sq;
       const double cv = hh * (1.0 + (st * x - ct * y) * inv_sq);
-      double2* ps = reinterpret_cast<double2*>(a.recs + i);
-      float4* ps4 = reinterpret_cast<float4*>(a.recs + i);
+      double2* ps = reinterpret_cast<double2*>(a.recs + ri);
+      float4* ps4 = reinterpret_cast<float4*>(a.recs + ri);
       const double sa_d = __dmul_rn(a.alpha_max, sig);
       // guard band of the affine U, V: >= 1e4 x their error bound
       const double du = 1e-11 * (fabs(au) * a.W + fabs(bu) * a.H + fabs(cu) + (wt - 1) + 1.0);
@@ -321,7 +361,26 @@ __global__ void __launch_bounds__(kPrimThreads) k_prim(PreArgs a) {
     }
   }
   }  // any record in this warp
+  if (sc_t0 >= 0) sc_put(sc_t0, sc_p0);
+  if (sc_t1 >= 0) sc_put(sc_t1, sc_p1);
+  for (int k0 = c + 16; k0 < sc_nt; k0 += 32) {
+    int t4[4], p4[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = k0 + 8 * q;
+      t4[q] = k < sc_nt ? sc_tile(k) : -1;
+      if (t4[q] >= 0) p4[q] = atomicAdd(a.slots.cnt + t4[q], 1);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (t4[q] >= 0) sc_put(t4[q], p4[q]);
+  }
+  // an edited primitive re-scattered next to its previous entries: the
+  // producers validate and de-duplicate this step's lists
+  if (!ADAM && a.src && sc_nt > 0 && c == 0) a.slots.ctl[kSlotDirty] = 1u;
   }  // a.records
+
+
 
   if (ADAM) {
     // this block's loss sums of the step (fixed-order fold of its chunk of
@@ -900,13 +959,53 @@ static int fill_pre_args(PreArgs& a, double* params, int n, double alpha_max, do
   a.s = carve(scratch, n, capacity);
   a.ad = AdamPart{};
   a.tl = pf_timeline_ptr();
+  a.slots = SlotBins{};
+  a.ntx = ntx;
+  a.n_tiles = n_rows * ntx;
   return PF_OK;
 }
 
+// Slot mode (slots != NULL): slot scratch of pf_slot_bytes(n_tiles, m, capacity);
+// tile must be the render tile.  (tile_classes: the fit step's prologue builds
+// the classes; accepted for symmetry with pf_fit_step.)
+static int attach_slots(PreArgs& a, void* slots, int slot_m, int32_t* tile_classes,
+                        int capacity) {
+  (void)tile_classes;
+  if (!slots) return PF_OK;
+  if (a.tile != kTile || slot_m < 1) return PF_ERR_ARG;
+  a.slots = slot_carve(slots, a.n_tiles, slot_m, capacity);
+  return PF_OK;
+}
+
+extern "C" size_t pf_slot_bytes(int n_tiles, int m, int capacity) {
+  if (n_tiles < 0 || m < 1 || capacity < 0) return 0;
+  return slot_carve(nullptr, n_tiles, m, capacity).total;
+}
+
+// Empty slot lists and tile classes (before a full pf_preprocess in slot mode).
+extern "C" int pf_slot_reset(void* slots, int n_tiles, int m, int capacity,
+                             int32_t* tile_classes, void* stream) {
+  if (!slots || n_tiles < 0 || m < 1 || capacity < 0) return PF_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const SlotBins s = slot_carve(slots, n_tiles, m, capacity);
+  cudaError_t e = cudaMemsetAsync(s.ctl, 0, sizeof(uint32_t) * kSlotCtlWords, st);
+  if (e == cudaSuccess && n_tiles > 0)
+    e = cudaMemsetAsync(s.cnt, 0, sizeof(int32_t) * (size_t)n_tiles, st);
+  if (e == cudaSuccess && tile_classes)
+    e = cudaMemsetAsync(tile_classes, 0, sizeof(int32_t) * kTileClasses, st);
+  return (int)e;
+}
+
+static int sms_count();
 static int launch_prim(bool adam, const PreArgs& a, cudaStream_t st) {
   const int blocks = div_up(a.n > 0 ? a.n * 8 : 1, kPrimThreads);
-  if (adam) return (int)launch_pdl(k_prim<true>, blocks, kPrimThreads, 0, st, a);
-  if (a.n > 0) return (int)launch_pdl(k_prim<false>, blocks, kPrimThreads, 0, st, a);
+  const bool hi = blocks > kPrimMinBlocksLo * sms_count();
+  if (adam)
+    return (int)launch_pdl(hi ? k_prim<true, kPrimMinBlocksHi> : k_prim<true, kPrimMinBlocksLo>,
+                           blocks, kPrimThreads, 0, st, a);
+  if (a.n > 0)
+    return (int)launch_pdl(hi ? k_prim<false, kPrimMinBlocksHi> : k_prim<false, kPrimMinBlocksLo>,
+                           blocks, kPrimThreads, 0, st, a);
   return (int)cudaGetLastError();
 }
 
@@ -971,11 +1070,11 @@ extern "C" int pf_scratch_init(void* scratch, size_t scratch_bytes, const int32_
 extern "C" int pf_preprocess(const double* params, int n, double alpha_max, double mu_blend,
                              double padding, int W, int H, int tile, int ty_begin, int ty_end,
                              int capacity, void* rec, void* scratch, size_t scratch_bytes,
-                             void* stream) {
+                             void* slots, int slot_m, int32_t* tile_classes, void* stream) {
   PreArgs a;
-  const int rc = fill_pre_args(a, const_cast<double*>(params), n, alpha_max, mu_blend, padding,
-                               W, H, tile, ty_begin, ty_end, capacity, rec, scratch,
-                               scratch_bytes);
+  int rc = fill_pre_args(a, const_cast<double*>(params), n, alpha_max, mu_blend, padding,
+                         W, H, tile, ty_begin, ty_end, capacity, rec, scratch, scratch_bytes);
+  if (rc == PF_OK) rc = attach_slots(a, slots, slot_m, tile_classes, capacity);
   if (rc != PF_OK) return rc;
   return launch_prim(false, a, (cudaStream_t)stream);
 }
@@ -983,11 +1082,14 @@ extern "C" int pf_preprocess(const double* params, int n, double alpha_max, doub
 extern "C" int pf_preprocess_sync(double* params, const double* src, int n, double alpha_max,
                                   double mu_blend, double padding, int W, int H, int tile,
                                   int ty_begin, int ty_end, int capacity, void* rec, void* scratch,
-                                  size_t scratch_bytes, void* stream) {
+                                  size_t scratch_bytes, void* slots, int slot_m,
+                                  int32_t* tile_classes, void* stream) {
   if (n > 0 && !src) return PF_ERR_ARG;
   PreArgs a;
-  const int rc = fill_pre_args(a, params, n, alpha_max, mu_blend, padding, W, H, tile, ty_begin,
-                               ty_end, capacity, rec, scratch, scratch_bytes);
+  int rc = fill_pre_args(a, params, n, alpha_max, mu_blend, padding, W, H, tile, ty_begin,
+                         ty_end, capacity, rec, scratch, scratch_bytes);
+  // (slot mode: only edited primitives are scattered again; the classes stand)
+  if (rc == PF_OK) rc = attach_slots(a, slots, slot_m, tile_classes, capacity);
   if (rc != PF_OK) return rc;
   a.src = src;
   return launch_prim(false, a, (cudaStream_t)stream);
@@ -1004,7 +1106,8 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
                                   double mu_blend,
                                   double padding, int W, int H, int tile, int ty_begin,
                                   int ty_end, int capacity, void* rec, void* scratch,
-                                  size_t scratch_bytes, double* mirror, void* stream) {
+                                  size_t scratch_bytes, double* mirror, void* slots, int slot_m,
+                                  int32_t* tile_classes, void* stream) {
   PreArgs a;
   // rec == NULL: Adam only (no records / rects; the caller runs pf_preprocess
   // before the next pf_bin, e.g. a host-driven step that re-reads the parameters)
@@ -1014,6 +1117,7 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
   if (rc != PF_OK) return rc;
   a.records = rec != nullptr;
   a.mirror = mirror;
+  if (const int rs = attach_slots(a, slots, slot_m, tile_classes, capacity)) return rs;
   if (!lr_table || !bc1_table || !bc2_table || (n > 0 && (!grads || !m || !v)))
     return PF_ERR_ARG;
   if (part && n_part < 0) return PF_ERR_ARG;

@@ -57,6 +57,61 @@ static inline BinScratch carve(void* base, int n, int cap, int n_tiles = 0) {
   return s;
 }
 
+// Slot binning (the fit step's tile lists without a binning kernel).  K1 puts
+// every (tile, primitive) pair of a primitive's band-clipped rect straight into
+// the tile's slot array -- slot = atomicAdd(cnt[tile], 1), value = the
+// primitive's z rank -- so the lists come out in arrival order; pf_fit_step's
+// producer warp sorts each tile's list by z rank before staging it, which gives
+// exactly the reference's z-ascending list (z ranks are a permutation).
+// Entries past a tile's m slots go to an overflow list of (tile, z rank); the
+// producer's general path gathers them.  Sized from the exact capacity bound,
+// so nothing is ever dropped (a second scatter of host-edited primitives in
+// one step is covered by the factor 2; the error word catches anything else).
+enum SlotCtl : int {
+  kSlotOvf = 0,     // overflow entries used
+  kSlotPool = 1,    // general-path list pool bump (entries), reset per fit step
+  kSlotDirty = 2,   // pf_preprocess_sync re-scattered edited primitives this step
+  kSlotK = 3,       // total list entries of the fit step being run (published to status[0])
+  kSlotGather = 4,  // gather-scratch bump of the producer's general path
+  kSlotErr = 5,     // overflow list exhausted (never with the capacity bound)
+  kSlotCtlWords = 64
+};
+struct SlotBins {
+  uint32_t* ctl;   // [kSlotCtlWords]
+  int32_t* cnt;    // [n_tiles] arrivals (K1 atomics; the producer re-zeroes its tile)
+  uint32_t* slot;  // [n_tiles][m] z ranks, arrival order (z-sorted by pf_fit_step's prologue)
+  int2* ovf;       // [ovf_cap] (tile, z rank) past a tile's m slots
+  uint32_t* pool;  // [pool_cap] (= slot + n_tiles * m) z-sorted general-path lists
+  uint32_t* gat;   // [gat_cap] the general path's gather scratch
+  int m, n_tiles, ovf_cap, pool_cap, gat_cap;
+  size_t total;
+};
+
+static inline SlotBins slot_carve(void* base, int n_tiles, int m, int cap) {
+  SlotBins s;
+  char* p = (char*)base;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* q = p ? p + off : nullptr;
+    off = align_up(off + (bytes > 0 ? bytes : 1), 256);
+    return (void*)q;
+  };
+  s.m = m;
+  s.n_tiles = n_tiles;
+  s.ovf_cap = 2 * cap + 64;
+  s.pool_cap = cap + 64;
+  s.gat_cap = 4 * cap + 256;
+  s.ctl = (uint32_t*)take(sizeof(uint32_t) * kSlotCtlWords);
+  s.cnt = (int32_t*)take(sizeof(int32_t) * (size_t)n_tiles);
+  // (the pool follows the slots: one list array, base tile * m or n_tiles * m + offset)
+  s.slot = (uint32_t*)take(sizeof(uint32_t) * ((size_t)n_tiles * (size_t)m + (size_t)s.pool_cap));
+  s.pool = s.slot ? s.slot + (size_t)n_tiles * (size_t)m : nullptr;
+  s.ovf = (int2*)take(sizeof(int2) * (size_t)s.ovf_cap);
+  s.gat = (uint32_t*)take(sizeof(uint32_t) * (size_t)s.gat_cap);
+  s.total = off;
+  return s;
+}
+
 // Block-wide exclusive scan of one int per thread (<= 1024 threads).
 // Returns the exclusive prefix; *total receives the block sum.
 __device__ __forceinline__ int block_excl_scan(int v, int* warp_sums, int* total) {

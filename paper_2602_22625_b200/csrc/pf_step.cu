@@ -38,6 +38,7 @@
 #include <type_traits>
 
 #include "../../include/primfit_b200.h"
+#include "pf_bins.cuh"
 #include "pf_common.cuh"
 
 namespace pf {
@@ -48,6 +49,7 @@ constexpr int kCW = kTilePix / 32;                      // consumer warps per gr
 // list entries staged per tile: ST = 32, or 64 for long-list scenes (template
 // parameter of k_step; pf_fit_step's `stage` hint picks it)
 constexpr int kNBuf = 2;                                // stage buffers per group (ring)
+constexpr int kSlotArena = 64;  // spill entries per group for slot-mode fast-path tiles (L <= 64)
 constexpr int kKS = 5;                                  // contribution-stack depth in smem
 constexpr uint32_t kEntBytes = sizeof(RecS) + sizeof(RecC);
 // CTA shape for G groups: warps [0, 8G) consume (group = warp / 8), warps
@@ -109,7 +111,53 @@ struct StepArgs {
   int32_t* tile_cost;      // [n_tiles] measured work of each tile (next step's classes)
   unsigned long long* prof;  // diagnostics (PF_STEP_PROF=1): [warp slot][6], else NULL
   unsigned long long* tl;    // diagnostics timeline or NULL
+  // slot mode (sb.cnt != NULL): the tile lists are K1's slot scatter, sorted here
+  // by the producers (see SlotBins); no pf_bin launch precedes this kernel
+  SlotBins sb;
+  const int4* rect;      // K1's band-clipped rects per z rank (dirty-step validation)
+  uint32_t* done;        // Adam iteration counter words (advanced here in slot mode)
+  int32_t* status_rw;    // [2] published K, error flag (slot mode)
 };
+
+// Warp bitonic sort, ascending, of 32 keys (k0 at element lane) or 64 (k1 at
+// element lane + 32): the producer's per-tile list sort in slot mode.
+__device__ __forceinline__ uint32_t bitonic_xchg(uint32_t v, int e, int kk, int j) {
+  const uint32_t p = __shfl_xor_sync(kFull, v, j);
+  return (((e & kk) == 0) == ((e & j) == 0)) ? min(v, p) : max(v, p);
+}
+__device__ __forceinline__ void sort_keys(uint32_t& k0, uint32_t& k1, bool two) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      k0 = bitonic_xchg(k0, lane, kk, j);
+      if (two) k1 = bitonic_xchg(k1, lane + 32, kk, j);
+    }
+  }
+  if (two) {
+    const uint32_t lo = min(k0, k1), hi = max(k0, k1);
+    k0 = lo;
+    k1 = hi;
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+      k0 = bitonic_xchg(k0, lane, 64, j);
+      k1 = bitonic_xchg(k1, lane + 32, 64, j);
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -244,10 +292,10 @@ struct MixedRecs {
   const RecC* gc;
   const int32_t* idx;  // bin_idx + b0
   __device__ __forceinline__ const RecS& rec(int j) const {
-    return j < ST ? s[j] : gs[__ldg(idx + j)];
+    return j < ST ? s[j] : gs[__ldcg(idx + j)];
   }
   __device__ __forceinline__ const RecC& cull(int j) const {
-    return j < ST ? c[j] : gc[__ldg(idx + j)];
+    return j < ST ? c[j] : gc[__ldcg(idx + j)];
   }
 };
 
@@ -505,6 +553,188 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
 
 }  // namespace
 
+// Slot-mode prologue of pf_fit_step (every warp of every CTA, before the role
+// split): each tile's slot list -- K1's arrival-order scatter, see SlotBins --
+// becomes the z-sorted list of bin_tiles (raster.py:227-265), written back in
+// place (list base tile * m) or, for long / overflowed lists, into the pool
+// (base n_tiles * m + pool offset); a dirty step (host edits re-scattered by
+// pf_preprocess_sync) first drops entries whose primitive no longer covers the
+// tile and duplicates.  The tile then joins its cost class (cost measured by the
+// previous step, else its length) with the CSR-shaped entry (tile, list base,
+// L, tx | ty << 16) the producers read, and its count is zeroed for the next
+// K1.  A grid barrier (all CTAs are resident: one per SM) ends the phase.
+constexpr int kSortRound = 1024;  // tiles per CTA and round (scratch: 20 B each)
+__device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* scratch) {
+  const SlotBins& sb = a.sb;
+  __shared__ int s_ccnt[kTileClasses], s_cbase[kTileClasses];
+  __shared__ unsigned s_k;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nwarps = blockDim.x >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const bool dirty = __ldcg(sb.ctl + kSlotDirty) != 0u;
+  const int nslot = sb.n_tiles * sb.m;
+  int4* ent = reinterpret_cast<int4*>(scratch);
+  int* cls = reinterpret_cast<int*>(ent + kSortRound);
+  int32_t* cost = a.classes_rw + tile_cost_offset(a.n_tiles);
+  int4* clists = reinterpret_cast<int4*>(a.classes_rw + kTileClasses);
+  const int per = (a.n_tiles + gridDim.x - 1) / gridDim.x;
+  const int c0 = min(a.n_tiles, (int)blockIdx.x * per), c1 = min(a.n_tiles, c0 + per);
+  unsigned kacc = 0;
+  if (t == 0) s_k = 0u;
+  auto covers = [&](uint32_t z, int txy) {
+    if (z == ~0u) return false;
+    const int4 r = __ldcg(a.rect + z);
+    const int tx = txy & 0xffff, ty = txy >> 16;
+    return r.y <= ty && ty <= r.w && (r.x & 0xffff) <= tx && tx <= (r.x >> 16);
+  };
+  for (int r0 = c0; r0 < c1; r0 += kSortRound) {
+    const int nr = min(kSortRound, c1 - r0);
+    if (t < kTileClasses) s_ccnt[t] = 0;
+    __syncthreads();
+    // a warp's tiles in batches of kB: every batch's loads in flight first
+    constexpr int kB = 4;
+    for (int ib = warp; ib < nr; ib += nwarps * kB) {
+      int braw[kB], bw[kB];
+      uint32_t bk0[kB], bk1[kB];
+#pragma unroll
+      for (int q = 0; q < kB; ++q) {
+        const int i = ib + q * nwarps;
+        braw[q] = bw[q] = 0;
+        bk0[q] = bk1[q] = ~0u;
+        if (i < nr) {
+          const uint32_t* sl = sb.slot + (size_t)(r0 + i) * sb.m;
+          if (lane == 0) {
+            braw[q] = __ldcg(sb.cnt + r0 + i);
+            bw[q] = __ldcg(cost + r0 + i);
+          }
+          if (lane < sb.m) bk0[q] = __ldcg(sl + lane);
+          if (lane + 32 < sb.m) bk1[q] = __ldcg(sl + 32 + lane);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kB; ++q) {
+        const int i = ib + q * nwarps;
+        if (i >= nr) break;  // (warp-uniform)
+        const int tile = r0 + i;
+        const int txy = (tile % a.ntx) | ((a.ty_begin + tile / a.ntx) << 16);
+        uint32_t* sl = sb.slot + (size_t)tile * sb.m;
+        int raw = __shfl_sync(kFull, braw[q], 0);
+        uint32_t k0 = bk0[q], k1 = bk1[q];
+        int L = 0, b0 = tile * sb.m;
+        if (raw <= 64 && raw <= sb.m) {
+          if (lane >= raw) k0 = ~0u;
+          if (lane + 32 >= raw) k1 = ~0u;
+          if (dirty) {
+            if (!covers(k0, txy)) k0 = ~0u;
+            if (!covers(k1, txy)) k1 = ~0u;
+          }
+          sort_keys(k0, k1, raw > 32);
+          if (dirty) {
+            // duplicates are adjacent after the sort: drop all but the first, re-sort
+            const uint32_t p0 = __shfl_up_sync(kFull, k0, 1);
+            const uint32_t l0 = __shfl_sync(kFull, k0, 31);
+            const uint32_t q1 = __shfl_up_sync(kFull, k1, 1);
+            const bool d0 = lane > 0 && k0 == p0;
+            const bool d1 = lane == 0 ? k1 == l0 : k1 == q1;
+            if (d0) k0 = ~0u;
+            if (d1) k1 = ~0u;
+            sort_keys(k0, k1, raw > 32);
+          }
+          L = __popc(__ballot_sync(kFull, k0 != ~0u)) + __popc(__ballot_sync(kFull, k1 != ~0u));
+          if (lane < L) sl[lane] = k0;
+          if (lane + 32 < L) sl[lane + 32] = k1;
+        } else {
+          // general path (long or overflowed lists; rare): gather the slots and
+          // the tile's overflow entries into scratch, keep valid first
+          // occurrences, rank by z into the pool
+          int gb = 0;
+          if (lane == 0) gb = (int)atomicAdd(sb.ctl + kSlotGather, 2u * (uint32_t)raw);
+          gb = __shfl_sync(kFull, gb, 0);
+          if (gb + 2 * raw > sb.gat_cap) {
+            if (lane == 0) sb.ctl[kSlotErr] = 1u;
+            raw = 0;
+          }
+          uint32_t* g1 = sb.gat + gb;
+          uint32_t* g2 = g1 + raw;
+          const int n_in = min(raw, sb.m);
+          for (int k = lane; k < n_in; k += 32) g1[k] = __ldcg(sl + k);
+          int pos = n_in;
+          if (raw > sb.m) {
+            const int novf = min((int)__ldcg(sb.ctl + kSlotOvf), sb.ovf_cap);
+            for (int o0 = 0; o0 < novf && pos < raw; o0 += 32) {
+              const int o = o0 + lane;
+              const int2 e = o < novf ? __ldcg(sb.ovf + o) : make_int2(-1, 0);
+              const bool hit = e.x == tile;
+              const unsigned hm = __ballot_sync(kFull, hit);
+              const int at = pos + __popc(hm & lt_mask);
+              if (hit && at < raw) g1[at] = (uint32_t)e.y;
+              pos = min(raw, pos + __popc(hm));
+            }
+          }
+          __syncwarp();
+          for (int q0 = 0; q0 < pos; q0 += 32) {
+            const int k = q0 + lane;
+            const uint32_t key = k < pos ? __ldcg(g1 + k) : ~0u;
+            bool keep = key != ~0u && (!dirty || covers(key, txy));
+            if (dirty && keep)
+              for (int j = 0; j < k; ++j)
+                if (__ldcg(g1 + j) == key) {
+                  keep = false;
+                  break;
+                }
+            if (k < pos) g2[k] = keep ? key : ~0u;
+            L += __popc(__ballot_sync(kFull, keep));
+          }
+          __syncwarp();
+          int pb = 0;
+          if (lane == 0) pb = (int)atomicAdd(sb.ctl + kSlotPool, (uint32_t)L);
+          pb = __shfl_sync(kFull, pb, 0);
+          if (pb + L > sb.pool_cap) {
+            if (lane == 0) sb.ctl[kSlotErr] = 1u;
+            L = 0;
+          }
+          for (int q0 = 0; q0 < pos && L > 0; q0 += 32) {
+            const int k = q0 + lane;
+            const uint32_t key = k < pos ? __ldcg(g2 + k) : ~0u;
+            if (key != ~0u) {
+              int rk = 0;
+              for (int j = 0; j < pos; ++j) rk += __ldcg(g2 + j) < key;
+              sb.pool[pb + rk] = key;
+            }
+          }
+          b0 = nslot + pb;
+        }
+        if (lane == 0) {
+          sb.cnt[tile] = 0;  // (read above by this lane) ready for the next K1
+          cost[tile] = 0;
+          const int w = bw[q];
+          const int cl = tile_class(w > 0 ? w : L);
+          const int rank = atomicAdd(&s_ccnt[cl], 1);
+          ent[i] = make_int4(tile, b0, L, txy);
+          cls[i] = cl | (rank << 8);
+          kacc += (unsigned)L;
+        }
+      }
+    }
+    __syncthreads();
+    if (t < kTileClasses) s_cbase[t] = s_ccnt[t] ? atomicAdd(a.classes_rw + t, s_ccnt[t]) : 0;
+    __syncthreads();
+    for (int i = t; i < nr; i += blockDim.x) {
+      const int cl = cls[i] & 0xff, rank = cls[i] >> 8;
+      clists[(size_t)cl * a.n_tiles + s_cbase[cl] + rank] = ent[i];
+    }
+    __syncthreads();
+  }
+  if (lane == 0 && kacc) atomicAdd(&s_k, kacc);
+  __syncthreads();
+  // grid barrier: the lists, classes and counts of every CTA are complete
+  if (t == 0) {
+    if (s_k) atomicAdd(sb.ctl + kSlotK, s_k);
+    atom_add_acq_rel(a.ctr + 2, 1u);
+    while (ld_acquire(a.ctr + 2) < gridDim.x) __nanosleep(64);
+  }
+  __syncthreads();
+}
+
 // Persistent, warp-specialised.  One CTA per SM; G groups of one producer warp
 // and 8 consumer warps (one 8x4 pixel sub-tile each).  Warps [0, 8G) consume
 // (group = warp / 8), warps [8G, 9G) produce, padded to whole warpgroups: the
@@ -519,7 +749,7 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
 // The padded alpha atlas is loaded into shared memory once per CTA: float64
 // (ATL == 2) when it fits, else float32 (ATL == 1); ATL == 0 reads the global
 // fp32 plane.
-template <int LOSS, int ATL, int G, bool BG, int ST>
+template <int LOSS, int ATL, int G, bool BG, int ST, bool SLOT>
 __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t full[G][kNBuf], empty[G][kNBuf];
@@ -566,16 +796,31 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   pdl_wait();  // bins, classes and records of this step are complete from here on
   tl_mark(a.tl, 1, 1);
+  constexpr bool slot_mode = SLOT;  // (a template parameter: consumer registers)
+  // (no fences in this kernel: any fence makes ptxas turn every gradient RED
+  // into a returning ATOM -- 10 % of the kernel's time)
+  __shared__ unsigned s_adv;
+  if (slot_mode && blockIdx.x == 0 && t == 0) {
+    // (no pf_bin in slot mode) the Adam step before this one is complete: advance
+    // the iteration counter the next Adam launch reads before its own wait.
+    // Returning atomics, their values consumed before the block barrier that
+    // precedes this CTA's trigger: performed at L2 before the dependent launches.
+    unsigned adv = 0u;
+    if (atomicExch(a.done + 2, 0u) != 0u) adv = atomicAdd(a.done + 1, 1u) + 1u;
+    s_adv = adv;
+  }
+  __syncthreads();
   // after the wait (so a dependent that starts early knows K2 -- and by induction
   // the previous Adam step -- has completed): the Adam kernel may start loading
   // its inputs that this kernel does not write
   pdl_trigger();
-  __syncthreads();
-  if (a.status[1]) {
+  if (slot_mode ? __ldcg(a.sb.ctl + kSlotErr) != 0u : a.status[1] != 0) {
     // bin overflow (grid-uniform): lists are not valid; leave clean counters
     if (blockIdx.x == 0 && a.classes && t < kTileClasses) a.classes_rw[t] = 0;
+    if (slot_mode && blockIdx.x == 0 && t == 0) a.status_rw[1] = 1;
     return;
   }
+  if constexpr (SLOT) slot_prologue(a, sm);
 
   const bool consumer = warp < G * kCW;
   const int g = consumer ? warp / kCW : warp - G * kCW;
@@ -616,14 +861,15 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
     if (g >= G) return;  // padding warp
     // ---------------- producer warp
     // Dynamic schedule: a global ticket t is mapped to a tile through the
-    // per-class tile lists pf_bin wrote (classes by list length, heaviest
-    // first: longest-processing-time order, so the tail of the launch is made
-    // of light tiles).  The next tile's ticket and list are fetched right
-    // after the current tile's copies go out, overlapping the wait for the
-    // next free ring slot.  (a.sched_lazy: fetch only once the slot is free.)
+    // per-class tile lists (pf_bin's, or the slot-mode prologue's; classes by
+    // cost, heaviest first: longest-processing-time order, so the tail of the
+    // launch is made of light tiles).  The next tile's ticket and list are
+    // fetched right after the current tile's copies go out, overlapping the wait
+    // for the next free ring slot.  (Everything here may have been written by
+    // this launch's prologue in slot mode: L2 loads, not the nc path.)
     int cls_pre = 0;  // lane l < kTileClasses: tiles in classes heaviest..l (inclusive)
     if (a.classes) {
-      const int c = lane < kTileClasses ? __ldg(a.classes + (kTileClasses - 1 - lane)) : 0;
+      const int c = lane < kTileClasses ? __ldcg(a.classes + (kTileClasses - 1 - lane)) : 0;
       cls_pre = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -631,6 +877,8 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
         if (lane >= o) cls_pre += y;
       }
     }
+    // list base: CSR bin_idx, or (slot mode) the slot + pool lists
+    const int32_t* lists = SLOT ? reinterpret_cast<const int32_t*>(a.sb.slot) : a.bin_idx;
     // tickets: the first one of each producer is static (blockIdx, group), later
     // ones come from the global counter (offset by the static range)
     int ticket_k = 0;
@@ -648,10 +896,10 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
         const int ci = __popc(below);  // rank of the class holding ticket t
         const int before = __shfl_sync(kFull, cls_pre, max(ci - 1, 0));
         const int idx = t - (ci > 0 ? before : 0);
-        // (ci == kTileClasses: counts do not cover t -- never with pf_bin's lists)
+        // (ci == kTileClasses: counts do not cover t -- never with complete lists)
         if (ci < kTileClasses) {
-          const int4 e = __ldg(reinterpret_cast<const int4*>(a.classes + kTileClasses) +
-                               (size_t)(kTileClasses - 1 - ci) * a.n_tiles + idx);
+          const int4 e = __ldcg(reinterpret_cast<const int4*>(a.classes + kTileClasses) +
+                                (size_t)(kTileClasses - 1 - ci) * a.n_tiles + idx);
           tile = e.x;
           b0 = e.y;
           L = e.z;
@@ -665,23 +913,27 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
       }
     };
     auto load_list = [&]() {
-      if (tile < a.n_tiles) i0 = lane < L ? __ldg(a.bin_idx + b0 + lane) : 0;
-      if (ST > 32 && tile < a.n_tiles) i1 = lane + 32 < L ? __ldg(a.bin_idx + b0 + lane + 32) : 0;
+      if (tile < a.n_tiles) i0 = lane < L ? __ldcg(lists + b0 + lane) : 0;
+      if (ST > 32 && tile < a.n_tiles) i1 = lane + 32 < L ? __ldcg(lists + b0 + lane + 32) : 0;
     };
-    next_tile();
-    load_list();
     int buf = 0;
     uint32_t eph = 0;  // parity of the empty barrier we wait on next, per slot (bit b)
+    // one fetch site: the next tile's ticket and list are fetched right after the
+    // previous tile's copies went out, before waiting for its ring slot
+#pragma unroll 1
     for (int k = 0;; ++k) {
+      const unsigned long long cp = a.prof ? clock64() : 0;
+      next_tile();
+      load_list();
+      if (a.prof) {  // producer "work" = ticket + list fetch
+        p_work += clock64() - cp;
+        ++p_n;
+      }
       if (k >= kNBuf) {
         const unsigned long long c0 = a.prof ? clock64() : 0;
         mbar_wait_sleep(&empty[g][buf], (eph >> buf) & 1u, a.psleep);
         if (a.prof) p_wait += clock64() - c0;
         eph ^= 1u << buf;
-        if (a.sched_lazy && k > 0) {
-          next_tile();
-          load_list();
-        }
       }
       if (tile >= a.n_tiles) {
         int last = 0;
@@ -691,11 +943,21 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
           last = atomicAdd(a.ctr + 1, 1u) == gridDim.x * G - 1;
         }
         // the last producer out resets the ticket and (every producer read them
-        // at its start) the class counts for the next step
+        // at its start) the class counts for the next step; slot mode: publishes
+        // K, resets the per-step slot words and the prologue's grid barrier
         if (__shfl_sync(kFull, last, 0)) {
           if (lane == 0) {
             atomicExch(a.ctr, 0u);
             atomicExch(a.ctr + 1, 0u);
+            if (SLOT) {
+              atomicExch(a.ctr + 2, 0u);  // the prologue's grid barrier
+              a.status_rw[0] = (int32_t)atomicExch(a.sb.ctl + kSlotK, 0u);
+              a.status_rw[1] = __ldcg(a.sb.ctl + kSlotErr) != 0u ? 1 : 0;
+              a.sb.ctl[kSlotPool] = 0u;
+              a.sb.ctl[kSlotGather] = 0u;
+              a.sb.ctl[kSlotOvf] = 0u;
+              a.sb.ctl[kSlotDirty] = 0u;
+            }
           }
           if (a.classes && lane < kTileClasses) a.classes_rw[lane] = 0;
         }
@@ -726,10 +988,6 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
         if (has_bg) bulk_g2s(buf_bg(buf) + lane * kTile, a.bg4 + row, row_bytes, &full[g][buf]);
       }
       buf = buf + 1 == kNBuf ? 0 : buf + 1;
-      if (!a.sched_lazy || k + 1 < kNBuf) {
-        next_tile();
-        load_list();
-      }
     }
     finish();
   } else {
@@ -753,11 +1011,20 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
       const RecC* rc = buf_cull(buf);
       const float4* tgs = buf_tgt(buf);
       const float4* bgs = has_bg ? buf_bg(buf) : nullptr;
+      // spill entry base: the CSR offset; slot mode: the group's arena for a list
+      // in the tile's own slots, its pool range for a general-path list
+      int sbase = h.y;
+      if constexpr (SLOT) {
+        const int nslot = a.sb.n_tiles * a.sb.m;
+        sbase = h.y >= nslot ? (int)gridDim.x * G * kSlotArena + (h.y - nslot)
+                             : (int)(blockIdx.x * G + g) * kSlotArena;
+      }
       if (h.z <= ST) {
-        warp_tile<LOSS>(a, StagedRecs{rs, rc}, atl, tgs, bgs, stA, stB, h.x, h.y, h.z, h.w, wg);
+        warp_tile<LOSS>(a, StagedRecs{rs, rc}, atl, tgs, bgs, stA, stB, h.x, sbase, h.z, h.w, wg);
       } else {
-        warp_tile<LOSS>(a, MixedRecs<ST>{rs, rc, a.recs, a.recc, a.bin_idx + h.y}, atl, tgs, bgs,
-                        stA, stB, h.x, h.y, h.z, h.w, wg);
+        const int32_t* lst = (SLOT ? reinterpret_cast<const int32_t*>(a.sb.slot) : a.bin_idx) + h.y;
+        warp_tile<LOSS>(a, MixedRecs<ST>{rs, rc, a.recs, a.recc, lst}, atl, tgs, bgs,
+                        stA, stB, h.x, sbase, h.z, h.w, wg);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[g][buf]);
@@ -815,8 +1082,12 @@ extern "C" int pf_fold_loss(const double* part, int n_part, double* sums, void* 
   return (int)cudaGetLastError();
 }
 
+// (capacity entries for CSR offsets / the slot-mode pool, plus the slot-mode
+// per-group arenas of kSlotArena entries: one CTA of 3 groups per SM)
 extern "C" size_t pf_step_spill_bytes(int capacity) {
-  return (size_t)(capacity > 0 ? capacity : 1) * kTilePix * 2 * sizeof(float4);
+  const size_t entries = (size_t)(capacity > 0 ? capacity : 1) + 64 +
+                         (size_t)dev_attrs().sms * 3 * kSlotArena;
+  return entries * kTilePix * 2 * sizeof(float4);
 }
 
 static unsigned long long* g_prof_buf = nullptr;
@@ -848,10 +1119,14 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
                            double alpha_w, double w_mse, double w_gray, double inv_3P,
                            double inv_P, void* spill, float* img4,
                            double* part, double* grads, uint32_t* counters,
-                           const int32_t* tile_classes, int stage, void* stream) {
-  if (W < 1 || H < 1 || n < 0 || !bin_off || !bin_idx || !status || !tex || !apad || !tgt4 ||
+                           const int32_t* tile_classes, int stage, void* scratch,
+                           size_t scratch_bytes, int capacity, void* slots, int slot_m,
+                           void* stream) {
+  if (W < 1 || H < 1 || n < 0 || !status || !tex || !apad || !tgt4 ||
       !spill || !part || !grads || !counters || pad_texels < 0 || (pad_texels & 3))
     return PF_ERR_ARG;
+  if (!slots && (!bin_off || !bin_idx)) return PF_ERR_ARG;
+  if (slots && (slot_m < 1 || !tile_classes || !scratch || capacity < 0)) return PF_ERR_ARG;
   if (loss_kind != PF_LOSS_MSE && loss_kind != PF_LOSS_SPATIAL && loss_kind != PF_LOSS_COMBINED)
     return PF_ERR_ARG;
   const int ntx = div_up(W, kTile), nty = div_up(H, kTile);
@@ -907,6 +1182,18 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
                              : nullptr;
   a.prof = nullptr;
   a.tl = pf_timeline_ptr();
+  a.sb = SlotBins{};
+  a.rect = nullptr;
+  a.done = nullptr;
+  a.status_rw = const_cast<int32_t*>(status);
+  if (slots) {
+    if (scratch_bytes < carve(nullptr, n, capacity, n_tiles).total) return PF_ERR_SCRATCH;
+    const BinScratch bs = carve(scratch, n, capacity, n_tiles);
+    a.sb = slot_carve(slots, n_tiles, slot_m, capacity);
+    a.rect = bs.rect;
+    a.done = bs.done;
+    if (dg.step_nolpt || !a.classes) return PF_ERR_ARG;  // slot mode needs K1's classes
+  }
   static unsigned long long* prof_buf = nullptr;
   if (dg.step_prof) {
     if (!prof_buf) cudaMalloc(&prof_buf, sizeof(unsigned long long) * (6 * 148 * 32 + 65536 * 8));
@@ -937,11 +1224,19 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   }
   const size_t smem = G * gb + (atl == 2 ? a64 : atl == 1 ? a32 : 0);
   void (*kern)(StepArgs);
-#define PF_PICK3(LS, SS)                                                                     \
-  kern = bg ? (atl == 2 ? k_step<LS, 2, 3, true, SS> : atl == 1 ? k_step<LS, 1, 3, true, SS>     \
-                                                            : k_step<LS, 0, 3, true, SS>)        \
-            : (atl == 2 ? k_step<LS, 2, 3, false, SS> : atl == 1 ? k_step<LS, 1, 3, false, SS>   \
-                                                             : k_step<LS, 0, 3, false, SS>);
+#define PF_PICK4(LS, SS, SL)                                                                    \
+  kern = bg ? (atl == 2   ? k_step<LS, 2, 3, true, SS, SL>                                      \
+               : atl == 1 ? k_step<LS, 1, 3, true, SS, SL>                                      \
+                          : k_step<LS, 0, 3, true, SS, SL>)                                     \
+            : (atl == 2   ? k_step<LS, 2, 3, false, SS, SL>                                     \
+               : atl == 1 ? k_step<LS, 1, 3, false, SS, SL>                                     \
+                          : k_step<LS, 0, 3, false, SS, SL>);
+#define PF_PICK3(LS, SS)    \
+  if (slots) {              \
+    PF_PICK4(LS, SS, true)  \
+  } else {                  \
+    PF_PICK4(LS, SS, false) \
+  }
 #define PF_PICK(LS)      \
   if (ST == 64) {        \
     PF_PICK3(LS, 64)     \
@@ -955,6 +1250,7 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   } else {
     PF_PICK(PF_LOSS_SPATIAL)
   }
+#undef PF_PICK4
 #undef PF_PICK3
 #undef PF_PICK
   if (const cudaError_t e = ensure_dyn_smem((const void*)kern, smem)) return (int)e;

@@ -381,7 +381,14 @@ class StepEngine:
         # come from the texture; PF_TWO_KERNEL=1 forces K3 + K4 (A/B checks)
         self.fused = scene.mu_blend == 0.0 and os.environ.get("PF_TWO_KERNEL", "0") != "1"
         if self.fused:
-            self.comp.enable_step_schedule()
+            # slot binning: K1 scatters the tile lists, K34 sorts them (no K2);
+            # PF_CSR_STEP=1 keeps pf_bin's CSR lists (A/B), PF_SLOT_M overrides the
+            # slots per tile (tests force the overflow path with a small value)
+            slot_m = 0
+            if os.environ.get("PF_CSR_STEP", "0") != "1":
+                slot_m = int(os.environ.get("PF_SLOT_M", "0")) or slot_count(
+                    vec.reshape(n, 8), tid, self.atlas.hyp, self.padding, W, H, band)
+            self.comp.enable_step_schedule(slot_m)
         else:
             self.comp.alloc_render(save=True, loss=True)
         # per-iteration loss sums per Adam block (history; folded in order on the host)
@@ -653,6 +660,37 @@ class StepEngine:
         loss, ps = self.loss_psnr(self.iteration_sums(part))
         return [HistoryEntry(i, float(loss[i]), float(ps[i]) if compute_psnr else math.nan,
                              self.lr_host[i], 0) for i in range(k)]
+
+
+def slot_count(params: np.ndarray, tids: np.ndarray, hyp: np.ndarray, padding: float, W: int,
+               H: int, band: Band) -> int:
+    """Slots per tile for slot binning: twice the longest tile list of the
+    initial state (bbox as bin_tiles, raster.py:246-257), a power of two in
+    [64, 1024].  Only a size: longer lists later take the overflow path."""
+    n = len(params)
+    if n == 0:
+        return 64
+    ntx, nty = -(-W // 16), -(-H // 16)
+    x, y, s = params[:, 0], params[:, 1], params[:, 2]
+    r = s * hyp[tids] + padding
+    with np.errstate(invalid="ignore"):
+        lo_x = np.maximum(np.ceil(x - r), 0.0)
+        hi_x = np.minimum(np.floor(x + r), W - 1.0)
+        lo_y = np.maximum(np.ceil(y - r), 0.0)
+        hi_y = np.minimum(np.floor(y + r), H - 1.0)
+        ok = (lo_x <= hi_x) & (lo_y <= hi_y)
+    tx0, tx1 = (lo_x[ok] // 16).astype(np.int64), (hi_x[ok] // 16).astype(np.int64)
+    ty0 = np.maximum((lo_y[ok] // 16).astype(np.int64), band.ty_begin)
+    ty1 = np.minimum((hi_y[ok] // 16).astype(np.int64), band.ty_end - 1)
+    keep = ty0 <= ty1
+    diff = np.zeros((nty + 1, ntx + 1), dtype=np.int64)
+    np.add.at(diff, (ty0[keep], tx0[keep]), 1)
+    np.add.at(diff, (ty0[keep], tx1[keep] + 1), -1)
+    np.add.at(diff, (ty1[keep] + 1, tx0[keep]), -1)
+    np.add.at(diff, (ty1[keep] + 1, tx1[keep] + 1), 1)
+    cnt = diff.cumsum(0).cumsum(1)[:nty, :ntx]
+    mx = int(cnt.max()) if cnt.size else 0
+    return int(min(1024, max(64, 1 << max(0, 2 * mx - 1).bit_length())))
 
 
 def should_reinit(iteration: int, total: int, period: int, warmup: int) -> bool:

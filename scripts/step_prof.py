@@ -36,8 +36,9 @@ t0 = d[:, 3].min()
 print(f"slots {n}: kernel span {(d[:, 4].max() - t0) / 1e3:.1f} us; start spread {(d[:, 3].max() - t0) / 1e3:.1f} us")
 for name, m in (("consumer", cons), ("producer", prod)):
     x = d[m]
-    print(f"{name}: wait {x[:, 0].mean() / 1965:.1f} us  work {x[:, 1].mean() / 1965:.1f} us  tiles {x[:, 2].mean():.2f}  "
-          f"end spread {(x[:, 4].min() - t0) / 1e3:.1f}..{(x[:, 4].max() - t0) / 1e3:.1f} us  first wait {first[m].mean() / 1965:.1f} us")
+    print(f"{name}: wait {x[:, 0].mean() / 1965:.1f} us  work {x[:, 1].mean() / 1965:.1f} us  n {x[:, 2].mean():.2f}  "
+          f"end spread {(x[:, 4].min() - t0) / 1e3:.1f}..{(x[:, 4].max() - t0) / 1e3:.1f} us  "
+          f"first {first[m].mean() / 1965:.1f} us")
 
 xe = (d[cons][:, 4] - t0) / 1e3
 xs = (d[cons][:, 3] - t0) / 1e3
@@ -51,7 +52,11 @@ tb = np.zeros((nt, 8), dtype=np.uint64)
 lib.pf_step_prof_tiles(tb.ctypes.data_as(C.c_void_p), nt)
 dur = (tb & 0xffffffff).astype(np.float64) / 1965.0  # us per (tile, warp)
 endt = (tb >> 32).astype(np.float64)
-off = eng.comp.bin_off.cpu().numpy()
+if eng.comp.slots is not None:  # slot mode: the lists of the current parameters
+    eng.refresh()
+    off, _ = eng.comp.slot_lists()
+else:
+    off = eng.comp.bin_off.cpu().numpy()
 L = np.diff(off)
 tmax = dur.max(axis=1)
 print(f"tile max-warp time: mean {tmax.mean():.2f} p50 {np.median(tmax):.2f} p90 {np.percentile(tmax, 90):.2f} max {tmax.max():.2f} us; warp mean {dur.mean():.2f}")

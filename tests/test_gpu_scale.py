@@ -136,6 +136,7 @@ def test_bins_two_level_bit_exact(diag_reload, torch_cuda, oracle, monkeypatch, 
         assert launches == (1 if two == "0" else 4)
         from paper_2602_22625_b200.fit import StepEngine
 
+        monkeypatch.setenv("PF_CSR_STEP", "1")  # the engines' pf_bin (CSR) path
         for band in row_bands(nty, 8):
             eng = StepEngine(sc, w.cfg, w.loss, 1, band=band, use_graph=False)
             eng.refresh()
