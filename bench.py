@@ -230,16 +230,20 @@ def _config(name: str, w) -> dict:
 KNAME = {"step": "k_step", "forward": "k_forward", "backward": "k_backward"}
 
 
-def ncu_summary(kernel_prefix: str) -> dict | None:
+def ncu_summary(kernel_prefix: str, config: str = "c3") -> dict | None:
     """The named kernel's entry of the newest committed ncu --set full summary
-    under profiles/ (scripts/ncu_extract.py), or None."""
-    def version(f: Path) -> tuple:  # (round, version): r02_* after r01_*_v11
-        rnd = f.stem.split("_", 1)[0]
+    of this config under profiles/ (scripts/ncu_extract.py), or None."""
+    import re
+
+    def version(f: Path) -> tuple:  # r02b_* after r02_* after r01_*_v11
+        m = re.match(r"r(\d+)([a-z]?)_", f.stem)
         tail = f.stem.rsplit("_v", 1)
-        return (int(rnd[1:]) if rnd[1:].isdigit() else -1,
+        return (int(m.group(1)) if m else -1, m.group(2) if m else "",
                 int(tail[1]) if len(tail) == 2 and tail[1].isdigit() else -1)
 
     files = sorted((ROOT / "profiles").glob("*ncu_kernels*.json"), key=version)
+    # summaries named for a config (r02*_ncu_kernels_<config>.json) count only for it
+    files = [f for f in files if not re.search(r"_c\d", f.stem) or f.stem.endswith("_" + config)]
     for f in reversed(files):
         try:
             d = json.loads(f.read_text())
@@ -251,19 +255,20 @@ def ncu_summary(kernel_prefix: str) -> dict | None:
     return None
 
 
-def issue_frac(kernel_prefix: str, sms: int = 148, mhz: float = 1965.0) -> float | None:
+def issue_frac(kernel_prefix: str, config: str = "c3", sms: int = 148,
+               mhz: float = 1965.0) -> float | None:
     """Issued warp instructions per SM per cycle / 4 (one issue per SMSP per cycle)
     for the named kernel, from the committed ncu summary (duration at SM clock)."""
-    v = ncu_summary(kernel_prefix)
+    v = ncu_summary(kernel_prefix, config)
     if not v or not v.get("warp_instructions") or not v.get("duration_ns"):
         return None
     cycles = float(v["duration_ns"]) * 1e-9 * mhz * 1e6
     return float(v["warp_instructions"]) / (sms * cycles) / 4.0
 
 
-def ncu_traffic(kernel_prefix: str) -> float | None:
+def ncu_traffic(kernel_prefix: str, config: str = "c3") -> float | None:
     """dram bytes (read + write) per launch of the named kernel (ncu summary), or None."""
-    v = ncu_summary(kernel_prefix)
+    v = ncu_summary(kernel_prefix, config)
     return float(v["dram_traffic_bytes"]) if v else None
 
 
@@ -291,7 +296,7 @@ def autograd_bench(w, steps: int, warmup: int, flush) -> dict:
     n = params.shape[0]
     m = torch.zeros(n * 8, dtype=torch.float64, device=dev)
     v = torch.zeros_like(m)
-    total = warmup + steps
+    total = 2 * (warmup + steps) + 4  # eager warm-up + timed, then the graphed run
     lr = torch.tensor([lr_schedule(i, total, cfg.learning_rate) for i in range(total)],
                       dtype=torch.float64, device=dev)
     bc1 = torch.tensor([1 - 0.9 ** (i + 1) for i in range(total)], dtype=torch.float64, device=dev)
@@ -323,9 +328,36 @@ def autograd_bench(w, steps: int, warmup: int, flush) -> dict:
     torch.cuda.synchronize()
     r.check()
     ms = sum(a.elapsed_time(b) for a, b in evs) / steps
+    # the same training step captured once in a CUDA graph (torch.cuda.graph
+    # recipe: side-stream warm-up, capture, replay) -- the launch-bound eager
+    # loop without its Python / ctypes overhead
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(2):
+            step()
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for _ in range(warmup):
+        g.replay()
+    torch.cuda.synchronize()
+    gevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(steps)]
+    for e0, e1 in gevs:
+        flush.zero_()
+        e0.record()
+        g.replay()
+        e1.record()
+    torch.cuda.synchronize()
+    r.check()
+    gms = sum(a.elapsed_time(b) for a, b in gevs) / steps
     return {"value": 1e3 / ms, "unit": UNIT, "ms_per_step": ms,
             "path": "autograd.Renderer forward (K1+K2+K3) + torch MSE + backward (K4) + pf_adam; "
                     "no host sync per step",
+            "graphed": {"value": 1e3 / gms, "unit": UNIT, "ms_per_step": gms,
+                        "path": "the same step captured in one CUDA graph (torch.cuda.graph)"},
             "l2": "flushed (256 MiB write) before every timed step"}
 
 
@@ -499,7 +531,7 @@ def run_ours(args) -> None:
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved,
                      "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"],
-                     "traffic": ncu_traffic(KNAME[dom]),
+                     "traffic": ncu_traffic(KNAME[dom], args.config),
                      "peak_src": peaks["src"], "algorithmic_bytes": ab[dom],
                      "bytes_model": "SURVEY 8(d) share of the dominant kernel: "
                                     "68 P + 8 K16 + 32 N + 16 texels",
@@ -512,12 +544,12 @@ def run_ours(args) -> None:
                      "compulsory_frac": comp_b / (stage_ms[dom] * 1e-3) / 1e9 / peaks["hbm_gbs"],
                      # what does bound it: instruction issue (ncu summary of the
                      # same kernel: warp instructions per SM cycle against 4)
-                     "issue_frac": issue_frac(KNAME[dom])},
+                     "issue_frac": issue_frac(KNAME[dom], args.config)},
         # SURVEY 8(d) secondary unit: binned (pixel, list entry) evaluations per
         # second (256 pixels per tile-list entry at tile 16), plus the ncu L1/tex
         # hit rate and warp execution efficiency of the dominant kernel
         "secondary": {"pair_evals_per_s": 256.0 * K16 * value, "unit": "pairs/s",
-                      "ncu": {k: (ncu_summary(KNAME[dom]) or {}).get(k)
+                      "ncu": {k: (ncu_summary(KNAME[dom], args.config) or {}).get(k)
                               for k in ("l1tex_hit_pct", "warp_exec_efficiency_threads",
                                         "fp64_pipe_pct", "warps_active_pct")}},
         "run_loop": loop,

@@ -31,7 +31,8 @@ class _Composite(torch.autograd.Function):
         comp.preprocess(params)
         comp.bin()
         comp.forward(save=True, eps_skip=renderer.eps_skip, bg_rgb=renderer.bg_rgb, bg4=bg4)
-        renderer._watch(comp)
+        if not torch.cuda.is_current_stream_capturing():
+            renderer._watch(comp)
         img, alpha = comp.color().clone(), comp.alpha().clone()
         if ctx.needs_input_grad[0]:
             ctx.comp = comp  # the saved contribution lists: held until backward
@@ -45,7 +46,8 @@ class _Composite(torch.autograd.Function):
     def backward(ctx, d_img, d_alpha):
         comp: Compositor = ctx.comp
         r = ctx.renderer
-        r._raise_pending()
+        if not torch.cuda.is_current_stream_capturing():
+            r._raise_pending()
         n = comp.n
         grads = r._grads(n)
         d4 = r._d4()
@@ -73,6 +75,12 @@ class Renderer:
     ``BinOverflow`` is raised at the next backward / call once the flagged
     forward has completed, or at ``check()``.  Without ``s_max`` every call sizes
     the capacity from the current scales (one device-to-host read).
+
+    A whole training step through the Function (forward, torch loss, backward,
+    an optimizer that keeps its state on the device) can be captured in a CUDA
+    graph once ``s_max`` is set (the usual torch.cuda.graph recipe: eager
+    warm-up on a side stream, then capture); inside a capture the asynchronous
+    overflow watch is skipped -- the capacity bound makes it unnecessary.
     """
 
     def __init__(self, templates, template_id, z, canvas_w: int, canvas_h: int, *,
@@ -106,7 +114,8 @@ class Renderer:
                             -(-self.W // 16), -(-self.H // 16))
 
     def _lease(self, params: torch.Tensor) -> Compositor:
-        self._raise_pending()
+        if not torch.cuda.is_current_stream_capturing():
+            self._raise_pending()
         cap = self._capacity(params)
         for i, c in enumerate(self._free):
             if c.capacity >= cap:

@@ -1,27 +1,49 @@
 #!/bin/bash
 # Round evidence on one GPU: default bench line, ncu launch list of the same
 # command, ncu --set full captures (c3 fused step, c3 two-kernel path, c5 step),
-# kernel timeline, racecheck with the full hazard list.
+# kernel timelines, band scaling, sanitizer runs of the slot-binning step.
 set -u
-mkdir -p gpurun_out/ev
-timeout 900 python bench.py > gpurun_out/ev/bench.json 2> gpurun_out/ev/bench.err; echo "bench rc=$?"
-tail -1 gpurun_out/ev/bench.json | cut -c1-300
+O=gpurun_out/ev2
+mkdir -p $O
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
+tail -1 $O/bench.json | cut -c1-300
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-   --log-file gpurun_out/ev/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-autograd \
-   > gpurun_out/ev/ncu_launch.log 2>&1; echo "launch list rc=$?"
+   --log-file $O/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-autograd \
+   > $O/ncu_launch.log 2>&1; echo "launch list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on \
-   -k regex:"k_step|k_bin_rows|k_prim" -s 30 -c 6 \
-   -o gpurun_out/ev/prof_c3 -f python bench.py --steps 3 --warmup 3 --no-cpu --no-autograd \
-   > gpurun_out/ev/ncu_c3.log 2>&1; echo "ncu c3 rc=$?"
+   -k regex:"k_step|k_prim" -s 20 -c 4 \
+   -o $O/prof_c3 -f python bench.py --steps 3 --warmup 3 --no-cpu --no-autograd \
+   > $O/ncu_c3.log 2>&1; echo "ncu c3 rc=$?"
 PF_TWO_KERNEL=1 timeout 900 ncu --set full --clock-control none --import-source on \
-   -k regex:"k_forward|k_backward" -s 20 -c 4 \
-   -o gpurun_out/ev/prof_c3_2k -f python bench.py --steps 3 --warmup 3 --no-cpu --no-autograd \
-   > gpurun_out/ev/ncu_c3_2k.log 2>&1; echo "ncu c3 two-kernel rc=$?"
+   -k regex:"k_forward|k_backward|k_bin_rows" -s 30 -c 6 \
+   -o $O/prof_c3_2k -f python bench.py --steps 3 --warmup 3 --no-cpu --no-autograd \
+   > $O/ncu_c3_2k.log 2>&1; echo "ncu c3 two-kernel rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on \
-   -k regex:"k_step|k_bin_rows|k_row|k_prim" -s 40 -c 8 \
-   -o gpurun_out/ev/prof_c5 -f python bench.py --config c5 --steps 3 --warmup 3 --no-cpu --no-autograd \
-   > gpurun_out/ev/ncu_c5.log 2>&1; echo "ncu c5 rc=$?"
-timeout 300 python scripts/timeline.py c3 > gpurun_out/ev/timeline_c3.txt 2>&1; echo "timeline rc=$?"
-NV_COMPUTE_SANITIZER_MAX_RACECHECK_HAZARDS=100000 timeout 900 compute-sanitizer --tool racecheck \
-   python scripts/sanitize_step.py c3 2 > gpurun_out/ev/c3_racecheck_full.log 2>&1; echo "racecheck rc=$?"
-ls -la gpurun_out/ev
+   -k regex:"k_step|k_prim" -s 20 -c 4 \
+   -o $O/prof_c5 -f python bench.py --config c5 --steps 3 --warmup 3 --no-cpu --no-autograd \
+   > $O/ncu_c5.log 2>&1; echo "ncu c5 rc=$?"
+for a in "c3" "c5" "c5 band=8:3" "c3 hostio"; do
+  echo "== $a"; timeout 300 python scripts/timeline.py $a 2>&1 | tail -8
+done > $O/timelines.txt
+timeout 900 python scripts/band_scaling.py c5 1 2 4 8 > $O/band_scaling.txt 2>&1; echo "band rc=$?"
+cp gpurun_out/band_scaling_c5.json $O/ 2>/dev/null
+mkdir -p gpurun_out/sanitize
+for case in c1 c3 c5band; do
+  for tool in memcheck racecheck; do
+    extra=""; [ "$tool" = "memcheck" ] && extra="--leak-check no"
+    timeout 900 compute-sanitizer --tool $tool $extra --print-limit 50 \
+      python scripts/sanitize_step.py $case 2 > $O/san_${case}_${tool}.log 2>&1
+    echo "$case $tool rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' $O/san_${case}_${tool}.log | tail -1)"
+  done
+done
+# summaries on the box (the reports are too large to bring back together)
+for r in prof_c3 prof_c3_2k prof_c5; do
+  python scripts/ncu_extract.py $O/$r.ncu-rep $O/${r}_kernels.json > /dev/null 2>&1
+  ncu -i $O/$r.ncu-rep --page source --print-source cuda,sass --csv -k regex:"k_step|k_forward" \
+     --launch-count 1 > $O/${r}_src.csv 2>/dev/null
+  python scripts/ncu_lines.py $O/${r}_src.csv 40 > $O/${r}_lines.txt 2>&1
+  rm -f $O/${r}_src.csv
+done
+ncu -i $O/prof_c3.ncu-rep --page raw --csv > $O/prof_c3_raw.csv 2>/dev/null
+rm -f $O/prof_c3_2k.ncu-rep $O/prof_c5.ncu-rep
+ls -la $O

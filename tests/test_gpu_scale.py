@@ -638,3 +638,59 @@ def test_two_kernel_step_engine_matches_oracle_loop(torch_cuda, oracle, name, to
     assert close.mean() > (0.99 if loss == "mse" else 0.98), close.mean()
     gains = np.asarray([10, 10, 10, 1, 1.5, 1, 1, 1.0])
     assert np.all(np.abs(p_gpu - p_ref) <= 2 * w.cfg.learning_rate * gains[None, :] * total)
+
+
+def test_autograd_step_graph_capture_matches_eager(torch_cuda):
+    """A training step through the autograd Function (forward, torch MSE,
+    backward, a device-side update) captured in one CUDA graph replays the
+    eager step exactly (no host sync, no allocation inside the Function)."""
+    torch = torch_cuda
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.autograd import Renderer
+    from paper_2602_22625_b200.fit import effective_padding
+    from paper_2602_22625_b200.scene import param_matrix, structure_arrays
+
+    w = synth.make_workload("c1")
+    sc = w.scene
+    tid, z = structure_arrays(sc)
+
+    def run(graphed: bool, steps: int = 4):
+        r = Renderer(sc.templates, tid, z, sc.canvas_w, sc.canvas_h,
+                     background=tuple(sc.background), alpha_max=sc.alpha_max,
+                     padding=effective_padding(w.cfg), s_max=w.cfg.scale_max)
+        params = torch.tensor(param_matrix(sc), device="cuda", requires_grad=True)
+        target = torch.tensor(w.target, device="cuda", dtype=torch.float32)
+        losses = []
+
+        def step():
+            img, _ = r(params)
+            loss = ((img - target) ** 2).mean()
+            loss.backward()
+            with torch.no_grad():
+                params.sub_(1e-3 * params.grad)
+                params.grad.zero_()
+            return loss
+
+        if not graphed:
+            for _ in range(steps + 2):
+                losses.append(float(step()))
+            return params.detach().cpu().numpy(), losses[2:]
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                step()
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            out = step()
+        for _ in range(steps):
+            g.replay()
+            losses.append(float(out))
+        r.check()
+        return params.detach().cpu().numpy(), losses
+
+    p_e, l_e = run(False)
+    p_g, l_g = run(True)
+    np.testing.assert_allclose(l_g, l_e, rtol=1e-6)
+    np.testing.assert_allclose(p_g, p_e, rtol=1e-9, atol=1e-9)
