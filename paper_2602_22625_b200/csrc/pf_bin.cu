@@ -84,7 +84,10 @@ constexpr int kPrimThreads = 256;
 // resident blocks per SM the two K1 variants are compiled for: 3 (80 registers)
 // while the grid fits one wave at that occupancy (c3: 157 blocks), else 5 (48
 // registers, some spills; c5: 625 blocks in one wave instead of two)
-constexpr int kPrimMinBlocksLo = 3, kPrimMinBlocksHi = 5;
+#ifndef PF_PRIM_HI
+#define PF_PRIM_HI 5
+#endif
+constexpr int kPrimMinBlocksLo = 3, kPrimMinBlocksHi = PF_PRIM_HI;
 
 // adam_step for one scalar (fit.py:224-237), reference op order, no contraction.
 // m, v, frozen are loaded by the caller before the PDL wait (k_step does not
