@@ -169,6 +169,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(su32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
 }
@@ -190,9 +197,28 @@ __device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: the warp is parked by the hardware until
+// the phase completes (or the hint elapses), no polling loop in the issue slots
+__device__ __forceinline__ bool mbar_try_suspend(uint64_t* b, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(su32(b)), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
 // wait with an explicit back-off (the waiting warp leaves the issue slots alone)
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity, unsigned ns) {
+#ifdef PF_SUSPEND_WAIT
+  (void)ns;
+  while (!mbar_try_suspend(b, parity, PF_SUSPEND_WAIT)) {
+  }
+#else
   while (!mbar_try(b, parity)) __nanosleep(ns);
+#endif
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -590,35 +616,41 @@ __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* 
     const int nr = min(kSortRound, c1 - r0);
     if (t < kTileClasses) s_ccnt[t] = 0;
     __syncthreads();
-    // a warp's tiles in batches of kB: every batch's loads in flight first
+    // a warp's tiles in batches of kB: every batch's slot rows land in shared
+    // memory by async copies (and the counts / costs in lanes 0..kB-1) before the
+    // first sort; the per-tile processing is a rolled loop (one copy of the sort
+    // code: this phase runs once per launch, instruction-cache misses dominate
+    // an unrolled version)
     constexpr int kB = 4;
+    uint32_t* kbuf = reinterpret_cast<uint32_t*>(cls + kSortRound) + warp * (kB * 64);
     for (int ib = warp; ib < nr; ib += nwarps * kB) {
-      int braw[kB], bw[kB];
-      uint32_t bk0[kB], bk1[kB];
+      int qraw = 0, qw = 0;
+      if (lane < kB && ib + lane * nwarps < nr) {
+        qraw = __ldcg(sb.cnt + r0 + ib + lane * nwarps);
+        qw = __ldcg(cost + r0 + ib + lane * nwarps);
+      }
 #pragma unroll
       for (int q = 0; q < kB; ++q) {
         const int i = ib + q * nwarps;
-        braw[q] = bw[q] = 0;
-        bk0[q] = bk1[q] = ~0u;
         if (i < nr) {
           const uint32_t* sl = sb.slot + (size_t)(r0 + i) * sb.m;
-          if (lane == 0) {
-            braw[q] = __ldcg(sb.cnt + r0 + i);
-            bw[q] = __ldcg(cost + r0 + i);
-          }
-          if (lane < sb.m) bk0[q] = __ldcg(sl + lane);
-          if (lane + 32 < sb.m) bk1[q] = __ldcg(sl + 32 + lane);
+          if (lane < sb.m) cp_async4(kbuf + q * 64 + lane, sl + lane);
+          if (lane + 32 < sb.m) cp_async4(kbuf + q * 64 + 32 + lane, sl + 32 + lane);
         }
       }
-#pragma unroll
+      cp_async_wait_all();
+      __syncwarp();
+#pragma unroll 1
       for (int q = 0; q < kB; ++q) {
         const int i = ib + q * nwarps;
         if (i >= nr) break;  // (warp-uniform)
         const int tile = r0 + i;
         const int txy = (tile % a.ntx) | ((a.ty_begin + tile / a.ntx) << 16);
         uint32_t* sl = sb.slot + (size_t)tile * sb.m;
-        int raw = __shfl_sync(kFull, braw[q], 0);
-        uint32_t k0 = bk0[q], k1 = bk1[q];
+        int raw = __shfl_sync(kFull, qraw, q);
+        const int wq = __shfl_sync(kFull, qw, q);
+        uint32_t k0 = lane < sb.m ? kbuf[q * 64 + lane] : ~0u;
+        uint32_t k1 = lane + 32 < sb.m ? kbuf[q * 64 + 32 + lane] : ~0u;
         int L = 0, b0 = tile * sb.m;
         if (raw <= 64 && raw <= sb.m) {
           if (lane >= raw) k0 = ~0u;
@@ -627,17 +659,19 @@ __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* 
             if (!covers(k0, txy)) k0 = ~0u;
             if (!covers(k1, txy)) k1 = ~0u;
           }
-          sort_keys(k0, k1, raw > 32);
-          if (dirty) {
-            // duplicates are adjacent after the sort: drop all but the first, re-sort
-            const uint32_t p0 = __shfl_up_sync(kFull, k0, 1);
-            const uint32_t l0 = __shfl_sync(kFull, k0, 31);
-            const uint32_t q1 = __shfl_up_sync(kFull, k1, 1);
-            const bool d0 = lane > 0 && k0 == p0;
-            const bool d1 = lane == 0 ? k1 == l0 : k1 == q1;
-            if (d0) k0 = ~0u;
-            if (d1) k1 = ~0u;
+#pragma unroll 1
+          for (int pass = 0; pass < (dirty ? 2 : 1); ++pass) {
             sort_keys(k0, k1, raw > 32);
+            if (pass == 0 && dirty) {
+              // duplicates are adjacent after the sort: drop all but the first, re-sort
+              const uint32_t p0 = __shfl_up_sync(kFull, k0, 1);
+              const uint32_t l0 = __shfl_sync(kFull, k0, 31);
+              const uint32_t q1 = __shfl_up_sync(kFull, k1, 1);
+              const bool d0 = lane > 0 && k0 == p0;
+              const bool d1 = lane == 0 ? k1 == l0 : k1 == q1;
+              if (d0) k0 = ~0u;
+              if (d1) k1 = ~0u;
+            }
           }
           L = __popc(__ballot_sync(kFull, k0 != ~0u)) + __popc(__ballot_sync(kFull, k1 != ~0u));
           if (lane < L) sl[lane] = k0;
@@ -706,8 +740,7 @@ __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* 
         if (lane == 0) {
           sb.cnt[tile] = 0;  // (read above by this lane) ready for the next K1
           cost[tile] = 0;
-          const int w = bw[q];
-          const int cl = tile_class(w > 0 ? w : L);
+          const int cl = tile_class(wq > 0 ? wq : L);
           const int rank = atomicAdd(&s_ccnt[cl], 1);
           ent[i] = make_int4(tile, b0, L, txy);
           cls[i] = cl | (rank << 8);
@@ -725,6 +758,7 @@ __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* 
     __syncthreads();
   }
   if (lane == 0 && kacc) atomicAdd(&s_k, kacc);
+  tl_mark(a.tl, 14, 1);
   __syncthreads();
   // grid barrier: the lists, classes and counts of every CTA are complete
   if (t == 0) {
@@ -733,6 +767,7 @@ __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* 
     while (ld_acquire(a.ctr + 2) < gridDim.x) __nanosleep(64);
   }
   __syncthreads();
+  tl_mark(a.tl, 15, 1);
 }
 
 // Persistent, warp-specialised.  One CTA per SM; G groups of one producer warp

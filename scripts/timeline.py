@@ -30,7 +30,8 @@ flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 lib = nat.load()
 names = {0: "k_bin_rows", 1: "k_step", 2: "k_prim<adam>", 3: "k_prim<pre>", 4: " .adam done",
          5: " .fold done", 6: " .records done", 7: " .ticket done", 8: " bin.scan done",
-         9: " bin.list done", 10: " bin.counts done", 11: "k_row_counts", 12: "k_row_scatter", 13: "k_row_offsets"}
+         9: " bin.list done", 10: " bin.counts done", 11: "k_row_counts", 12: "k_row_scatter", 13: "k_row_offsets",
+         14: " .lists sorted", 15: " .barrier passed"}
 for rep in range(12):
     flush.zero_()
     torch.cuda.synchronize()
@@ -44,7 +45,7 @@ for rep in range(12):
     lib.pf_timeline_dump(buf.ctypes.data_as(C.c_void_p))
 if True:
     b = buf.reshape(16, 4).astype(np.float64)
-    valid = [k for k in range(14) if b[k, 3] > 0 or b[k, 2] > 0]
+    valid = [k for k in range(16) if b[k, 3] > 0 or b[k, 2] > 0]
     t0 = min(b[k, 0] for k in valid if b[k, 3] > 0)
     print(f"step (events) {e0.elapsed_time(e1) * 1e3:.1f} us; kernels (start / wait-done min..max / end, us from first start):")
     for k in valid:
