@@ -81,13 +81,14 @@ struct PreArgs {
 
 constexpr double kB1 = 0.9, kB2 = 0.999, kAdamEps = 1e-8;
 constexpr int kPrimThreads = 256;
-// resident blocks per SM the two K1 variants are compiled for: 3 (80 registers)
-// while the grid fits one wave at that occupancy (c3: 157 blocks), else 5 (48
-// registers, some spills; c5: 625 blocks in one wave instead of two)
-#ifndef PF_PRIM_HI
-#define PF_PRIM_HI 5
-#endif
-constexpr int kPrimMinBlocksLo = 3, kPrimMinBlocksHi = PF_PRIM_HI;
+// K1 runs 3 blocks per SM (80 registers, no spills) with 8 lanes per primitive
+// while that grid fits one wave (c3: 157 blocks), else with 4 lanes per
+// primitive (c5: 313 blocks instead of 625 -- one wave; a 5-block, 48-register
+// variant of the 8-lane kernel spilled and its record chain took twice as long)
+constexpr int kPrimMinBlocks = 3;
+static int prim_lanes(int n) {
+  return div_up(n > 0 ? n * 8 : 1, kPrimThreads) <= kPrimMinBlocks * dev_attrs().sms ? 8 : 4;
+}
 
 // adam_step for one scalar (fit.py:224-237), reference op order, no contraction.
 // m, v, frozen are loaded by the caller before the PDL wait (k_step does not
@@ -109,12 +110,17 @@ __device__ __forceinline__ double adam_scalar(const AdamPart& d, size_t idx, int
   return p;
 }
 
-template <bool ADAM, int MINB>
-__global__ void __launch_bounds__(kPrimThreads, MINB) k_prim(PreArgs a) {
+// LPP lanes per primitive: 8 (one parameter column each), or 4 (columns c and
+// c + 4) when 8 lanes per primitive would not fit one wave at this occupancy
+// (c5: 20k primitives) -- the same work on half the threads, no second wave.
+template <bool ADAM, int LPP>
+__global__ void __launch_bounds__(kPrimThreads, kPrimMinBlocks) k_prim(PreArgs a) {
+  static_assert(LPP == 8 || LPP == 4, "lanes per primitive");
+  constexpr int NC = 8 / LPP;  // parameter columns per lane
   tl_mark(a.tl, ADAM ? 2 : 3, 0);
   const int g = blockIdx.x * kPrimThreads + threadIdx.x;
-  const int i = g >> 3, c = g & 7;  // primitive, parameter column
-  const int lane = threadIdx.x & 31, gb = lane & ~7;
+  const int i = g / LPP, c = g % LPP;  // primitive, first parameter column
+  const int lane = threadIdx.x & 31, gb = lane & ~(LPP - 1);
   const bool live = i < a.n;
   // static structure: one 48-byte record, independent of the parameter loads
   PrimInfo pi{2, 2, 0, 0, 1.0, 1.0, 0, 0, 0, 0};
@@ -126,18 +132,26 @@ __global__ void __launch_bounds__(kPrimThreads, MINB) k_prim(PreArgs a) {
     pi.hyp = __hiloint2double(w1.w, w1.z);
     pi.zrank = w2.x; pi.tid = w2.y;
   }
-  const size_t pidx = (size_t)i * 8 + c;
-  double pc = live ? a.params[pidx] : 1.0;
+  // this lane's columns: c + LPP * k, k < NC
+  double pc[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) pc[k] = live ? a.params[(size_t)i * 8 + c + LPP * k] : 1.0;
   // incremental preprocess (src != NULL): the parameters come from src; only
   // primitives whose 8 values differ from the device copy are copied and get
   // new records / rects (the Adam launch before wrote the others' already)
   bool grp_changed = true;
   if (!ADAM && a.src) {
-    const double hv = live ? a.src[pidx] : 1.0;
-    const bool ch = __double_as_longlong(hv) != __double_as_longlong(pc);
-    grp_changed = ((__ballot_sync(kFull, ch) >> gb) & 0xffu) != 0u;
-    if (ch && live) a.params[pidx] = hv;
-    pc = hv;
+    bool ch = false;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const size_t pidx = (size_t)i * 8 + c + LPP * k;
+      const double hv = live ? a.src[pidx] : 1.0;
+      const bool chk = __double_as_longlong(hv) != __double_as_longlong(pc[k]);
+      if (chk && live) a.params[pidx] = hv;
+      ch |= chk;
+      pc[k] = hv;
+    }
+    grp_changed = ((__ballot_sync(kFull, ch) >> gb) & ((1u << LPP) - 1u)) != 0u;
   }
   int it = 0;
   double fv0 = 0.0, fv1 = 0.0, fv2 = 0.0;  // loss-fold partial sums of this thread
@@ -145,14 +159,22 @@ __global__ void __launch_bounds__(kPrimThreads, MINB) k_prim(PreArgs a) {
     // everything k_step (the predecessor) does not write, before the PDL wait
     it = (int)a.s.done[1];  // advanced by the next pf_bin / slot-mode pf_fit_step
     const double lr = a.ad.lr_table[it], bc1 = a.ad.bc1_table[it], bc2 = a.ad.bc2_table[it];
-    const double m0 = live ? a.ad.m[pidx] : 0.0, v0 = live ? a.ad.v[pidx] : 0.0;
+    double m0[NC], v0[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const size_t pidx = (size_t)i * 8 + c + LPP * k;
+      m0[k] = live ? a.ad.m[pidx] : 0.0;
+      v0[k] = live ? a.ad.v[pidx] : 0.0;
+    }
     const bool live_p = live && (a.ad.frozen == nullptr || a.ad.frozen[i] == 0);
     pdl_trigger();
     pdl_wait();
     tl_mark(a.tl, 2, 1);
     // this step's gradient and (first fold level) this block's chunk of k_step's
     // loss partials: both loads in flight before any math
-    const double gr = live ? a.ad.grads[pidx] : 0.0;
+    double gr[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) gr[k] = live ? a.ad.grads[(size_t)i * 8 + c + LPP * k] : 0.0;
     if (a.ad.part) {
       const int chunk = (a.ad.n_part + gridDim.x - 1) / gridDim.x;
       const int beg = blockIdx.x * chunk, end = min(beg + chunk, a.ad.n_part);
@@ -163,10 +185,15 @@ __global__ void __launch_bounds__(kPrimThreads, MINB) k_prim(PreArgs a) {
       }
     }
     if (live) {
-      a.ad.grads[pidx] = 0.0;  // ready for the next backward
-      pc = adam_scalar(a.ad, pidx, c, live_p, pc, gr, m0, v0, lr, bc1, bc2);
-      a.params[pidx] = pc;
-      if (a.mirror) a.mirror[pidx] = pc;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        const size_t pidx = (size_t)i * 8 + c + LPP * k;
+        a.ad.grads[pidx] = 0.0;  // ready for the next backward
+        pc[k] = adam_scalar(a.ad, pidx, c + LPP * k, live_p, pc[k], gr[k], m0[k], v0[k], lr, bc1,
+                            bc2);
+        a.params[pidx] = pc[k];
+        if (a.mirror) a.mirror[pidx] = pc[k];
+      }
     }
     tl_mark(a.tl, 4, 1);
   }
@@ -177,11 +204,11 @@ __global__ void __launch_bounds__(kPrimThreads, MINB) k_prim(PreArgs a) {
   }
   if (ADAM) tl_mark(a.tl, 5, 1);
   if (a.records) {
-  // gather the primitive's 8 parameters from its lane group
-  const double x = __shfl_sync(kFull, pc, gb + 0), y = __shfl_sync(kFull, pc, gb + 1);
-  const double s = __shfl_sync(kFull, pc, gb + 2), rot = __shfl_sync(kFull, pc, gb + 3);
-  const double nu = __shfl_sync(kFull, pc, gb + 4), cl0 = __shfl_sync(kFull, pc, gb + 5);
-  const double cl1 = __shfl_sync(kFull, pc, gb + 6), cl2 = __shfl_sync(kFull, pc, gb + 7);
+  // gather the primitive's 8 parameters from its lane group (column j lives in
+  // lane j % LPP, slot j / LPP)
+  auto col = [&](int j) { return __shfl_sync(kFull, pc[j / LPP], gb + j % LPP); };
+  const double x = col(0), y = col(1), s = col(2), rot = col(3);
+  const double nu = col(4), cl0 = col(5), cl1 = col(6), cl2 = col(7);
   const int t = pi.tid, wt = pi.wt, ht = pi.ht;
   const double q = pi.q, hyp = pi.hyp;
   const double sq = __dmul_rn(s, q);
@@ -206,7 +233,7 @@ __global__ void __launch_bounds__(kPrimThreads, MINB) k_prim(PreArgs a) {
       if (ty0 <= ty1) rc = make_int4(tx0 | (tx1 << 16), ty0, i, ty1);
     }
   }
-  if (live && c == 0 && grp_changed) a.s.rect[pi.zrank] = rc;
+  if (live && c == 0 && grp_changed) a.s.rect[pi.zrank] = rc;  // (lane 0 of the group)
   // records only for primitives in some tile of this band: nothing reads the
   // others' (every consumer walks the tile lists) -- on a row band of a
   // multi-GPU split most primitives skip the work below
@@ -238,29 +265,59 @@ __global__ void __launch_bounds__(kPrimThreads, MINB) k_prim(PreArgs a) {
     sc_t0 = sc_tile(c);
     sc_p0 = atomicAdd(a.slots.cnt + sc_t0, 1);
   }
-  if (c + 8 < sc_nt) {
-    sc_t1 = sc_tile(c + 8);
+  if (c + LPP < sc_nt) {
+    sc_t1 = sc_tile(c + LPP);
     sc_p1 = atomicAdd(a.slots.cnt + sc_t1, 1);
   }
   if (__any_sync(kFull, need)) {
   // transcendental / division work split across the lane group
   double r0 = 0.0, r1 = 0.0;
-  if (c == 0) {
-    sincos(rot, &r1, &r0);  // r0 = cos, r1 = sin
-  } else if (c <= 4) {
-    r0 = sigmoid(c == 1 ? nu : c == 2 ? cl0 : c == 3 ? cl1 : cl2);
-  } else if (c == 5) {
-    r0 = __ddiv_rn(1.0, s);
-    r1 = __ddiv_rn(1.0, sq);
+  double ct, st, sig, sc0, sc1, sc2, inv_s, inv_sq;
+  if (LPP == 8) {
+    if (c == 0) {
+      sincos(rot, &r1, &r0);  // r0 = cos, r1 = sin
+    } else if (c <= 4) {
+      r0 = sigmoid(c == 1 ? nu : c == 2 ? cl0 : c == 3 ? cl1 : cl2);
+    } else if (c == 5) {
+      r0 = __ddiv_rn(1.0, s);
+      r1 = __ddiv_rn(1.0, sq);
+    }
+    ct = __shfl_sync(kFull, r0, gb + 0);
+    st = __shfl_sync(kFull, r1, gb + 0);
+    sig = __shfl_sync(kFull, r0, gb + 1);
+    sc0 = __shfl_sync(kFull, r0, gb + 2);
+    sc1 = __shfl_sync(kFull, r0, gb + 3);
+    sc2 = __shfl_sync(kFull, r0, gb + 4);
+    inv_s = __shfl_sync(kFull, r0, gb + 5);
+    inv_sq = __shfl_sync(kFull, r1, gb + 5);
+  } else {
+    if (c == 0) {
+      sincos(rot, &r1, &r0);
+    } else if (c == 1) {
+      r0 = sigmoid(nu);
+      r1 = sigmoid(cl0);
+    } else if (c == 2) {
+      r0 = sigmoid(cl1);
+      r1 = sigmoid(cl2);
+    } else {
+      r0 = __ddiv_rn(1.0, s);
+      r1 = __ddiv_rn(1.0, sq);
+    }
+    ct = __shfl_sync(kFull, r0, gb + 0);
+    st = __shfl_sync(kFull, r1, gb + 0);
+    sig = __shfl_sync(kFull, r0, gb + 1);
+    sc0 = __shfl_sync(kFull, r1, gb + 1);
+    sc1 = __shfl_sync(kFull, r0, gb + 2);
+    sc2 = __shfl_sync(kFull, r1, gb + 2);
+    inv_s = __shfl_sync(kFull, r0, gb + 3);
+    inv_sq = __shfl_sync(kFull, r1, gb + 3);
   }
-  const double ct = __shfl_sync(kFull, r0, gb + 0), st = __shfl_sync(kFull, r1, gb + 0);
-  const double sig = __shfl_sync(kFull, r0, gb + 1);
-  const double sc0 = __shfl_sync(kFull, r0, gb + 2), sc1 = __shfl_sync(kFull, r0, gb + 3);
-  const double sc2 = __shfl_sync(kFull, r0, gb + 4);
-  const double inv_s = __shfl_sync(kFull, r0, gb + 5), inv_sq = __shfl_sync(kFull, r1, gb + 5);
   const double omm = __dsub_rn(1.0, a.mu_blend);
 
   if (need) {
+#pragma unroll
+  for (int kc = 0; kc < NC; ++kc) {
+    const int c = lane % LPP + LPP * kc;  // the slice index this pass stores (0..7)
     // each lane stores one 16-byte slice of RecF (8 slices) and of RecG (5) / RecC (2)
     double2* pf = reinterpret_cast<double2*>(a.recf + i);
     switch (c) {
@@ -362,15 +419,17 @@ __global__ void __launch_bounds__(kPrimThreads, MINB) k_prim(PreArgs a) {
         default: break;
       }
     }
+  }  // the lane's slices
   }
   }  // any record in this warp
+  if (ADAM && need) tl_mark(a.tl, 8, 2);  // (diagnostics: records stored)
   if (sc_t0 >= 0) sc_put(sc_t0, sc_p0);
   if (sc_t1 >= 0) sc_put(sc_t1, sc_p1);
-  for (int k0 = c + 16; k0 < sc_nt; k0 += 32) {
+  for (int k0 = c + 2 * LPP; k0 < sc_nt; k0 += 4 * LPP) {
     int t4[4], p4[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int k = k0 + 8 * q;
+      const int k = k0 + LPP * q;
       t4[q] = k < sc_nt ? sc_tile(k) : -1;
       if (t4[q] >= 0) p4[q] = atomicAdd(a.slots.cnt + t4[q], 1);
     }
@@ -378,6 +437,7 @@ __global__ void __launch_bounds__(kPrimThreads, MINB) k_prim(PreArgs a) {
     for (int q = 0; q < 4; ++q)
       if (t4[q] >= 0) sc_put(t4[q], p4[q]);
   }
+  if (ADAM && need) tl_mark(a.tl, 9, 2);  // (diagnostics: scatter done)
   // an edited primitive re-scattered next to its previous entries: the
   // producers validate and de-duplicate this step's lists
   if (!ADAM && a.src && sc_nt > 0 && c == 0) a.slots.ctl[kSlotDirty] = 1u;
@@ -999,16 +1059,15 @@ extern "C" int pf_slot_reset(void* slots, int n_tiles, int m, int capacity,
   return (int)e;
 }
 
-static int sms_count();
 static int launch_prim(bool adam, const PreArgs& a, cudaStream_t st) {
-  const int blocks = div_up(a.n > 0 ? a.n * 8 : 1, kPrimThreads);
-  const bool hi = blocks > kPrimMinBlocksLo * sms_count();
+  const int lpp = prim_lanes(a.n);
+  const int blocks = div_up(a.n > 0 ? a.n * lpp : 1, kPrimThreads);
   if (adam)
-    return (int)launch_pdl(hi ? k_prim<true, kPrimMinBlocksHi> : k_prim<true, kPrimMinBlocksLo>,
-                           blocks, kPrimThreads, 0, st, a);
+    return (int)launch_pdl(lpp == 8 ? k_prim<true, 8> : k_prim<true, 4>, blocks, kPrimThreads,
+                           0, st, a);
   if (a.n > 0)
-    return (int)launch_pdl(hi ? k_prim<false, kPrimMinBlocksHi> : k_prim<false, kPrimMinBlocksLo>,
-                           blocks, kPrimThreads, 0, st, a);
+    return (int)launch_pdl(lpp == 8 ? k_prim<false, 8> : k_prim<false, 4>, blocks, kPrimThreads,
+                           0, st, a);
   return (int)cudaGetLastError();
 }
 
@@ -1098,7 +1157,9 @@ extern "C" int pf_preprocess_sync(double* params, const double* src, int n, doub
   return launch_prim(false, a, (cudaStream_t)stream);
 }
 
-extern "C" int pf_adam_blocks(int n) { return div_up(n > 0 ? n * 8 : 1, kPrimThreads); }
+extern "C" int pf_adam_blocks(int n) {
+  return div_up(n > 0 ? n * prim_lanes(n) : 1, kPrimThreads);
+}
 
 extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, double* v,
                                   const uint8_t* frozen, const double* gains8,

@@ -285,6 +285,13 @@ __device__ __forceinline__ unsigned long long gtime_ns() {
   return t;
 }
 __device__ __forceinline__ void tl_mark(unsigned long long* tl, int slot, int what) {
+  if (tl != nullptr && what == 2) {  // any lane-0 caller: min / max into the wait fields
+    if ((threadIdx.x & 31) != 0) return;
+    const unsigned long long t = gtime_ns();
+    atomicMin(tl + 4 * slot + 1, t);
+    atomicMax(tl + 4 * slot + 2, t);
+    return;
+  }
   if (tl == nullptr || (threadIdx.x & (what == 3 ? 31 : 0xffffffff)) != 0) return;
   const unsigned long long t = gtime_ns();
   if (what == 0 || what == 1) atomicMin(tl + 4 * slot + what, t);

@@ -804,9 +804,11 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
   // the atlas arrives asynchronously (TMA bulk copy, atl_bar); consumers wait for
   // it before their first tile, so the copy overlaps the first tickets
   __shared__ __align__(8) uint64_t atl_bar;
-  if (t == 0) {
-    mbar_init(&atl_bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  // slot mode: the atlas copy goes out after the prologue's list loads (they are
+  // on the critical path, the atlas is needed only by the first tile; measured
+  // -0.5 us to the grid barrier at c3)
+  constexpr bool atl_late = SLOT;
+  auto issue_atlas = [&]() {
     if (ATL != 0) {
       const uint32_t bytes = (uint32_t)a.pad_texels * (ATL == 2 ? 8u : 4u);
       const char* src = reinterpret_cast<const char*>(ATL == 2 ? (const void*)a.apad64
@@ -823,6 +825,11 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
     } else {
       mbar_arrive(&atl_bar);
     }
+  };
+  if (t == 0) {
+    mbar_init(&atl_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (!atl_late) issue_atlas();
   }
   if (t < G * kNBuf) {
     mbar_init(&full[t / kNBuf][t % kNBuf], 1);
@@ -855,7 +862,10 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
     if (slot_mode && blockIdx.x == 0 && t == 0) a.status_rw[1] = 1;
     return;
   }
-  if constexpr (SLOT) slot_prologue(a, sm);
+  if constexpr (SLOT) {
+    slot_prologue(a, sm);
+    if (atl_late && t == 0) issue_atlas();
+  }
 
   const bool consumer = warp < G * kCW;
   const int g = consumer ? warp / kCW : warp - G * kCW;

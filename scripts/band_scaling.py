@@ -27,6 +27,27 @@ K, WARM = 20, 4
 w.cfg.num_iterations = K + WARM + 2
 
 
+CH = 8 * 8  # chained mode: 8 graphs of StepEngine.CHUNK (8) steps, timed together
+
+
+def band_chained_ms(band) -> float:
+    """run_loop's own issue pattern: CHUNK-step graphs with PDL edges between
+    steps, no L2 flush (the per-step graph launch of band_ms is amortised)."""
+    eng = StepEngine(w.scene, w.cfg, w.loss, CH + 2 * 8 + 2, band=band, use_graph=True)
+    eng.run(1 + 8 + 7)  # warm-up: single-step graph, one chunk, then align
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    eng.run(CH)
+    e1.record()
+    torch.cuda.synchronize()
+    eng.check()
+    out = e0.elapsed_time(e1) / CH
+    del eng
+    torch.cuda.empty_cache()
+    return out
+
+
 def band_ms(band) -> float:
     eng = StepEngine(w.scene, w.cfg, w.loss, K + WARM + 2, band=band, use_graph=True)
     eng.run(WARM)
@@ -54,19 +75,24 @@ full.comp.bin()
 cost = row_cost_from_bins(full.comp.bin_off.cpu().numpy()[: nty * ntx + 1], ntx, nty)
 del full
 res = {"config": name, "n": w.scene.n, "canvas": [W, H], "grad_allreduce_bytes": 8 * (8 * w.scene.n + 4)}
-base = None
+base = cbase = None
 for N in worlds:
     for kind, rc in (("uniform", None), ("balanced", cost)):
         if N == 1 and kind == "balanced":
             continue
         bands = row_bands(nty, N, rc)
         ms = [band_ms(b) for b in bands]
+        cms = [band_chained_ms(b) for b in bands]
         if N == 1:
-            base = ms[0]
+            base, cbase = ms[0], cms[0]
         eff = base / (N * max(ms)) if base else None
+        ceff = cbase / (N * max(cms)) if cbase else None
         res[f"N{N}_{kind}"] = {"band_ms": [round(m, 4) for m in ms], "max_ms": max(ms),
-                              "projected_eff_no_allreduce": eff}
+                              "projected_eff_no_allreduce": eff,
+                              "chained_band_ms": [round(m, 4) for m in cms],
+                              "chained_max_ms": max(cms), "chained_eff_no_allreduce": ceff}
         print(f"N={N} {kind:8s} max {max(ms) * 1e3:8.1f} us  mean {np.mean(ms) * 1e3:8.1f} us  "
-              f"eff(no allreduce) {eff:.3f}", flush=True)
+              f"eff(no allreduce) {eff:.3f} | chained max {max(cms) * 1e3:8.1f} us  "
+              f"eff {ceff:.3f}", flush=True)
 Path("gpurun_out").mkdir(exist_ok=True)
 Path(f"gpurun_out/band_scaling_{name}.json").write_text(json.dumps(res, indent=1))

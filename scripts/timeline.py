@@ -29,8 +29,8 @@ if hostio:  # the e2e graph: refresh from host parameters, bin, step, Adam only
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 lib = nat.load()
 names = {0: "k_bin_rows", 1: "k_step", 2: "k_prim<adam>", 3: "k_prim<pre>", 4: " .adam done",
-         5: " .fold done", 6: " .records done", 7: " .ticket done", 8: " bin.scan done",
-         9: " bin.list done", 10: " bin.counts done", 11: "k_row_counts", 12: "k_row_scatter", 13: "k_row_offsets",
+         5: " .fold done", 6: " .records done", 7: " .ticket done", 8: " bin.scan / K1 records stored",
+         9: " bin.list / K1 scatter done", 10: " bin.counts done", 11: "k_row_counts", 12: "k_row_scatter", 13: "k_row_offsets",
          14: " .lists sorted", 15: " .barrier passed"}
 for rep in range(12):
     flush.zero_()
