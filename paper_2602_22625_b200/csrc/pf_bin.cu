@@ -333,7 +333,10 @@ __global__ void __launch_bounds__(kPrimThreads, kPrimMinBlocks) k_prim(PreArgs a
         break;
     }
     float4* pg = reinterpret_cast<float4*>(a.recg + i);
-    switch (c) {
+    // (slot mode: RecG is K4's record only -- lanes 0-5 skip it; 6-7 write RecC)
+    switch (slots && c < 6 ? -1 : c) {
+      case -1:
+        break;
       case 0:
         pg[0] = make_float4((float)(a.alpha_max * sig), (float)(omm * sc0), (float)(omm * sc1),
                             (float)(omm * sc2));
