@@ -5,7 +5,7 @@ initialiser, restated so that the bench can build its inputs on a box where
 the reference package is absent.  The initialiser consumes the numpy PCG64
 stream in the reference's documented order (prep.py:10-14: positions, then
 rotations, then colour noise, then template choices) so a given seed yields
-the reference's own initial scene (checked in tests/test_synth.py against a
+the reference's own initial scene (checked in tests/test_abi_host.py::test_synth_reproduces_reference_structure_aware_init against a
 golden fingerprint made with the reference).
 
 Sources restated: gaussian_blur_template (prep.py:51-73), radial_falloff
