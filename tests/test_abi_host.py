@@ -191,3 +191,31 @@ def test_video_host_logic_matches_reference_semantics():
     with pytest.raises(ValueError):
         video.optimize_video([np.zeros((4, 4, 3))], None,
                              types.SimpleNamespace(loss="spatial", seed=0))
+
+
+def test_synth_template_preparation_matches_reference():
+    """Non-circular check of the bench inputs' template pipeline: synth.prepare
+    (blur) and synth.radial_falloff against the reference's own
+    prepare_templates / radial_falloff (prep.py:76-89, 260-275), imported from
+    /root/reference when it is present (the GPU box does not have it)."""
+    import sys
+    from pathlib import Path
+
+    ref_src = Path("/root/reference/pkg/src")
+    if not (ref_src / "primfit").is_dir():
+        pytest.skip("reference package not present")
+    sys.path.insert(0, str(ref_src))
+    try:
+        from primfit import prep as rprep
+        from primfit.scene import PrimitiveTemplate as RT
+    finally:
+        sys.path.remove(str(ref_src))
+    from paper_2602_22625_b200 import synth
+
+    for raw in (synth.disc(32), synth.logo(48), synth.fingerprint(40), synth.autograph(24, 48),
+                synth.flower(32)):
+        ours = synth.prepare([raw])[0].rgba
+        ref = rprep.prepare_templates([RT(raw.copy())], blur_sigma=1.0, do_blur=True)[0].rgba
+        np.testing.assert_allclose(ours, ref, rtol=0, atol=1e-15)
+        np.testing.assert_allclose(synth.radial_falloff(raw), rprep.radial_falloff(RT(raw.copy())).rgba,
+                                   rtol=0, atol=1e-15)
