@@ -53,6 +53,8 @@ extern "C" {
 #define PF_LOSS_MSE 1        /* loss_mse, fit.py:112-116 */
 #define PF_LOSS_SPATIAL 2    /* loss_spatial, fit.py:128-151 */
 #define PF_LOSS_COMBINED 3   /* mse_w * loss_mse + gray_l1_w * loss_grayscale_l1, fit.py:119-125, 162-168 */
+#define PF_LOSS_EXTERN 4     /* pf_fit_step only: dL/dI, dL/dA given per pixel in tgt4 (a torch loss
+                                upstream: the autograd Function's backward), no loss sums */
 
 /* ABI version; bumped on any signature change. */
 int pf_abi_version(void);  /* 6 */
@@ -321,6 +323,11 @@ int pf_fit_step(const void* rec, int n, const double* tex, const float* apad,
                 double* grads, uint32_t* counters,
                 const int32_t* tile_classes, int stage, void* scratch, size_t scratch_bytes,
                 int capacity, void* slots, int slot_m, void* stream);
+
+/* Upstream gradients for PF_LOSS_EXTERN: rgb float32 [P][3] (dL/dI) and alpha
+ * float32 [P] (dL/dA, or NULL = 0) into out4 float32 [P][4], the per-pixel rows
+ * pf_fit_step stages (the autograd Function's backward). */
+int pf_pack_grad4(const float* rgb, const float* alpha, int P, float* out4, void* stream);
 
 /* Fixed-order fold of n_part partial triples into sums[3] (deterministic). */
 int pf_fold_loss(const double* part, int n_part, double* sums, void* stream);

@@ -28,6 +28,7 @@ PF_LOSS_NONE = 0
 PF_LOSS_MSE = 1
 PF_LOSS_SPATIAL = 2
 PF_LOSS_COMBINED = 3
+PF_LOSS_EXTERN = 4
 
 _P = C.c_void_p
 _I = C.c_int
@@ -49,6 +50,7 @@ SIGNATURES: dict[str, tuple] = {
     "pf_preprocess_sync": (_I, [_P, _P, _I, _D, _D, _D, _I, _I, _I, _I, _I, _I, _P, _P, _Z, _P,
                                 _I, _P, _P]),
     "pf_slot_bytes": (_Z, [_I, _I, _I]),
+    "pf_pack_grad4": (_I, [_P, _P, _I, _P, _P]),
     "pf_slot_reset": (_I, [_P, _I, _I, _I, _P, _P]),
     "pf_scratch_init": (_I, [_P, _Z, _P, _P, _I, _P, _P, _P, _P, _P, _P, _I, _I, _P]),
     "pf_adam_blocks": (_I, [_I]),

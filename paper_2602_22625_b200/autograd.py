@@ -2,7 +2,8 @@
 
 The reference's renderer entry point is the pair render_forward(save=True) /
 backward (raster.py:290-363, grad.py:134-187); here it is one autograd
-Function whose forward runs K1+K2+K3 and whose backward runs K4, so the
+Function whose forward runs K1+K2+K3 and whose backward runs the fit-step
+kernel on the upstream gradients (K4 on saved lists when mu_blend > 0), so the
 compositor composes with any torch loss:
 
     r = Renderer(templates, template_id, z, W, H, background=(1, 1, 1))
@@ -19,21 +20,33 @@ from __future__ import annotations
 import numpy as np
 import torch
 
+from . import _native as nat
 from .compositor import Compositor, bin_capacity, cached_atlas
 from .errors import BinOverflow
 from .raster import DEFAULT_EPS_SKIP
 
 
 class _Composite(torch.autograd.Function):
+    # mu_blend == 0 (colour from the primitive): the forward renders without saving
+    # the contribution lists and the backward re-runs the forward on chip inside
+    # the fit-step kernel with the upstream dL/dI, dL/dA per pixel (PF_LOSS_EXTERN)
+    # -- no 16-byte saved entry per contribution written and read back through
+    # HBM; mu_blend > 0 keeps K3(save) + K4.
     @staticmethod
     def forward(ctx, params, renderer: "Renderer", bg4):
         comp = renderer._lease(params)
         comp.preprocess(params)
         comp.bin()
-        comp.forward(save=True, eps_skip=renderer.eps_skip, bg_rgb=renderer.bg_rgb, bg4=bg4)
+        recompute = renderer.mu_blend == 0.0
+        # a fresh (r, g, b, alpha) buffer per call: the outputs are views of it, no
+        # copies (the caching allocator makes this free)
+        comp.img4 = torch.empty(renderer.H * renderer.W * 4, dtype=torch.float32,
+                                device=renderer.dev)
+        comp.forward(save=not recompute, eps_skip=renderer.eps_skip, bg_rgb=renderer.bg_rgb,
+                     bg4=bg4)
         if not torch.cuda.is_current_stream_capturing():
             renderer._watch(comp)
-        img, alpha = comp.color().clone(), comp.alpha().clone()
+        img, alpha = comp.color(), comp.alpha()
         if ctx.needs_input_grad[0]:
             ctx.comp = comp  # the saved contribution lists: held until backward
         else:
@@ -51,12 +64,17 @@ class _Composite(torch.autograd.Function):
         n = comp.n
         grads = r._grads(n)
         d4 = r._d4()
-        d4.zero_()
-        if d_img is not None:
-            d4[:, :, :3] = d_img
-        if d_alpha is not None:
-            d4[:, :, 3] = d_alpha
-        comp.backward(d4.view(-1), grads, bg_rgb=r.bg_rgb, bg4=ctx.bg4)
+        if d_img is None:
+            d_img = torch.zeros(r.H, r.W, 3, dtype=torch.float32, device=r.dev)
+        nat.check(nat.load().pf_pack_grad4(
+            d_img.to(torch.float32).contiguous().data_ptr(),
+            nat.ptr(d_alpha.to(torch.float32).contiguous() if d_alpha is not None else None),
+            r.H * r.W, d4.data_ptr(), torch.cuda.current_stream().cuda_stream), "pf_pack_grad4")
+        if r.mu_blend == 0.0:
+            comp.fit_step(grads, None, eps_skip=r.eps_skip, bg_rgb=r.bg_rgb, bg4=ctx.bg4,
+                          loss_kind=nat.PF_LOSS_EXTERN, tgt4=d4.view(-1))
+        else:
+            comp.backward(d4.view(-1), grads, bg_rgb=r.bg_rgb, bg4=ctx.bg4)
         out = grads[: n * 8].view(n, 8).clone()
         ctx.comp = None
         r._give_back(comp)

@@ -329,6 +329,25 @@ __global__ void __launch_bounds__(kStuckThreads) k_remove_stuck(StuckArgs a) {
 
 using namespace pf;
 
+// Upstream image gradients of the autograd backward into the fit step's
+// per-pixel float4 rows: (dL/dI r, g, b, dL/dA), dL/dA = 0 when `alpha` is NULL.
+__global__ void k_pack4(const float* __restrict__ rgb, const float* __restrict__ alpha, int P,
+                        float4* __restrict__ out) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  out[p] = make_float4(rgb[3 * (size_t)p], rgb[3 * (size_t)p + 1], rgb[3 * (size_t)p + 2],
+                       alpha ? alpha[p] : 0.0f);
+}
+
+extern "C" int pf_pack_grad4(const float* rgb, const float* alpha, int P, float* out4,
+                             void* stream) {
+  if (P < 0 || (P > 0 && (!rgb || !out4))) return PF_ERR_ARG;
+  if (P == 0) return PF_OK;
+  k_pack4<<<(P + 255) / 256, 256, 0, (cudaStream_t)stream>>>(rgb, alpha, P,
+                                                              reinterpret_cast<float4*>(out4));
+  return (int)cudaGetLastError();
+}
+
 extern "C" int pf_layer_bboxes(const double* params, const int32_t* template_id,
                                const double* tpl_hyp, int n, int W, int H, int rho, int32_t* bbox,
                                long long* area, long long* offsets, void* stream) {

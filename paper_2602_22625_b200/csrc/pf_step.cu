@@ -50,7 +50,10 @@ constexpr int kCW = kTilePix / 32;                      // consumer warps per gr
 // parameter of k_step; pf_fit_step's `stage` hint picks it)
 constexpr int kNBuf = 2;                                // stage buffers per group (ring)
 constexpr int kSlotArena = 64;  // spill entries per group for slot-mode fast-path tiles (L <= 64)
-constexpr int kKS = 5;                                  // contribution-stack depth in smem
+#ifndef PF_KS
+#define PF_KS 5
+#endif
+constexpr int kKS = PF_KS;                              // contribution-stack depth in smem
 constexpr uint32_t kEntBytes = sizeof(RecS) + sizeof(RecC);
 // CTA shape for G groups: warps [0, 8G) consume (group = warp / 8), warps
 // [8G, 9G) produce, padded to whole warpgroups so the producers' warpgroup can
@@ -432,7 +435,16 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
 #ifndef PF_LOSS32
 #define PF_LOSS32 1
 #endif
-  if (valid && PF_LOSS32 && LOSS == PF_LOSS_MSE) {
+  if (LOSS == PF_LOSS_EXTERN) {
+    // gradients from upstream (the autograd backward): the staged rows hold
+    // (dL/dI r, g, b, dL/dA) per pixel; no loss here
+    if (valid) {
+      dI0 = tg.x;
+      dI1 = tg.y;
+      dI2 = tg.z;
+      dA = tg.w;
+    }
+  } else if (valid && PF_LOSS32 && LOSS == PF_LOSS_MSE) {
     // MSE in fp32 end to end: the image is stored as fp32 and the per-warp
     // partials are fp32 sums already; (I - t) to ~1 ulp of I (< 1e-7)
     const float I0 = fmaf(T, g0, C0), I1 = fmaf(T, g1, C1), I2 = fmaf(T, g2, C2);
@@ -480,6 +492,7 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
       dA = (float)(a.alpha_w * 2.0 * ad * a.inv_P);
     }
   }
+  if (LOSS != PF_LOSS_EXTERN) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     l0 += __shfl_xor_sync(kFull, l0, o);
@@ -488,8 +501,9 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
       l2 += __shfl_xor_sync(kFull, l2, o);
     }
   }
+  }
   if (LOSS == PF_LOSS_MSE) l1 = l0;
-  if (lane == 0) {
+  if (LOSS != PF_LOSS_EXTERN && lane == 0) {
     double* pp = a.part + ((size_t)tile * kCW + w) * 3;
     pp[0] = l0;
     pp[1] = l1;
@@ -1172,8 +1186,10 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
     return PF_ERR_ARG;
   if (!slots && (!bin_off || !bin_idx)) return PF_ERR_ARG;
   if (slots && (slot_m < 1 || !tile_classes || !scratch || capacity < 0)) return PF_ERR_ARG;
-  if (loss_kind != PF_LOSS_MSE && loss_kind != PF_LOSS_SPATIAL && loss_kind != PF_LOSS_COMBINED)
+  if (loss_kind != PF_LOSS_MSE && loss_kind != PF_LOSS_SPATIAL && loss_kind != PF_LOSS_COMBINED &&
+      loss_kind != PF_LOSS_EXTERN)
     return PF_ERR_ARG;
+  if (loss_kind == PF_LOSS_EXTERN && slots) return PF_ERR_ARG;  // (CSR lists only)
   const int ntx = div_up(W, kTile), nty = div_up(H, kTile);
   if (ty_begin < 0 || ty_end > nty || ty_begin > ty_end) return PF_ERR_ARG;
   const int n_tiles = (ty_end - ty_begin) * ntx;
@@ -1290,6 +1306,12 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   }
   if (loss_kind == PF_LOSS_MSE) {
     PF_PICK(PF_LOSS_MSE)
+  } else if (loss_kind == PF_LOSS_EXTERN) {
+    if (ST == 64) {
+      PF_PICK4(PF_LOSS_EXTERN, 64, false)
+    } else {
+      PF_PICK4(PF_LOSS_EXTERN, 32, false)
+    }
   } else if (loss_kind == PF_LOSS_COMBINED) {
     PF_PICK(PF_LOSS_COMBINED)
   } else {
