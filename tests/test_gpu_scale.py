@@ -669,7 +669,7 @@ def test_autograd_step_graph_capture_matches_eager(torch_cuda):
             with torch.no_grad():
                 params.sub_(1e-3 * params.grad)
                 params.grad.zero_()
-            return loss
+            return loss.detach()
 
         if not graphed:
             for _ in range(steps + 2):
