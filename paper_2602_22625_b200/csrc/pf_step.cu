@@ -604,7 +604,9 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
 // L, tx | ty << 16) the producers read, and its count is zeroed for the next
 // K1.  A grid barrier (all CTAs are resident: one per SM) ends the phase.
 constexpr int kSortRound = 1024;  // tiles per CTA and round (scratch: 20 B each)
-__device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* scratch) {
+template <int G>
+__device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* scratch,
+                                              int4* first) {
   const SlotBins& sb = a.sb;
   __shared__ int s_ccnt[kTileClasses], s_cbase[kTileClasses];
   __shared__ unsigned s_k;
@@ -754,18 +756,33 @@ __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* 
         if (lane == 0) {
           sb.cnt[tile] = 0;  // (read above by this lane) ready for the next K1
           cost[tile] = 0;
-          const int cl = tile_class(wq > 0 ? wq : L);
-          const int rank = atomicAdd(&s_ccnt[cl], 1);
           ent[i] = make_int4(tile, b0, L, txy);
-          cls[i] = cl | (rank << 8);
+          cls[i] = wq > 0 ? wq : L;  // weight (class below)
           kacc += (unsigned)L;
         }
       }
     }
     __syncthreads();
+    if (r0 == c0 && t < G) {
+      // the CTA's first G tiles are its producers' first tiles: they start on
+      // CTA-local lists right away, while other CTAs still finish (no grid
+      // barrier before the first copies); they stay out of the global classes
+      // (choosing the heaviest G measured the same and cost a selection pass)
+      first[t] = t < nr ? ent[t] : make_int4(-1, 0, 0, 0);
+      if (t < nr) cls[t] = -1;
+    }
+    __syncthreads();
+    for (int i = t; i < nr; i += blockDim.x) {
+      if (cls[i] < 0) continue;
+      const int cl = tile_class(cls[i]);
+      const int rank = atomicAdd(&s_ccnt[cl], 1);
+      cls[i] = cl | (rank << 8);
+    }
+    __syncthreads();
     if (t < kTileClasses) s_cbase[t] = s_ccnt[t] ? atomicAdd(a.classes_rw + t, s_ccnt[t]) : 0;
     __syncthreads();
     for (int i = t; i < nr; i += blockDim.x) {
+      if (cls[i] < 0) continue;
       const int cl = cls[i] & 0xff, rank = cls[i] >> 8;
       clists[(size_t)cl * a.n_tiles + s_cbase[cl] + rank] = ent[i];
     }
@@ -774,14 +791,12 @@ __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* 
   if (lane == 0 && kacc) atomicAdd(&s_k, kacc);
   tl_mark(a.tl, 14, 1);
   __syncthreads();
-  // grid barrier: the lists, classes and counts of every CTA are complete
+  // arrive on the grid barrier: this CTA's lists and class entries are complete
+  // (the producers wait for every CTA before their first global ticket)
   if (t == 0) {
     if (s_k) atomicAdd(sb.ctl + kSlotK, s_k);
     atom_add_acq_rel(a.ctr + 2, 1u);
-    while (ld_acquire(a.ctr + 2) < gridDim.x) __nanosleep(64);
   }
-  __syncthreads();
-  tl_mark(a.tl, 15, 1);
 }
 
 // Persistent, warp-specialised.  One CTA per SM; G groups of one producer warp
@@ -821,7 +836,11 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
   // slot mode: the atlas copy goes out after the prologue's list loads (they are
   // on the critical path, the atlas is needed only by the first tile; measured
   // -0.5 us to the grid barrier at c3)
+#ifdef PF_ATLAS_EARLY
+  constexpr bool atl_late = false;  // (A/B)
+#else
   constexpr bool atl_late = SLOT;
+#endif
   auto issue_atlas = [&]() {
     if (ATL != 0) {
       const uint32_t bytes = (uint32_t)a.pad_texels * (ATL == 2 ? 8u : 4u);
@@ -876,8 +895,11 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
     if (slot_mode && blockIdx.x == 0 && t == 0) a.status_rw[1] = 1;
     return;
   }
+  __shared__ int4 s_first[G];  // slot mode: each producer's CTA-local first tile
+  if (SLOT && t < G) s_first[t] = make_int4(-1, 0, 0, 0);
   if constexpr (SLOT) {
-    slot_prologue(a, sm);
+    __syncthreads();
+    slot_prologue<G>(a, sm, s_first);
     if (atl_late && t == 0) issue_atlas();
   }
 
@@ -927,7 +949,7 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
     // for the next free ring slot.  (Everything here may have been written by
     // this launch's prologue in slot mode: L2 loads, not the nc path.)
     int cls_pre = 0;  // lane l < kTileClasses: tiles in classes heaviest..l (inclusive)
-    if (a.classes) {
+    auto load_classes = [&]() {
       const int c = lane < kTileClasses ? __ldcg(a.classes + (kTileClasses - 1 - lane)) : 0;
       cls_pre = c;
 #pragma unroll
@@ -935,7 +957,9 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
         const int y = __shfl_up_sync(kFull, cls_pre, o);
         if (lane >= o) cls_pre += y;
       }
-    }
+    };
+    // (slot mode: the class counts are complete only after the grid barrier)
+    if (!SLOT && a.classes) load_classes();
     // list base: CSR bin_idx, or (slot mode) the slot + pool lists
     const int32_t* lists = SLOT ? reinterpret_cast<const int32_t*>(a.sb.slot) : a.bin_idx;
     // tickets: the first one of each producer is static (blockIdx, group), later
@@ -944,7 +968,29 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
     int tile = a.n_tiles, b0 = 0, L = 0, txy = 0, i0 = 0, i1 = 0;
     auto next_tile = [&]() {
       int t = blockIdx.x * G + g;
-      if (ticket_k++ > 0) {
+      if constexpr (SLOT) {
+        if (ticket_k == 0) {
+          ticket_k = 1;
+          const int4 f = s_first[g];  // CTA-local first tile (no ticket)
+          if (f.x >= 0) {
+            tile = f.x;
+            b0 = f.y;
+            L = f.z;
+            txy = f.w;
+            return;
+          }
+        }
+        if (ticket_k == 1) {
+          // first global ticket: every CTA's lists and classes are complete
+          if (lane == 0)
+            while (ld_acquire(a.ctr + 2) < gridDim.x) __nanosleep(64);
+          __syncwarp();
+          load_classes();
+          ticket_k = 2;
+        }
+        if (lane == 0) t = (int)atomicAdd(a.ctr, 1u);
+        t = __shfl_sync(kFull, t, 0);
+      } else if (ticket_k++ > 0) {
         if (lane == 0) t = (int)atomicAdd(a.ctr, 1u) + (int)gridDim.x * G;
         t = __shfl_sync(kFull, t, 0);
       }
