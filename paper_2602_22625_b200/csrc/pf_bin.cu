@@ -80,12 +80,15 @@ struct PreArgs {
 };
 
 constexpr double kB1 = 0.9, kB2 = 0.999, kAdamEps = 1e-8;
-constexpr int kPrimThreads = 256;
+#ifndef PF_PRIM_THREADS
+#define PF_PRIM_THREADS 256
+#endif
+constexpr int kPrimThreads = PF_PRIM_THREADS;
 // K1 runs 3 blocks per SM (80 registers, no spills) with 8 lanes per primitive
 // while that grid fits one wave (c3: 157 blocks), else with 4 lanes per
 // primitive (c5: 313 blocks instead of 625 -- one wave; a 5-block, 48-register
 // variant of the 8-lane kernel spilled and its record chain took twice as long)
-constexpr int kPrimMinBlocks = 3;
+constexpr int kPrimMinBlocks = 3 * 256 / kPrimThreads;
 static int prim_lanes(int n) {
   return div_up(n > 0 ? n * 8 : 1, kPrimThreads) <= kPrimMinBlocks * dev_attrs().sms ? 8 : 4;
 }
