@@ -148,7 +148,7 @@ def policy_from_config(cfg) -> StuckPolicy:
                        triggers=tuple(g("stuck_triggers", (20, 45, 70))))
 
 
-def optimize_video(frames, templates, cfg):
+def optimize_video(frames, templates, cfg, rng: np.random.Generator | None = None):
     """Fit one scene per frame, warm-starting each from the previous
     (dyn.py:180-238), every step in the GPU fit loop (fit.run_loop).
 
@@ -162,7 +162,8 @@ def optimize_video(frames, templates, cfg):
     whose binning box misses every changed pixel frozen (``freeze_static``;
     diff_mask + freeze_flags on the GPU) and the stuck-primitive decay at the
     policy's trigger iterations (``remove_stuck``).  Extension: a prepared
-    ``Scene`` in place of ``templates`` is used as frame 0's scene directly.
+    ``Scene`` in place of ``templates`` is used as frame 0's scene directly, and
+    ``rng`` (default ``default_rng(cfg.seed)``) can be supplied (frame sharding).
     Returns (scenes, histories), one per frame.
     """
     from .fit import LossSpec, OptimState, effective_padding, run_loop
@@ -177,7 +178,7 @@ def optimize_video(frames, templates, cfg):
             raise ShapeMismatch("all frames must share one shape")
     if cfg.loss in ("spatial", "spatial_constrained"):
         raise ValueError("spatial loss is single-image only")
-    rng = np.random.default_rng(cfg.seed)
+    rng = np.random.default_rng(cfg.seed) if rng is None else rng
     g = lambda k, d: getattr(cfg, k, d)  # noqa: E731  (duck-typed FitConfig)
     if isinstance(templates, Scene):
         scene = templates
@@ -212,4 +213,65 @@ def optimize_video(frames, templates, cfg):
                                       state=state, hooks=hooks)
         scenes.append(scene)
         histories.append(hist)
+    return scenes, histories
+
+
+def frame_chunks(n_frames: int, world: int) -> list[range]:
+    """Contiguous, balanced frame ranges, one per rank (earlier ranks take the
+    remainder)."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    base, extra = divmod(n_frames, world)
+    out, start = [], 0
+    for r in range(world):
+        k = base + (1 if r < extra else 0)
+        out.append(range(start, start + k))
+        start += k
+    return out
+
+
+def chunk_rng(seed: int, chunk: int) -> np.random.Generator:
+    """The rng of a frame chunk: chunk 0 draws from ``default_rng(seed)`` exactly
+    as the sequential reference does; later chunks from ``default_rng([seed, c])``."""
+    return np.random.default_rng(seed) if chunk == 0 else np.random.default_rng([seed, chunk])
+
+
+def optimize_video_sharded(frames, templates, cfg, *, rank: int | None = None,
+                           world: int | None = None, group=None):
+    """BASELINE.json c4 ("frames sharded across 8 GPUs"): the frames are split into
+    ``world`` contiguous chunks and rank r runs optimize_video's warm-start chain
+    on chunk r on its own device -- no collective inside the fit; the per-frame
+    scenes and histories are gathered to every rank at the end
+    (``torch.distributed.all_gather_object``; without an initialised process
+    group, or world == 1, this is optimize_video on the whole list).
+
+    Difference from the sequential reference (dyn.py:180-238), by construction:
+    the chain restarts at every chunk boundary -- the chunk's first frame is
+    initialised with init_scene and runs the frame-0 budget ``num_iterations``
+    -- so frames after the first chunk differ from a single sequential chain;
+    chunk 0 (frames 0..k-1, ``default_rng(cfg.seed)``) is bit for bit the
+    sequential run of those frames.  Returns (scenes, histories) for all frames.
+    """
+    import torch.distributed as dist
+
+    if not frames:
+        raise ValueError("need at least one frame")
+    if world is None:
+        world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    if rank is None:
+        rank = dist.get_rank(group) if world > 1 else 0
+    if world == 1:
+        return optimize_video(frames, templates, cfg)
+    chunks = frame_chunks(len(frames), world)
+    mine = chunks[rank]
+    local = ([], [])
+    if len(mine):
+        local = optimize_video([frames[i] for i in mine], templates, cfg,
+                               rng=chunk_rng(int(getattr(cfg, "seed", 0)), rank))
+    parts = [None] * world
+    dist.all_gather_object(parts, local, group=group)
+    scenes, histories = [], []
+    for sc, hi in parts:
+        scenes.extend(sc)
+        histories.extend(hi)
     return scenes, histories

@@ -158,3 +158,76 @@ def test_sum_bands_fixed_order(torch_cuda):
     sum_bands(bufs)  # in place
     for b in bufs:
         assert torch.equal(b.cpu(), ref)
+
+
+def _video_frames():
+    from paper_2602_22625_b200 import synth
+
+    w = synth.make_workload("c1")
+    f0 = w.target
+    frames = [f0]
+    for k in range(1, 4):  # a region that changes from frame to frame
+        f = frames[-1].copy()
+        f[40 * k : 40 * k + 50, 30:90] = 1.0 - f[40 * k : 40 * k + 50, 30:90]
+        frames.append(f)
+    return w, frames
+
+
+def _video_cfg(w):
+    import copy
+
+    cfg = copy.deepcopy(w.cfg)
+    cfg.num_iterations, cfg.sequential_iterations = 8, 6
+    cfg.freeze_static = True
+    return cfg
+
+
+def _video_rank_main(rank, world, out_dir):
+    sys.path.insert(0, str(ROOT))
+    import copy
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2602_22625_b200 import video
+    from paper_2602_22625_b200.scene import pack_params
+
+    w, frames = _video_frames()
+    scenes, hists = video.optimize_video_sharded(frames, copy.deepcopy(w.scene), _video_cfg(w))
+    np.savez(os.path.join(out_dir, f"video{rank}.npz"),
+             params=np.stack([pack_params(s)[0] for s in scenes]),
+             loss=np.concatenate([[h.loss for h in hi] for hi in hists]),
+             lens=np.array([len(h) for h in hists]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_video_frames_sharded_across_ranks(torch_cuda, tmp_path):
+    """BASELINE c4's frame sharding: 2 ranks (gloo, one GPU) each run the
+    warm-start chain on their chunk of 4 frames; every rank gathers the same
+    per-frame results, and each chunk equals optimize_video on that chunk alone
+    (chunk 0 with the sequential reference's rng)."""
+    import copy
+
+    import torch.multiprocessing as mp
+
+    from paper_2602_22625_b200 import video
+    from paper_2602_22625_b200.scene import pack_params
+
+    os.environ["MASTER_PORT"] = str(29700 + (os.getpid() % 1000))
+    mp.spawn(_video_rank_main, args=(2, str(tmp_path)), nprocs=2, join=True)
+    runs = [dict(np.load(tmp_path / f"video{r}.npz")) for r in range(2)]
+    np.testing.assert_array_equal(runs[0]["params"], runs[1]["params"])
+    np.testing.assert_array_equal(runs[0]["loss"], runs[1]["loss"])
+    assert list(runs[0]["lens"]) == [8, 6, 8, 6]  # chunk starts run the frame-0 budget
+    w, frames = _video_frames()
+    cfg = _video_cfg(w)
+    for c, chunk in enumerate(video.frame_chunks(4, 2)):
+        sc, _ = video.optimize_video([frames[i] for i in chunk], copy.deepcopy(w.scene), cfg,
+                                     rng=video.chunk_rng(cfg.seed, c))
+        for j, i in enumerate(chunk):
+            _adam_bar(runs[0]["params"][i].reshape(-1, 8), pack_params(sc[j])[0].reshape(-1, 8),
+                      cfg, 14)
