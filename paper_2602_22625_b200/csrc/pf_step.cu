@@ -49,7 +49,7 @@ constexpr int kCW = kTilePix / 32;                      // consumer warps per gr
 // list entries staged per tile: ST = 32, or 64 for long-list scenes (template
 // parameter of k_step; pf_fit_step's `stage` hint picks it)
 constexpr int kNBuf = 2;                                // stage buffers per group (ring)
-constexpr int kSlotArena = 64;  // spill entries per group for slot-mode fast-path tiles (L <= 64)
+constexpr int kSlotArena = 128;  // spill entries per group for slot-mode in-place lists (L <= 128)
 #ifndef PF_KS
 #define PF_KS 5
 #endif
@@ -146,6 +146,32 @@ __device__ __forceinline__ void sort_keys(uint32_t& k0, uint32_t& k1, bool two) 
     for (int j = 16; j > 0; j >>= 1) {
       k0 = bitonic_xchg(k0, lane, 64, j);
       k1 = bitonic_xchg(k1, lane + 32, 64, j);
+    }
+  }
+}
+
+// 128 keys, four per lane (element lane + 32 r): the prologue's medium path
+__device__ __forceinline__ void sort_keys4(uint32_t (&k)[4]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int kk = 2; kk <= 128; kk <<= 1) {
+#pragma unroll
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int rj = j >> 5;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if ((r & rj) == 0) {  // (r, r | rj): same lane, elements 32 j apart
+            const bool up = ((lane + 32 * r) & kk) == 0;
+            const uint32_t x = k[r], y = k[r | rj];
+            k[r] = up ? min(x, y) : max(x, y);
+            k[r | rj] = up ? max(x, y) : min(x, y);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) k[r] = bitonic_xchg(k[r], lane + 32 * r, kk, j);
+      }
     }
   }
 }
@@ -692,6 +718,19 @@ __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* 
           L = __popc(__ballot_sync(kFull, k0 != ~0u)) + __popc(__ballot_sync(kFull, k1 != ~0u));
           if (lane < L) sl[lane] = k0;
           if (lane + 32 < L) sl[lane + 32] = k1;
+        } else if (raw <= 128 && raw <= sb.m && !dirty) {
+          // medium path (c2-like long lists): 128 keys in registers, sorted in place
+          uint32_t k4[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int e = lane + 32 * r;
+            k4[r] = e < raw ? __ldcg(sl + e) : ~0u;
+          }
+          sort_keys4(k4);
+          L = raw;
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            if (lane + 32 * r < L) sl[lane + 32 * r] = k4[r];
         } else {
           // general path (long or overflowed lists; rare): gather the slots and
           // the tile's overflow entries into scratch, keep valid first
