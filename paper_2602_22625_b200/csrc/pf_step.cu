@@ -663,7 +663,10 @@ __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* 
     // first sort; the per-tile processing is a rolled loop (one copy of the sort
     // code: this phase runs once per launch, instruction-cache misses dominate
     // an unrolled version)
-    constexpr int kB = 4;
+#ifndef PF_SORT_BATCH
+#define PF_SORT_BATCH 4
+#endif
+    constexpr int kB = PF_SORT_BATCH;
     uint32_t* kbuf = reinterpret_cast<uint32_t*>(cls + kSortRound) + warp * (kB * 64);
     for (int ib = warp; ib < nr; ib += nwarps * kB) {
       int qraw = 0, qw = 0;
