@@ -1139,6 +1139,7 @@ extern "C" int pf_preprocess(const double* params, int n, double alpha_max, doub
                              double padding, int W, int H, int tile, int ty_begin, int ty_end,
                              int capacity, void* rec, void* scratch, size_t scratch_bytes,
                              void* slots, int slot_m, int32_t* tile_classes, void* stream) {
+  pf::NvtxRange nvtx_range("pf_preprocess");
   PreArgs a;
   int rc = fill_pre_args(a, const_cast<double*>(params), n, alpha_max, mu_blend, padding,
                          W, H, tile, ty_begin, ty_end, capacity, rec, scratch, scratch_bytes);
@@ -1152,6 +1153,7 @@ extern "C" int pf_preprocess_sync(double* params, const double* src, int n, doub
                                   int ty_begin, int ty_end, int capacity, void* rec, void* scratch,
                                   size_t scratch_bytes, void* slots, int slot_m,
                                   int32_t* tile_classes, void* stream) {
+  pf::NvtxRange nvtx_range("pf_preprocess_sync");
   if (n > 0 && !src) return PF_ERR_ARG;
   PreArgs a;
   int rc = fill_pre_args(a, params, n, alpha_max, mu_blend, padding, W, H, tile, ty_begin,
@@ -1178,6 +1180,7 @@ extern "C" int pf_adam_preprocess(double* params, double* grads, double* m, doub
                                   int ty_end, int capacity, void* rec, void* scratch,
                                   size_t scratch_bytes, double* mirror, void* slots, int slot_m,
                                   int32_t* tile_classes, void* stream) {
+  pf::NvtxRange nvtx_range("pf_adam_preprocess");
   PreArgs a;
   // rec == NULL: Adam only (no records / rects; the caller runs pf_preprocess
   // before the next pf_bin, e.g. a host-driven step that re-reads the parameters)
@@ -1246,6 +1249,7 @@ extern "C" int pf_bin_launches(int n, int W, int H, int tile, int ty_begin, int 
 extern "C" int pf_bin(int n, int W, int H, int tile, int ty_begin, int ty_end, int capacity,
                       void* scratch, size_t scratch_bytes, int32_t* bin_off, int32_t* bin_idx,
                       int32_t* status, int32_t* tile_classes, void* stream) {
+  pf::NvtxRange nvtx_range("pf_bin");
   int ntx, n_rows;
   if (n < 0 || capacity < 0 || !band_ok(W, H, tile, ty_begin, ty_end, &ntx, &n_rows))
     return PF_ERR_ARG;

@@ -14,8 +14,18 @@
 #include <cstdlib>
 #include <utility>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: a no-op unless a tool (nsys, ncu) injects
 
 namespace pf {
+
+// NVTX range over one C-ABI entry point (host side: the launch call it names;
+// nsys / ncu --nvtx show each stage by name).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 constexpr int kTile = 16;                 // render tile edge (16x16 pixels / block)
 constexpr int kTilePix = kTile * kTile;   // 256 threads per render block

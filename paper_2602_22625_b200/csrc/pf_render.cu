@@ -465,6 +465,7 @@ extern "C" int pf_forward(const void* rec, int n, const double* tex, const float
                           long long saved_entries, int32_t* ent_n, float* img4, int loss_kind,
                           const float* tgt4, double alpha_w, double w_mse, double w_gray,
                           double inv_3P, double inv_P, float* d4, double* part, void* stream) {
+  pf::NvtxRange nvtx_range("pf_forward");
   if (W < 1 || H < 1 || n < 0 || !bin_off || !img4 || !tex || !quad) return PF_ERR_ARG;
   const int ntx = div_up(W, kTile), nty = div_up(H, kTile);
   if (ty_begin < 0 || ty_end > nty || ty_begin > ty_end) return PF_ERR_ARG;
@@ -537,6 +538,7 @@ extern "C" int pf_backward(const void* rec, int n, const double* tex, const floa
                            double bg_b, const float* bg4, double mu_blend, int W, int H,
                            int ty_begin, int ty_end, double* grads, const double* part,
                            double* sums, void* stream) {
+  pf::NvtxRange nvtx_range("pf_backward");
   if (W < 1 || H < 1 || n < 0 || !bin_off || !saved || saved_entries < 0 || !ent_n || !d4 ||
       !grads || !tex || !quad || (part && !sums))
     return PF_ERR_ARG;

@@ -1269,6 +1269,7 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
                            const int32_t* tile_classes, int stage, void* scratch,
                            size_t scratch_bytes, int capacity, void* slots, int slot_m,
                            void* stream) {
+  pf::NvtxRange nvtx_range("pf_fit_step");
   if (W < 1 || H < 1 || n < 0 || !status || !tex || !apad || !tgt4 ||
       !spill || !part || !grads || !counters || pad_texels < 0 || (pad_texels & 3))
     return PF_ERR_ARG;
