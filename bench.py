@@ -372,9 +372,18 @@ def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # (diagnostics: PF_DIST_BACKEND=gloo runs the N > 1 code path with every rank on
+    # one device -- the c4 frame replicas only: a gloo allreduce cannot be captured
+    # in the row-band step graph)
+    backend = os.environ.get("PF_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     w = synth.make_workload(args.config)
     sc = w.scene
     H, W = sc.canvas_h, sc.canvas_w
