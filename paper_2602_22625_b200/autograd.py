@@ -125,7 +125,11 @@ class Renderer:
     def _capacity(self, params: torch.Tensor) -> int:
         n = len(self.tid)
         if self.s_max is not None:
-            scales = np.full(n, float(self.s_max))
+            if getattr(self, "_cap_smax", None) is None:  # constant: computed once
+                self._cap_smax = bin_capacity(np.full(n, float(self.s_max)), self.tid,
+                                              self.atlas.hyp, self.padding, 16,
+                                              -(-self.W // 16), -(-self.H // 16))
+            return self._cap_smax
         else:
             scales = params[:, 2].detach().double().cpu().numpy() if n else np.zeros(0)
         return bin_capacity(scales, self.tid, self.atlas.hyp, self.padding, 16,
@@ -160,20 +164,26 @@ class Renderer:
 
     # -- asynchronous overflow check
     def _watch(self, comp: Compositor) -> None:
-        st = torch.empty(2, dtype=torch.int32, pin_memory=True)
+        # (pinned status copy + event pairs are recycled once checked)
+        pool = self.__dict__.setdefault("_wpool", [])
+        if pool:
+            ev, st = pool.pop()
+        else:
+            ev, st = torch.cuda.Event(), torch.empty(2, dtype=torch.int32, pin_memory=True)
         st.copy_(comp.status[:2], non_blocking=True)
-        ev = torch.cuda.Event()
         ev.record()
         self._pending.append((ev, st, comp.capacity))
 
     def _raise_pending(self, wait: bool = False) -> None:
         keep = []
+        pool = self.__dict__.setdefault("_wpool", [])
         for ev, st, cap in self._pending:
             if wait:
                 ev.synchronize()
             elif not ev.query():
                 keep.append((ev, st, cap))
                 continue
+            pool.append((ev, st))
             if int(st[1]):
                 self._pending = []
                 raise BinOverflow(f"{int(st[0])} bin entries exceed capacity {cap}: a scale "

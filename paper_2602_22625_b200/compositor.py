@@ -33,8 +33,11 @@ RENDER_TILE = 16
 
 
 def _stream_handle(stream: torch.cuda.Stream | None = None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    # the current stream's raw handle without building a Stream object (that
+    # costs ~20 us of Python per call: 7 launches per eager autograd step)
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 class DeviceAtlas:
