@@ -630,6 +630,9 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
 // L, tx | ty << 16) the producers read, and its count is zeroed for the next
 // K1.  A grid barrier (all CTAs are resident: one per SM) ends the phase.
 constexpr int kSortRound = 1024;  // tiles per CTA and round (scratch: 20 B each)
+#ifndef PF_PROLOGUE_MARKS
+#define PF_PROLOGUE_MARKS 1  // (diagnostics, PF_STEP_PROF only: phase times of the prologue)
+#endif
 template <int G>
 __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* scratch,
                                               int4* first) {
@@ -685,6 +688,8 @@ __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* 
       }
       cp_async_wait_all();
       __syncwarp();
+      if (PF_PROLOGUE_MARKS && a.prof && t == 0 && ib == warp && blockIdx.x < 256)
+        a.prof[6 * 148 * 32 + 65536 * 8 + 512 + 4 * blockIdx.x + 0] = gtimer();
 #pragma unroll 1
       for (int q = 0; q < kB; ++q) {
         const int i = ib + q * nwarps;
@@ -798,29 +803,26 @@ __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* 
         if (lane == 0) {
           sb.cnt[tile] = 0;  // (read above by this lane) ready for the next K1
           cost[tile] = 0;
-          ent[i] = make_int4(tile, b0, L, txy);
-          cls[i] = wq > 0 ? wq : L;  // weight (class below)
+          const int4 e = make_int4(tile, b0, L, txy);
+          ent[i] = e;
+          if (r0 == c0 && i < G) {
+            // the CTA's first G tiles are its producers' first tiles: they start
+            // on CTA-local lists right away, while other CTAs still finish (no
+            // grid barrier before the first copies); they stay out of the global
+            // classes (choosing the heaviest G instead measured the same)
+            first[i] = e;
+            cls[i] = -1;
+          } else {
+            const int cl = tile_class(wq > 0 ? wq : L);
+            cls[i] = cl | (atomicAdd(&s_ccnt[cl], 1) << 8);
+          }
           kacc += (unsigned)L;
         }
       }
     }
     __syncthreads();
-    if (r0 == c0 && t < G) {
-      // the CTA's first G tiles are its producers' first tiles: they start on
-      // CTA-local lists right away, while other CTAs still finish (no grid
-      // barrier before the first copies); they stay out of the global classes
-      // (choosing the heaviest G measured the same and cost a selection pass)
-      first[t] = t < nr ? ent[t] : make_int4(-1, 0, 0, 0);
-      if (t < nr) cls[t] = -1;
-    }
-    __syncthreads();
-    for (int i = t; i < nr; i += blockDim.x) {
-      if (cls[i] < 0) continue;
-      const int cl = tile_class(cls[i]);
-      const int rank = atomicAdd(&s_ccnt[cl], 1);
-      cls[i] = cl | (rank << 8);
-    }
-    __syncthreads();
+    if (PF_PROLOGUE_MARKS && a.prof && t == 0 && blockIdx.x < 256)
+      a.prof[6 * 148 * 32 + 65536 * 8 + 512 + 4 * blockIdx.x + 1] = gtimer();
     if (t < kTileClasses) s_cbase[t] = s_ccnt[t] ? atomicAdd(a.classes_rw + t, s_ccnt[t]) : 0;
     __syncthreads();
     for (int i = t; i < nr; i += blockDim.x) {
@@ -830,6 +832,8 @@ __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* 
     }
     __syncthreads();
   }
+  if (PF_PROLOGUE_MARKS && a.prof && t == 0 && blockIdx.x < 256)
+    a.prof[6 * 148 * 32 + 65536 * 8 + 512 + 4 * blockIdx.x + 2] = gtimer();
   if (lane == 0 && kacc) atomicAdd(&s_k, kacc);
   tl_mark(a.tl, 14, 1);
   __syncthreads();
@@ -941,7 +945,13 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
   if (SLOT && t < G) s_first[t] = make_int4(-1, 0, 0, 0);
   if constexpr (SLOT) {
     __syncthreads();
+    const unsigned long long pro0 = a.prof ? gtimer() : 0;
     slot_prologue<G>(a, sm, s_first);
+    if (a.prof && t == 0 && blockIdx.x < 256) {  // (diagnostics: prologue span per CTA)
+      unsigned long long* pp = a.prof + 6 * 148 * 32 + 65536 * 8 + 2 * blockIdx.x;
+      pp[0] = pro0;
+      pp[1] = gtimer();
+    }
     if (atl_late && t == 0) issue_atlas();
   }
 
@@ -1250,6 +1260,17 @@ extern "C" int pf_step_prof_dump(unsigned long long* host, int max_slots) {
   return n;
 }
 
+extern "C" int pf_step_prof_prologue(unsigned long long* host, int n_ctas) {
+  if (!g_prof_buf) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, g_prof_buf + 6 * 148 * 32 + 65536 * 8, sizeof(unsigned long long) * 2 * n_ctas,
+             cudaMemcpyDeviceToHost);
+  // then 4 phase marks per CTA (batch landed, tiles sorted, classes, end)
+  cudaMemcpy(host + 2 * n_ctas, g_prof_buf + 6 * 148 * 32 + 65536 * 8 + 512,
+             sizeof(unsigned long long) * 4 * n_ctas, cudaMemcpyDeviceToHost);
+  return n_ctas;
+}
+
 extern "C" int pf_step_prof_tiles(unsigned long long* host, int n_tiles) {
   if (!g_prof_buf) return 0;
   cudaDeviceSynchronize();
@@ -1346,7 +1367,8 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   }
   static unsigned long long* prof_buf = nullptr;
   if (dg.step_prof) {
-    if (!prof_buf) cudaMalloc(&prof_buf, sizeof(unsigned long long) * (6 * 148 * 32 + 65536 * 8));
+    if (!prof_buf)
+      cudaMalloc(&prof_buf, sizeof(unsigned long long) * (6 * 148 * 32 + 65536 * 8 + 512 + 1024));
     a.prof = prof_buf;
   }
   g_prof_buf = prof_buf;

@@ -15,7 +15,13 @@ from paper_2602_22625_b200.fit import StepEngine
 
 w = synth.make_workload(sys.argv[1] if len(sys.argv) > 1 else "c3")
 w.cfg.num_iterations = 40
-eng = StepEngine(w.scene, w.cfg, w.loss, 40, use_graph=False)
+band = None
+for arg in sys.argv[2:]:
+    if arg.startswith("band="):  # band=N:r -- rank r of an N-way uniform row split
+        from paper_2602_22625_b200.dist import row_bands
+        N, r = (int(v) for v in arg[5:].split(":"))
+        band = row_bands(-(-w.scene.canvas_h // 16), N)[r]
+eng = StepEngine(w.scene, w.cfg, w.loss, 40, use_graph=False, band=band)
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 for _ in range(12):
     flush.zero_()
@@ -69,3 +75,24 @@ for lo, hi in ((0, 8), (8, 16), (16, 24), (24, 33), (33, 999)):
 e = endt.max(axis=1)
 order = np.argsort(e)[-10:]
 print("last tiles:", [(int(t), int(L[t]), round(float(tmax[t]), 1)) for t in order])
+
+# slot-mode prologue span per CTA (wait done -> lists sorted)
+allp = np.zeros(148 * 6, dtype=np.uint64)
+lib.pf_step_prof_prologue(allp.ctypes.data_as(C.c_void_p), 148)
+pro = allp[: 2 * 148].reshape(148, 2)
+ph = allp[2 * 148 :].reshape(148, 4).astype(np.float64)
+ok = pro[:, 1] > 0
+if ok.any():
+    p0 = pro[ok].astype(np.float64)
+    span = (p0[:, 1] - p0[:, 0]) / 1e3
+    st = (p0[:, 0] - p0[:, 0].min()) / 1e3
+    print("prologue span per CTA (us) p0/p50/p90/p100:",
+          [round(float(np.percentile(span, q)), 2) for q in (0, 50, 90, 100)],
+          " start offset max", round(float(st.max()), 2),
+          " slowest CTAs:", list(np.argsort(span)[-5:]))
+    okp = ok & (ph[:, 0] > 0)
+    if okp.any():
+        b0 = pro[okp, 0].astype(np.float64)
+        for k, name in enumerate(("first batch landed", "tiles sorted", "classes written")):
+            d = (ph[okp, k] - b0) / 1e3
+            print(f"  {name:20s} after prologue start: p50 {np.median(d):.2f} max {d.max():.2f} us")
