@@ -33,6 +33,13 @@
 //   incremental variant (pf_preprocess_sync) only for primitives whose
 //   parameters changed since the device copy.
 // The CSR bins are bit-identical to the reference's offsets/indices.
+//
+// Slot mode (the fit step; ABI 6, see SlotBins in pf_bins.cuh): K1 also appends
+// every (tile, primitive) pair of a primitive's band-clipped rect to the tile's
+// slot list -- pos = atomicAdd(cnt[tile], 1), slot[tile][pos] = z rank -- and
+// writes the fit step's records at the z rank; pf_fit_step's prologue sorts the
+// lists, so no K2 launch sits between K1 and the fit step.  K1 runs 8 lanes per
+// primitive, or 4 when 8 would not fit one wave of 3 blocks per SM (c5).
 #include "../../include/primfit_b200.h"
 #include "pf_bins.cuh"
 #include "pf_common.cuh"

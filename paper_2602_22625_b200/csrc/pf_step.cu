@@ -34,6 +34,17 @@
 //           u, v from the float64 affine map; warp transpose-butterfly reduction
 //           and float64 RED atomics into grads.
 // mu_blend > 0 (colour from the texture) keeps the two-kernel path.
+//
+// Slot mode (template SLOT, the fit loop): the tile lists come from K1's slot
+// scatter instead of pf_bin; a prologue run by every warp z-sorts each tile's
+// list (warp bitonic sorts in registers; long / overflowed lists through a
+// gather + rank sort), builds the longest-first classes, gives each producer a
+// CTA-local first tile, and arrives on a grid barrier that the producers wait
+// on only before their first global ticket.  No fence instruction anywhere in
+// this file's kernel: a fence makes ptxas emit the gradient REDs as returning
+// ATOMs (+10 %); ordering uses acquire / release atomics instead.
+// LOSS == PF_LOSS_EXTERN: dL/dI, dL/dA per pixel are staged in place of the
+// target (the autograd Function's backward; forward recomputed on chip).
 #include <cstdlib>
 #include <type_traits>
 
