@@ -16,6 +16,12 @@ from pathlib import Path
 
 LIB_DIR = Path(__file__).resolve().parent / "_lib"
 LIB_PATH = LIB_DIR / "libprimfit_b200.so"
+# the diagnostics build (PF_DIAG=1: globaltimer timeline, per-warp step profile)
+# is a second library; the product build compiles that code out (4 % of the
+# fit-step kernel's time).  PF_TIMELINE / PF_STEP_PROF select it.
+LIB_DIAG_PATH = LIB_DIR / "libprimfit_b200_diag.so"
+if os.environ.get("PF_TIMELINE") or os.environ.get("PF_STEP_PROF"):
+    LIB_PATH = LIB_DIAG_PATH
 # diagnostics: PF_LIB=<path> loads another build (A/B runs on one box)
 if os.environ.get("PF_LIB"):
     LIB_PATH = Path(os.environ["PF_LIB"])

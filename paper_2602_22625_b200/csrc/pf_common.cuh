@@ -294,7 +294,11 @@ __device__ __forceinline__ unsigned long long gtime_ns() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+#ifndef PF_DIAG
+#define PF_DIAG 1  // diagnostics code compiled in (the product library is built with 0)
+#endif
 __device__ __forceinline__ void tl_mark(unsigned long long* tl, int slot, int what) {
+  if (!PF_DIAG) return;
   if (tl != nullptr && what == 2) {  // any lane-0 caller: min / max into the wait fields
     if ((threadIdx.x & 31) != 0) return;
     const unsigned long long t = gtime_ns();

@@ -641,6 +641,7 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
 // L, tx | ty << 16) the producers read, and its count is zeroed for the next
 // K1.  A grid barrier (all CTAs are resident: one per SM) ends the phase.
 constexpr int kSortRound = 1024;  // tiles per CTA and round (scratch: 20 B each)
+constexpr bool kDiag = PF_DIAG != 0;  // (pf_common.cuh: 0 in the product library)
 #ifndef PF_PROLOGUE_MARKS
 #define PF_PROLOGUE_MARKS 1  // (diagnostics, PF_STEP_PROF only: phase times of the prologue)
 #endif
@@ -648,6 +649,8 @@ template <int G>
 __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* scratch,
                                               int4* first) {
   const SlotBins& sb = a.sb;
+  unsigned long long* const prof_ = kDiag ? a.prof : nullptr;
+  unsigned long long* const tl_ = kDiag ? a.tl : nullptr;
   __shared__ int s_ccnt[kTileClasses], s_cbase[kTileClasses];
   __shared__ unsigned s_k;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nwarps = blockDim.x >> 5;
@@ -699,8 +702,8 @@ __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* 
       }
       cp_async_wait_all();
       __syncwarp();
-      if (PF_PROLOGUE_MARKS && a.prof && t == 0 && ib == warp && blockIdx.x < 256)
-        a.prof[6 * 148 * 32 + 65536 * 8 + 512 + 4 * blockIdx.x + 0] = gtimer();
+      if (PF_PROLOGUE_MARKS && prof_ && t == 0 && ib == warp && blockIdx.x < 256)
+        prof_[6 * 148 * 32 + 65536 * 8 + 512 + 4 * blockIdx.x + 0] = gtimer();
 #pragma unroll 1
       for (int q = 0; q < kB; ++q) {
         const int i = ib + q * nwarps;
@@ -832,8 +835,8 @@ __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* 
       }
     }
     __syncthreads();
-    if (PF_PROLOGUE_MARKS && a.prof && t == 0 && blockIdx.x < 256)
-      a.prof[6 * 148 * 32 + 65536 * 8 + 512 + 4 * blockIdx.x + 1] = gtimer();
+    if (PF_PROLOGUE_MARKS && prof_ && t == 0 && blockIdx.x < 256)
+      prof_[6 * 148 * 32 + 65536 * 8 + 512 + 4 * blockIdx.x + 1] = gtimer();
     if (t < kTileClasses) s_cbase[t] = s_ccnt[t] ? atomicAdd(a.classes_rw + t, s_ccnt[t]) : 0;
     __syncthreads();
     for (int i = t; i < nr; i += blockDim.x) {
@@ -843,10 +846,10 @@ __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* 
     }
     __syncthreads();
   }
-  if (PF_PROLOGUE_MARKS && a.prof && t == 0 && blockIdx.x < 256)
-    a.prof[6 * 148 * 32 + 65536 * 8 + 512 + 4 * blockIdx.x + 2] = gtimer();
+  if (PF_PROLOGUE_MARKS && prof_ && t == 0 && blockIdx.x < 256)
+    prof_[6 * 148 * 32 + 65536 * 8 + 512 + 4 * blockIdx.x + 2] = gtimer();
   if (lane == 0 && kacc) atomicAdd(&s_k, kacc);
-  tl_mark(a.tl, 14, 1);
+  tl_mark(tl_, 14, 1);
   __syncthreads();
   // arrive on the grid barrier: this CTA's lists and class entries are complete
   // (the producers wait for every CTA before their first global ticket)
@@ -873,10 +876,13 @@ __device__ __forceinline__ void slot_prologue(const StepArgs& a, unsigned char* 
 template <int LOSS, int ATL, int G, bool BG, int ST, bool SLOT>
 __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
   extern __shared__ __align__(128) unsigned char sm[];
+  // diagnostics pointers (PF_STEP_PROF / PF_TIMELINE); a PF_DIAG=0 build drops them
+  unsigned long long* const prof_ = kDiag ? a.prof : nullptr;
+  unsigned long long* const tl_ = kDiag ? a.tl : nullptr;
   __shared__ __align__(8) uint64_t full[G][kNBuf], empty[G][kNBuf];
   __shared__ int4 hdr[G][kNBuf];
 
-  tl_mark(a.tl, 1, 0);
+  tl_mark(tl_, 1, 0);
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
   constexpr bool has_bg = BG;
@@ -927,7 +933,7 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
   }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   pdl_wait();  // bins, classes and records of this step are complete from here on
-  tl_mark(a.tl, 1, 1);
+  tl_mark(tl_, 1, 1);
   constexpr bool slot_mode = SLOT;  // (a template parameter: consumer registers)
   // (no fences in this kernel: any fence makes ptxas turn every gradient RED
   // into a returning ATOM -- 10 % of the kernel's time)
@@ -956,10 +962,10 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
   if (SLOT && t < G) s_first[t] = make_int4(-1, 0, 0, 0);
   if constexpr (SLOT) {
     __syncthreads();
-    const unsigned long long pro0 = a.prof ? gtimer() : 0;
+    const unsigned long long pro0 = prof_ ? gtimer() : 0;
     slot_prologue<G>(a, sm, s_first);
-    if (a.prof && t == 0 && blockIdx.x < 256) {  // (diagnostics: prologue span per CTA)
-      unsigned long long* pp = a.prof + 6 * 148 * 32 + 65536 * 8 + 2 * blockIdx.x;
+    if (prof_ && t == 0 && blockIdx.x < 256) {  // (diagnostics: prologue span per CTA)
+      unsigned long long* pp = prof_ + 6 * 148 * 32 + 65536 * 8 + 2 * blockIdx.x;
       pp[0] = pro0;
       pp[1] = gtimer();
     }
@@ -983,11 +989,11 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
     return reinterpret_cast<float4*>(gs + b * bbytes + buf_rec_bytes(ST) + kBufPix);
   };
 
-  unsigned long long p_wait = 0, p_work = 0, p_n = 0, p_first = 0, p_t0 = a.prof ? gtimer() : 0;
+  unsigned long long p_wait = 0, p_work = 0, p_n = 0, p_first = 0, p_t0 = prof_ ? gtimer() : 0;
   auto finish = [&]() {
-    tl_mark(a.tl, 1, 3);
-    if (a.prof && lane == 0) {
-      unsigned long long* o = a.prof + ((size_t)blockIdx.x * blockDim.x / 32 + warp) * 6;
+    tl_mark(tl_, 1, 3);
+    if (prof_ && lane == 0) {
+      unsigned long long* o = prof_ + ((size_t)blockIdx.x * blockDim.x / 32 + warp) * 6;
       o[0] = p_wait;
       o[1] = p_work;
       o[2] = p_n;
@@ -1090,17 +1096,17 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
     // previous tile's copies went out, before waiting for its ring slot
 #pragma unroll 1
     for (int k = 0;; ++k) {
-      const unsigned long long cp = a.prof ? clock64() : 0;
+      const unsigned long long cp = prof_ ? clock64() : 0;
       next_tile();
       load_list();
-      if (a.prof) {  // producer "work" = ticket + list fetch
+      if (prof_) {  // producer "work" = ticket + list fetch
         p_work += clock64() - cp;
         ++p_n;
       }
       if (k >= kNBuf) {
-        const unsigned long long c0 = a.prof ? clock64() : 0;
+        const unsigned long long c0 = prof_ ? clock64() : 0;
         mbar_wait_sleep(&empty[g][buf], (eph >> buf) & 1u, a.psleep);
-        if (a.prof) p_wait += clock64() - c0;
+        if (prof_) p_wait += clock64() - c0;
         eph ^= 1u << buf;
       }
       if (tile >= a.n_tiles) {
@@ -1165,10 +1171,10 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
     uint32_t fph = 0;
     mbar_wait_sleep(&atl_bar, 0, 100);  // the shared-memory atlas has landed
     for (;;) {
-      const unsigned long long c0 = a.prof ? clock64() : 0;
+      const unsigned long long c0 = prof_ ? clock64() : 0;
       mbar_wait_sleep(&full[g][buf], (fph >> buf) & 1u, a.csleep);
-      const unsigned long long c1 = a.prof ? clock64() : 0;
-      if (a.prof) {
+      const unsigned long long c1 = prof_ ? clock64() : 0;
+      if (prof_) {
         p_wait += c1 - c0;
         if (p_n == 0) p_first = c1 - c0;
       }
@@ -1196,12 +1202,12 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[g][buf]);
-      if (a.prof) {
+      if (prof_) {
         const unsigned long long dt = clock64() - c1;
         p_work += dt;
         ++p_n;
         if (lane == 0 && h.x < 65536)
-          a.prof[6 * 148 * 32 + (size_t)h.x * kCW + wg] = dt | ((unsigned long long)(gtimer() & 0xffffffffu) << 32);
+          prof_[6 * 148 * 32 + (size_t)h.x * kCW + wg] = dt | ((unsigned long long)(gtimer() & 0xffffffffu) << 32);
       }
       buf = buf + 1 == kNBuf ? 0 : buf + 1;
     }
