@@ -157,7 +157,6 @@ static pf::Diag read_diag() {
     auto num = [](const char* k, int dflt) { const char* e = getenv(k); return e ? atoi(e) : dflt; };
     Diag v;
     v.no_pdl = flag("PF_NO_PDL");
-    v.step_lazy = flag("PF_STEP_LAZY");
     v.step_nolpt = flag("PF_STEP_NOLPT");
     v.step_prof = flag("PF_STEP_PROF");
     v.step_atl32 = flag("PF_STEP_ATL32");

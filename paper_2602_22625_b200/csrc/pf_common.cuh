@@ -336,7 +336,7 @@ cudaError_t ensure_dyn_smem(const void* kern, size_t smem);
 // Diagnostics switches (A/B runs, profiling), read from the environment once per
 // process -- never on the launch path.
 struct Diag {
-  bool no_pdl, step_lazy, step_nolpt, step_prof, step_atl32, step_atl0, timeline;
+  bool no_pdl, step_nolpt, step_prof, step_atl32, step_atl0, timeline;
   unsigned csleep, psleep;
   int bin_ncb, bin_two_level;  // -1: not set
 };

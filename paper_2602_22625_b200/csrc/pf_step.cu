@@ -118,7 +118,6 @@ struct StepArgs {
   float4* spill;         // [slot][2] for stack depth >= kKS
   double* grads;
   unsigned* ctr;         // [2]: tile ticket, finished producers (self-resetting)
-  int sched_lazy;        // 1: fetch the next ticket only once a ring slot is free
   unsigned csleep, psleep;  // back-off (ns) of consumer / producer barrier waits
   const int32_t* classes;  // pf_bin's tile classes (counts + lists) or NULL: tile = ticket
   int32_t* classes_rw;
@@ -1361,7 +1360,6 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   a.grads = grads;
   a.ctr = counters;
   const Diag& dg = diag();
-  a.sched_lazy = dg.step_lazy ? 1 : 0;
   a.csleep = dg.csleep;
   a.psleep = dg.psleep;
   a.classes = dg.step_nolpt ? nullptr : tile_classes;
