@@ -403,7 +403,7 @@ def _edge_scene(kind: str):
         sc.primitives[5].scale = 200.0  # covers the whole canvas
         sc.primitives[5].opacity_logit = -1.0
         return sc, w.cfg, w.loss
-    W, H, n = (13, 9, 6) if kind == "tiny" else (40, 36, 1)
+    W, H, n = {"tiny": (13, 9, 6), "single": (40, 36, 1), "empty": (40, 36, 0)}[kind]
     prims = [PrimitiveParams(x=float(rng.uniform(0, W)), y=float(rng.uniform(0, H)),
                              scale=float(rng.uniform(3, 9)), rotation=float(rng.uniform(-3, 3)),
                              opacity_logit=float(rng.uniform(-1, 2)),
@@ -414,7 +414,7 @@ def _edge_scene(kind: str):
     return sc, w.cfg, LossSpec(kind="mse", target=target)
 
 
-@pytest.mark.parametrize("kind", ["offcanvas", "tiny", "single"])
+@pytest.mark.parametrize("kind", ["offcanvas", "tiny", "single", "empty"])
 def test_fused_step_edge_scenes(torch_cuda, oracle, kind):
     from paper_2602_22625_b200.fit import StepEngine, effective_padding
 
@@ -431,6 +431,9 @@ def test_fused_step_edge_scenes(torch_cuda, oracle, kind):
     assert ok, f"{kind} alpha rel err {err}"
     diff = img - loss.target
     np.testing.assert_allclose(sums[0], np.sum(diff**2), rtol=1e-5)
+    if kind == "empty":  # no primitive: the background alone, no gradient
+        assert g.size == 0
+        return
     g_ref = oracle.backward(pk, sv, 2.0 * diff / diff.size, None)
     ok, err = grad_close(g, g_ref)
     assert ok, f"{kind} grad rel err {err}"
