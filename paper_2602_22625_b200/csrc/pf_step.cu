@@ -236,6 +236,7 @@ __device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+#ifdef PF_SUSPEND_WAIT  // (A/B variant: measured equal to the nanosleep back-off)
 // try_wait with a suspend-time hint: the warp is parked by the hardware until
 // the phase completes (or the hint elapses), no polling loop in the issue slots
 __device__ __forceinline__ bool mbar_try_suspend(uint64_t* b, uint32_t parity, uint32_t ns) {
@@ -249,6 +250,7 @@ __device__ __forceinline__ bool mbar_try_suspend(uint64_t* b, uint32_t parity, u
       : "memory");
   return ok != 0;
 }
+#endif
 // wait with an explicit back-off (the waiting warp leaves the issue slots alone)
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity, unsigned ns) {
 #ifdef PF_SUSPEND_WAIT
