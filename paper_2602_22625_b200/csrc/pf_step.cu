@@ -64,6 +64,13 @@ constexpr int kSlotArena = 128;  // spill entries per group for slot-mode in-pla
 #ifndef PF_KS
 #define PF_KS 5
 #endif
+#ifndef PF_F32_LERP
+// fp32 bilinear alpha / eps decision / dm-dU, dm-dV in the fit step with fp32
+// atlas taps (the float64 chain only inside the guard bands); measured +1.4 % at
+// c3 with the fp32 shared atlas, +4 % at c5 (global atlas) over the float64 path
+// with the fp64 shared atlas.  0 restores the float64 path (A/B).
+#define PF_F32_LERP 1
+#endif
 constexpr int kKS = PF_KS;                              // contribution-stack depth in smem
 constexpr uint32_t kEntBytes = sizeof(RecS) + sizeof(RecC);
 // CTA shape for G groups: warps [0, 8G) consume (group = warp / 8), warps
@@ -107,6 +114,7 @@ struct StepArgs {
   int W, H, ntx, ty_begin, n_tiles;
   double eps_skip;
   double eps_band;       // eps re-check band (see warp_tile)
+  float eps_f, eps_band_f;  // the same for the fp32 bilinear path (PF_F32_LERP)
   float k2_3P;           // (float)(2 / (3 P)): fp32 MSE gradient scale
   double bg0, bg1, bg2;
   float bgf0, bgf1, bgf2;  // the same as float (backward)
@@ -311,6 +319,8 @@ __device__ __forceinline__ double f32_to_f64_alu(uint32_t b) {
   return (b & 0x7f800000u) ? __hiloint2double((int)hi, (int)lo) : 0.0;
 }
 
+// (the float64 and fp32 accessors are each unused in one PF_F32_LERP variant)
+#pragma nv_diag_suppress 177
 // Padded alpha atlas access, float64 result: shared fp64 copy (LDS.64),
 // shared fp32 copy, or the global fp32 plane.
 struct AtlasS64 {
@@ -320,6 +330,7 @@ struct AtlasS64 {
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(base + 8u * (uint32_t)i));
     return v;
   }
+  __device__ __forceinline__ float f(int i) const { return (float)(*this)(i); }
 };
 struct AtlasS32 {
   uint32_t base;
@@ -328,10 +339,16 @@ struct AtlasS32 {
     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(base + 4u * (uint32_t)i));
     return f32_to_f64_alu(v);
   }
+  __device__ __forceinline__ float f(int i) const {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(base + 4u * (uint32_t)i));
+    return __uint_as_float(v);
+  }
 };
 struct AtlasG32 {
   const uint32_t* p;
   __device__ __forceinline__ double operator()(int i) const { return f32_to_f64_alu(__ldg(p + i)); }
+  __device__ __forceinline__ float f(int i) const { return __uint_as_float(__ldg(p + i)); }
 };
 
 // floor(U) and U - floor(U) for 0 <= U < 2^31 with two DADDs (round-down add of
@@ -419,6 +436,37 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
       cell_of(U, u0, wu);
       cell_of(V, v0, wv);
       int tp = r.pbase + v0 * r.wp + u0;
+#if PF_F32_LERP
+      // the common case in fp32: bilinear alpha from fp32 taps, eps decision
+      // outside a 1e-6 band around eps (>> the fp32 error), dm/dU, dm/dV; the
+      // cell and weights come from the float64 U, V (exact cell choice)
+      float wuf = (float)wu, wvf = (float)wv;
+      float f00 = atl.f(tp), f01 = atl.f(tp + 1), f10 = atl.f(tp + r.wp), f11 = atl.f(tp + r.wp + 1);
+      const float lf0 = fmaf(wuf, f01 - f00, f00), lf1 = fmaf(wuf, f11 - f10, f10);
+      float mf = fmaf(wvf, lf1 - lf0, lf0);
+      if (exact || fabsf(mf - a.eps_f) <= a.eps_band_f) {
+        // rare: the reference's exact chain for the decision and the value
+        const RecF& f = a.recf[r.gidx];
+        if (!exact) (void)texel_coords(f, xx, yy, U, V);
+        const Cell c = make_cell(U, V);
+        const double m = bilinear(plane_a, f.base, f.wt, f.ht, c);
+        if (m < a.eps_skip) continue;
+        mf = (float)m;
+        wuf = (float)c.wu;
+        wvf = (float)c.wv;
+        tp = r.pbase + c.v0 * r.wp + c.u0;
+        f00 = atl.f(tp);
+        f01 = atl.f(tp + 1);
+        f10 = atl.f(tp + r.wp);
+        f11 = atl.f(tp + r.wp + 1);
+      } else if (mf < a.eps_f) {
+        continue;
+      }
+      const float gUf = fmaf(wvf, (f11 - f10) - (f01 - f00), f01 - f00);
+      const float gVf = fmaf(wuf, (f11 - f01) - (f10 - f00), f10 - f00);
+      const float4 ea = make_float4(__int_as_float(j), T, mf, gUf);
+      const float eb = gVf;
+#else
       double t00 = atl(tp), t01 = atl(tp + 1), t10 = atl(tp + r.wp), t11 = atl(tp + r.wp + 1);
       const double l0 = fma(wu, t01 - t00, t00), l1 = fma(wu, t11 - t10, t10);
       double m = fma(wv, l1 - l0, l0);
@@ -443,6 +491,7 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
       const float mf = (float)m;
       const float4 ea = make_float4(__int_as_float(j), T, mf, (float)gU);
       const float eb = (float)gV;
+#endif
       if (ns < kKS) {
         stA[ns * kTilePix + ct] = ea;
         stB[ns * kTilePix + ct] = eb;
@@ -1342,6 +1391,8 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   a.eps_skip = eps_skip;
   // eps re-check band: fp32 taps (<= 6e-8 relative) + affine U, V (<= 1e-10 texel)
   a.eps_band = 1e-6 * eps_skip + 1e-9;
+  a.eps_f = (float)eps_skip;
+  a.eps_band_f = (float)(1e-6 + 1e-6 * eps_skip);  // >> fp32 taps + lerp error (~2e-7)
   a.k2_3P = (float)(2.0 * inv_3P);
   a.bg0 = bg_r;
   a.bg1 = bg_g;
@@ -1408,11 +1459,18 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
   // 2 groups + shared fp32 atlas 485 us)
   int atl = 0;
   if (!dg.step_atl0) {  // (diagnostics: force the global plane)
-    if (apad64 && !no64 && G * gb + a64 <= budget) atl = 2;
+    // (the fp32 bilinear path reads fp32 taps: the fp64 copy would only add
+    // conversions)
+    if (!PF_F32_LERP && apad64 && !no64 && G * gb + a64 <= budget) atl = 2;
     else if (G * gb + a32 <= budget) atl = 1;
   }
   const size_t smem = G * gb + (atl == 2 ? a64 : atl == 1 ? a32 : 0);
   void (*kern)(StepArgs);
+#if PF_F32_LERP
+#define PF_PICK4(LS, SS, SL)                                                                    \
+  kern = bg ? (atl == 1 ? k_step<LS, 1, 3, true, SS, SL> : k_step<LS, 0, 3, true, SS, SL>)     \
+            : (atl == 1 ? k_step<LS, 1, 3, false, SS, SL> : k_step<LS, 0, 3, false, SS, SL>);
+#else
 #define PF_PICK4(LS, SS, SL)                                                                    \
   kern = bg ? (atl == 2   ? k_step<LS, 2, 3, true, SS, SL>                                      \
                : atl == 1 ? k_step<LS, 1, 3, true, SS, SL>                                      \
@@ -1420,6 +1478,7 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
             : (atl == 2   ? k_step<LS, 2, 3, false, SS, SL>                                     \
                : atl == 1 ? k_step<LS, 1, 3, false, SS, SL>                                     \
                           : k_step<LS, 0, 3, false, SS, SL>);
+#endif
 #define PF_PICK3(LS, SS)    \
   if (slots) {              \
     PF_PICK4(LS, SS, true)  \
