@@ -59,7 +59,10 @@ namespace {
 constexpr int kCW = kTilePix / 32;                      // consumer warps per group (one tile)
 // list entries staged per tile: ST = 32, or 64 for long-list scenes (template
 // parameter of k_step; pf_fit_step's `stage` hint picks it)
-constexpr int kNBuf = 2;                                // stage buffers per group (ring)
+#ifndef PF_NBUF
+#define PF_NBUF 2
+#endif
+constexpr int kNBuf = PF_NBUF;                          // stage buffers per group (ring)
 constexpr int kSlotArena = 128;  // spill entries per group for slot-mode in-place lists (L <= 128)
 #ifndef PF_KS
 #define PF_KS 5
