@@ -3,7 +3,7 @@
 # command, ncu --set full captures (c3 fused step, c3 two-kernel path, c5 step),
 # kernel timelines, band scaling, sanitizer runs of the slot-binning step.
 set -u
-O=gpurun_out/ev5
+O=gpurun_out/ev6
 mkdir -p $O
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
 tail -1 $O/bench.json | cut -c1-300
