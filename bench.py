@@ -274,12 +274,14 @@ def ncu_traffic(kernel_prefix: str, config: str = "c3") -> float | None:
 
 def autograd_bench(w, steps: int, warmup: int, flush) -> dict:
     """The north_star's autograd entry point in a plain training loop: the
-    Renderer's torch.autograd.Function (K1+K2+K3 forward, K4 backward) under a
-    torch MSE loss, then the device Adam (pf_adam table mode), no host sync per
-    step (s_max bounds the capacity).  CUDA-event timed, L2 flushed per step."""
+    Renderer's torch.autograd.Function (K1+K2+K3 forward; backward = the fit-step
+    kernel on the upstream gradients) under a torch MSE loss, then the device Adam
+    (pf_adam table mode), no host sync per step (s_max bounds the capacity).
+    Again with the fused ``autograd.loss_mse`` in place of the torch loss.
+    CUDA-event timed, L2 flushed per step."""
     import torch
 
-    from paper_2602_22625_b200.autograd import Renderer
+    from paper_2602_22625_b200.autograd import Renderer, loss_mse
     from paper_2602_22625_b200.compositor import adam_launch
     from paper_2602_22625_b200.fit import _cfg_gains, effective_padding, lr_schedule
     from paper_2602_22625_b200.scene import param_matrix, structure_arrays
@@ -296,7 +298,7 @@ def autograd_bench(w, steps: int, warmup: int, flush) -> dict:
     n = params.shape[0]
     m = torch.zeros(n * 8, dtype=torch.float64, device=dev)
     v = torch.zeros_like(m)
-    total = 2 * (warmup + steps) + 4  # eager warm-up + timed, then the graphed run
+    total = 4 * (warmup + steps) + 8  # eager warm-up + timed, then the graphed run (x2)
     lr = torch.tensor([lr_schedule(i, total, cfg.learning_rate) for i in range(total)],
                       dtype=torch.float64, device=dev)
     bc1 = torch.tensor([1 - 0.9 ** (i + 1) for i in range(total)], dtype=torch.float64, device=dev)
@@ -306,58 +308,69 @@ def autograd_bench(w, steps: int, warmup: int, flush) -> dict:
     ctr = torch.zeros(1, dtype=torch.int32, device=dev)
     gains = _cfg_gains(cfg)
 
+    fused = [False]
+
     def step():
         img, _ = r(params)
-        loss = ((img - target) ** 2).mean()
+        loss = loss_mse(img, target) if fused[0] else ((img - target) ** 2).mean()
         loss.backward()
         with torch.no_grad():
             adam_launch(params.view(-1), params.grad.view(-1), m, v, gains=gains, n=n,
                         lr_table=lr, bc1_table=bc1, bc2_table=bc2, iter_counter=it, counter=ctr,
                         clamp=True, s_min=cfg.scale_min, s_max=cfg.scale_max, zero_grads=True)
 
-    for _ in range(warmup):
-        step()
-    torch.cuda.synchronize()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(steps)]
-    for e0, e1 in evs:
-        flush.zero_()
-        e0.record()
-        step()
-        e1.record()
-    torch.cuda.synchronize()
-    r.check()
-    ms = sum(a.elapsed_time(b) for a, b in evs) / steps
-    # the same training step captured once in a CUDA graph (torch.cuda.graph
-    # recipe: side-stream warm-up, capture, replay) -- the launch-bound eager
-    # loop without its Python / ctypes overhead
-    side = torch.cuda.Stream()
-    side.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(side):
-        for _ in range(2):
+    def measure() -> tuple[float, float]:
+        for _ in range(warmup):
             step()
-    torch.cuda.current_stream().wait_stream(side)
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        step()
-    for _ in range(warmup):
-        g.replay()
-    torch.cuda.synchronize()
-    gevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            for _ in range(steps)]
-    for e0, e1 in gevs:
-        flush.zero_()
-        e0.record()
-        g.replay()
-        e1.record()
-    torch.cuda.synchronize()
-    r.check()
-    gms = sum(a.elapsed_time(b) for a, b in gevs) / steps
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)]
+        for e0, e1 in evs:
+            flush.zero_()
+            e0.record()
+            step()
+            e1.record()
+        torch.cuda.synchronize()
+        r.check()
+        ms = sum(a.elapsed_time(b) for a, b in evs) / steps
+        # the same training step captured once in a CUDA graph (torch.cuda.graph
+        # recipe: side-stream warm-up, capture, replay) -- the launch-bound eager
+        # loop without its Python / ctypes overhead
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                step()
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        for _ in range(warmup):
+            g.replay()
+        torch.cuda.synchronize()
+        gevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(steps)]
+        for e0, e1 in gevs:
+            flush.zero_()
+            e0.record()
+            g.replay()
+            e1.record()
+        torch.cuda.synchronize()
+        r.check()
+        return ms, sum(a.elapsed_time(b) for a, b in gevs) / steps
+
+    ms, gms = measure()
+    fused[0] = True
+    fms, fgms = measure()
     return {"value": 1e3 / ms, "unit": UNIT, "ms_per_step": ms,
-            "path": "autograd.Renderer forward (K1+K2+K3) + torch MSE + backward (K4) + pf_adam; "
-                    "no host sync per step",
+            "path": "autograd.Renderer forward (K1+K2+K3) + torch MSE + backward (the fit-step "
+                    "kernel on the upstream gradients) + pf_adam; no host sync per step",
             "graphed": {"value": 1e3 / gms, "unit": UNIT, "ms_per_step": gms,
                         "path": "the same step captured in one CUDA graph (torch.cuda.graph)"},
+            "fused_loss": {"value": 1e3 / fms, "unit": UNIT, "ms_per_step": fms,
+                           "graphed": {"value": 1e3 / fgms, "unit": UNIT, "ms_per_step": fgms},
+                           "path": "the same step with autograd.loss_mse (fused MSE op) in "
+                                   "place of the torch loss"},
             "l2": "flushed (256 MiB write) before every timed step"}
 
 

@@ -57,7 +57,7 @@ extern "C" {
                                 upstream: the autograd Function's backward), no loss sums */
 
 /* ABI version; bumped on any signature change. */
-int pf_abi_version(void);  /* 6 */
+int pf_abi_version(void);  /* 7 */
 
 /* Diagnostics: the PF_* environment switches (A/B variants, profiling) are read
  * once at load; this re-reads them (tests that flip a switch at run time). */
@@ -328,6 +328,19 @@ int pf_fit_step(const void* rec, int n, const double* tex, const float* apad,
  * float32 [P] (dL/dA, or NULL = 0) into out4 float32 [P][4], the per-pixel rows
  * pf_fit_step stages (the autograd Function's backward). */
 int pf_pack_grad4(const float* rgb, const float* alpha, int P, float* out4, void* stream);
+
+/* loss_mse (fit.py:110-115) on the autograd path (ABI 7).  img4: the renderer's
+ * (r, g, b, alpha) float32 rows [P][4]; target float32 [P][3].  pf_mse4 writes
+ * mean((I - t)^2) over P x 3 to loss[0] (float32; per-pixel error in float32,
+ * float64 partials folded in a fixed order); scratch: PF_MSE4_SCRATCH zeroed
+ * doubles owned by the caller (self-resetting; one launch at a time per scratch).
+ * pf_mse4_grad writes grad_out[0] * 2 (I - t) / (3 P) as (r, g, b, 0) rows into
+ * out4 [P][4] -- the rows pf_fit_step(PF_LOSS_EXTERN) reads, no pf_pack_grad4. */
+#define PF_MSE4_SCRATCH 2048
+int pf_mse4(const float* img4, const float* target, int P, double* scratch, float* loss,
+            void* stream);
+int pf_mse4_grad(const float* img4, const float* target, int P, const float* grad_out,
+                 float* out4, void* stream);
 
 /* Fixed-order fold of n_part partial triples into sums[3] (deterministic). */
 int pf_fold_loss(const double* part, int n_part, double* sums, void* stream);

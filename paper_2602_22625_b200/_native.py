@@ -57,6 +57,8 @@ SIGNATURES: dict[str, tuple] = {
                                 _I, _P, _P]),
     "pf_slot_bytes": (_Z, [_I, _I, _I]),
     "pf_pack_grad4": (_I, [_P, _P, _I, _P, _P]),
+    "pf_mse4": (_I, [_P, _P, _I, _P, _P, _P]),
+    "pf_mse4_grad": (_I, [_P, _P, _I, _P, _P, _P]),
     "pf_slot_reset": (_I, [_P, _I, _I, _I, _P, _P]),
     "pf_scratch_init": (_I, [_P, _Z, _P, _P, _I, _P, _P, _P, _P, _P, _P, _I, _I, _P]),
     "pf_adam_blocks": (_I, [_I]),

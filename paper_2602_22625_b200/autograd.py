@@ -10,6 +10,11 @@ compositor composes with any torch loss:
     img, alpha = r(params)            # params: (N, 8) float64 CUDA, requires_grad
     ((img - target) ** 2).mean().backward()   # params.grad = dL/dparams
 
+``loss_mse(img, target)`` is the reference's loss_mse (fit.py:110-115) as a
+fused autograd op on the renderer's output: one reduction kernel forward, one
+kernel backward that writes the gradient straight into the rows the fit-step
+kernel reads (the renderer's backward then skips its repacking pass).
+
 The saved contribution lists live in a pooled Compositor held by ctx until
 the backward (the reference keeps them in SavedForward + a fingerprint;
 autograd's graph ownership replaces the fingerprint check).
@@ -53,6 +58,8 @@ class _Composite(torch.autograd.Function):
             renderer._give_back(comp)
         ctx.renderer = renderer
         ctx.bg4 = bg4
+        # an unused output's gradient arrives as None, not as a zero tensor
+        ctx.set_materialize_grads(False)
         return img, alpha
 
     @staticmethod
@@ -64,12 +71,19 @@ class _Composite(torch.autograd.Function):
         n = comp.n
         grads = r._grads(n)
         d4 = r._d4()
-        if d_img is None:
-            d_img = torch.zeros(r.H, r.W, 3, dtype=torch.float32, device=r.dev)
-        nat.check(nat.load().pf_pack_grad4(
-            d_img.to(torch.float32).contiguous().data_ptr(),
-            nat.ptr(d_alpha.to(torch.float32).contiguous() if d_alpha is not None else None),
-            r.H * r.W, d4.data_ptr(), torch.cuda.current_stream().cuda_stream), "pf_pack_grad4")
+        base = d_img._base if d_img is not None else None
+        if (d_alpha is None and base is not None and getattr(base, "_pf_grad4", False)
+                and d_img.stride() == (4 * r.W, 4, 1) and d_img.shape == (r.H, r.W, 3)
+                and d_img.data_ptr() == base.data_ptr()):
+            d4 = base  # loss_mse's (r, g, b, 0) rows: already the fit step's layout
+        else:
+            if d_img is None:
+                d_img = torch.zeros(r.H, r.W, 3, dtype=torch.float32, device=r.dev)
+            nat.check(nat.load().pf_pack_grad4(
+                d_img.to(torch.float32).contiguous().data_ptr(),
+                nat.ptr(d_alpha.to(torch.float32).contiguous() if d_alpha is not None else None),
+                r.H * r.W, d4.data_ptr(), torch.cuda.current_stream().cuda_stream),
+                "pf_pack_grad4")
         if r.mu_blend == 0.0:
             comp.fit_step(grads, None, eps_skip=r.eps_skip, bg_rgb=r.bg_rgb, bg4=ctx.bg4,
                           loss_kind=nat.PF_LOSS_EXTERN, tgt4=d4.view(-1))
@@ -79,6 +93,60 @@ class _Composite(torch.autograd.Function):
         ctx.comp = None
         r._give_back(comp)
         return out, None, None
+
+
+def _rows4(img: torch.Tensor) -> bool:
+    """img is the (H, W, 3) colour view of (r, g, b, alpha) float32 rows."""
+    return (img.is_cuda and img.dtype == torch.float32 and img.dim() == 3
+            and img.shape[2] == 3 and img.stride() == (4 * img.shape[1], 4, 1)
+            and img.data_ptr() % 16 == 0)
+
+
+_MSE_SCRATCH: dict = {}  # device -> zeroed PF_MSE4_SCRATCH doubles (self-resetting)
+
+
+class _LossMSE(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, img, target):
+        P = img.shape[0] * img.shape[1]
+        sc = _MSE_SCRATCH.get(img.device)
+        if sc is None:
+            sc = _MSE_SCRATCH[img.device] = torch.zeros(2048, dtype=torch.float64,
+                                                        device=img.device)
+        loss = torch.empty((), dtype=torch.float32, device=img.device)
+        st = torch.cuda.current_stream().cuda_stream
+        nat.check(nat.load().pf_mse4(img.data_ptr(), target.data_ptr(), P, sc.data_ptr(),
+                                     loss.data_ptr(), st), "pf_mse4")
+        ctx.save_for_backward(img, target)
+        return loss
+
+    @staticmethod
+    def backward(ctx, g):
+        img, target = ctx.saved_tensors
+        H, W = img.shape[0], img.shape[1]
+        out4 = torch.empty(H, W, 4, dtype=torch.float32, device=img.device)
+        out4._pf_grad4 = True  # (r, g, b, 0) rows: _Composite.backward takes them as is
+        g = g.to(torch.float32).contiguous()
+        nat.check(nat.load().pf_mse4_grad(img.data_ptr(), target.data_ptr(), H * W, g.data_ptr(),
+                                          out4.data_ptr(), torch.cuda.current_stream().cuda_stream),
+                  "pf_mse4_grad")
+        return out4[:, :, :3], None
+
+
+def loss_mse(img: torch.Tensor, target: torch.Tensor) -> torch.Tensor:
+    """mean((img - target)^2) over all pixels and channels (fit.py:110-115) as an
+    autograd op.  ``img`` is a Renderer's colour output (the (H, W, 3) view of its
+    (r, g, b, alpha) rows); ``target`` (H, W, 3).  Returns a float32 scalar.
+    Raises ShapeMismatch like the reference; any other image layout is rejected
+    (ValueError) rather than copied."""
+    from .errors import ShapeMismatch
+    if tuple(img.shape) != tuple(target.shape):
+        raise ShapeMismatch(f"shape {tuple(img.shape)} vs {tuple(target.shape)}")
+    if not _rows4(img):
+        raise ValueError("loss_mse: img must be a Renderer colour output ((H, W, 3) view of "
+                         "float32 (r, g, b, alpha) rows on the GPU)")
+    target = target.to(device=img.device, dtype=torch.float32).contiguous()
+    return _LossMSE.apply(img, target)
 
 
 class Renderer:

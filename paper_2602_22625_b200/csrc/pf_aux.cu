@@ -348,6 +348,79 @@ extern "C" int pf_pack_grad4(const float* rgb, const float* alpha, int P, float*
   return (int)cudaGetLastError();
 }
 
+// loss_mse (fit.py:110-115) on the autograd path: the image is the renderer's
+// (r, g, b, alpha) rows, the target (P, 3).  Per-pixel squared error in fp32 (as
+// the fit step's MSE), float64 per-block partials, folded in block order by the
+// last block to finish (deterministic for a given grid); the counter self-resets.
+constexpr int kMseThreads = 256;
+constexpr int kMseBlocks = 148 * 8;  // <= PF_MSE4_SCRATCH - 1 partials
+
+__global__ void __launch_bounds__(kMseThreads)
+    k_mse4(const float4* __restrict__ img4, const float* __restrict__ tgt, int P,
+           double* __restrict__ part, unsigned* __restrict__ ctr, double inv_n,
+           float* __restrict__ loss) {
+  double s = 0.0;
+  for (int p = blockIdx.x * kMseThreads + threadIdx.x; p < P; p += gridDim.x * kMseThreads) {
+    const float4 I = img4[p];
+    const float r0 = I.x - tgt[3 * (size_t)p], r1 = I.y - tgt[3 * (size_t)p + 1],
+                r2 = I.z - tgt[3 * (size_t)p + 2];
+    s += (double)fmaf(r0, r0, fmaf(r1, r1, r2 * r2));
+  }
+  __shared__ double ws[kMseThreads / 32];
+  __shared__ bool last;
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < kMseThreads / 32; ++w) b += ws[w];
+    part[blockIdx.x] = b;
+    __threadfence();
+    last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x >= 32) return;
+  __threadfence();
+  double t = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) t += __ldcg(part + b);
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (threadIdx.x == 0) {
+    loss[0] = (float)(t * inv_n);
+    *ctr = 0u;
+  }
+}
+
+// dL/dI = grad_out * 2 (I - t) / (3 P) into the fit step's (r, g, b, 0) rows
+__global__ void k_mse4_grad(const float4* __restrict__ img4, const float* __restrict__ tgt, int P,
+                            const float* __restrict__ grad_out, float k,
+                            float4* __restrict__ out) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const float g = k * grad_out[0];
+  const float4 I = img4[p];
+  out[p] = make_float4(g * (I.x - tgt[3 * (size_t)p]), g * (I.y - tgt[3 * (size_t)p + 1]),
+                       g * (I.z - tgt[3 * (size_t)p + 2]), 0.0f);
+}
+
+extern "C" int pf_mse4(const float* img4, const float* target, int P, double* scratch,
+                       float* loss, void* stream) {
+  if (P < 1 || !img4 || !target || !scratch || !loss) return PF_ERR_ARG;
+  const int blocks = min(div_up(P, kMseThreads), kMseBlocks);
+  k_mse4<<<blocks, kMseThreads, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float4*>(img4), target, P, scratch + 1,
+      reinterpret_cast<unsigned*>(scratch), 1.0 / (3.0 * (double)P), loss);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int pf_mse4_grad(const float* img4, const float* target, int P, const float* grad_out,
+                            float* out4, void* stream) {
+  if (P < 1 || !img4 || !target || !grad_out || !out4) return PF_ERR_ARG;
+  k_mse4_grad<<<div_up(P, 256), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float4*>(img4), target, P, grad_out, (float)(2.0 / (3.0 * (double)P)),
+      reinterpret_cast<float4*>(out4));
+  return (int)cudaGetLastError();
+}
+
 extern "C" int pf_layer_bboxes(const double* params, const int32_t* template_id,
                                const double* tpl_hyp, int n, int W, int H, int rho, int32_t* bbox,
                                long long* area, long long* offsets, void* stream) {

@@ -243,6 +243,59 @@ def test_autograd_function_matches_api(torch_cuda):
     assert ok, err
 
 
+def test_autograd_loss_mse_matches_reference_and_torch(torch_cuda, monkeypatch):
+    """autograd.loss_mse (the reference's loss_mse, fit.py:110-115, as a fused op):
+    loss value against the reference's float64 loss_mse on the same image,
+    gradients against the reference backward and the torch-loss path, and the
+    renderer's backward takes loss_mse's rows without the repacking kernel."""
+    torch = torch_cuda
+    from paper_2602_22625_b200 import _native as nat, autograd, grad, raster
+    from paper_2602_22625_b200.autograd import Renderer, loss_mse
+    from paper_2602_22625_b200.errors import ShapeMismatch
+    from paper_2602_22625_b200.scene import param_matrix, structure_arrays
+    from conftest import load_case, scene_from
+
+    d = load_case("medium_n300")
+    sc = scene_from(d)
+    tid, z = structure_arrays(sc)
+    r = Renderer(sc.templates, tid, z, sc.canvas_w, sc.canvas_h, background=sc.background,
+                 alpha_max=sc.alpha_max, mu_blend=sc.mu_blend)
+    target = torch.tensor(d["target"], device="cuda", dtype=torch.float32)
+    packs = []
+    real = nat.load()
+
+    class Lib:  # counts pf_pack_grad4 calls, forwards everything
+        def __getattr__(self, k):
+            if k == "pf_pack_grad4":
+                packs.append(1)
+            return getattr(real, k)
+
+    monkeypatch.setattr(autograd.nat, "load", lambda: Lib())
+    p1 = torch.tensor(param_matrix(sc), device="cuda", requires_grad=True)
+    img, _ = r(p1)
+    loss = loss_mse(img, target)
+    loss.backward()
+    assert not packs  # loss_mse's rows went to the fit step as they are
+    p2 = torch.tensor(param_matrix(sc), device="cuda", requires_grad=True)
+    img2, _ = r(p2)
+    ((img2 - target) ** 2).mean().backward()
+    assert packs
+    out, saved = raster.render_forward(sc, save=True)
+    ref = float(np.mean((out.color - d["target"]) ** 2))
+    assert abs(float(loss.detach()) - ref) <= 1e-6 * ref
+    dI = 2.0 * (out.color - d["target"]) / out.color.size
+    ok, err = grad_close(p1.grad.cpu().numpy(), grad.backward(sc, saved, dI).data)
+    assert ok, err
+    ok, err = grad_close(p1.grad.cpu().numpy(), p2.grad.cpu().numpy(), rel=1e-4)
+    assert ok, err
+    # deterministic: the same image gives the same bits
+    assert float(loss_mse(img.detach(), target)) == float(loss.detach())
+    with pytest.raises(ShapeMismatch):
+        loss_mse(img, target[:-1])
+    with pytest.raises(ValueError):
+        loss_mse(img.contiguous(), target)
+
+
 def _fused_grads(eng, image=True):
     """One K2 + K34 launch on the engine's current parameters (no Adam)."""
     eng.refresh()
