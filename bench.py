@@ -317,7 +317,8 @@ def autograd_bench(w, steps: int, warmup: int, flush) -> dict:
         with torch.no_grad():
             adam_launch(params.view(-1), params.grad.view(-1), m, v, gains=gains, n=n,
                         lr_table=lr, bc1_table=bc1, bc2_table=bc2, iter_counter=it, counter=ctr,
-                        clamp=True, s_min=cfg.scale_min, s_max=cfg.scale_max, zero_grads=True)
+                        clamp=True, s_min=cfg.scale_min, s_max=cfg.scale_max, zero_grads=False)
+        params.grad = None  # (torch's zero_grad(set_to_none=True))
 
     def measure() -> tuple[float, float]:
         for _ in range(warmup):

@@ -55,6 +55,9 @@ extern "C" {
 #define PF_LOSS_COMBINED 3   /* mse_w * loss_mse + gray_l1_w * loss_grayscale_l1, fit.py:119-125, 162-168 */
 #define PF_LOSS_EXTERN 4     /* pf_fit_step only: dL/dI, dL/dA given per pixel in tgt4 (a torch loss
                                 upstream: the autograd Function's backward), no loss sums */
+#define PF_LOSS_RENDER 5     /* pf_fit_step only (ABI 7, CSR lists): render only -- img4 written, no
+                                loss, no gradients; tgt4 / part / grads may be NULL (the autograd
+                                Function's forward) */
 
 /* ABI version; bumped on any signature change. */
 int pf_abi_version(void);  /* 7 */

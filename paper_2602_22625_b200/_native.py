@@ -35,6 +35,7 @@ PF_LOSS_MSE = 1
 PF_LOSS_SPATIAL = 2
 PF_LOSS_COMBINED = 3
 PF_LOSS_EXTERN = 4
+PF_LOSS_RENDER = 5
 
 _P = C.c_void_p
 _I = C.c_int

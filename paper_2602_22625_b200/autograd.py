@@ -22,6 +22,8 @@ autograd's graph ownership replaces the fingerprint check).
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -47,14 +49,21 @@ class _Composite(torch.autograd.Function):
         # copies (the caching allocator makes this free)
         comp.img4 = torch.empty(renderer.H * renderer.W * 4, dtype=torch.float32,
                                 device=renderer.dev)
-        comp.forward(save=not recompute, eps_skip=renderer.eps_skip, bg_rgb=renderer.bg_rgb,
-                     bg4=bg4)
+        if recompute and renderer.render_k34:
+            # the fit-step kernel as a forward: the lists and their tile classes
+            # stay for the backward's pass
+            comp.render(eps_skip=renderer.eps_skip, bg_rgb=renderer.bg_rgb, bg4=bg4)
+        else:
+            comp.forward(save=not recompute, eps_skip=renderer.eps_skip, bg_rgb=renderer.bg_rgb,
+                         bg4=bg4)
         if not torch.cuda.is_current_stream_capturing():
             renderer._watch(comp)
         img, alpha = comp.color(), comp.alpha()
         if ctx.needs_input_grad[0]:
             ctx.comp = comp  # the saved contribution lists: held until backward
         else:
+            if comp.tile_classes is not None:
+                comp.tile_classes[:16].zero_()  # (no backward pass to consume them)
             renderer._give_back(comp)
         ctx.renderer = renderer
         ctx.bg4 = bg4
@@ -89,7 +98,7 @@ class _Composite(torch.autograd.Function):
                           loss_kind=nat.PF_LOSS_EXTERN, tgt4=d4.view(-1))
         else:
             comp.backward(d4.view(-1), grads, bg_rgb=r.bg_rgb, bg4=ctx.bg4)
-        out = grads[: n * 8].view(n, 8).clone()
+        out = grads[: n * 8].view(n, 8)  # (a fresh buffer per call: no copy)
         ctx.comp = None
         r._give_back(comp)
         return out, None, None
@@ -186,8 +195,11 @@ class Renderer:
         self.bg_rgb = tuple(float(c) for c in background)
         self._free: list[Compositor] = []
         self._pending: list[tuple] = []  # (event, pinned status copy, capacity)
-        self._gbuf = None
         self._d4buf = None
+        # forward through the fit-step kernel (PF_LOSS_RENDER) rather than K3 (A/B
+        # switch PF_RENDER_K3=1)
+        self.render_k34 = os.environ.get("PF_RENDER_K3", "0") != "1"
+        self.lpt = os.environ.get("PF_RENDER_LPT", "1") == "1"
 
     # -- pooled per-call state
     def _capacity(self, params: torch.Tensor) -> int:
@@ -210,20 +222,22 @@ class Renderer:
         for i, c in enumerate(self._free):
             if c.capacity >= cap:
                 return self._free.pop(i)
-        return Compositor(self.tid, self.z, self.atlas, self.W, self.H, alpha_max=self.alpha_max,
+        comp = Compositor(self.tid, self.z, self.atlas, self.W, self.H, alpha_max=self.alpha_max,
                           mu_blend=self.mu_blend, padding=self.padding, capacity=cap,
                           device=self.dev, d_tid=self.d_tid, d_zorder=self.d_zorder)
+        if self.render_k34 and self.mu_blend == 0.0 and self.lpt:
+            comp.enable_step_schedule()  # longest-first tile classes for both passes
+        return comp
 
     def _give_back(self, comp: Compositor) -> None:
         if len(self._free) < 2:
             self._free.append(comp)
 
     def _grads(self, n: int) -> torch.Tensor:
-        if self._gbuf is None:
-            self._gbuf = torch.zeros(n * 8 + 4, dtype=torch.float64, device=self.dev)
-        else:
-            self._gbuf.zero_()
-        return self._gbuf
+        # per call (the caching allocator makes it a memset): handed to autograd
+        # as the parameter gradient without a copy -- with params.grad None (the
+        # usual zero_grad(set_to_none=True)) it becomes params.grad as is
+        return torch.zeros(n * 8 + 4, dtype=torch.float64, device=self.dev)
 
     def _d4(self) -> torch.Tensor:
         if self._d4buf is None:

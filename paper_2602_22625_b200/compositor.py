@@ -354,9 +354,9 @@ class Compositor:
         self.launches += 1
 
     # -- K34 (fit step: forward + loss + backward in one kernel)
-    def fit_step(self, grads: torch.Tensor, sums: torch.Tensor | None, *, eps_skip: float,
+    def fit_step(self, grads: torch.Tensor | None, sums: torch.Tensor | None, *, eps_skip: float,
                  bg_rgb=(1.0, 1.0, 1.0), bg4: torch.Tensor | None = None,
-                 loss_kind: int = nat.PF_LOSS_MSE, tgt4: torch.Tensor, alpha_w: float = 0.0,
+                 loss_kind: int = nat.PF_LOSS_MSE, tgt4: torch.Tensor | None, alpha_w: float = 0.0,
                  w_mse: float = 1.0, w_gray: float = 0.0,
                  P_total: int | None = None, image: bool = False, stream=None) -> None:
         if self.mu_blend > 0.0:
@@ -383,16 +383,24 @@ class Compositor:
                 self.bin_off.data_ptr(), self.bin_idx.data_ptr(), self.status.data_ptr(),
                 self.W, self.H, self.band.ty_begin, self.band.ty_end, float(eps_skip),
                 float(bg_rgb[0]), float(bg_rgb[1]), float(bg_rgb[2]), p(bg4), int(loss_kind),
-                tgt4.data_ptr(), float(alpha_w), float(w_mse), float(w_gray), 1.0 / (3.0 * Pt),
+                p(tgt4), float(alpha_w), float(w_mse), float(w_gray), 1.0 / (3.0 * Pt),
                 1.0 / Pt,
                 self.spill.data_ptr(), p(self.img4) if image else None, self.part.data_ptr(),
-                grads.data_ptr(), self.step_ctr.data_ptr(), nat.ptr(self.tile_classes),
+                p(grads), self.step_ctr.data_ptr(), nat.ptr(self.tile_classes),
                 self.stage_hint, self.scratch.data_ptr(), self.scratch_bytes, self.capacity,
                 nat.ptr(self.slots), self.slot_m, _stream_handle(stream)),
             "pf_fit_step")
         self.launches += 1
         if sums is not None:
             self.fold_loss(sums, stream)
+
+    def render(self, *, eps_skip: float, bg_rgb=(1.0, 1.0, 1.0), bg4: torch.Tensor | None = None,
+               stream=None) -> None:
+        """The fit-step kernel as a forward only (PF_LOSS_RENDER): img4 from the
+        pf_bin lists, which stay valid (with their tile classes) for a following
+        fit_step(PF_LOSS_EXTERN) -- the autograd Function's forward."""
+        self.fit_step(None, None, eps_skip=eps_skip, bg_rgb=bg_rgb, bg4=bg4,
+                      loss_kind=nat.PF_LOSS_RENDER, tgt4=None, image=True, stream=stream)
 
     @property
     def n_part(self) -> int:

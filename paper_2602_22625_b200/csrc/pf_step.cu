@@ -495,7 +495,9 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
       const float4 ea = make_float4(__int_as_float(j), T, mf, (float)gU);
       const float eb = (float)gV;
 #endif
-      if (ns < kKS) {
+      if (LOSS == PF_LOSS_RENDER) {
+        // (forward only: no contribution stack)
+      } else if (ns < kKS) {
         stA[ns * kTilePix + ct] = ea;
         stB[ns * kTilePix + ct] = eb;
       } else {
@@ -515,11 +517,17 @@ __device__ __forceinline__ void warp_tile(const StepArgs& a, const RECS& R, cons
   }
 
   // ---- loss (fit.py:112-151), pixel-local
-  const float4 tg = tgs[tp_];
   const float4 bgp = bgs ? bgs[tp_] : make_float4(0.f, 0.f, 0.f, 0.f);
   const float g0 = a.bg4 ? bgp.x : a.bgf0;
   const float g1 = a.bg4 ? bgp.y : a.bgf1;
   const float g2 = a.bg4 ? bgp.z : a.bgf2;
+  if (LOSS == PF_LOSS_RENDER) {
+    // render only (the autograd forward): the image, no loss, no backward
+    if (valid) a.img4[pix] = make_float4(fmaf(T, g0, C0), fmaf(T, g1, C1), fmaf(T, g2, C2), Aacc);
+    if (a.tile_cost && lane == 0) atomicMax(a.tile_cost + tile, work);
+    return;
+  }
+  const float4 tg = tgs[tp_];
   float dI0 = 0.f, dI1 = 0.f, dI2 = 0.f, dA = 0.f;
   float l0 = 0.f, l1 = 0.f, l2 = 0.f;
 #ifndef PF_LOSS32
@@ -1186,7 +1194,9 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
               a.sb.ctl[kSlotDirty] = 0u;
             }
           }
-          if (a.classes && lane < kTileClasses) a.classes_rw[lane] = 0;
+          // (a render-only pass leaves them: the backward pass on the same lists
+          // schedules from them next)
+          if (LOSS != PF_LOSS_RENDER && a.classes && lane < kTileClasses) a.classes_rw[lane] = 0;
         }
         break;
       }
@@ -1195,10 +1205,11 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
       const int vw = min(kTile, a.W - tx * kTile);
       const int vh = min(kTile, a.H - ty * kTile);
       const uint32_t row_bytes = (uint32_t)vw * sizeof(float4);
+      constexpr uint32_t kTgtRows = LOSS == PF_LOSS_RENDER ? 0u : 1u;  // (no target to stage)
       if (lane == 0) {
         hdr[g][buf] = make_int4(tile, b0, L, txy);
         mbar_arrive_tx(&full[g][buf], (uint32_t)nst * kEntBytes +
-                                          (uint32_t)vh * row_bytes * (has_bg ? 2u : 1u));
+                                          (uint32_t)vh * row_bytes * ((has_bg ? 1u : 0u) + kTgtRows));
       }
       __syncwarp();
       if (lane < nst) {
@@ -1211,7 +1222,7 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
       }
       if (lane < vh) {
         const size_t row = (size_t)(ty * kTile + lane) * a.W + (size_t)tx * kTile;
-        bulk_g2s(buf_tgt(buf) + lane * kTile, a.tgt4 + row, row_bytes, &full[g][buf]);
+        if (kTgtRows) bulk_g2s(buf_tgt(buf) + lane * kTile, a.tgt4 + row, row_bytes, &full[g][buf]);
         if (has_bg) bulk_g2s(buf_bg(buf) + lane * kTile, a.bg4 + row, row_bytes, &full[g][buf]);
       }
       buf = buf + 1 == kNBuf ? 0 : buf + 1;
@@ -1361,15 +1372,16 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
                            size_t scratch_bytes, int capacity, void* slots, int slot_m,
                            void* stream) {
   pf::NvtxRange nvtx_range("pf_fit_step");
-  if (W < 1 || H < 1 || n < 0 || !status || !tex || !apad || !tgt4 ||
-      !spill || !part || !grads || !counters || pad_texels < 0 || (pad_texels & 3))
+  const bool render = loss_kind == PF_LOSS_RENDER;  // forward only: no target / partials / grads
+  if (W < 1 || H < 1 || n < 0 || !status || !tex || !apad || (!render && (!tgt4 || !part || !grads)) ||
+      (render && !img4) || !spill || !counters || pad_texels < 0 || (pad_texels & 3))
     return PF_ERR_ARG;
   if (!slots && (!bin_off || !bin_idx)) return PF_ERR_ARG;
   if (slots && (slot_m < 1 || !tile_classes || !scratch || capacity < 0)) return PF_ERR_ARG;
   if (loss_kind != PF_LOSS_MSE && loss_kind != PF_LOSS_SPATIAL && loss_kind != PF_LOSS_COMBINED &&
-      loss_kind != PF_LOSS_EXTERN)
+      loss_kind != PF_LOSS_EXTERN && !render)
     return PF_ERR_ARG;
-  if (loss_kind == PF_LOSS_EXTERN && slots) return PF_ERR_ARG;  // (CSR lists only)
+  if ((loss_kind == PF_LOSS_EXTERN || render) && slots) return PF_ERR_ARG;  // (CSR lists only)
   const int ntx = div_up(W, kTile), nty = div_up(H, kTile);
   if (ty_begin < 0 || ty_end > nty || ty_begin > ty_end) return PF_ERR_ARG;
   const int n_tiles = (ty_end - ty_begin) * ntx;
@@ -1501,6 +1513,12 @@ extern "C" int pf_fit_step(const void* rec, int n, const double* tex, const floa
       PF_PICK4(PF_LOSS_EXTERN, 64, false)
     } else {
       PF_PICK4(PF_LOSS_EXTERN, 32, false)
+    }
+  } else if (render) {
+    if (ST == 64) {
+      PF_PICK4(PF_LOSS_RENDER, 64, false)
+    } else {
+      PF_PICK4(PF_LOSS_RENDER, 32, false)
     }
   } else if (loss_kind == PF_LOSS_COMBINED) {
     PF_PICK(PF_LOSS_COMBINED)

@@ -236,10 +236,51 @@ def test_autograd_function_matches_api(torch_cuda):
     loss = ((img - target) ** 2).mean()
     loss.backward()
     out, saved = raster.render_forward(sc, save=True)
-    np.testing.assert_allclose(img.detach().cpu().numpy(), out.color, rtol=0, atol=1e-7)
+    # (the forward runs the fit-step kernel in render mode: fp32 compositing,
+    # ~1e-7 relative; the north_star bar is 1e-5)
+    ok, err = fwd_close(img.detach().cpu().numpy(), out.color)
+    assert ok, err
+    ok, err = fwd_close(alpha.detach().cpu().numpy(), out.alpha)
+    assert ok, err
     dI = 2.0 * (out.color - d["target"]) / out.color.size
     g = grad.backward(sc, saved, dI)
     ok, err = grad_close(params.grad.cpu().numpy(), g.data)
+    assert ok, err
+
+
+@pytest.mark.parametrize("case", ["medium_n300", "saturated", "random_s3"])
+def test_autograd_render_mode_matches_k3(torch_cuda, monkeypatch, case):
+    """The Renderer's forward through the fit-step kernel (PF_LOSS_RENDER) against
+    the K3 forward (PF_RENDER_K3=1): image within the forward bar, gradients of the
+    following backward (which reuses the same lists) within the gradient bar of each other."""
+    torch = torch_cuda
+    from paper_2602_22625_b200.autograd import Renderer
+    from paper_2602_22625_b200.scene import param_matrix, structure_arrays
+    from conftest import load_case, scene_from
+
+    d = load_case(case)
+    sc = scene_from(d)
+    tid, z = structure_arrays(sc)
+    target = torch.tensor(d["target"], device="cuda", dtype=torch.float32)
+    out = []
+    for k3 in ("0", "1"):
+        monkeypatch.setenv("PF_RENDER_K3", k3)
+        r = Renderer(sc.templates, tid, z, sc.canvas_w, sc.canvas_h, background=sc.background,
+                     alpha_max=sc.alpha_max, mu_blend=sc.mu_blend)
+        assert r.render_k34 == (k3 == "0")
+        p = torch.tensor(param_matrix(sc), device="cuda", requires_grad=True)
+        for _ in range(2):  # twice: the pooled compositor's second use
+            p.grad = None
+            img, alpha = r(p)
+            (((img - target) ** 2).mean() + 0.5 * (alpha ** 2).mean()).backward()
+        out.append((img.detach().cpu().numpy(), alpha.detach().cpu().numpy(),
+                    p.grad.cpu().numpy()))
+    (i0, a0, g0), (i1, a1, g1) = out
+    ok, err = fwd_close(i0, i1)
+    assert ok, err
+    ok, err = fwd_close(a0, a1)
+    assert ok, err
+    ok, err = grad_close(g0, g1)
     assert ok, err
 
 
