@@ -248,8 +248,9 @@ def test_autograd_function_matches_api(torch_cuda):
     assert ok, err
 
 
-@pytest.mark.parametrize("case", ["medium_n300", "saturated", "random_s3"])
-def test_autograd_render_mode_matches_k3(torch_cuda, monkeypatch, case):
+@pytest.mark.parametrize("case,bg", [("medium_n300", False), ("saturated", False),
+                                     ("random_s3", False), ("random_s3", True)])
+def test_autograd_render_mode_matches_k3(torch_cuda, monkeypatch, case, bg):
     """The Renderer's forward through the fit-step kernel (PF_LOSS_RENDER) against
     the K3 forward (PF_RENDER_K3=1): image within the forward bar, gradients of the
     following backward (which reuses the same lists) within the gradient bar of each other."""
@@ -262,6 +263,9 @@ def test_autograd_render_mode_matches_k3(torch_cuda, monkeypatch, case):
     sc = scene_from(d)
     tid, z = structure_arrays(sc)
     target = torch.tensor(d["target"], device="cuda", dtype=torch.float32)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    bg_img = (torch.rand(sc.canvas_h, sc.canvas_w, 3, device="cuda", generator=g)
+              if bg else None)
     out = []
     for k3 in ("0", "1"):
         monkeypatch.setenv("PF_RENDER_K3", k3)
@@ -269,9 +273,12 @@ def test_autograd_render_mode_matches_k3(torch_cuda, monkeypatch, case):
                      alpha_max=sc.alpha_max, mu_blend=sc.mu_blend)
         assert r.render_k34 == (k3 == "0")
         p = torch.tensor(param_matrix(sc), device="cuda", requires_grad=True)
+        with torch.no_grad():  # forwards without a backward pass (classes left clean)
+            r(p, bg_img)
+            r(p, bg_img)
         for _ in range(2):  # twice: the pooled compositor's second use
             p.grad = None
-            img, alpha = r(p)
+            img, alpha = r(p, bg_img)
             (((img - target) ** 2).mean() + 0.5 * (alpha ** 2).mean()).backward()
         out.append((img.detach().cpu().numpy(), alpha.detach().cpu().numpy(),
                     p.grad.cpu().numpy()))
