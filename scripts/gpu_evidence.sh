@@ -1,9 +1,9 @@
 #!/bin/bash
 # Round evidence on one GPU: default bench line, ncu launch list of the same
 # command, ncu --set full captures (c3 fused step, c3 two-kernel path, c5 step),
-# kernel timelines, band scaling, sanitizer runs of the slot-binning step.
+# kernel timelines, band scaling, (no sanitizer: closed on this pool).
 set -u
-O=gpurun_out/ev6
+O=gpurun_out/ev7
 mkdir -p $O
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
 tail -1 $O/bench.json | cut -c1-300
@@ -27,15 +27,7 @@ for a in "c3" "c5" "c5 band=8:3" "c3 hostio"; do
 done > $O/timelines.txt
 timeout 900 python scripts/band_scaling.py c5 1 2 4 8 > $O/band_scaling.txt 2>&1; echo "band rc=$?"
 cp gpurun_out/band_scaling_c5.json $O/ 2>/dev/null
-mkdir -p gpurun_out/sanitize
-for case in c1 c3 c5band; do
-  for tool in memcheck racecheck; do
-    extra=""; [ "$tool" = "memcheck" ] && extra="--leak-check no"
-    timeout 900 compute-sanitizer --tool $tool $extra --print-limit 50 \
-      python scripts/sanitize_step.py $case 2 > $O/san_${case}_${tool}.log 2>&1
-    echo "$case $tool rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' $O/san_${case}_${tool}.log | tail -1)"
-  done
-done
+# (compute-sanitizer is closed on this pool: the r02f logs under profiles/ are the last runs)
 # summaries on the box (the reports are too large to bring back together)
 for r in prof_c3 prof_c3_2k prof_c5; do
   python scripts/ncu_extract.py $O/$r.ncu-rep $O/${r}_kernels.json > /dev/null 2>&1

@@ -356,7 +356,65 @@ def loop_cases():
     print("video", hists[0][-1].loss, hists[1][-1].loss)
 
 
+def hook_cases():
+    """run_loop's remaining contract, from the reference's own run: hooks that
+    rewrite the scene before an iteration's render (fit.py:436-439; test_fit.py's
+    test_run_loop_hook_rewrites_scene), frozen rows in the optimizer state, lr
+    gains and the decaying schedule, the combined loss (fit.py:163-170), then a
+    resumed run_loop on the same OptimState with an explicit iteration count and
+    the spatial loss (fit.py:128-151; test_run_loop_reuses_optimizer_state)."""
+    from dataclasses import replace as _rep
+
+    from paper_2602_22625_b200 import synth
+
+    tpls = [PrimitiveTemplate(t.rgba) for t in synth.prepare([synth.disc(32)])]
+    target = synth.smooth_target(64, 48, seed=11)
+    cfg = rconfig.FitConfig(num_iterations=6, num_primitives=40, seed=6, scale_min=2.0,
+                            scale_max=9.0, do_decay=True, decay_final_fraction=0.2,
+                            lr_gain_x=2.0, lr_gain_y=0.5, lr_gain_scale=3.0,
+                            lr_gain_rotation=0.7, lr_gain_opacity=1.3, lr_gain_color=0.8)
+    scene = rfit.init_scene(target, tpls, cfg, np.random.default_rng(6))
+    vec, layout = pack_params(scene)
+    st0 = rfit.OptimState.fresh(layout)
+    st0.frozen[[0, 5, 9]] = True
+    seen = []
+
+    def fade(s, state):  # iteration 2: every third primitive nearly transparent
+        seen.append(("fade", state.step))
+        return _rep(s, primitives=[_rep(p, opacity_logit=-6.0) if i % 3 == 0 else p
+                                   for i, p in enumerate(s.primitives)])
+
+    def shift(s, state):  # iteration 4: even primitives move right by 3 px
+        seen.append(("shift", state.step))
+        return _rep(s, primitives=[_rep(p, x=p.x + 3.0) if i % 2 == 0 else p
+                                   for i, p in enumerate(s.primitives)])
+
+    spec1 = rfit.LossSpec(kind="combined", target=target, mse_w=0.7, gray_l1_w=0.4)
+    s1, h1, st = rfit.run_loop(scene, cfg, spec1, np.random.default_rng(7), state=st0,
+                               hooks={2: fade, 4: shift})
+    p1 = pack_params(s1)[0].reshape(-1, 8)
+    ta = np.zeros((48, 64))
+    ta[6:40, 10:50] = 0.8
+    spec2 = rfit.LossSpec(kind="spatial_constrained", target=target, target_alpha=ta,
+                          alpha_w=0.5)
+    s2, h2, st = rfit.run_loop(s1, cfg, spec2, np.random.default_rng(8), iterations=4,
+                               state=st)
+    d = scene_arrays(scene)
+    d.update(target=target, target_alpha=ta, frozen=st0.frozen.copy(), params1=p1,
+             final_params=pack_params(s2)[0].reshape(-1, 8),
+             h1_loss=np.asarray([h.loss for h in h1]), h1_psnr=np.asarray([h.psnr for h in h1]),
+             h1_lr=np.asarray([h.lr for h in h1]),
+             h2_loss=np.asarray([h.loss for h in h2]), h2_lr=np.asarray([h.lr for h in h2]),
+             hook_steps=np.asarray([s for _, s in seen]), final_step=np.int64(st.step),
+             m=st.m, v=st.v, scale_min=2.0, scale_max=9.0)
+    np.savez_compressed(OUT / "run_loop_hook_resume.npz", **d)
+    print("hook/resume", seen, h1[-1].loss, h2[-1].loss, st.step)
+
+
 if __name__ == "__main__":
+    if "--hooks" in sys.argv:
+        hook_cases()
+        raise SystemExit(0)
     if "--loops" in sys.argv:
         loop_cases()
         raise SystemExit(0)

@@ -82,6 +82,41 @@ def test_gpu_backward_matches_reference(pf, case):
         assert np.abs(g2.data[:, 4]).max() > 0.0
 
 
+@pytest.mark.parametrize("case", ["gradcheck_s1", "gradcheck_s7"])
+def test_gpu_backward_matches_finite_differences(pf, case):
+    """The reference's finite-difference check (test_grad.py:33-46, steps of
+    grad.py:48-55, central differences, its tolerance 1e-5 abs or 1e-2 rel), run
+    entirely on the CUDA path: the backward's gradient of the MSE against central
+    differences of the GPU forward (eps_skip 0) on the reference's gradcheck
+    scenes (smooth templates)."""
+    raster, grad, _ = pf
+    from paper_2602_22625_b200.scene import pack_params, unpack_params
+
+    d = load_case(case)
+    sc = scene_from(d)
+    target = d["target"]
+    out, saved = raster.render_forward(sc, save=True, eps_skip=0.0)
+    dL = 2.0 * (np.asarray(out.color) - target) / target.size
+    g = grad.backward(sc, saved, dL).data
+    steps = (1e-2, 1e-2, 1e-2, 1e-3, 1e-3, 1e-3, 1e-3, 1e-3)
+    vec, layout = pack_params(sc)
+    fd = np.empty_like(vec)
+    for i in range(vec.size):
+        h = steps[i % 8]
+        lo = []
+        for sgn in (1.0, -1.0):
+            probe = vec.copy()
+            probe[i] = vec[i] + sgn * h
+            o, _ = raster.render_forward(unpack_params(probe, layout, sc), eps_skip=0.0)
+            lo.append(float(np.mean((np.asarray(o.color, dtype=np.float64) - target) ** 2)))
+        fd[i] = (lo[0] - lo[1]) / (2.0 * h)
+    fd = fd.reshape(-1, 8)
+    for i in range(sc.n):
+        for j in range(8):
+            a, n = g[i, j], fd[i, j]
+            assert abs(a - n) <= 1e-5 or abs(a - n) / max(abs(a), abs(n)) <= 1e-2, (i, j, a, n)
+
+
 def test_gpu_saturated_alpha_exact(pf):
     # test_grad.py:73-115: alpha == 1 exactly; no division by (1 - alpha)
     raster, grad, _ = pf
@@ -185,6 +220,62 @@ def test_gpu_run_loop_reinit(pf, case):
     got = pack_params(end)[0].reshape(-1, 8)
     np.testing.assert_allclose(got, d["final_params"], rtol=1e-4, atol=1e-5)
     assert st.step == int(d["iters"])
+
+
+def test_gpu_run_loop_hooks_and_resume(pf):
+    """run_loop's contract against the reference's own run (make_golden.py
+    --hooks): scene-rewriting hooks before iterations 2 and 4 (fit.py:436-439),
+    frozen rows in the passed OptimState, lr gains and the decaying schedule,
+    the combined loss; then a resumed run_loop on the same state with
+    iterations=4 and the spatial loss (test_fit.py:304-336 as goldens)."""
+    from dataclasses import replace as _rep
+
+    _, _, fit = pf
+    from paper_2602_22625_b200.scene import pack_params
+
+    d = load_case("run_loop_hook_resume")
+    sc = scene_from(d)
+    cfg = fit.FitConfig(num_iterations=6, num_primitives=sc.n, seed=6,
+                        scale_min=float(d["scale_min"]), scale_max=float(d["scale_max"]),
+                        do_decay=True, decay_final_fraction=0.2, lr_gain_x=2.0, lr_gain_y=0.5,
+                        lr_gain_scale=3.0, lr_gain_rotation=0.7, lr_gain_opacity=1.3,
+                        lr_gain_color=0.8)
+    st0 = fit.OptimState.fresh(pack_params(sc)[1])
+    st0.frozen[:] = d["frozen"]
+    seen = []
+
+    def fade(s, state):
+        seen.append(state.step)
+        return _rep(s, primitives=[_rep(p, opacity_logit=-6.0) if i % 3 == 0 else p
+                                   for i, p in enumerate(s.primitives)])
+
+    def shift(s, state):
+        seen.append(state.step)
+        return _rep(s, primitives=[_rep(p, x=p.x + 3.0) if i % 2 == 0 else p
+                                   for i, p in enumerate(s.primitives)])
+
+    spec1 = fit.LossSpec(kind="combined", target=d["target"], mse_w=0.7, gray_l1_w=0.4)
+    s1, h1, st = fit.run_loop(sc, cfg, spec1, np.random.default_rng(7), state=st0,
+                              hooks={2: fade, 4: shift})
+    assert seen == list(d["hook_steps"])
+    np.testing.assert_allclose([h.loss for h in h1], d["h1_loss"], rtol=1e-5)
+    np.testing.assert_allclose([h.psnr for h in h1], d["h1_psnr"], rtol=1e-6)
+    np.testing.assert_allclose([h.lr for h in h1], d["h1_lr"], rtol=0, atol=0)
+    p1 = pack_params(s1)[0].reshape(-1, 8)
+    np.testing.assert_allclose(p1, d["params1"], rtol=1e-4, atol=1e-5)
+    frozen = np.asarray(d["frozen"])
+    # frozen rows: Adam leaves them alone, only the hooks' edits apply (bit for bit)
+    assert np.array_equal(p1[frozen], np.asarray(d["params1"])[frozen])
+    spec2 = fit.LossSpec(kind="spatial_constrained", target=d["target"],
+                         target_alpha=d["target_alpha"], alpha_w=0.5)
+    s2, h2, st = fit.run_loop(s1, cfg, spec2, np.random.default_rng(8), iterations=4, state=st)
+    np.testing.assert_allclose([h.loss for h in h2], d["h2_loss"], rtol=1e-5)
+    np.testing.assert_allclose([h.lr for h in h2], d["h2_lr"], rtol=0, atol=0)
+    np.testing.assert_allclose(pack_params(s2)[0].reshape(-1, 8), d["final_params"],
+                               rtol=1e-4, atol=1e-5)
+    assert st.step == int(d["final_step"])
+    np.testing.assert_allclose(st.m, d["m"], rtol=1e-3, atol=1e-7)
+    np.testing.assert_allclose(st.v, d["v"], rtol=1e-3, atol=1e-9)
 
 
 def test_gpu_optimize_video_dropin(pf):
