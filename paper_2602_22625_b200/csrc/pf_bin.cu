@@ -87,6 +87,11 @@ struct PreArgs {
 };
 
 constexpr double kB1 = 0.9, kB2 = 0.999, kAdamEps = 1e-8;
+#ifndef PF_SCAT_BATCH
+#define PF_SCAT_BATCH 4
+#endif
+// slot-scatter atomics in flight per lane and round past the first two (A/B switch)
+constexpr int kScatB = PF_SCAT_BATCH;
 #ifndef PF_PRIM_THREADS
 #define PF_PRIM_THREADS 256
 #endif
@@ -438,16 +443,16 @@ __global__ void __launch_bounds__(kPrimThreads, kPrimMinBlocks) k_prim(PreArgs a
   if (ADAM && need) tl_mark(a.tl, 8, 2);  // (diagnostics: records stored)
   if (sc_t0 >= 0) sc_put(sc_t0, sc_p0);
   if (sc_t1 >= 0) sc_put(sc_t1, sc_p1);
-  for (int k0 = c + 2 * LPP; k0 < sc_nt; k0 += 4 * LPP) {
-    int t4[4], p4[4];
+  for (int k0 = c + 2 * LPP; k0 < sc_nt; k0 += kScatB * LPP) {
+    int t4[kScatB], p4[kScatB];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kScatB; ++q) {
       const int k = k0 + LPP * q;
       t4[q] = k < sc_nt ? sc_tile(k) : -1;
       if (t4[q] >= 0) p4[q] = atomicAdd(a.slots.cnt + t4[q], 1);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < kScatB; ++q)
       if (t4[q] >= 0) sc_put(t4[q], p4[q]);
   }
   if (ADAM && need) tl_mark(a.tl, 9, 2);  // (diagnostics: scatter done)
