@@ -28,9 +28,16 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .compositor import Compositor, bin_capacity, cached_atlas
+from .compositor import Compositor, _stream_handle, bin_capacity, cached_atlas
 from .errors import BinOverflow
 from .raster import DEFAULT_EPS_SKIP
+
+
+def _current_stream() -> torch.cuda.Stream:
+    # torch.cuda.current_stream() without its device-index resolution (~15 us of
+    # Python per call on the eager path)
+    sid, dev, dtype = torch._C._cuda_getCurrentStream(torch._C._cuda_getDevice())
+    return torch.cuda.Stream(stream_id=sid, device_index=dev, device_type=dtype)
 
 
 class _Composite(torch.autograd.Function):
@@ -91,7 +98,7 @@ class _Composite(torch.autograd.Function):
             nat.check(nat.load().pf_pack_grad4(
                 d_img.to(torch.float32).contiguous().data_ptr(),
                 nat.ptr(d_alpha.to(torch.float32).contiguous() if d_alpha is not None else None),
-                r.H * r.W, d4.data_ptr(), torch.cuda.current_stream().cuda_stream),
+                r.H * r.W, d4.data_ptr(), _stream_handle()),
                 "pf_pack_grad4")
         if r.mu_blend == 0.0:
             comp.fit_step(grads, None, eps_skip=r.eps_skip, bg_rgb=r.bg_rgb, bg4=ctx.bg4,
@@ -123,7 +130,7 @@ class _LossMSE(torch.autograd.Function):
             sc = _MSE_SCRATCH[img.device] = torch.zeros(2048, dtype=torch.float64,
                                                         device=img.device)
         loss = torch.empty((), dtype=torch.float32, device=img.device)
-        st = torch.cuda.current_stream().cuda_stream
+        st = _stream_handle()
         nat.check(nat.load().pf_mse4(img.data_ptr(), target.data_ptr(), P, sc.data_ptr(),
                                      loss.data_ptr(), st), "pf_mse4")
         ctx.save_for_backward(img, target)
@@ -137,7 +144,7 @@ class _LossMSE(torch.autograd.Function):
         out4._pf_grad4 = True  # (r, g, b, 0) rows: _Composite.backward takes them as is
         g = g.to(torch.float32).contiguous()
         nat.check(nat.load().pf_mse4_grad(img.data_ptr(), target.data_ptr(), H * W, g.data_ptr(),
-                                          out4.data_ptr(), torch.cuda.current_stream().cuda_stream),
+                                          out4.data_ptr(), _stream_handle()),
                   "pf_mse4_grad")
         return out4[:, :, :3], None
 
@@ -253,7 +260,7 @@ class Renderer:
         else:
             ev, st = torch.cuda.Event(), torch.empty(2, dtype=torch.int32, pin_memory=True)
         st.copy_(comp.status[:2], non_blocking=True)
-        ev.record()
+        ev.record(_current_stream())
         self._pending.append((ev, st, comp.capacity))
 
     def _raise_pending(self, wait: bool = False) -> None:
