@@ -411,7 +411,37 @@ def hook_cases():
     print("hook/resume", seen, h1[-1].loss, h2[-1].loss, st.step)
 
 
+def acceptance_cases():
+    """The reference's acceptance criteria on this path (test_acceptance.py):
+    01 -- run_gradcheck(20) (grad.py:378-420): the 20 gradcheck scenes with the
+    reference's central finite differences through render_naive; 02 -- the 50
+    random scenes (n = 4..200 on 128x128) of the tiled-vs-naive forward check
+    (scenes only: the GPU test checks them against the pinned oracle)."""
+    d = {}
+    for seed in range(20):
+        scene, target = rgrad.gradcheck_scene(seed)
+
+        def loss_fn(o, target=target):
+            return float(np.mean((o.color - target) ** 2))
+
+        fd = rgrad.finite_diff_grad(scene, loss_fn)
+        for k, v in scene_arrays(scene).items():
+            d[f"g{seed}_{k}"] = v
+        d[f"g{seed}_target"] = target
+        d[f"g{seed}_fd"] = fd.data
+    for seed in range(50):
+        n = 4 + (196 * seed) // 49
+        scene = random_scene(seed, n=n, w=128, h=128)
+        for k, v in scene_arrays(scene).items():
+            d[f"r{seed}_{k}"] = v
+    np.savez_compressed(OUT / "acceptance.npz", **d)
+    print("acceptance", len(d))
+
+
 if __name__ == "__main__":
+    if "--acceptance" in sys.argv:
+        acceptance_cases()
+        raise SystemExit(0)
     if "--hooks" in sys.argv:
         hook_cases()
         raise SystemExit(0)

@@ -1,0 +1,166 @@
+"""The reference's acceptance criteria that cover this path, on the CUDA path.
+
+test_acceptance.py (reference):
+  01  run_gradcheck(20): analytic gradients vs central finite differences on the
+      20 gradcheck scenes, a scalar passing when rel <= 1e-2 (relative to the
+      finite difference) or abs <= 1e-5 (grad.py:378-420).  Here: the GPU
+      backward against the reference's own finite differences (golden).
+  02  tiled forward vs the sequential reference on 50 random scenes (n = 4..200,
+      128x128), worst |diff| <= 1e-6 at eps_skip = 0.  Here: the GPU forward
+      against the pinned oracle (itself within 1e-13 of the reference).
+  04  compositing invariants: coverage identity (alpha + prod(1 - a_i) = 1),
+      an opaque front primitive occludes everything behind it exactly, and
+      raising any opacity never lowers coverage.
+Scenes: tests/golden/acceptance.npz (make_golden.py --acceptance).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+from conftest import load_case, scene_from
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pf():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_22625_b200 import grad, raster
+
+    return raster, grad
+
+
+@pytest.fixture(scope="module")
+def acc():
+    return load_case("acceptance")
+
+
+def _sub(d, prefix: str) -> dict:
+    return {k[len(prefix):]: d[k] for k in d if k.startswith(prefix)}
+
+
+def test_criterion_01_gradcheck_20_scenes(pf, acc):
+    raster, grad = pf
+    n_checked = n_fail = 0
+    worst = 0.0
+    for seed in range(20):
+        d = _sub(acc, f"g{seed}_")
+        sc = scene_from(d)
+        target = d["target"]
+        out, saved = raster.render_forward(sc, save=True, eps_skip=0.0)
+        dL = 2.0 * (np.asarray(out.color, dtype=np.float64) - target) / target.size
+        g = grad.backward(sc, saved, dL).data
+        fd = d["fd"]
+        adiff = np.abs(g - fd)
+        rel = adiff / np.maximum(np.abs(fd), 1e-300)
+        ok = (rel <= 1e-2) | (adiff <= 1e-5)
+        n_checked += ok.size
+        n_fail += int((~ok).sum())
+        over = rel[adiff > 1e-5]
+        if over.size:
+            worst = max(worst, float(over.max()))
+    assert n_checked > 0 and n_fail == 0, f"{n_fail}/{n_checked} failures, worst rel {worst:.2e}"
+
+
+def test_criterion_02_forward_50_scenes(pf, acc, oracle):
+    raster, _ = pf
+    worst = 0.0
+    for seed in range(50):
+        sc = scene_from(_sub(acc, f"r{seed}_"))
+        assert sc.n == 4 + (196 * seed) // 49
+        pk = oracle.Packed(sc)
+        off, idx = oracle.bin_tiles(pk, 32, 2.0)
+        img, alpha, _ = oracle.render_forward(pk, off, idx, 32, oracle.background(sc), False,
+                                              0.0)
+        out, _ = raster.render_forward(sc, eps_skip=0.0)
+        worst = max(worst, float(np.abs(np.asarray(out.color) - img).max()),
+                    float(np.abs(np.asarray(out.alpha) - alpha).max()))
+    assert worst <= 1e-6, f"worst |diff| {worst:.2e}"
+
+
+def _soft_disk(size: int = 15) -> np.ndarray:
+    # the reference test fixture (tests/conftest.py:25-36)
+    yy, xx = np.mgrid[0:size, 0:size].astype(np.float64)
+    c = (size - 1) / 2
+    r = np.hypot(yy - c, xx - c) / c
+    rgba = np.zeros((size, size, 4))
+    rgba[:, :, 0], rgba[:, :, 1], rgba[:, :, 2] = 0.9, 0.5, 0.3
+    rgba[:, :, 3] = np.clip(1.0 - r**2, 0.0, 1.0) ** 2
+    return rgba
+
+
+def _alpha_plane(sc, i: int, W: int, H: int) -> np.ndarray:
+    """a_i at every pixel centre: raster.py canvas_to_prim / prim_to_texel /
+    sample_bilinear / primitive_alpha in numpy float64 (no eps skip)."""
+    p = sc.primitives[i]
+    rgba = np.asarray(sc.templates[p.template_id].rgba)
+    ht, wt = rgba.shape[:2]
+    yy, xx = np.mgrid[0:H, 0:W].astype(np.float64)
+    dx, dy = xx - p.x, yy - p.y
+    c, s = math.cos(p.rotation), math.sin(p.rotation)
+    u = (c * dx + s * dy) / p.scale
+    v = (-s * dx + c * dy) / p.scale
+    U = (u + 1.0) * 0.5 * (wt - 1)
+    V = (v + 1.0) * 0.5 * (ht - 1)
+    inside = (U >= 0) & (U <= wt - 1) & (V >= 0) & (V <= ht - 1)
+    pad = np.zeros((ht + 1, wt + 1))
+    pad[:ht, :wt] = rgba[:, :, 3]
+    u0 = np.clip(np.floor(U), 0, wt - 1).astype(int)
+    v0 = np.clip(np.floor(V), 0, ht - 1).astype(int)
+    wu, wv = U - u0, V - v0
+    m = ((1 - wu) * (1 - wv) * pad[v0, u0] + wu * (1 - wv) * pad[v0, u0 + 1]
+         + (1 - wu) * wv * pad[v0 + 1, u0] + wu * wv * pad[v0 + 1, u0 + 1])
+    sig = 1.0 / (1.0 + math.exp(-p.opacity_logit))
+    return np.where(inside, sc.alpha_max * sig * m, 0.0)
+
+
+def test_criterion_04_compositing_invariants(pf):
+    raster, _ = pf
+    from paper_2602_22625_b200.scene import PrimitiveParams, PrimitiveTemplate, Scene
+
+    tpl_soft = PrimitiveTemplate(_soft_disk(15))
+    ones = np.ones((9, 9, 4))
+    ones[:, :, 0], ones[:, :, 1], ones[:, :, 2] = 0.8, 0.2, 0.1
+    tpl_hard = PrimitiveTemplate(ones)
+
+    def prim(x, y, s, nu, z, tid=0):
+        return PrimitiveParams(x=x, y=y, scale=s, rotation=0.4 * z, opacity_logit=nu,
+                               color_logits=(0.5, -0.2, 0.1), template_id=tid, z=z)
+
+    # coverage identity: alpha and the residual transmittance sum to 1 (the GPU
+    # stores float32: 1e-6 instead of the reference's float64 1e-12)
+    sc = Scene([prim(9.0, 11.0, 5.0, 0.8, 0), prim(14.0, 12.0, 6.0, -0.5, 1),
+                prim(20.0, 9.0, 4.0, 2.0, 2)], [tpl_soft], 28, 24,
+               background=(0.3, 0.6, 0.9), alpha_max=0.9)
+    out, _ = raster.render_forward(sc, eps_skip=0.0)
+    T = np.ones((24, 28))
+    for i in range(sc.n):
+        T *= 1.0 - _alpha_plane(sc, i, 28, 24)
+    assert float(np.abs(np.asarray(out.alpha) + T - 1.0).max()) <= 1e-6
+    # opaque front: the pixels it saturates are untouched by anything behind
+    front, back = prim(10.0, 10.0, 4.0, 50.0, 0), prim(11.0, 10.0, 5.0, 1.0, 1)
+    pair = Scene([front, back], [tpl_hard], 24, 20, background=(0.1, 0.1, 0.1))
+    alone = replace(pair, primitives=[front])
+    out_pair, _ = raster.render_forward(pair, eps_skip=0.0)
+    out_alone, _ = raster.render_forward(alone, eps_skip=0.0)
+    sat = _alpha_plane(pair, 0, 24, 20) == 1.0
+    assert sat.sum() > 20
+    assert np.array_equal(np.asarray(out_pair.color)[sat], np.asarray(out_alone.color)[sat])
+    assert np.all(np.asarray(out_pair.alpha)[sat] == 1.0)
+    # coverage only rises as any opacity rises
+    a0 = np.asarray(out.alpha)
+    for k in range(sc.n):
+        prims = list(sc.primitives)
+        prims[k] = replace(prims[k], opacity_logit=prims[k].opacity_logit + 2.0)
+        bumped, _ = raster.render_forward(replace(sc, primitives=prims), eps_skip=0.0)
+        b = np.asarray(bumped.alpha)
+        assert np.all(b >= a0 - 1e-7)
+        assert b.max() > a0.max() - 1e-7

@@ -135,3 +135,23 @@ def test_oracle_video_heuristics_match_reference(oracle):
     np.testing.assert_allclose(nu, d["stuck_params"][:, 4], rtol=0, atol=1e-15)
     _, dec0 = oracle.remove_stuck(pk, d["z"], None, (3, 4), 2, 0.02, 0.3, 0.3, 0.5)
     assert dec0 == list(d["stuck_decayed_nofrozen"])
+
+
+def test_oracle_gradcheck_criterion_01(oracle):
+    """Acceptance criterion 01 (test_acceptance.py:63-72, grad.py:378-420) for the
+    checker itself: the oracle's backward against the reference's own central
+    finite differences on the 20 gradcheck scenes, its gate (rel 1e-2 or abs 1e-5)."""
+    acc = load_case("acceptance")
+    fails = checked = 0
+    for seed in range(20):
+        d = {k[len(f"g{seed}_"):]: acc[k] for k in acc if k.startswith(f"g{seed}_")}
+        sc = scene_from(d)
+        pk = oracle.Packed(sc)
+        off, idx = oracle.bin_tiles(pk, 32, 2.0)
+        img, _, sv = oracle.render_forward(pk, off, idx, 32, oracle.background(sc), True, 0.0)
+        g = oracle.backward(pk, sv, 2.0 * (img - d["target"]) / d["target"].size, None)
+        adiff = np.abs(g - d["fd"])
+        ok = (adiff / np.maximum(np.abs(d["fd"]), 1e-300) <= 1e-2) | (adiff <= 1e-5)
+        checked += ok.size
+        fails += int((~ok).sum())
+    assert checked > 0 and fails == 0, f"{fails}/{checked}"
