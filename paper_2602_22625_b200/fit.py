@@ -834,3 +834,33 @@ def run_loop(scene, cfg, loss_spec: LossSpec, rng: np.random.Generator,
             for h in history:
                 w.writerow([h.iteration, repr(h.loss), str(h.psnr), repr(h.lr), h.reinit_count])
     return unpack_params(eng.params_host(), layout, scene), history, state
+
+
+def loss_spec_from_config(cfg, target: FloatArray, target_alpha: FloatArray | None) -> LossSpec:
+    """The config's loss (fit.py:344-355): ``loss`` "spatial" is the spatial
+    constraint, weights from mse_weight / gray_l1_weight / alpha_loss_weight."""
+    kind = {"spatial": "spatial_constrained"}.get(cfg.loss, cfg.loss)
+    return LossSpec(kind=kind, target=target, target_alpha=target_alpha, mse_w=cfg.mse_weight,
+                    gray_l1_w=cfg.gray_l1_weight, alpha_w=cfg.alpha_loss_weight)
+
+
+def optimize(target, templates, cfg, target_alpha=None, log_path=None, dump_dir=None):
+    """Fit a fresh scene to one image (fit.py:524-555): the config's rng seed,
+    prepare_templates (blur / falloff) on the given or default templates,
+    init_scene, the config's loss, the target's local variance map for reinit,
+    then the GPU run_loop.  Returns (scene, history)."""
+    from .prep import default_templates, init_scene, local_variance_map, prepare_templates
+
+    target = np.asarray(target, dtype=np.float64)
+    if target.ndim != 3 or target.shape[2] != 3:
+        raise ShapeMismatch(f"target shape {target.shape} is not (H, W, 3)")
+    rng = np.random.default_rng(cfg.seed)
+    tpls = prepare_templates(list(templates) if templates else default_templates(),
+                             blur_sigma=cfg.blur_sigma, do_blur=cfg.do_gaussian_blur,
+                             falloff=cfg.radial_falloff)
+    scene = init_scene(target, tpls, cfg, rng)
+    spec = loss_spec_from_config(cfg, target, target_alpha)
+    nlv = local_variance_map(target, cfg.variance_window_size)
+    scene, history, _ = run_loop(scene, cfg, spec, rng, nlv=nlv, log_path=log_path,
+                                 dump_dir=dump_dir)
+    return scene, history

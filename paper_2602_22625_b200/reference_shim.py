@@ -6,17 +6,19 @@ defining module misses them.  ``enable()`` rebinds every module-level name a
 §8(b) caller resolves at call time:
 
   defining modules   raster.bin_tiles / render_forward (raster.py:227, 290),
-                     grad.backward (grad.py:134), fit.adam_step / run_loop
-                     (fit.py:195, 403), dyn.diff_mask / freeze_flags /
+                     grad.backward (grad.py:134), fit.adam_step / run_loop /
+                     optimize (fit.py:195, 403, 524), dyn.diff_mask / freeze_flags /
                      remove_stuck / optimize_video (dyn.py:86-238),
                      exportio.export_layers (exportio.py:345)
   by-name importers  fit.{bin_tiles, render_forward, backward} (fit.py:28, 38),
                      dyn.run_loop (dyn.py:22-29),
-                     cli.{render_forward, backward, export_layers, optimize_video}
+                     cli.{render_forward, backward, export_layers, optimize_video,
+                     optimize}
                      (cli.py:20-33: run_bench 180-230, _cmd_render 64-70,
                      _final_composite 249-260),
                      exportio.render_forward (exportio.py:54-62, the composite),
-                     estimator.{render_forward, optimize_video} (estimator.py:19-22)
+                     estimator.{render_forward, optimize_video, optimize}
+                     (estimator.py:19-22)
   package surface    primfit.<name> re-exports (__init__.py:32-100)
 
 ``run_gradcheck`` (grad.py:396-398) imports raster.render_forward inside the
@@ -47,6 +49,7 @@ REBINDS: dict[tuple[str, str], object] = {
     ("grad", "backward"): _grad.backward,
     ("fit", "adam_step"): _fit.adam_step,
     ("fit", "run_loop"): _fit.run_loop,
+    ("fit", "optimize"): _fit.optimize,
     ("fit", "bin_tiles"): _raster.bin_tiles,
     ("fit", "render_forward"): _raster.render_forward,
     ("fit", "backward"): _grad.backward,
@@ -61,11 +64,13 @@ REBINDS: dict[tuple[str, str], object] = {
     ("cli", "backward"): _grad.backward,
     ("cli", "export_layers"): _export.export_layers,
     ("cli", "optimize_video"): _video.optimize_video,
+    ("cli", "optimize"): _fit.optimize,
     ("estimator", "render_forward"): _raster.render_forward,
     ("estimator", "optimize_video"): _video.optimize_video,
+    ("estimator", "optimize"): _fit.optimize,
 }
 # names the package re-exports at its top level
-PACKAGE_NAMES = ("bin_tiles", "render_forward", "backward", "adam_step", "run_loop",
+PACKAGE_NAMES = ("bin_tiles", "render_forward", "backward", "adam_step", "run_loop", "optimize",
                  "diff_mask", "freeze_flags", "remove_stuck", "optimize_video", "export_layers")
 
 _saved: dict[tuple[str, str], object] = {}

@@ -410,6 +410,30 @@ def hook_cases():
     np.savez_compressed(OUT / "run_loop_hook_resume.npz", **d)
     print("hook/resume", seen, h1[-1].loss, h2[-1].loss, st.step)
 
+    # optimize (fit.py:524-555): seed -> prepare_templates -> init_scene -> config
+    # loss -> run_loop, on the acceptance suite's hard disk (make_assets.py:70-79)
+    size = 25
+    yy, xx = np.mgrid[0:size, 0:size].astype(np.float64)
+    c = (size - 1) / 2
+    disk = np.zeros((size, size, 4))
+    disk[:, :, :3] = 1.0
+    disk[:, :, 3] = (np.hypot(yy - c, xx - c) <= c - 1.0).astype(np.float64)
+    target = synth.smooth_target(64, 48, seed=12)
+    ta = np.zeros((48, 64))
+    ta[8:40, 12:52] = 1.0
+    cfg = rconfig.FitConfig(num_primitives=40, num_iterations=8, seed=2, loss="spatial",
+                            alpha_loss_weight=0.3, do_reinit=True, reinit_period=3,
+                            reinit_warmup=2)
+    sc, hist = rfit.optimize(target, [PrimitiveTemplate(disk)], cfg, target_alpha=ta)
+    np.savez_compressed(OUT / "optimize_small.npz", target=target, target_alpha=ta, disk=disk,
+                        final_params=pack_params(sc)[0].reshape(-1, 8),
+                        tid=np.asarray([p.template_id for p in sc.primitives]),
+                        z=np.asarray([p.z for p in sc.primitives]),
+                        hist_loss=np.asarray([h.loss for h in hist]),
+                        hist_psnr=np.asarray([h.psnr for h in hist]),
+                        hist_reinit=np.asarray([h.reinit_count for h in hist]))
+    print("optimize", hist[0].loss, hist[-1].loss, [h.reinit_count for h in hist])
+
 
 def acceptance_cases():
     """The reference's acceptance criteria on this path (test_acceptance.py):

@@ -164,3 +164,106 @@ def test_criterion_04_compositing_invariants(pf):
         b = np.asarray(bumped.alpha)
         assert np.all(b >= a0 - 1e-7)
         assert b.max() > a0.max() - 1e-7
+
+
+def _hard_disk(size: int = 25) -> np.ndarray:
+    # the acceptance suite's template (scripts/make_assets.py:70-79)
+    yy, xx = np.mgrid[0:size, 0:size].astype(np.float64)
+    c = (size - 1) / 2
+    rgba = np.zeros((size, size, 4))
+    rgba[:, :, :3] = 1.0
+    rgba[:, :, 3] = (np.hypot(yy - c, xx - c) <= c - 1.0).astype(np.float64)
+    return rgba
+
+
+def test_optimize_matches_reference(pf):
+    """fit.optimize (fit.py:524-555) against the reference's own run: seeded
+    template preparation, init_scene, the config's spatial loss and reinit
+    boundaries, then the GPU run_loop (make_golden.py --hooks)."""
+    from paper_2602_22625_b200 import fit
+    from paper_2602_22625_b200.scene import PrimitiveTemplate, pack_params
+
+    d = load_case("optimize_small")
+    assert np.array_equal(d["disk"], _hard_disk())
+    cfg = fit.FitConfig(num_primitives=40, num_iterations=8, seed=2, loss="spatial",
+                        alpha_loss_weight=0.3, do_reinit=True, reinit_period=3, reinit_warmup=2)
+    sc, hist = fit.optimize(d["target"], [PrimitiveTemplate(_hard_disk())], cfg,
+                            target_alpha=d["target_alpha"])
+    assert [h.reinit_count for h in hist] == list(d["hist_reinit"])
+    np.testing.assert_allclose([h.loss for h in hist], d["hist_loss"], rtol=1e-5)
+    np.testing.assert_allclose([h.psnr for h in hist], d["hist_psnr"], rtol=1e-6)
+    np.testing.assert_array_equal([p.template_id for p in sc.primitives], d["tid"])
+    np.testing.assert_allclose(pack_params(sc)[0].reshape(-1, 8), d["final_params"],
+                               rtol=1e-4, atol=1e-5)
+
+
+def _gaussian_smooth(rng_seed: int, sigma: float, size: int = 128) -> np.ndarray:
+    from scipy.ndimage import gaussian_filter
+
+    tex = gaussian_filter(np.random.default_rng(rng_seed).random((size, size, 3)),
+                          sigma=(sigma, sigma, 0))
+    return (tex - tex.min()) / (tex.max() - tex.min())
+
+
+def test_criterion_06_noisy_background_forces_coverage(pf):
+    """test_acceptance.py:229-252 through fit.optimize on the GPU: fitting
+    against a noise background raises the coverage of a white target region by
+    >= 0.2 over fitting against white."""
+    raster, _ = pf
+    from paper_2602_22625_b200 import fit
+    from paper_2602_22625_b200.scene import PrimitiveTemplate
+
+    target = np.clip(0.2 + 0.6 * _gaussian_smooth(77, 3.0), 0.0, 1.0)
+    target[36:92, 36:92] = 1.0
+    region = np.zeros((128, 128), dtype=bool)
+    region[36:92, 36:92] = True
+
+    def coverage(bg):
+        cfg = fit.FitConfig(num_primitives=250, num_iterations=100, bg_color=bg, seed=0,
+                            compute_psnr=False)
+        scene, _ = fit.optimize(target, [PrimitiveTemplate(_hard_disk())], cfg)
+        out, _ = raster.render_forward(scene, raster.bin_tiles(scene),
+                                       background=(1.0, 1.0, 1.0))
+        return float(np.asarray(out.alpha)[region].mean())
+
+    solid, noisy = coverage("white"), coverage("noise")
+    assert noisy - solid >= 0.2, (solid, noisy)
+
+
+def test_criterion_07_spatial_constraint_confines_opacity(pf):
+    """test_acceptance.py:255-313 through fit.optimize on the GPU: with the
+    spatial loss, primitives entirely outside the mask end at mean opacity < 0.1
+    and the in-mask PSNR stays within 1 dB of the plain MSE fit."""
+    raster, _ = pf
+    from paper_2602_22625_b200 import fit
+    from paper_2602_22625_b200.scene import PrimitiveTemplate
+
+    target = np.clip(0.15 + 0.8 * _gaussian_smooth(55, 2.5), 0.0, 1.0)
+    yy, xx = np.mgrid[0:128, 0:128]
+    mask = (((yy - 64.0) ** 2 + (xx - 64.0) ** 2) <= 48.0**2).astype(np.float64)
+    inside = mask > 0
+
+    def run(kind):
+        cfg = fit.FitConfig(num_primitives=250, num_iterations=150, loss=kind,
+                            alpha_loss_weight=0.3, do_reinit=True, reinit_period=30,
+                            reinit_warmup=59, seed=0, compute_psnr=False)
+        scene, _ = fit.optimize(target, [PrimitiveTemplate(_hard_disk())], cfg,
+                                target_alpha=mask if kind == "spatial" else None)
+        out, _ = raster.render_forward(scene, raster.bin_tiles(scene),
+                                       background=(1.0, 1.0, 1.0))
+        return scene, np.asarray(out.color, dtype=np.float64)
+
+    sc_sp, col_sp = run("spatial")
+    _, col_ms = run("mse")
+    outside = []
+    for p in sc_sp.primitives:
+        r = p.scale * math.hypot(1.0, 1.0)  # bbox_half_side(scale) (raster.py:222-224)
+        x0, x1 = max(math.ceil(p.x - r), 0), min(math.floor(p.x + r), 127)
+        y0, y1 = max(math.ceil(p.y - r), 0), min(math.floor(p.y + r), 127)
+        if x0 > x1 or y0 > y1 or not inside[y0:y1 + 1, x0:x1 + 1].any():
+            outside.append(1.0 / (1.0 + math.exp(-p.opacity_logit)))
+    mean_outside = float(np.mean(outside)) if outside else 0.0
+    psnr_sp = 10 * math.log10(1.0 / float(np.mean((col_sp[inside] - target[inside]) ** 2)))
+    psnr_ms = 10 * math.log10(1.0 / float(np.mean((col_ms[inside] - target[inside]) ** 2)))
+    assert mean_outside < 0.1, (len(outside), mean_outside)
+    assert psnr_sp >= psnr_ms - 1.0, (psnr_sp, psnr_ms)
