@@ -11,6 +11,8 @@ test_acceptance.py (reference):
   04  compositing invariants: coverage identity (alpha + prod(1 - a_i) = 1),
       an opaque front primitive occludes everything behind it exactly, and
       raising any opacity never lowers coverage.
+  06, 07, 08a, 08b  behaviour of the fit loop, the spatial loss and the video
+      heuristics, through fit.optimize / video.optimize_video / run_loop hooks.
 Scenes: tests/golden/acceptance.npz (make_golden.py --acceptance).
 """
 
@@ -267,3 +269,105 @@ def test_criterion_07_spatial_constraint_confines_opacity(pf):
     psnr_ms = 10 * math.log10(1.0 / float(np.mean((col_ms[inside] - target[inside]) ** 2)))
     assert mean_outside < 0.1, (len(outside), mean_outside)
     assert psnr_sp >= psnr_ms - 1.0, (psnr_sp, psnr_ms)
+
+
+def _square_video():
+    # test_acceptance.py:_square_video: a red square sliding over a static backdrop
+    from scipy.ndimage import gaussian_filter
+
+    rng = np.random.default_rng(99)
+    backdrop = np.full((64, 64, 3), 0.55)
+    band = gaussian_filter(rng.random((24, 64, 3)), sigma=(2, 2, 0))
+    backdrop[40:64] = 0.15 + 0.7 * (band - band.min()) / (band.max() - band.min())
+    frames = []
+    for t in range(8):
+        f = backdrop.copy()
+        x0 = 6 + 6 * t
+        f[8:18, x0:x0 + 10] = (0.95, 0.3, 0.2)
+        frames.append(np.clip(f, 0.0, 1.0))
+    return frames
+
+
+def test_criterion_08a_freezing_keeps_static_primitives_bit_identical(pf):
+    """test_acceptance.py:316-350 through video.optimize_video on the GPU: every
+    primitive frozen for a transition is bit-identical across it, unfrozen ones
+    move, and some primitives stay frozen (and identical) end to end."""
+    from paper_2602_22625_b200 import fit, video
+    from paper_2602_22625_b200.scene import PrimitiveTemplate
+
+    frames = _square_video()
+    cfg = fit.FitConfig(num_primitives=120, num_iterations=80, sequential_iterations=40,
+                        scale_min=1.5, scale_max=4.0, freeze_static=True, seed=3,
+                        compute_psnr=False)
+    scenes, _ = video.optimize_video(frames, [PrimitiveTemplate(_hard_disk())], cfg)
+    pad = fit.effective_padding(cfg)
+    min_frozen, changed_counts, always = cfg.num_primitives, [], None
+    for t in range(1, 8):
+        mask = video.diff_mask(frames[t - 1], frames[t], cfg.diff_threshold)
+        flags = video.freeze_flags(scenes[t - 1], mask, pad)
+        min_frozen = min(min_frozen, int(flags.sum()))
+        changed = 0
+        for i, flag in enumerate(flags):
+            same = scenes[t].primitives[i] == scenes[t - 1].primitives[i]
+            if flag:
+                assert same, (t, i)
+            elif not same:
+                changed += 1
+        changed_counts.append(changed)
+        held = set(np.nonzero(flags)[0].tolist())
+        always = held if always is None else (always & held)
+    assert min_frozen > 0 and min(changed_counts) > 0 and len(always) > 0
+    assert all(scenes[7].primitives[i] == scenes[0].primitives[i] for i in always)
+
+
+def test_criterion_08b_stuck_decay_lowers_video_error(pf):
+    """test_acceptance.py:353-406 on the GPU run_loop with video.remove_stuck as
+    hooks: decaying the dominant (stuck) primitive strictly lowers the error."""
+    raster, _ = pf
+    from paper_2602_22625_b200 import fit, video
+    from paper_2602_22625_b200.scene import (PrimitiveParams, PrimitiveTemplate, Scene,
+                                             pack_params)
+
+    c1, c2 = (0.95, 0.90, 0.10), (0.05, 0.10, 0.20)
+    mean = tuple((a + b) / 2 for a, b in zip(c1, c2))
+
+    def logit(c):
+        return tuple(float(math.log(v / (1 - v))) for v in c)
+
+    target = np.ones((64, 64, 3))
+    for cy in range(4):
+        for cx in range(4):
+            target[32 + cy * 4:36 + cy * 4, 32 + cx * 4:36 + cx * 4] = \
+                c1 if (cy + cx) % 2 == 0 else c2
+
+    def build():
+        prims = [PrimitiveParams(x=39.5, y=39.5, scale=13.0, rotation=0.0, opacity_logit=2.5,
+                                 color_logits=logit(mean), template_id=0, z=0)]
+        z = 1
+        for cy in range(4):
+            for cx in range(4):
+                prims.append(PrimitiveParams(
+                    x=32 + cx * 4 + 1.5, y=32 + cy * 4 + 1.5, scale=2.8, rotation=0.0,
+                    opacity_logit=-4.0, color_logits=logit(c1 if (cy + cx) % 2 == 0 else c2),
+                    template_id=0, z=z))
+                z += 1
+        return Scene(prims, [PrimitiveTemplate(_hard_disk())], 64, 64,
+                     background=(1.0, 1.0, 1.0))
+
+    triggers = (10, 25, 40)
+    policy = video.StuckPolicy(triggers=triggers)
+
+    def final_mse(with_decay):
+        scene = build()
+        cfg = fit.FitConfig(num_iterations=80, eps_skip=0.0, compute_psnr=False)
+        spec = fit.LossSpec(kind="mse", target=target)
+        state = fit.OptimState.fresh(pack_params(scene)[1])
+        hooks = ({t: (lambda s, st: video.remove_stuck(s, st.frozen, policy)[0])
+                  for t in triggers} if with_decay else None)
+        out_scene, _, _ = fit.run_loop(scene, cfg, spec, np.random.default_rng(0),
+                                       iterations=80, state=state, hooks=hooks)
+        out, _ = raster.render_forward(out_scene, raster.bin_tiles(out_scene))
+        return float(np.mean((np.asarray(out.color, dtype=np.float64) - target) ** 2))
+
+    off, on = final_mse(False), final_mse(True)
+    assert on < off, (off, on)
