@@ -231,3 +231,57 @@ def test_video_frames_sharded_across_ranks(torch_cuda, tmp_path):
         for j, i in enumerate(chunk):
             _adam_bar(runs[0]["params"][i].reshape(-1, 8), pack_params(sc[j])[0].reshape(-1, 8),
                       cfg, 14)
+
+
+def _nccl_rank_main(rank, world, name, steps, out_dir):
+    sys.path.insert(0, str(ROOT))
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", 0))
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.dist import make_allreduce, row_bands
+    from paper_2602_22625_b200.fit import StepEngine
+
+    w = synth.make_workload(name)
+    w.cfg.num_iterations = steps
+    nty = -(-w.scene.canvas_h // 16)
+    eng = StepEngine(w.scene, w.cfg, w.loss, steps, band=row_bands(nty, world)[rank],
+                     allreduce=make_allreduce(), use_graph=True)
+    for _ in range(steps):
+        eng.step()
+    torch.cuda.synchronize()
+    eng.check()
+    np.savez(os.path.join(out_dir, f"nccl{rank}.npz"), params=eng.params_host(),
+             loss=np.array([h.loss for h in eng.history()]), graph=np.bool_(eng.graph is not None))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_nccl_allreduce_in_step_graph(torch_cuda, tmp_path):
+    """The multi-GPU step's exact code path on hardware with the one GPU there
+    is: an NCCL process group (world 1: NCCL refuses two ranks on one device),
+    the gradient + loss allreduce captured inside the step's CUDA graph between
+    the fit-step kernel and the Adam + records launch.  A one-rank sum is the
+    identity, so the run equals the engine without an allreduce (under the
+    Adam-noise bar of the float64 gradient atomics' order)."""
+    import torch.multiprocessing as mp
+
+    from paper_2602_22625_b200 import synth
+    from paper_2602_22625_b200.fit import StepEngine
+
+    os.environ["MASTER_PORT"] = str(29700 + (os.getpid() % 1000))
+    mp.spawn(_nccl_rank_main, args=(1, "c3", STEPS, str(tmp_path)), nprocs=1, join=True)
+    r = dict(np.load(tmp_path / "nccl0.npz"))
+    assert bool(r["graph"])
+    w = synth.make_workload("c3")
+    w.cfg.num_iterations = STEPS
+    eng = StepEngine(w.scene, w.cfg, w.loss, STEPS, use_graph=True)
+    for _ in range(STEPS):
+        eng.step()
+    eng.check()
+    np.testing.assert_allclose(r["loss"], [h.loss for h in eng.history()], rtol=1e-6)
+    _adam_bar(r["params"].reshape(-1, 8), eng.params_host().reshape(-1, 8), w.cfg, STEPS)
