@@ -60,7 +60,7 @@ extern "C" {
                                 Function's forward) */
 
 /* ABI version; bumped on any signature change. */
-int pf_abi_version(void);  /* 7 */
+int pf_abi_version(void);  /* 8 */
 
 /* Diagnostics: the PF_* environment switches (A/B variants, profiling) are read
  * once at load; this re-reads them (tests that flip a switch at run time). */
@@ -345,8 +345,12 @@ int pf_mse4(const float* img4, const float* target, int P, double* scratch, floa
 int pf_mse4_grad(const float* img4, const float* target, int P, const float* grad_out,
                  float* out4, void* stream);
 
-/* Fixed-order fold of n_part partial triples into sums[3] (deterministic). */
-int pf_fold_loss(const double* part, int n_part, double* sums, void* stream);
+/* Fixed-order fold of n_part partial triples into sums[3] (deterministic: the
+ * order depends on n_part only), many blocks + a last-block fold (ABI 8).
+ * scratch: pf_fold_scratch_bytes(n_part) bytes, zeroed once at allocation
+ * (self-resetting); one fold at a time per scratch. */
+size_t pf_fold_scratch_bytes(int n_part);
+int pf_fold_loss(const double* part, int n_part, double* sums, void* scratch, void* stream);
 
 /*
  * Cross-band gradient exchange (row-band split; replaces the

@@ -82,7 +82,8 @@ SIGNATURES: dict[str, tuple] = {
         [_P, _I, _P, _P, _P, _I, _I, _P, _P, _P, _I, _I, _I, _I, _D, _D, _D, _D, _P, _I, _P, _D,
          _D, _D, _D, _D, _P, _P, _P, _P, _P, _P, _I, _P, _Z, _I, _P, _I, _P],
     ),
-    "pf_fold_loss": (_I, [_P, _I, _P, _P]),
+    "pf_fold_loss": (_I, [_P, _I, _P, _P, _P]),
+    "pf_fold_scratch_bytes": (_Z, [_I]),
     "pf_sum_bands": (_I, [_P, _I, _P, _I, C.c_longlong, C.c_longlong, _P]),
     "pf_backward": (
         _I,

@@ -408,8 +408,12 @@ class Compositor:
         return self.n_tiles * 8
 
     def fold_loss(self, sums: torch.Tensor, stream=None) -> None:
+        if getattr(self, "fold_scratch", None) is None:
+            self.fold_scratch = torch.zeros(int(self.lib.pf_fold_scratch_bytes(self.n_part)),
+                                            dtype=torch.uint8, device=self.device)
         nat.check(self.lib.pf_fold_loss(self.part.data_ptr(), self.n_part, sums.data_ptr(),
-                                        _stream_handle(stream)), "pf_fold_loss")
+                                        self.fold_scratch.data_ptr(), _stream_handle(stream)),
+                  "pf_fold_loss")
         self.launches += 1
 
     # -- K4

@@ -144,7 +144,7 @@ extern "C" int pf_adam(double* params, double* grads, double* m, double* v, cons
   return (int)cudaGetLastError();
 }
 
-extern "C" int pf_abi_version(void) { return 7; }
+extern "C" int pf_abi_version(void) { return 8; }
 extern "C" size_t pf_record_bytes(void) { return sizeof(RecF) + sizeof(RecG) + sizeof(RecC) + sizeof(RecS); }
 extern "C" int pf_render_tile(void) { return kTile; }
 extern "C" long long pf_saved_capacity(int capacity) {

@@ -1279,18 +1279,16 @@ __global__ void __launch_bounds__(step_threads(G), 1) k_step(StepArgs a) {
   }
 }
 
-// Fixed-order fold of pf_fit_step's per-warp loss partials into sums[3] (one
-// block; used before a cross-rank allreduce -- single-rank steps fold inside
-// pf_adam_preprocess instead).
-__global__ void __launch_bounds__(1024) k_fold(const double* __restrict__ part, int n_part,
-                                               double* sums) {
-  __shared__ double red[32][3];
-  double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-  for (int k = threadIdx.x; k < n_part; k += 1024) {
-    v0 += part[3 * k + 0];
-    v1 += part[3 * k + 1];
-    v2 += part[3 * k + 2];
-  }
+// Fixed-order fold of pf_fit_step's per-warp loss partials into sums[3], used
+// before a cross-rank allreduce (single-rank steps fold inside
+// pf_adam_preprocess instead).  Many blocks: block b folds the contiguous chunk
+// [b*chunk, (b+1)*chunk) (strided by thread, warp butterfly, warps in order) into
+// bsum[b]; the last block to finish folds bsum[0..nb) the same way.  The order
+// depends on n_part only, never on timing: deterministic.  (One block over all
+// partials took 60 us at c5: a serial step on the multi-GPU critical path.)
+constexpr int kFoldThreads = 256;
+__device__ __forceinline__ void fold3_block(double& v0, double& v1, double& v2,
+                                            double (*red)[3]) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     v0 += __shfl_xor_sync(kFull, v0, o);
@@ -1303,20 +1301,70 @@ __global__ void __launch_bounds__(1024) k_fold(const double* __restrict__ part, 
     red[threadIdx.x >> 5][2] = v2;
   }
   __syncthreads();
-  if (threadIdx.x < 3) {
-    double s = 0.0;
-    for (int w = 0; w < 32; ++w) s += red[w][threadIdx.x];
-    sums[threadIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(kFoldThreads) k_fold(const double* __restrict__ part,
+                                                       int n_part, int chunk, double* bsum,
+                                                       unsigned* ctr, double* sums) {
+  __shared__ double red[kFoldThreads / 32][3];
+  __shared__ bool last;
+  const int t = threadIdx.x;
+  const int c0 = blockIdx.x * chunk, c1 = min(n_part, c0 + chunk);
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+  for (int k = c0 + t; k < c1; k += kFoldThreads) {
+    v0 += part[3 * (size_t)k + 0];
+    v1 += part[3 * (size_t)k + 1];
+    v2 += part[3 * (size_t)k + 2];
   }
+  fold3_block(v0, v1, v2, red);
+  if (t < 3) {
+    double s = 0.0;
+    for (int w = 0; w < kFoldThreads / 32; ++w) s += red[w][t];
+    bsum[3 * blockIdx.x + t] = s;
+    __threadfence();  // (the block sums before the ticket)
+  }
+  __syncthreads();
+  if (t == 0) last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  v0 = v1 = v2 = 0.0;
+  for (int b = t; b < (int)gridDim.x; b += kFoldThreads) {
+    v0 += __ldcg(bsum + 3 * b + 0);
+    v1 += __ldcg(bsum + 3 * b + 1);
+    v2 += __ldcg(bsum + 3 * b + 2);
+  }
+  __syncthreads();  // (red reused)
+  fold3_block(v0, v1, v2, red);
+  if (t < 3) {
+    double s = 0.0;
+    for (int w = 0; w < kFoldThreads / 32; ++w) s += red[w][t];
+    sums[t] = s;
+  }
+  if (t == 0) *ctr = 0u;  // self-resetting for the next launch / graph replay
+}
+
+static int fold_blocks(int n_part) {
+  const int nb = (n_part + 511) / 512;
+  return nb < 1 ? 1 : (nb > 4 * 148 ? 4 * 148 : nb);
 }
 
 }  // namespace pf
 
 using namespace pf;
 
-extern "C" int pf_fold_loss(const double* part, int n_part, double* sums, void* stream) {
-  if (!part || !sums || n_part < 0) return PF_ERR_ARG;
-  k_fold<<<1, 1024, 0, (cudaStream_t)stream>>>(part, n_part, sums);
+extern "C" size_t pf_fold_scratch_bytes(int n_part) {
+  return n_part < 0 ? 0 : (size_t)fold_blocks(n_part) * 3 * sizeof(double) + 16;
+}
+
+extern "C" int pf_fold_loss(const double* part, int n_part, double* sums, void* scratch,
+                            void* stream) {
+  if (!part || !sums || !scratch || n_part < 0) return PF_ERR_ARG;
+  const int nb = fold_blocks(n_part);
+  const int chunk = n_part > 0 ? (n_part + nb - 1) / nb : 1;
+  double* bsum = static_cast<double*>(scratch);
+  unsigned* ctr = reinterpret_cast<unsigned*>(bsum + 3 * (size_t)nb);
+  k_fold<<<nb, kFoldThreads, 0, (cudaStream_t)stream>>>(part, n_part, chunk, bsum, ctr, sums);
   return (int)cudaGetLastError();
 }
 

@@ -37,7 +37,7 @@ def test_native_library_exports_every_declared_symbol():
         assert hasattr(lib, s), s
     assert set(_declared_symbols()) == set(_native.SIGNATURES)
     typed = _native.load()
-    assert typed.pf_abi_version() == 7
+    assert typed.pf_abi_version() == 8
     assert typed.pf_record_bytes() == 480
     assert typed.pf_render_tile() == 16
     assert typed.pf_saved_capacity(10) == 2560
