@@ -5,6 +5,7 @@ N-GPU step is max over bands + the gradient allreduce (not measurable here).
     python scripts/band_scaling.py c5 1 2 4 8
 """
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -17,6 +18,18 @@ from paper_2602_22625_b200 import synth
 from paper_2602_22625_b200.dist import row_bands, row_cost_from_bins
 from paper_2602_22625_b200.fit import StepEngine
 
+# PF_BAND_NCCL=1: every band step carries the exchange node -- a one-rank NCCL
+# communicator's allreduce captured in the step graph (the fold, the NCCL kernel
+# and the PDL overlap it breaks are measured; only the NVSwitch transfer is not)
+NCCL = os.environ.get("PF_BAND_NCCL") == "1"
+if NCCL:
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29812")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    from paper_2602_22625_b200.dist import make_allreduce
 name = sys.argv[1]
 worlds = [int(v) for v in sys.argv[2:]] or [1, 2, 4, 8]
 w = synth.make_workload(name)
@@ -33,7 +46,8 @@ CH = 8 * 8  # chained mode: 8 graphs of StepEngine.CHUNK (8) steps, timed togeth
 def band_chained_ms(band) -> float:
     """run_loop's own issue pattern: CHUNK-step graphs with PDL edges between
     steps, no L2 flush (the per-step graph launch of band_ms is amortised)."""
-    eng = StepEngine(w.scene, w.cfg, w.loss, CH + 2 * 8 + 2, band=band, use_graph=True)
+    eng = StepEngine(w.scene, w.cfg, w.loss, CH + 2 * 8 + 2, band=band, use_graph=True,
+                     allreduce=make_allreduce() if NCCL else None)
     eng.run(1 + 8 + 7)  # warm-up: single-step graph, one chunk, then align
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -49,7 +63,8 @@ def band_chained_ms(band) -> float:
 
 
 def band_ms(band) -> float:
-    eng = StepEngine(w.scene, w.cfg, w.loss, K + WARM + 2, band=band, use_graph=True)
+    eng = StepEngine(w.scene, w.cfg, w.loss, K + WARM + 2, band=band, use_graph=True,
+                     allreduce=make_allreduce() if NCCL else None)
     eng.run(WARM)
     torch.cuda.synchronize()
     ts = []
@@ -95,4 +110,6 @@ for N in worlds:
               f"eff(no allreduce) {eff:.3f} | chained max {max(cms) * 1e3:8.1f} us  "
               f"eff {ceff:.3f}", flush=True)
 Path("gpurun_out").mkdir(exist_ok=True)
-Path(f"gpurun_out/band_scaling_{name}.json").write_text(json.dumps(res, indent=1))
+res["exchange_node"] = "one-rank NCCL allreduce in every step graph" if NCCL else "none"
+Path(f"gpurun_out/band_scaling_{name}{'_nccl' if NCCL else ''}.json").write_text(
+    json.dumps(res, indent=1))
