@@ -1308,6 +1308,8 @@ __global__ void __launch_bounds__(kFoldThreads) k_fold(const double* __restrict_
                                                        unsigned* ctr, double* sums) {
   __shared__ double red[kFoldThreads / 32][3];
   __shared__ bool last;
+  pdl_wait();     // the fit step's partials (launched as its programmatic dependent)
+  pdl_trigger();  // (the next node -- the allreduce or Adam -- waits for this grid)
   const int t = threadIdx.x;
   const int c0 = blockIdx.x * chunk, c1 = min(n_part, c0 + chunk);
   double v0 = 0.0, v1 = 0.0, v2 = 0.0;
@@ -1364,8 +1366,8 @@ extern "C" int pf_fold_loss(const double* part, int n_part, double* sums, void* 
   const int chunk = n_part > 0 ? (n_part + nb - 1) / nb : 1;
   double* bsum = static_cast<double*>(scratch);
   unsigned* ctr = reinterpret_cast<unsigned*>(bsum + 3 * (size_t)nb);
-  k_fold<<<nb, kFoldThreads, 0, (cudaStream_t)stream>>>(part, n_part, chunk, bsum, ctr, sums);
-  return (int)cudaGetLastError();
+  return (int)launch_pdl(k_fold, nb, kFoldThreads, 0, (cudaStream_t)stream, part, n_part, chunk,
+                         bsum, ctr, sums);
 }
 
 // (capacity entries for CSR offsets / the slot-mode pool, plus the slot-mode
