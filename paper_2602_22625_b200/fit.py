@@ -596,7 +596,9 @@ class StepEngine:
         out as CHUNK-step graph replays once the single-step graph exists; the
         device iteration counter indexes the lr / bias-correction tables, so the
         result is identical to k single steps (test_chunked_run_equals_steps)."""
-        chunked = self.use_graph and not self.noise_bg and self.allreduce is None
+        # (with an allreduce every step of the chunk graph carries its own captured
+        # collective: ranks replay the same chunks in lockstep)
+        chunked = self.use_graph and not self.noise_bg
         while k > 0:
             if chunked and self.graph is not None and k >= self.CHUNK and \
                     self.done + self.CHUNK <= self.total:

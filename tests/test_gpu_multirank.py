@@ -251,8 +251,7 @@ def _nccl_rank_main(rank, world, name, steps, out_dir):
     nty = -(-w.scene.canvas_h // 16)
     eng = StepEngine(w.scene, w.cfg, w.loss, steps, band=row_bands(nty, world)[rank],
                      allreduce=make_allreduce(), use_graph=True)
-    for _ in range(steps):
-        eng.step()
+    eng.run(steps)  # one single-step graph, then CHUNK-step graphs (a collective per step)
     torch.cuda.synchronize()
     eng.check()
     np.savez(os.path.join(out_dir, f"nccl{rank}.npz"), params=eng.params_host(),
@@ -265,7 +264,8 @@ def test_nccl_allreduce_in_step_graph(torch_cuda, tmp_path):
     """The multi-GPU step's exact code path on hardware with the one GPU there
     is: an NCCL process group (world 1: NCCL refuses two ranks on one device),
     the gradient + loss allreduce captured inside the step's CUDA graph between
-    the fit-step kernel and the Adam + records launch.  A one-rank sum is the
+    the fit-step kernel and the Adam + records launch, also in run()'s CHUNK-step
+    graphs (a collective per captured step).  A one-rank sum is the
     identity, so the run equals the engine without an allreduce (under the
     Adam-noise bar of the float64 gradient atomics' order)."""
     import torch.multiprocessing as mp
@@ -274,14 +274,15 @@ def test_nccl_allreduce_in_step_graph(torch_cuda, tmp_path):
     from paper_2602_22625_b200.fit import StepEngine
 
     os.environ["MASTER_PORT"] = str(29700 + (os.getpid() % 1000))
-    mp.spawn(_nccl_rank_main, args=(1, "c3", STEPS, str(tmp_path)), nprocs=1, join=True)
+    steps = 1 + 2 * StepEngine.CHUNK + 1
+    mp.spawn(_nccl_rank_main, args=(1, "c3", steps, str(tmp_path)), nprocs=1, join=True)
     r = dict(np.load(tmp_path / "nccl0.npz"))
     assert bool(r["graph"])
     w = synth.make_workload("c3")
-    w.cfg.num_iterations = STEPS
-    eng = StepEngine(w.scene, w.cfg, w.loss, STEPS, use_graph=True)
-    for _ in range(STEPS):
+    w.cfg.num_iterations = steps
+    eng = StepEngine(w.scene, w.cfg, w.loss, steps, use_graph=True)
+    for _ in range(steps):
         eng.step()
     eng.check()
-    np.testing.assert_allclose(r["loss"], [h.loss for h in eng.history()], rtol=1e-6)
-    _adam_bar(r["params"].reshape(-1, 8), eng.params_host().reshape(-1, 8), w.cfg, STEPS)
+    np.testing.assert_allclose(r["loss"], [h.loss for h in eng.history()], rtol=1e-5)
+    _adam_bar(r["params"].reshape(-1, 8), eng.params_host().reshape(-1, 8), w.cfg, steps)
