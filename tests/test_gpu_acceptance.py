@@ -371,3 +371,56 @@ def test_criterion_08b_stuck_decay_lowers_video_error(pf):
 
     off, on = final_mse(False), final_mse(True)
     assert on < off, (off, on)
+
+
+# -- compositing algebra known-answer tests (test_raster.py:118-190) on the GPU --------
+
+def _one_prim_scene(opacity_logit=2.0, alpha_max=1.0):
+    from paper_2602_22625_b200.scene import PrimitiveParams, PrimitiveTemplate, Scene
+
+    t = np.zeros((5, 5, 4))
+    t[:, :, 3] = 1.0
+    t[:, :, :3] = 0.5
+    prim = PrimitiveParams(x=8.0, y=8.0, scale=3.0, rotation=0.0, opacity_logit=opacity_logit,
+                           color_logits=(4.0, -4.0, 0.0))
+    return Scene([prim], [PrimitiveTemplate(t)], 16, 16, background=(0.0, 0.0, 1.0),
+                 alpha_max=alpha_max)
+
+
+def test_single_primitive_center_pixel_algebra(pf):
+    # test_raster.py:130-137 (atol 1e-12 on float64; the GPU image is float32)
+    raster, _ = pf
+    out, _ = raster.render_forward(_one_prim_scene(), eps_skip=0.0)
+    a = 1.0 / (1.0 + np.exp(-2.0))
+    c = np.array([1 / (1 + np.exp(-4.0)), 1 / (1 + np.exp(4.0)), 0.5])
+    expect = a * c + (1 - a) * np.array([0.0, 0.0, 1.0])
+    np.testing.assert_allclose(np.asarray(out.color)[8, 8], expect, atol=1e-7)
+    assert float(np.asarray(out.alpha)[8, 8]) == pytest.approx(a, abs=1e-7)
+
+
+def test_two_primitive_over_order_front_wins(pf):
+    # test_raster.py:140-153: the z-front opaque layer hides the one behind it
+    raster, _ = pf
+    from paper_2602_22625_b200.scene import PrimitiveParams, PrimitiveTemplate, Scene
+
+    t = np.zeros((5, 5, 4))
+    t[:, :, 3] = 1.0
+    t[:, :, :3] = 0.5
+    front = PrimitiveParams(x=8, y=8, scale=4, opacity_logit=50.0,
+                            color_logits=(9.0, -9.0, -9.0), z=0)
+    back = PrimitiveParams(x=8, y=8, scale=4, opacity_logit=50.0,
+                           color_logits=(-9.0, 9.0, -9.0), z=1)
+    sc = Scene([back, front], [PrimitiveTemplate(t)], 16, 16, background=(0, 0, 0))
+    out, _ = raster.render_forward(sc, eps_skip=0.0)
+    np.testing.assert_allclose(np.asarray(out.color)[8, 8], [1, 0, 0], atol=1e-3)
+
+
+def test_eps_skip_zero_vs_default_differ_only_slightly(pf):
+    # test_raster.py:165-170 (there on random_scene(3, n=15); here the golden random_s3 =
+    # random_scene(3, n=12, 40x36))
+    raster, _ = pf
+    sc = scene_from(load_case("random_s3"))
+    exact, _ = raster.render_forward(sc, eps_skip=0.0)
+    fast, _ = raster.render_forward(sc)
+    d = np.abs(np.asarray(exact.color) - np.asarray(fast.color)).max()
+    assert 0.0 < d < 5e-2
