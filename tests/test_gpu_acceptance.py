@@ -424,3 +424,36 @@ def test_eps_skip_zero_vs_default_differ_only_slightly(pf):
     fast, _ = raster.render_forward(sc)
     d = np.abs(np.asarray(exact.color) - np.asarray(fast.color)).max()
     assert 0.0 < d < 5e-2
+
+
+def test_optimize_reduces_loss_logs_and_dumps(pf, tmp_path):
+    """test_fit.py:283-301 through fit.optimize on the GPU (default templates,
+    the reference's smoke config), plus the dump_dir / dump_every images
+    (fit.py:509-518: the pre-update render of every dump_every-th iteration)."""
+    import csv
+
+    from scipy.ndimage import gaussian_filter
+
+    from paper_2602_22625_b200 import fit
+
+    img = gaussian_filter(np.random.default_rng(0).random((32, 32, 3)), (6, 6, 0))
+    target = (img - img.min()) / (img.max() - img.min())
+    log = tmp_path / "fit_log.csv"
+    cfg = fit.FitConfig(num_primitives=20, num_iterations=80, seed=0, tile_size=16,
+                        scale_min=2.0, scale_max=8.0, do_reinit=False, compute_psnr=True,
+                        bg_color="black", dump_every=40)
+    scene, history = fit.optimize(target, None, cfg, log_path=log, dump_dir=tmp_path / "dump")
+    assert scene.n == 20 and len(history) == 80
+    first, last = history[0], history[-1]
+    assert last.loss < first.loss * 0.5
+    assert last.psnr > first.psnr
+    assert history[0].lr == pytest.approx(cfg.learning_rate)
+    assert history[-1].lr == pytest.approx(cfg.learning_rate * cfg.decay_final_fraction)
+    with open(log, newline="") as f:
+        rows = list(csv.reader(f))
+    assert rows[0] == ["iter", "loss", "psnr", "lr", "reinit_count"]
+    assert len(rows) == 81
+    assert float(rows[1][1]) == pytest.approx(first.loss)
+    assert int(rows[-1][0]) == 79
+    dumps = sorted(p.name for p in (tmp_path / "dump").iterdir())
+    assert dumps == ["iter_00000.png", "iter_00040.png"]
