@@ -25,7 +25,7 @@ RENDER_CASES = sorted(
     Path(p).stem for p in glob.glob(str(GOLDEN / "*.npz"))
     if Path(p).stem not in ("adam_rollout", "run_loop_small", "synth_c1_init", "video_heuristics",
                             "reinit_unit", "run_loop_reinit", "run_loop_reinit_noise",
-                            "video_dropin", "run_loop_hook_resume", "acceptance", "optimize_small")
+                            "video_dropin", "run_loop_hook_resume", "acceptance", "optimize_small", "export_tests")
     and not Path(p).stem.startswith("export_")
 )
 

@@ -460,6 +460,13 @@ def acceptance_cases():
             d[f"r{seed}_{k}"] = v
     np.savez_compressed(OUT / "acceptance.npz", **d)
     print("acceptance", len(d))
+    # the scenes of the reference's export tests (test_export.py:226-293)
+    e = {}
+    for tag, (seed, n, w, h) in {"x8": (8, 5, 36, 28), "x9": (9, 2, 48, 48),
+                                 "x10": (10, 3, 20, 20), "x11": (11, 4, 24, 24)}.items():
+        for k, v in scene_arrays(random_scene(seed, n=n, w=w, h=h)).items():
+            e[f"{tag}_{k}"] = v
+    np.savez_compressed(OUT / "export_tests.npz", **e)
 
 
 if __name__ == "__main__":
