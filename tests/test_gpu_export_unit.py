@@ -1,4 +1,4 @@
-"""The reference's export tests (tests/test_export.py:226-293) on the GPU
+"""The reference's export tests (tests/test_export.py:191-293) on the GPU
 exporter (export.export_layers: primitive-parallel layer kernel + the composite
 through the GPU forward), on the reference's own scenes (golden export_tests.npz
 = conftest.random_scene with the same seeds and sizes)."""
@@ -94,3 +94,46 @@ def test_manifest_round_trip(ex, tmp_path):
     export, _ = ex
     manifest = export.export_layers(_scene("x11"), 2, tmp_path)
     assert export.read_manifest(tmp_path / "manifest.txt") == manifest
+
+
+def _one_prim_scene(x=14.0, y=10.0, scale=5.0, mu_blend=0.0, w=32, h=24):
+    # test_export.py:191-198
+    from paper_2602_22625_b200.scene import PrimitiveParams, PrimitiveTemplate, Scene
+
+    size = 13
+    yy, xx = np.mgrid[0:size, 0:size].astype(np.float64)
+    c = (size - 1) / 2
+    disk = np.zeros((size, size, 4))
+    disk[:, :, 0], disk[:, :, 1], disk[:, :, 2] = 0.9, 0.5, 0.3
+    disk[:, :, 3] = np.clip(1.0 - (np.hypot(yy - c, xx - c) / c) ** 2, 0.0, 1.0) ** 2
+    p = PrimitiveParams(x=x, y=y, scale=scale, rotation=0.7, opacity_logit=1.2,
+                        color_logits=(0.4, -0.3, 0.8), template_id=0, z=0)
+    return Scene([p], [PrimitiveTemplate(disk)], w, h, background=(0.25, 0.5, 0.75),
+                 mu_blend=mu_blend)
+
+
+def test_layer_bbox_matches_half_side(ex):
+    # test_export.py:201-211
+    import math
+
+    export, _ = ex
+    r = 5.0 * math.hypot(1.0, 1.0) + export.LAYER_BBOX_PAD
+    assert export.layer_bbox(_one_prim_scene(), 0) == (
+        max(math.floor(14.0 - r), 0), max(math.floor(10.0 - r), 0),
+        min(math.ceil(14.0 + r), 31), min(math.ceil(10.0 + r), 23))
+    with pytest.raises(export.DegenerateBBox):
+        export.layer_bbox(_one_prim_scene(x=-50.0, y=-50.0), 0)
+
+
+@pytest.mark.parametrize("mu_blend", [0.0, 0.35])
+def test_render_layer_reproduces_contribution(ex, mu_blend):
+    # test_export.py:214-223 (atol 1e-12 there on float64; the GPU layer is float32)
+    export, raster = ex
+    scene = _one_prim_scene(mu_blend=mu_blend)
+    (x0, y0, x1, y1), rgba = export.render_layer(scene, 0)
+    img = np.broadcast_to(np.asarray(scene.background), (24, 32, 3)).copy()
+    view = img[y0:y1 + 1, x0:x1 + 1]
+    view *= 1.0 - rgba[:, :, 3:4]
+    view += rgba[:, :, :3]
+    out, _ = raster.render_forward(scene, eps_skip=0.0)
+    np.testing.assert_allclose(img, np.asarray(out.color), atol=1e-6)
