@@ -1077,8 +1077,11 @@ extern "C" int pf_slot_reset(void* slots, int n_tiles, int m, int capacity,
   return (int)e;
 }
 
+#ifndef PF_PRIM_LPP
+#define PF_PRIM_LPP 0  // (A/B: 0 = by occupancy, 8 / 4 forced)
+#endif
 static int launch_prim(bool adam, const PreArgs& a, cudaStream_t st) {
-  const int lpp = prim_lanes(a.n);
+  const int lpp = PF_PRIM_LPP ? PF_PRIM_LPP : prim_lanes(a.n);
   const int blocks = div_up(a.n > 0 ? a.n * lpp : 1, kPrimThreads);
   if (adam)
     return (int)launch_pdl(lpp == 8 ? k_prim<true, 8> : k_prim<true, 4>, blocks, kPrimThreads,
