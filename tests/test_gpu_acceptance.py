@@ -457,3 +457,30 @@ def test_optimize_reduces_loss_logs_and_dumps(pf, tmp_path):
     assert int(rows[-1][0]) == 79
     dumps = sorted(p.name for p in (tmp_path / "dump").iterdir())
     assert dumps == ["iter_00000.png", "iter_00040.png"]
+
+
+def test_bin_tiles_culls_far_primitives(pf):
+    # test_raster.py:217-226 on the GPU binning
+    raster, _ = pf
+    from paper_2602_22625_b200.scene import PrimitiveParams, PrimitiveTemplate, Scene
+
+    near = PrimitiveParams(x=8.0, y=8.0, scale=3.0, z=0)
+    far = PrimitiveParams(x=100.0, y=100.0, scale=3.0, z=1)
+    sc = Scene([near, far], [PrimitiveTemplate(_soft_disk(15))], 128, 128)
+    bins = raster.bin_tiles(sc, tile_size=32, padding=2.0)
+    first = list(bins.tile_list(0, 0))
+    assert 0 in first and 1 not in first
+
+
+def test_render_ignores_fully_offcanvas_primitive(pf):
+    # test_raster.py:229-238: bit-identical image with and without an off-canvas primitive
+    raster, _ = pf
+    from paper_2602_22625_b200.scene import PrimitiveParams, PrimitiveTemplate, Scene
+
+    tpl = PrimitiveTemplate(_soft_disk(15))
+    both = Scene([PrimitiveParams(x=10.0, y=10.0, scale=4.0, z=0),
+                  PrimitiveParams(x=-50.0, y=-50.0, scale=4.0, z=1)], [tpl], 24, 24)
+    only = Scene([PrimitiveParams(x=10.0, y=10.0, scale=4.0, z=0)], [tpl], 24, 24)
+    a, _ = raster.render_forward(both, raster.bin_tiles(both), eps_skip=0.0)
+    b, _ = raster.render_forward(only, raster.bin_tiles(only), eps_skip=0.0)
+    np.testing.assert_array_equal(np.asarray(a.color), np.asarray(b.color))
