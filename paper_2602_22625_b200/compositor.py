@@ -375,21 +375,33 @@ class Compositor:
             self.img4 = torch.zeros(P * 4, dtype=torch.float32, device=dev)
         Pt = float(P_total if P_total is not None else P)
         p = nat.ptr
-        nat.check(
-            self.lib.pf_fit_step(
+        # the argument list minus the per-call pointers, built once per (mode,
+        # scalars, the buffers that may be (re)attached) and reused (the eager
+        # autograd step calls this twice per iteration)
+        key = (int(loss_kind), float(eps_skip), tuple(float(c) for c in bg_rgb), float(alpha_w),
+               float(w_mse), float(w_gray), Pt, self.part.data_ptr(), self.stage_hint,
+               p(self.tile_classes), p(self.slots))
+        cache = self.__dict__.setdefault("_fit_args", {})
+        args = cache.get(key)
+        if args is None:
+            args = cache[key] = [
                 self.rec.data_ptr(), self.n, self.atlas.tex.data_ptr(),
                 self.atlas.apad.data_ptr(), self.atlas.apad64.data_ptr(), self.atlas.pad_texels,
                 self.atlas.texels,
                 self.bin_off.data_ptr(), self.bin_idx.data_ptr(), self.status.data_ptr(),
                 self.W, self.H, self.band.ty_begin, self.band.ty_end, float(eps_skip),
-                float(bg_rgb[0]), float(bg_rgb[1]), float(bg_rgb[2]), p(bg4), int(loss_kind),
-                p(tgt4), float(alpha_w), float(w_mse), float(w_gray), 1.0 / (3.0 * Pt),
-                1.0 / Pt,
-                self.spill.data_ptr(), p(self.img4) if image else None, self.part.data_ptr(),
-                p(grads), self.step_ctr.data_ptr(), nat.ptr(self.tile_classes),
+                float(bg_rgb[0]), float(bg_rgb[1]), float(bg_rgb[2]), None, int(loss_kind),
+                None, float(alpha_w), float(w_mse), float(w_gray), 1.0 / (3.0 * Pt), 1.0 / Pt,
+                self.spill.data_ptr(), None, self.part.data_ptr(),
+                None, self.step_ctr.data_ptr(), nat.ptr(self.tile_classes),
                 self.stage_hint, self.scratch.data_ptr(), self.scratch_bytes, self.capacity,
-                nat.ptr(self.slots), self.slot_m, _stream_handle(stream)),
-            "pf_fit_step")
+                nat.ptr(self.slots), self.slot_m, None]
+        args = list(args)
+        args[18], args[20] = p(bg4), p(tgt4)
+        args[27] = p(self.img4) if image else None
+        args[29] = p(grads)
+        args[38] = _stream_handle(stream)
+        nat.check(self.lib.pf_fit_step(*args), "pf_fit_step")
         self.launches += 1
         if sums is not None:
             self.fold_loss(sums, stream)
