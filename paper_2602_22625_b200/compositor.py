@@ -256,13 +256,16 @@ class Compositor:
             nat.check(self.lib.pf_slot_reset(self.slots.data_ptr(), self.n_tiles, self.slot_m,
                                              self.capacity, self.tile_classes.data_ptr(),
                                              _stream_handle(stream)), "pf_slot_reset")
-        nat.check(
-            self.lib.pf_preprocess(
-                params.data_ptr(), self.n, self.alpha_max, self.mu_blend, self.padding, self.W,
-                self.H, self.tile, self.band.ty_begin, self.band.ty_end, self.capacity,
-                self.rec.data_ptr(), self.scratch.data_ptr(), self.scratch_bytes,
-                *self._slot_args(), _stream_handle(stream)),
-            "pf_preprocess")
+        key = (nat.ptr(self.slots), nat.ptr(self.tile_classes))
+        tail = self.__dict__.get("_pre_tail")
+        if tail is None or tail[0] != key:
+            # (everything after the parameter pointer except the stream: constant)
+            tail = self._pre_tail = (key, [
+                self.n, self.alpha_max, self.mu_blend, self.padding, self.W, self.H, self.tile,
+                self.band.ty_begin, self.band.ty_end, self.capacity, self.rec.data_ptr(),
+                self.scratch.data_ptr(), self.scratch_bytes, *self._slot_args()])
+        nat.check(self.lib.pf_preprocess(params.data_ptr(), *tail[1], _stream_handle(stream)),
+                  "pf_preprocess")
         self.launches += 1
 
     def preprocess_sync(self, params: torch.Tensor, src: torch.Tensor, stream=None) -> None:
@@ -459,6 +462,9 @@ def pixels4(rgb: np.ndarray, w: np.ndarray | float | None = None) -> np.ndarray:
     return out.reshape(-1)
 
 
+_GAINS8: dict[tuple, object] = {}  # gains -> ctypes double[8] (adam_launch)
+
+
 def adam_launch(params, grads, m, v, *, frozen=None, gains=None, n: int,
                 lr_table=None, bc1_table=None, bc2_table=None, iter_counter=None,
                 lr=0.0, bc1=1.0, bc2=1.0, clamp=False, s_min=0.0, s_max=0.0,
@@ -469,7 +475,10 @@ def adam_launch(params, grads, m, v, *, frozen=None, gains=None, n: int,
     p = nat.ptr
     g8 = None
     if gains is not None:
-        g8 = (C.c_double * 8)(*[float(g) for g in gains])
+        gk = tuple(float(g) for g in gains)
+        g8 = _GAINS8.get(gk)
+        if g8 is None:  # (kept alive here: the launch reads it by address)
+            g8 = _GAINS8[gk] = (C.c_double * 8)(*gk)
     P = float(P_total)
     nat.check(
         lib.pf_adam(
