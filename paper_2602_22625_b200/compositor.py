@@ -313,15 +313,18 @@ class Compositor:
         (slot mode: nothing to do -- K1 scattered the lists)."""
         if self.slots is not None:
             return
-        nat.check(
-            self.lib.pf_bin(self.n, self.W, self.H, self.tile, self.band.ty_begin,
-                            self.band.ty_end, self.capacity, self.scratch.data_ptr(),
-                            self.scratch_bytes, self.bin_off.data_ptr(),
-                            self.bin_idx.data_ptr(), self.status.data_ptr(),
-                            nat.ptr(self.tile_classes), _stream_handle(stream)),
-            "pf_bin")
-        self.launches += int(self.lib.pf_bin_launches(self.n, self.W, self.H, self.tile,
-                                                      self.band.ty_begin, self.band.ty_end))
+        key = nat.ptr(self.tile_classes)
+        cached = self.__dict__.get("_bin_args")
+        if cached is None or cached[0] != key:
+            # (constant per compositor but for the tile classes, attached later)
+            cached = self._bin_args = (key, [
+                self.n, self.W, self.H, self.tile, self.band.ty_begin, self.band.ty_end,
+                self.capacity, self.scratch.data_ptr(), self.scratch_bytes,
+                self.bin_off.data_ptr(), self.bin_idx.data_ptr(), self.status.data_ptr(), key],
+                int(self.lib.pf_bin_launches(self.n, self.W, self.H, self.tile,
+                                             self.band.ty_begin, self.band.ty_end)))
+        nat.check(self.lib.pf_bin(*cached[1], _stream_handle(stream)), "pf_bin")
+        self.launches += cached[2]
 
     def check_overflow(self) -> int:
         """Synchronising read of K; raises BinOverflow when capacity was exceeded."""
